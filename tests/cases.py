@@ -1,0 +1,216 @@
+"""Deterministic parity cases shared by the golden generator and the tests.
+
+Each case is a dict with ``image`` (H, W, C) float64, ``labels`` (H, W)
+uint8, ``guide`` ((H, W, 2) float64 or None), ``params`` (FillParams
+keyword dict) and ``tracked`` (bool).  The first group restates the
+reference's own engine/tracker test scenes (pkg/tests/test_engine.py,
+test_tracker.py, test_acceptance.py); the second group is randomized stress
+on the decision path (rotated balls at arbitrary guide angles, mu in
+{0, finite, inf}, every order, periodic x, Bystander islands).
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+READABLE, BYSTANDER, INPAINT = 0, 128, 255
+
+
+def _block(H, W, j0, j1, i0, i1):
+    lab = np.zeros((H, W), dtype=np.uint8)
+    lab[j0:j1, i0:i1] = INPAINT
+    return lab
+
+
+def _case(name, image, labels, guide=None, tracked=True, **params):
+    return dict(name=name, image=np.ascontiguousarray(image, dtype=np.float64),
+                labels=np.ascontiguousarray(labels, dtype=np.uint8),
+                guide=None if guide is None else np.ascontiguousarray(guide, dtype=np.float64),
+                params=params, tracked=tracked)
+
+
+def reference_scenes():
+    """Scenes of the reference test-suite (file:line in each name)."""
+    out = []
+    lab = _block(20, 20, 5, 15, 5, 15)
+    out.append(_case("onion_block test_engine.py:144", np.full((20, 20, 3), 0.25), lab,
+                     tracked=False, order="onion"))
+    lab = np.array([[READABLE, INPAINT, INPAINT, READABLE]], dtype=np.uint8)
+    img = np.zeros((1, 4, 1))
+    img[0, 3, 0] = 0.9
+    out.append(_case("snapshot test_engine.py:156", img, lab, tracked=False, r=1, order="onion"))
+    rng = np.random.default_rng(7)
+    img = rng.random((24, 24, 3))
+    lab = _block(24, 24, 8, 16, 8, 16)
+    img[lab == INPAINT] = 0.0
+    out.append(_case("rot_g0 test_engine.py:170", img, lab, tracked=False))
+    out.append(_case("axis_g0 test_engine.py:170", img, lab, tracked=False, neighborhood="axis_ball"))
+    rng = np.random.default_rng(3)
+    img = rng.random((30, 30, 3))
+    lab = _block(30, 30, 9, 21, 7, 23)
+    img[lab == INPAINT] = 0.0
+    g = np.zeros((30, 30, 2))
+    g[:, :, 0] = 0.7
+    out.append(_case("determinism test_engine.py:180", img, lab, g, tracked=False))
+    rng = np.random.default_rng(11)
+    img = rng.uniform(0.2, 0.6, size=(26, 26, 3))
+    lab = _block(26, 26, 6, 20, 6, 20)
+    img[lab == INPAINT] = 0.0
+    out.append(_case("hull test_engine.py:192", img, lab, tracked=False, order="onion"))
+    lab = np.zeros((12, 31), dtype=np.uint8)
+    lab[6:, :] = INPAINT
+    img = np.zeros((12, 31, 1))
+    img[:6, :, 0] = 0.8
+    out.append(_case("flat_front test_engine.py:226", img, lab, tracked=False, order="smart"))
+    rng = np.random.default_rng(5)
+    img = rng.random((20, 20, 1))
+    lab = _block(20, 20, 6, 14, 6, 14)
+    img[lab == INPAINT] = 0.0
+    out.append(_case("dt_latch test_engine.py:234", img, lab, np.zeros((20, 20, 2)),
+                     tracked=False, order="smart_with_data_term"))
+    lab = _block(14, 40, 5, 9, 4, 36)
+    img = np.full((14, 40, 1), 0.6)
+    img[lab == INPAINT] = 0.0
+    g = np.zeros((14, 40, 2))
+    g[:, :20, 0] = 1.0
+    out.append(_case("dt_defer test_engine.py:248", img, lab, g, tracked=False,
+                     order="smart_with_data_term"))
+    lab = np.full((7, 7), BYSTANDER, dtype=np.uint8)
+    lab[:3, :3] = READABLE
+    lab[3, 3] = INPAINT
+    img = np.zeros((7, 7, 1))
+    img[:3, :3, 0] = 0.45
+    out.append(_case("deadlock_mean test_engine.py:263", img, lab, tracked=False, r=1, order="onion"))
+    lab = np.zeros((8, 12), dtype=np.uint8)
+    lab[4:, :] = INPAINT
+    img = np.full((8, 12, 1), 0.3)
+    img[lab == INPAINT] = 0.0
+    th = math.radians(10.0)
+    g = np.zeros((8, 12, 2))
+    g[..., 0] = math.cos(th)
+    g[..., 1] = math.sin(th)
+    out.append(_case("deadlock_chain test_engine.py:277", img, lab, g, tracked=False, order="smart"))
+    lab = np.zeros((11, 11), dtype=np.uint8)
+    lab[3:8, 3:8] = BYSTANDER
+    lab[4:7, 4:7] = INPAINT
+    img = np.full((11, 11, 1), 0.7)
+    img[3:8, 3:8] = 0.0
+    out.append(_case("unfillable_pocket test_engine.py:294", img, lab, tracked=False, order="onion"))
+    out.append(_case("unfillable_all test_engine.py:309", np.zeros((5, 5, 2)),
+                     np.full((5, 5), INPAINT, dtype=np.uint8), tracked=False))
+    for kind in ("axis_ball", "rotated_ball"):
+        H, W, th = 80, 120, math.radians(73.0)
+        image = np.full((H, W, 1), 1.0)
+        jj, ii = np.mgrid[0:H, 0:W]
+        d = -math.sin(th) * (ii - W / 2) + math.cos(th) * (jj - H / 2)
+        lab = np.zeros((H, W), dtype=np.uint8)
+        lab[H // 2:, :] = INPAINT
+        image[(np.abs(d) <= 2.0) & (lab == READABLE), 0] = 0.0
+        g = np.zeros((H, W, 2))
+        g[..., 0] = math.cos(th)
+        g[..., 1] = math.sin(th)
+        out.append(_case(f"kink_{kind} test_engine.py:379", image, lab, g, tracked=False,
+                         order="onion", neighborhood=kind, mu=50.0))
+    rng = np.random.default_rng(19)
+    img = rng.random((28, 34, 3))
+    lab = np.zeros((28, 34), dtype=np.uint8)
+    lab[7:21, 9:27] = INPAINT
+    lab[12:15, 14:17] = BYSTANDER
+    img[lab != READABLE] = 0.0
+    g = np.zeros((28, 34, 2))
+    g[..., 0] = 0.8
+    g[..., 1] = 0.2
+    out.append(_case("trk_untracked test_tracker.py:81", img, lab, g, tracked=False))
+    out.append(_case("trk_tracked test_tracker.py:81", img, lab, g, tracked=True))
+    lab = np.zeros((14, 14), dtype=np.uint8)
+    lab[2:12, 2:12] = INPAINT
+    img = np.full((14, 14, 1), 0.9)
+    img[lab == INPAINT] = 0.0
+    out.append(_case("trk_threads test_tracker.py:101", img, lab, tracked=True, order="onion"))
+    lab = np.zeros((10, 12), dtype=np.uint8)
+    lab[3:7, :3] = INPAINT
+    lab[3:7, 9:] = INPAINT
+    img = np.full((10, 12, 1), 0.2)
+    img[lab == INPAINT] = 0.0
+    out.append(_case("trk_periodic test_tracker.py:143", img, lab, tracked=True, order="onion",
+                     periodic_x=True))
+    return out
+
+
+def islands_labels(rng, lo=24, hi=97):
+    """Random elliptic holes with Bystander islands (cf. test_acceptance.py:175-199)."""
+    H = int(rng.integers(lo, hi))
+    W = int(rng.integers(lo, hi))
+    lab = np.zeros((H, W), dtype=np.uint8)
+    jj, ii = np.mgrid[0:H, 0:W]
+    for _ in range(int(rng.integers(1, 4))):
+        cy, cx = rng.uniform(0, H), rng.uniform(0, W)
+        ry, rx = rng.uniform(3, H / 2), rng.uniform(3, W / 2)
+        lab[((jj - cy) / ry) ** 2 + ((ii - cx) / rx) ** 2 <= 1.0] = INPAINT
+    inp = np.argwhere(lab == INPAINT)
+    for _ in range(int(rng.integers(1, 4))):
+        if inp.size == 0:
+            break
+        j, i = inp[rng.integers(0, len(inp))]
+        lab[j:j + int(rng.integers(1, 4)), i:i + int(rng.integers(1, 4))] = BYSTANDER
+    for _ in range(int(rng.integers(0, 3))):
+        lab[rng.integers(0, H), rng.integers(0, W)] = BYSTANDER
+    return lab
+
+
+def random_scenes(n=40, seed=1837, lo=16, hi=64):
+    """Randomized decision-path stress: every order, ball, mu regime and g source."""
+    rng = np.random.default_rng(seed)
+    out = []
+    orders = ("onion", "smart", "smart_with_data_term")
+    for k in range(n):
+        lab = islands_labels(rng, lo, hi)
+        H, W = lab.shape
+        C = int(rng.integers(1, 5))
+        img = rng.uniform(size=(H, W, C))
+        img[lab == INPAINT] = 0.0
+        r = int(rng.integers(1, 7))
+        mu = float(rng.choice([0.0, 10.0, 50.0, 100.0, math.inf]))
+        order = orders[k % 3]
+        nb = "axis_ball" if k % 4 == 3 else "rotated_ball"
+        periodic = bool(k % 5 == 0)
+        gmode = k % 4
+        guide = None
+        extra = {}
+        if gmode == 0:
+            extra = dict(g_source="fixed", g_fixed=(float(rng.uniform(-1, 1)), float(rng.uniform(-1, 1))))
+        elif gmode == 1:
+            extra = dict(g_source="fixed", g_fixed=(0.6, 0.8))
+        elif gmode == 2:
+            ang = rng.uniform(0, 2 * math.pi, size=(H, W))
+            mag = rng.uniform(0, 1, size=(H, W)) * (rng.uniform(size=(H, W)) < 0.6)
+            guide = np.stack([mag * np.cos(ang), mag * np.sin(ang)], axis=-1)
+        out.append(_case(f"rand{k}", img, lab, guide, tracked=bool(k % 2 == 0), r=r, mu=mu,
+                         order=order, neighborhood=nb, periodic_x=periodic, **extra))
+    return out
+
+
+def guide_cases(n=12, seed=303):
+    """Random spline sets over random label maps for the rasteriser."""
+    rng = np.random.default_rng(seed)
+    out = []
+    for k in range(n):
+        lab = islands_labels(rng, 20, 90)
+        H, W = lab.shape
+        polys, dirs, kinds, raw = [], [], [], []
+        for s in range(int(rng.integers(0, 5))):
+            kind = "bezier" if rng.uniform() < 0.5 else "polyline"
+            if kind == "bezier":
+                pts = rng.uniform(-5, max(H, W) + 5, size=(3 * int(rng.integers(1, 3)) + 1, 2))
+            else:
+                pts = rng.uniform(-5, max(H, W) + 5, size=(int(rng.integers(2, 5)), 2))
+                if k == 0 and s == 0:
+                    pts = np.array([[3.0, 4.0], [3.0, 4.0 + 1e-9], [10.0, 12.0]])
+            ang = rng.uniform(0, 2 * math.pi)
+            mag = rng.uniform(0, 1)
+            raw.append(dict(points=pts, kind=kind, direction=(mag * math.cos(ang), mag * math.sin(ang))))
+        eta = float(rng.choice([3.0, 1.5, 4.0]))
+        out.append(dict(name=f"gf{k}", labels=lab, splines=raw, eta=eta))
+    return out
