@@ -1,0 +1,185 @@
+/*
+ * guidefill_b200.h -- C ABI of the B200-native Guidefill fill engine.
+ *
+ * Plain pointers and sizes only; every device pointer is CUDA global memory
+ * on the current device, every call is stream-ordered on `stream`
+ * (a cudaStream_t, NULL = legacy default stream) and re-entrant: there is no
+ * global mutable state, all scratch lives in the caller's workspace.
+ * Functions return GF_OK (0) or a negative GF_E* code; gf_last_error()
+ * returns a thread-local message for the last failure on the calling thread.
+ *
+ * The reference (arXiv 1611.05319, /root/reference/pkg) is pure Python with
+ * no FFI; each entry point below replaces one of its Python operators, cited
+ * as file:line under pkg/src/guidefill/.  INTEGRATION.md shows the ctypes
+ * binding a maintainer adds on the reference side.
+ */
+#ifndef GUIDEFILL_B200_H
+#define GUIDEFILL_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GF_ABI_VERSION 1
+
+/* status codes */
+#define GF_OK 0
+#define GF_E_INVALID (-1)   /* bad argument (maps to the reference's ValueError) */
+#define GF_E_CUDA (-2)      /* CUDA runtime failure */
+#define GF_E_WORKSPACE (-3) /* workspace too small */
+#define GF_E_UNSUPPORTED (-4)
+
+/* element types */
+#define GF_F32 0
+#define GF_F64 1
+
+/* FillParams.order (engine.py:28) */
+#define GF_ORDER_ONION 0
+#define GF_ORDER_SMART 1
+#define GF_ORDER_SMART_DATA 2
+/* FillParams.neighborhood (engine.py:29) */
+#define GF_BALL_ROTATED 0
+#define GF_BALL_AXIS 1
+/* guide source (engine.py:234-242): g = 0, FillParams.g_fixed, or a per-pixel field */
+#define GF_G_ZERO 0
+#define GF_G_FIXED 1
+#define GF_G_FIELD 2
+
+/* largest supported ball radius (disk of r = 12 has K = 440 samples) */
+#define GF_MAX_RADIUS 12
+
+/* per-frame statistics written by gf_fill (int32 each) */
+#define GF_STAT_ITERATIONS 0    /* FillReport.iterations   engine.py:96   */
+#define GF_STAT_FILLED 1        /* FillReport.filled       engine.py:97   */
+#define GF_STAT_DEADLOCK 2      /* FillReport.deadlock_fills engine.py:98 */
+#define GF_STAT_UNFILLABLE 3    /* 1: frontier emptied (or guard found no
+                                   readable neighbour) with Inpaint pixels
+                                   left; the caller runs the nearest-readable
+                                   fallback of engine.py:270-283 */
+#define GF_STAT_REMAINING 4     /* Inpaint pixels left unfilled */
+#define GF_STAT_INPAINT 5       /* |D| of the frame */
+#define GF_STAT_ROWS_OVERFLOW 6 /* 1 if iterations > rows_cap */
+#define GF_STAT_LAST_FRONTIER 7 /* frontier size of the shell that ended the
+                                   loop unfilled (0 when the fill completed) */
+#define GF_STATS 8
+
+/* FillParams (engine.py:33-60), minus the coherence-transport knobs */
+typedef struct gf_fill_params {
+  int32_t r;            /* ball radius epsilon in pixels, 1..GF_MAX_RADIUS */
+  double mu;            /* guidance strength, >= 0, +inf allowed           */
+  double c;             /* smart-order confidence threshold                */
+  double c2;            /* data-term threshold                             */
+  int32_t order;        /* GF_ORDER_*                                      */
+  int32_t neighborhood; /* GF_BALL_*                                       */
+  int32_t g_mode;       /* GF_G_*                                          */
+  double g_fixed[2];    /* used when g_mode == GF_G_FIXED                  */
+  int32_t periodic_x;   /* wrap the x axis                                 */
+  int32_t tracked;      /* 1: frontier tracking (tracker.py:143-172),
+                           0: full-lattice rescan every shell (engine.py:357-360) */
+} gf_fill_params;
+
+/* A batch of equally sized frames, each filled independently (video). */
+typedef struct gf_frames {
+  int32_t n_frames;
+  int32_t height;
+  int32_t width;
+  int32_t channels;      /* 1..4 */
+  int32_t dtype;         /* GF_F32 or GF_F64, for both image and out   */
+  const void* image;     /* [n_frames][H][W][C], values in [0, 1]        */
+  const uint8_t* labels; /* [n_frames][H][W], 0 / 128 / 255              */
+  const double* guide;   /* [n_frames][H][W][2] if g_mode == GF_G_FIELD  */
+  void* out;             /* [n_frames][H][W][C]                          */
+} gf_frames;
+
+typedef struct gf_fill_outputs {
+  int32_t* frame_stats; /* device [n_frames][GF_STATS]                        */
+  int32_t* rows;        /* device [n_frames][rows_cap][2]: (frontier_size, filled)
+                           per shell -- FillReport.rows columns 1 and 4        */
+  int32_t rows_cap;
+  int32_t* enter;       /* optional device [n_frames][H][W]: shell at which the
+                           pixel joined the frontier, -1 never (order log)     */
+  int32_t* fillshell;   /* optional device [n_frames][H][W]: shell in which the
+                           pixel was filled, -1 never                           */
+} gf_fill_outputs;
+
+/* Bytes of device workspace gf_fill needs for this batch. */
+size_t gf_fill_workspace_bytes(const gf_frames* frames, const gf_fill_params* params);
+
+/*
+ * Fill every Inpaint pixel of every frame: Algorithm 1 with Eq. 3.2 weights,
+ * ghost-pixel rotated balls, onion/smart/data-term order, deadlock guard and
+ * the final value-hull clip.  Replaces engine._fill_loop (engine.py:286-376)
+ * and its tracker hook (tracker.py:161-170) -- the seam both
+ * engine.inpaint (engine.py:379-408) and tracker.run_tracked
+ * (tracker.py:143-172) call.  Outputs match the reference bit for bit on the
+ * fill order and within 1e-4 on values (fp32 colour path, fp64 decisions).
+ */
+int gf_fill(const gf_frames* frames, const gf_fill_params* params,
+            const gf_fill_outputs* outputs, void* workspace, size_t workspace_bytes,
+            void* stream);
+
+/*
+ * Guide-field rasteriser: g(x) = dir_s * exp(-d^2 / (2 eta^2)) for the
+ * nearest spline s (first on ties), 0 beyond 3 eta and outside the Inpaint
+ * set.  Replaces guide.build_guide_field + _segment_min_distance
+ * (guide.py:286-327).  Splines arrive already flattened to polylines
+ * (Spline.polyline, splines.py:42-73, stays on the host):
+ *   seg[n_seg][4] = (ax, ay, bx, by) in polyline order,
+ *   seg_spline[n_seg] = owning spline index (non-decreasing),
+ *   dirs[n_splines][2] = spline directions.
+ * out_field: device [H][W][2] float64, fully written.
+ */
+int gf_guide_field(int32_t height, int32_t width, const uint8_t* labels,
+                   int32_t n_seg, const double* seg, const int32_t* seg_spline,
+                   int32_t n_splines, const double* dirs, double eta,
+                   double* out_field, void* stream);
+
+/*
+ * Ball sampler at arbitrary points: readable weight mass, total weight mass
+ * and weighted average colour.  Replaces engine._BallSampler.gather
+ * (engine.py:175-199) as used by engine.confidence / engine.fill_color
+ * (engine.py:202-221).  image: device float64 [H][W][C]; points: device
+ * [n][2] (x, y); g: device [n][2].  Outputs: rw[n], tw[n], vals[n][C].
+ */
+int gf_sample_points(int32_t height, int32_t width, int32_t channels,
+                     const double* image, const uint8_t* labels,
+                     int32_t n, const double* points, const double* g,
+                     const gf_fill_params* params,
+                     double* rw, double* tw, double* vals, void* stream);
+
+/*
+ * Strict bilinear ghost sampling at points (grid.bilinear_gather,
+ * grid.py:158-211).  Outputs vals[n][C] (zero where not readable), ok[n].
+ */
+int gf_bilinear_gather(int32_t height, int32_t width, int32_t channels,
+                       const double* image, const uint8_t* labels,
+                       int32_t n, const double* X, const double* Y, int32_t periodic_x,
+                       double* vals, uint8_t* ok, void* stream);
+
+/*
+ * Boundary masks of a label lattice (grid.py:84-106): active (Inpaint with
+ * a Readable 8-neighbour), inner (Inpaint with a non-Inpaint 8-neighbour),
+ * outer (non-Inpaint with an Inpaint 8-neighbour).  Any output may be NULL.
+ */
+int gf_boundary_masks(int32_t height, int32_t width, const uint8_t* labels,
+                      int32_t periodic_x, uint8_t* active, uint8_t* inner,
+                      uint8_t* outer, void* stream);
+
+/* Thread-local message for the last failing call on this thread. */
+const char* gf_last_error(void);
+int gf_abi_version(void);
+
+/* Host-side builds of the exact-math primitives the kernels use (same
+ * source, gf_math.cuh), exported so CPU tests can pin them to numpy. */
+void gf_host_exp(const double* x, double* y, int64_t n);
+void gf_host_hypot(const double* x, const double* y, double* out, int64_t n);
+double gf_host_pairwise_sum(const double* a, int32_t n);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GUIDEFILL_B200_H */

@@ -1,0 +1,178 @@
+"""Device-level entry points: torch CUDA tensors in, torch CUDA tensors out.
+
+These are thin wrappers around the C ABI (``_native``).  PyTorch provides
+the device memory, the caching allocator and the current stream; all
+compute happens in the sm_100a kernels of libgf_b200.so.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+
+import numpy as np
+
+from . import _native as N
+
+
+def params_to_c(params, tracked: bool, g_mode: int) -> N.FillParamsC:
+    pc = N.FillParamsC()
+    pc.r = int(params.r)
+    pc.mu = float(params.mu)
+    pc.c = float(params.c)
+    pc.c2 = float(params.c2)
+    pc.order = N.GF_ORDER[params.order]
+    pc.neighborhood = N.GF_BALL[params.neighborhood]
+    pc.g_mode = g_mode
+    gf = params.g_fixed or (0.0, 0.0)
+    pc.g_fixed[0] = float(gf[0])
+    pc.g_fixed[1] = float(gf[1])
+    pc.periodic_x = 1 if params.periodic_x else 0
+    pc.tracked = 1 if tracked else 0
+    return pc
+
+
+def resolve_g_mode(params, guide_present: bool) -> int:
+    """engine._resolve_g (engine.py:234-249) as a kernel mode."""
+    if params.g_source == "fixed":
+        return N.GF_G_FIXED
+    if params.g_source == "guide_field":
+        return N.GF_G_FIELD if guide_present else N.GF_G_ZERO
+    raise NotImplementedError(
+        "g_source='modified_structure_tensor' (coherence transport) is not part of the "
+        "B200 fill path yet (SURVEY.md section 8f-2)")
+
+
+def fill_device(image, labels, guide, params, tracked=True, order_log=False, rows_cap=None,
+                workspace=None):
+    """Fill a batch of frames on the GPU.
+
+    image: (N, H, W, C) float32/float64 CUDA tensor; labels: (N, H, W) uint8;
+    guide: (N, H, W, 2) float64 or None.  Returns a dict of CUDA tensors:
+    ``out`` (like image), ``stats`` (N, GF_STATS) int32, ``rows``
+    (N, rows_cap, 2) int32 and, with order_log, ``enter``/``fillshell``
+    (N, H, W) int32.
+    """
+    import torch
+
+    N.require_cuda()
+    lib = N.load()
+    assert image.is_cuda and image.is_contiguous() and image.dim() == 4
+    nF, H, W, C = image.shape
+    g_mode = resolve_g_mode(params, guide is not None)
+    if g_mode != N.GF_G_FIELD:
+        guide = None
+    dev = image.device
+    dtype = N.GF_F64 if image.dtype == torch.float64 else N.GF_F32
+    out = torch.empty_like(image)
+    stats = torch.zeros((nF, N.GF_STATS), dtype=torch.int32, device=dev)
+    if rows_cap is None:
+        rows_cap = min(H * W + 1, max(1024, (1 << 24) // max(1, nF)))
+    rows = torch.empty((nF, rows_cap, 2), dtype=torch.int32, device=dev)
+    enter = fillshell = None
+    if order_log:
+        enter = torch.empty((nF, H, W), dtype=torch.int32, device=dev)
+        fillshell = torch.empty((nF, H, W), dtype=torch.int32, device=dev)
+    fr = N.FramesC(nF, H, W, C, dtype, image.data_ptr(), labels.data_ptr(),
+                   0 if guide is None else guide.data_ptr(), out.data_ptr())
+    pc = params_to_c(params, tracked, g_mode)
+    oc = N.FillOutputsC(stats.data_ptr(), rows.data_ptr(), rows_cap,
+                        0 if enter is None else enter.data_ptr(),
+                        0 if fillshell is None else fillshell.data_ptr())
+    need = lib.gf_fill_workspace_bytes(ctypes.byref(fr), ctypes.byref(pc))
+    if workspace is None or workspace.numel() < need:
+        workspace = torch.empty(need, dtype=torch.uint8, device=dev)
+    N.check(lib.gf_fill(ctypes.byref(fr), ctypes.byref(pc), ctypes.byref(oc),
+                        ctypes.c_void_p(workspace.data_ptr()), need, N.stream_ptr()))
+    return dict(out=out, stats=stats, rows=rows, enter=enter, fillshell=fillshell,
+                workspace=workspace, rows_cap=rows_cap)
+
+
+def splines_to_segments(splines):
+    """Host-side polyline flattening (splines.py:42-73) -> segment arrays."""
+    segs, owner, dirs = [], [], []
+    for s_idx, sp in enumerate(splines):
+        poly = np.asarray(sp.polyline(), dtype=np.float64)
+        for k in range(len(poly) - 1):
+            segs.append((poly[k, 0], poly[k, 1], poly[k + 1, 0], poly[k + 1, 1]))
+            owner.append(s_idx)
+        dirs.append((float(sp.direction[0]), float(sp.direction[1])))
+    seg = np.asarray(segs, dtype=np.float64).reshape(-1, 4)
+    own = np.asarray(owner, dtype=np.int32)
+    dv = np.asarray(dirs, dtype=np.float64).reshape(-1, 2)
+    return seg, own, dv
+
+
+class SegmentSet:
+    """Flattened splines resident on the device (reused across frames)."""
+
+    def __init__(self, splines, device):
+        import torch
+
+        seg, own, dv = splines_to_segments(list(splines))
+        self.n_splines = len(dv)
+        self.n_seg = len(seg)
+        self.seg = torch.from_numpy(seg).to(device)
+        self.owner = torch.from_numpy(own).to(device)
+        self.dirs = torch.from_numpy(dv).to(device)
+
+
+def guide_field_device(labels, segset: SegmentSet, eta: float = 3.0, out=None):
+    """(H, W) uint8 CUDA labels -> (H, W, 2) float64 CUDA guide field."""
+    import torch
+
+    N.require_cuda()
+    lib = N.load()
+    H, W = labels.shape[-2:]
+    if out is None:
+        out = torch.empty((H, W, 2), dtype=torch.float64, device=labels.device)
+    N.check(lib.gf_guide_field(H, W, N.ptr(labels), segset.n_seg, N.ptr(segset.seg),
+                               N.ptr(segset.owner), segset.n_splines, N.ptr(segset.dirs),
+                               float(eta), N.ptr(out), N.stream_ptr()))
+    return out
+
+
+def sample_points_device(image, labels, points, g, params):
+    """Ball sampler at points: (rw, tw, vals) CUDA tensors."""
+    import torch
+
+    N.require_cuda()
+    lib = N.load()
+    H, W, C = image.shape
+    n = points.shape[0]
+    rw = torch.empty(n, dtype=torch.float64, device=image.device)
+    tw = torch.empty(n, dtype=torch.float64, device=image.device)
+    vals = torch.empty((n, C), dtype=torch.float64, device=image.device)
+    pc = params_to_c(params, True, N.GF_G_FIELD)
+    N.check(lib.gf_sample_points(H, W, C, N.ptr(image), N.ptr(labels), n, N.ptr(points), N.ptr(g),
+                                 ctypes.byref(pc), N.ptr(rw), N.ptr(tw), N.ptr(vals),
+                                 N.stream_ptr()))
+    return rw, tw, vals
+
+
+def bilinear_device(image, labels, X, Y, periodic_x):
+    import torch
+
+    N.require_cuda()
+    lib = N.load()
+    H, W, C = image.shape
+    n = X.numel()
+    vals = torch.empty((n, C), dtype=torch.float64, device=image.device)
+    ok = torch.empty(n, dtype=torch.uint8, device=image.device)
+    N.check(lib.gf_bilinear_gather(H, W, C, N.ptr(image), N.ptr(labels), n, N.ptr(X), N.ptr(Y),
+                                   1 if periodic_x else 0, N.ptr(vals), N.ptr(ok), N.stream_ptr()))
+    return vals, ok
+
+
+def boundary_device(labels, periodic_x):
+    import torch
+
+    N.require_cuda()
+    lib = N.load()
+    H, W = labels.shape
+    act = torch.empty((H, W), dtype=torch.uint8, device=labels.device)
+    inn = torch.empty_like(act)
+    out = torch.empty_like(act)
+    N.check(lib.gf_boundary_masks(H, W, N.ptr(labels), 1 if periodic_x else 0, N.ptr(act),
+                                  N.ptr(inn), N.ptr(out), N.stream_ptr()))
+    return act, inn, out

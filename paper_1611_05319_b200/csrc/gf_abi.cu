@@ -1,0 +1,189 @@
+// extern "C" boundary of libgf_b200.so (declared in include/guidefill_b200.h).
+//
+// Validates arguments (mirroring the reference's ValueError checks,
+// engine.py:50-60), derives the ball constants on the host -- disk offsets in
+// the reference's scan order (grid.py:109-124), the g = 0 weights
+// 1/hypot(n, m) and the numpy pairwise-summation plan for K samples -- and
+// dispatches to the kernels.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "gf_internal.cuh"
+
+namespace gf {
+
+static thread_local std::string g_last_error;
+
+int set_error(int code, const char* msg) {
+  g_last_error = msg ? msg : "";
+  return code;
+}
+
+// Disk offsets (n, m), n^2 + m^2 <= r^2, meshgrid order (m outer, n inner),
+// centre moved to the front and then dropped (engine.py:172).
+static int build_ball(const gf_fill_params* p, BallParams& P, BallTables& T) {
+  if (p->r < 1) return set_error(GF_E_INVALID, "r must be >= 1");
+  if (p->r > GF_MAX_RADIUS) return set_error(GF_E_UNSUPPORTED, "r exceeds GF_MAX_RADIUS");
+  if (!(p->mu >= 0.0)) return set_error(GF_E_INVALID, "mu must be >= 0 (inf allowed)");
+  if (p->order < 0 || p->order > 2) return set_error(GF_E_INVALID, "bad order");
+  if (p->neighborhood < 0 || p->neighborhood > 1) return set_error(GF_E_INVALID, "bad neighborhood");
+  if (p->g_mode < 0 || p->g_mode > 2) return set_error(GF_E_INVALID, "bad g_mode");
+  memset(&P, 0, sizeof(P));
+  memset(&T, 0, sizeof(T));
+  const int r = p->r;
+  int K = 0;
+  for (int m = -r; m <= r; ++m)
+    for (int n = -r; n <= r; ++n) {
+      if (n * n + m * m > r * r) continue;
+      if (n == 0 && m == 0) continue;
+      T.n[K] = (double)n;
+      T.m[K] = (double)m;
+      T.w0[K] = 1.0 / hypot_np((double)n, (double)m);
+      ++K;
+    }
+  P.r = r;
+  P.K = K;
+  P.rotated = p->neighborhood == GF_BALL_ROTATED;
+  P.periodic = p->periodic_x != 0;
+  P.mu_inf = isinf(p->mu) ? 1 : 0;
+  const double mu = p->mu;
+  P.coef = (-(mu * mu)) / (2.0 * (double)(r * r));
+  P.tol_inf = 1e-12 * std::max(1.0, (double)(r * r));
+  P.plan = make_plan(K);
+  if (P.plan.n_leaves > kMaxLeaves) return set_error(GF_E_UNSUPPORTED, "pairwise plan too deep");
+  return GF_OK;
+}
+
+static int check_frames(const gf_frames* f) {
+  if (!f) return set_error(GF_E_INVALID, "frames is NULL");
+  if (f->n_frames < 0 || f->height <= 0 || f->width <= 0)
+    return set_error(GF_E_INVALID, "bad frame geometry");
+  if (f->channels < 1 || f->channels > 4) return set_error(GF_E_INVALID, "channels must be 1..4");
+  if (f->dtype != GF_F32 && f->dtype != GF_F64) return set_error(GF_E_INVALID, "bad dtype");
+  if ((long long)f->height * f->width >= (1LL << 31)) return set_error(GF_E_UNSUPPORTED, "frame too large");
+  return GF_OK;
+}
+
+}  // namespace gf
+
+using namespace gf;
+
+extern "C" {
+
+const char* gf_last_error(void) { return g_last_error.c_str(); }
+
+int gf_abi_version(void) { return GF_ABI_VERSION; }
+
+size_t gf_fill_workspace_bytes(const gf_frames* frames, const gf_fill_params* params) {
+  (void)params;
+  if (check_frames(frames) != GF_OK) return 0;
+  const int nF = std::min(frames->n_frames, kMaxFramesPerLaunch);
+  return fill_workspace_bytes(nF, frames->height, frames->width, frames->channels);
+}
+
+int gf_fill(const gf_frames* frames, const gf_fill_params* params, const gf_fill_outputs* outputs,
+            void* workspace, size_t workspace_bytes, void* stream) {
+  int rc = check_frames(frames);
+  if (rc != GF_OK) return rc;
+  if (!params || !outputs) return set_error(GF_E_INVALID, "NULL params/outputs");
+  if (frames->n_frames == 0) return GF_OK;
+  if (params->g_mode == GF_G_FIELD && !frames->guide)
+    return set_error(GF_E_INVALID, "g_mode field needs a guide pointer");
+  if (!frames->image || !frames->labels || !frames->out || !outputs->frame_stats || !outputs->rows)
+    return set_error(GF_E_INVALID, "NULL device pointer");
+  if (outputs->rows_cap < 1) return set_error(GF_E_INVALID, "rows_cap must be >= 1");
+  BallParams P;
+  BallTables* T = new BallTables;
+  rc = build_ball(params, P, *T);
+  if (rc != GF_OK) {
+    delete T;
+    return rc;
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // batches larger than one launch are split into consecutive launches
+  const int H = frames->height, W = frames->width, C = frames->channels;
+  const size_t HW = (size_t)H * W;
+  const size_t esz = frames->dtype == GF_F64 ? 8 : 4;
+  for (int f0 = 0; f0 < frames->n_frames && rc == GF_OK; f0 += kMaxFramesPerLaunch) {
+    const int nF = std::min(kMaxFramesPerLaunch, frames->n_frames - f0);
+    gf_frames sub = *frames;
+    sub.n_frames = nF;
+    sub.image = static_cast<const char*>(frames->image) + f0 * HW * C * esz;
+    sub.out = static_cast<char*>(frames->out) + f0 * HW * C * esz;
+    sub.labels = frames->labels + f0 * HW;
+    sub.guide = frames->guide ? frames->guide + f0 * HW * 2 : nullptr;
+    gf_fill_outputs o = *outputs;
+    o.frame_stats = outputs->frame_stats + (size_t)f0 * GF_STATS;
+    o.rows = outputs->rows + (size_t)f0 * outputs->rows_cap * 2;
+    o.enter = outputs->enter ? outputs->enter + f0 * HW : nullptr;
+    o.fillshell = outputs->fillshell ? outputs->fillshell + f0 * HW : nullptr;
+    rc = fill_launch(&sub, params, &o, workspace, workspace_bytes, s, P, *T);
+  }
+  delete T;  // passed by value as a kernel parameter: safe to free now
+  return rc;
+}
+
+int gf_guide_field(int32_t height, int32_t width, const uint8_t* labels, int32_t n_seg,
+                   const double* seg, const int32_t* seg_spline, int32_t n_splines,
+                   const double* dirs, double eta, double* out_field, void* stream) {
+  if (height <= 0 || width <= 0) return set_error(GF_E_INVALID, "bad geometry");
+  if (!labels || !out_field) return set_error(GF_E_INVALID, "NULL device pointer");
+  if (n_seg < 0 || n_splines < 0) return set_error(GF_E_INVALID, "negative counts");
+  if (n_seg > 0 && (!seg || !seg_spline || !dirs)) return set_error(GF_E_INVALID, "NULL spline arrays");
+  return guide_launch(height, width, labels, n_seg, seg, seg_spline, n_splines, dirs, eta,
+                      out_field, static_cast<cudaStream_t>(stream));
+}
+
+int gf_sample_points(int32_t height, int32_t width, int32_t channels, const double* image,
+                     const uint8_t* labels, int32_t n, const double* points, const double* g,
+                     const gf_fill_params* params, double* rw, double* tw, double* vals,
+                     void* stream) {
+  if (height <= 0 || width <= 0 || channels < 1 || channels > 4)
+    return set_error(GF_E_INVALID, "bad geometry");
+  BallParams P;
+  BallTables* T = new BallTables;
+  int rc = build_ball(params, P, *T);
+  if (rc == GF_OK)
+    rc = sample_points_launch(height, width, channels, image, labels, n, points, g, P, *T, rw, tw,
+                              vals, static_cast<cudaStream_t>(stream));
+  delete T;
+  return rc;
+}
+
+int gf_bilinear_gather(int32_t height, int32_t width, int32_t channels, const double* image,
+                       const uint8_t* labels, int32_t n, const double* X, const double* Y,
+                       int32_t periodic_x, double* vals, uint8_t* ok, void* stream) {
+  if (height <= 0 || width <= 0 || channels < 1 || channels > 4)
+    return set_error(GF_E_INVALID, "bad geometry");
+  return bilinear_launch(height, width, channels, image, labels, n, X, Y, periodic_x, vals, ok,
+                         static_cast<cudaStream_t>(stream));
+}
+
+int gf_boundary_masks(int32_t height, int32_t width, const uint8_t* labels, int32_t periodic_x,
+                      uint8_t* active, uint8_t* inner, uint8_t* outer, void* stream) {
+  if (height <= 0 || width <= 0) return set_error(GF_E_INVALID, "bad geometry");
+  return boundary_launch(height, width, labels, periodic_x, active, inner, outer,
+                         static_cast<cudaStream_t>(stream));
+}
+
+void gf_host_exp(const double* x, double* y, int64_t n) {
+  for (int64_t i = 0; i < n; ++i) y[i] = exp_np(x[i]);
+}
+
+void gf_host_hypot(const double* x, const double* y, double* out, int64_t n) {
+  for (int64_t i = 0; i < n; ++i) out[i] = hypot_np(x[i], y[i]);
+}
+
+double gf_host_pairwise_sum(const double* a, int32_t n) {
+  const PairwisePlan p = make_plan(n);
+  return plan_sum(p, a);
+}
+
+}  // extern "C"

@@ -1,0 +1,84 @@
+// Internal declarations shared by the CUDA translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string.h>
+#include <algorithm>
+
+#include "../../include/guidefill_b200.h"
+#include "gf_sampler.cuh"
+
+namespace gf {
+
+constexpr int kMaxFramesPerLaunch = 1024;
+constexpr int kIntsPerFrame = 16;  // cnt[2] fills[2] anyg[2] + 10 scalars
+
+// Everything the fill kernels need, passed by value (__grid_constant__).
+struct FillArgs {
+  int nF, H, W, HW, C, cap;
+  int dtype;
+  const void* image;
+  const uint8_t* labels;
+  const double* guide;
+  void* out;
+  float4* work;
+  float* c3;
+  uint32_t* list0;
+  uint32_t* list1;
+  double* conf;
+  int* cnt;        // [2][nF] frontier sizes (ping-pong)
+  int* fills;      // [2][nF] pixels filled in the shell
+  int* anyg;       // [2][nF] frontier holds a g != 0 pixel (data-term latch)
+  int* remaining;  // [nF]
+  int* iters;      // [nF]
+  int* done;       // [nF] 0 running, 1 complete, 2 unfillable
+  int* deadlocks;  // [nF]
+  int* filled;     // [nF]
+  int* dt_live;    // [nF]
+  int* best_p;     // [nF]
+  int* inpaint;    // [nF]
+  int* overflow;   // [nF]
+  int* last_f;     // [nF] frontier size of a shell that ended unfilled
+  unsigned long long* best_key;  // [nF]
+  unsigned long long* hull;      // [nF][2] order-preserving encoded min/max
+  int* stats;
+  int* rows;
+  int rows_cap;
+  int* enter;
+  int* fillshell;
+  int order;
+  double c, c2;
+  int g_mode;
+  double gfx, gfy;
+  int periodic;
+};
+
+// thread-local error reporting (gf_abi.cu)
+int set_error(int code, const char* msg);
+
+// gf_fill.cu
+size_t fill_workspace_bytes(int nF, int H, int W, int C);
+int fill_launch(const gf_frames* fr, const gf_fill_params* prm, const gf_fill_outputs* out,
+                void* ws, size_t ws_bytes, cudaStream_t stream, const BallParams& P,
+                const BallTables& host_tab);
+void init_frames(const FillArgs& A, const gf_fill_params* prm, cudaStream_t stream);
+void copy_inpaint_counts(const FillArgs& A, cudaStream_t stream);
+
+// gf_points.cu
+int sample_points_launch(int H, int W, int C, const double* image, const uint8_t* labels, int n,
+                         const double* points, const double* g, const BallParams& P,
+                         const BallTables& tab, double* rw, double* tw, double* vals,
+                         cudaStream_t stream);
+int bilinear_launch(int H, int W, int C, const double* image, const uint8_t* labels, int n,
+                    const double* X, const double* Y, int periodic, double* vals, uint8_t* ok,
+                    cudaStream_t stream);
+int boundary_launch(int H, int W, const uint8_t* labels, int periodic, uint8_t* active,
+                    uint8_t* inner, uint8_t* outer, cudaStream_t stream);
+
+// gf_guide.cu
+int guide_launch(int H, int W, const uint8_t* labels, int n_seg, const double* seg,
+                 const int32_t* seg_spline, int n_splines, const double* dirs, double eta,
+                 double* out, cudaStream_t stream);
+
+}  // namespace gf

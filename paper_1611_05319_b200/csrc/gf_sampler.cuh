@@ -1,0 +1,324 @@
+// Ball sampler shared by the fill engine and the point-evaluation kernels.
+//
+// One item (frontier pixel) is evaluated by a group of 8 lanes.  Lane l owns
+// ball samples k = l, l+8, l+16, ... which is exactly numpy's pairwise-sum
+// accumulator assignment (element k -> accumulator k % 8), so the readable
+// and total weight masses come out bit-identical to
+// engine._BallSampler.gather (engine.py:175-199).  Geometry, weights and
+// masses are fp64 without contraction; colours are accumulated in fp64 from
+// the stored fp32 values.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <math.h>
+
+#include "gf_math.cuh"
+
+namespace gf {
+
+constexpr int kMaxK = 440;  // disk of radius 12, centre excluded
+constexpr int kGroup = 8;   // lanes per item
+
+// stamp encoding (int32, one per pixel): readable at shell k <=> stamp <= k
+constexpr int kStampReadable = 0;
+constexpr int kStampInactive = 0x7ffffffd;  // Inpaint, not in the frontier
+constexpr int kStampActive = 0x7ffffffe;    // Inpaint, in the frontier
+constexpr int kStampBystander = 0x7fffffff;
+
+struct BallParams {
+  int r, K;
+  int rotated;   // rotated_ball (engine.py:150-164) vs axis_ball
+  int periodic;  // periodic_x
+  int mu_inf;
+  double coef;     // -(mu*mu) / (2.0*float(r*r))      engine.py:147
+  double tol_inf;  // 1e-12 * max(1.0, float(r*r))    engine.py:143
+  PairwisePlan plan;
+};
+
+// Ball tables (offsets and the g = 0 weights 1/hypot(n, m) computed by the
+// host with numpy), staged in shared memory by the kernels.
+struct BallTables {
+  double n[kMaxK];
+  double m[kMaxK];
+  double w0[kMaxK];
+};
+
+struct SampleResult {
+  double rw, tw;  // readable / total weight mass (exact numpy bits)
+  double v[4];    // weighted average colour, 0 where rw == 0
+};
+
+// --------------------------------------------------------------- sources
+
+// Working frame of the fill engine: float4 (c0, c1, c2, stamp bits) per
+// pixel plus an optional 4th channel plane.
+struct WorkSource {
+  const float4* work;  // frame base
+  const float* c3;     // frame base or nullptr
+  int H, W, C;
+  int shell;
+  __device__ __forceinline__ bool load(int q, double* v) const {
+    const float4 px = work[q];
+    if (__float_as_int(px.w) > shell) return false;
+    v[0] = px.x;
+    v[1] = px.y;
+    v[2] = px.z;
+    v[3] = c3 ? (double)c3[q] : 0.0;
+    return true;
+  }
+};
+
+// Raw float64 image + label lattice (point-evaluation API).
+struct RawSource {
+  const double* img;
+  const uint8_t* lab;
+  int H, W, C;
+  __device__ __forceinline__ bool load(int q, double* v) const {
+    if (lab[q] != 0) return false;
+    const double* p = img + (size_t)q * C;
+    for (int c = 0; c < 4; ++c) v[c] = c < C ? p[c] : 0.0;
+    return true;
+  }
+};
+
+__device__ __forceinline__ int pos_mod(long long a, int W) {
+  long long r = a % W;
+  return (int)(r < 0 ? r + W : r);
+}
+
+// Strict bilinear ghost sample at (X, Y), grid.py:186-210.  Returns ok; adds
+// the interpolated colour into sv[] (only meaningful when ok).
+template <class Src>
+__device__ __forceinline__ bool ghost_sample(const Src& src, double X, double Y, int periodic,
+                                             double* sv) {
+  const double fx0 = floor(X), fy0 = floor(Y);
+  const double tx = X - fx0, ty = Y - fy0;
+  const long long x0 = (long long)fx0, y0 = (long long)fy0;
+  const double wxs[2] = {1.0 - tx, tx};
+  const double wys[2] = {1.0 - ty, ty};
+  bool ok = true;
+#pragma unroll
+  for (int a = 0; a < 2; ++a) {
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      const double wc = wxs[a] * wys[b];
+      if (wc == 0.0 || !ok) continue;
+      const long long cx = x0 + a, cy = y0 + b;
+      int col;
+      bool inside;
+      if (periodic) {
+        inside = (cy >= 0) && (cy < src.H);
+        col = pos_mod(cx, src.W);
+      } else {
+        inside = (cx >= 0) && (cx < src.W) && (cy >= 0) && (cy < src.H);
+        col = (int)cx;
+      }
+      if (!inside) {
+        ok = false;
+        continue;
+      }
+      double v[4];
+      if (!src.load((int)cy * src.W + col, v)) {
+        ok = false;
+        continue;
+      }
+#pragma unroll
+      for (int c = 0; c < 4; ++c) sv[c] += wc * v[c];
+    }
+  }
+  return ok;
+}
+
+// Lattice sample (g = 0): the only live corner is (x, y) itself.
+template <class Src>
+__device__ __forceinline__ bool lattice_sample(const Src& src, int x, int y, int periodic,
+                                               double* sv) {
+  if (y < 0 || y >= src.H) return false;
+  if (periodic) {
+    x = pos_mod(x, src.W);
+  } else if (x < 0 || x >= src.W) {
+    return false;
+  }
+  double v[4];
+  if (!src.load(y * src.W + x, v)) return false;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) sv[c] += v[c];
+  return true;
+}
+
+__device__ __forceinline__ double group_sum_tree(double v) {
+  // ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) lands in lane 0 of the group
+  v = v + __shfl_xor_sync(0xffffffffu, v, 1, kGroup);
+  v = v + __shfl_xor_sync(0xffffffffu, v, 2, kGroup);
+  v = v + __shfl_xor_sync(0xffffffffu, v, 4, kGroup);
+  return v;
+}
+
+__device__ __forceinline__ double min_prop(double a, double b) {
+  return (a != a || b != b) ? (a + b) : fmin(a, b);
+}
+
+// Evaluate one item.  Must be called by all 32 lanes of the warp
+// (groups with valid == false compute on dummy data and never write).
+// NL = number of pairwise leaves the kernel was specialised for: 1 covers
+// K <= 128 (r <= 6); kMaxLeaves covers every supported radius.
+// The result is valid in every lane of the group.
+template <int NL, class Src>
+__device__ __forceinline__ void eval_item(const BallParams& P, const BallTables& T,
+                                          const Src& src, int lane, bool valid, double fi,
+                                          double fj, bool integral, double gx, double gy,
+                                          SampleResult& out) {
+  const int K = P.K;
+  const bool gzero = (gx == 0.0) && (gy == 0.0);
+  double ux = 0.0, uy = 1.0;
+  if (P.rotated && !gzero) {
+    const double nr = hypot_np(gx, gy);
+    ux = gx / nr;
+    uy = gy / nr;
+  }
+  double safe = 1.0, thr = 0.0;
+  if (P.mu_inf) {
+    const double nr2 = sqrt(gx * gx + gy * gy);
+    safe = (nr2 == 0.0) ? 1.0 : nr2;
+    double mloc = INFINITY;
+    for (int k = lane; k < K; k += kGroup) {
+      double px = T.n[k], py = T.m[k];
+      if (P.rotated && !gzero) {
+        px = T.n[k] * uy + T.m[k] * ux;
+        py = (-T.n[k]) * ux + T.m[k] * uy;
+      }
+      const double d = ((-gy) * px + gx * py) / safe;
+      mloc = min_prop(mloc, d * d);
+    }
+    mloc = min_prop(mloc, __shfl_xor_sync(0xffffffffu, mloc, 1, kGroup));
+    mloc = min_prop(mloc, __shfl_xor_sync(0xffffffffu, mloc, 2, kGroup));
+    mloc = min_prop(mloc, __shfl_xor_sync(0xffffffffu, mloc, 4, kGroup));
+    thr = mloc + P.tol_inf;
+  }
+
+  double acc_rw[NL], acc_tw[NL], tl_rw[NL], tl_tw[NL];
+#pragma unroll
+  for (int L = 0; L < NL; ++L) acc_rw[L] = acc_tw[L] = tl_rw[L] = tl_tw[L] = 0.0;
+  double num[4] = {0.0, 0.0, 0.0, 0.0};
+
+  const int pi = (int)fi, pj = (int)fj;
+#pragma unroll 1
+  for (int k = lane; k < K; k += kGroup) {
+    double w;
+    double sv[4] = {0.0, 0.0, 0.0, 0.0};
+    bool ok;
+    if (gzero) {
+      w = T.w0[k];
+      ok = integral ? lattice_sample(src, pi + (int)T.n[k], pj + (int)T.m[k], P.periodic, sv)
+                    : ghost_sample(src, fi + T.n[k], fj + T.m[k], P.periodic, sv);
+    } else {
+      double px = T.n[k], py = T.m[k];
+      if (P.rotated) {
+        px = T.n[k] * uy + T.m[k] * ux;
+        py = (-T.n[k]) * ux + T.m[k] * uy;
+      }
+      const double dist = hypot_np(px, py);
+      if (P.mu_inf) {
+        const double d = ((-gy) * px + gx * py) / safe;
+        w = (d * d <= thr) ? 1.0 / dist : 0.0;
+      } else {
+        const double d = (-gy) * px + gx * py;
+        w = exp_np((P.coef * d) * d) / dist;
+      }
+      ok = ghost_sample(src, fi + px, fj + py, P.periodic, sv);
+    }
+    if (!valid) ok = false;
+    const double wr = ok ? w : 0.0;
+    if (ok) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) num[c] += wr * sv[c];
+    }
+#pragma unroll
+    for (int L = 0; L < NL; ++L) {
+      const int lo = P.plan.leaf_lo[L], n = P.plan.leaf_n[L];
+      const int kk = k - lo;
+      if (L < P.plan.n_leaves && kk >= 0 && kk < n) {
+        if (kk < n - (n % 8)) {
+          acc_rw[L] += wr;
+          acc_tw[L] += w;
+        } else {
+          tl_rw[L] = wr;
+          tl_tw[L] = w;
+        }
+      }
+    }
+  }
+
+  // leaf sums: 8-accumulator tree, then the sequential tail (lane 0 exact)
+  double leaf_rw[NL], leaf_tw[NL];
+#pragma unroll
+  for (int L = 0; L < NL; ++L) {
+    double srw = group_sum_tree(acc_rw[L]);
+    double stw = group_sum_tree(acc_tw[L]);
+    const int ntail = (L < P.plan.n_leaves) ? P.plan.leaf_n[L] % 8 : 0;
+    for (int t = 0; t < ntail; ++t) {
+      srw = srw + __shfl_sync(0xffffffffu, tl_rw[L], t, kGroup);
+      stw = stw + __shfl_sync(0xffffffffu, tl_tw[L], t, kGroup);
+    }
+    leaf_rw[L] = srw;
+    leaf_tw[L] = stw;
+  }
+  double rw, tw;
+  if (NL == 1) {
+    rw = leaf_rw[0];
+    tw = leaf_tw[0];
+  } else {
+    double st_rw[NL], st_tw[NL];
+    int sp = 0;
+    for (int i = 0; i < P.plan.n_prog; ++i) {
+      const int op = P.plan.prog[i];
+      if (op >= 0) {
+        double a = 0.0, b = 0.0;
+#pragma unroll
+        for (int L = 0; L < NL; ++L)
+          if (L == op) {
+            a = leaf_rw[L];
+            b = leaf_tw[L];
+          }
+#pragma unroll
+        for (int s = 0; s < NL; ++s)
+          if (s == sp) {
+            st_rw[s] = a;
+            st_tw[s] = b;
+          }
+        ++sp;
+      } else {
+        --sp;
+        double a = 0.0, b = 0.0, c = 0.0, d = 0.0;
+#pragma unroll
+        for (int s = 0; s < NL; ++s) {
+          if (s == sp) { a = st_rw[s]; b = st_tw[s]; }
+          if (s == sp - 1) { c = st_rw[s]; d = st_tw[s]; }
+        }
+#pragma unroll
+        for (int s = 0; s < NL; ++s)
+          if (s == sp - 1) {
+            st_rw[s] = c + a;
+            st_tw[s] = d + b;
+          }
+      }
+    }
+    rw = st_rw[0];
+    tw = st_tw[0];
+  }
+  rw = __shfl_sync(0xffffffffu, rw, 0, kGroup);
+  tw = __shfl_sync(0xffffffffu, tw, 0, kGroup);
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    double s = num[c];
+    s += __shfl_xor_sync(0xffffffffu, s, 1, kGroup);
+    s += __shfl_xor_sync(0xffffffffu, s, 2, kGroup);
+    s += __shfl_xor_sync(0xffffffffu, s, 4, kGroup);
+    out.v[c] = (rw != 0.0) ? s / rw : 0.0;
+  }
+  out.rw = rw;
+  out.tw = tw;
+}
+
+}  // namespace gf

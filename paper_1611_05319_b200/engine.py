@@ -1,0 +1,262 @@
+"""Shell-based Guidefill fill engine -- drop-in for the reference engine.py.
+
+Same public surface as /root/reference/pkg/src/guidefill/engine.py:
+``FillParams`` (engine.py:33-91), ``FillReport`` (:94-115), ``weight``
+(:118-128), ``confidence`` / ``fill_color`` (:202-221), ``ready``
+(:224-231) and ``inpaint`` (:379-408), with the same argument meaning,
+return layout and ValueError messages.  The fill itself runs on the GPU:
+``_run_fill`` hands the frame to the persistent sm_100a shell kernel through
+the C ABI (gf_fill) and only copies the result back.
+
+The one host-side step is the unfillable fallback (engine.py:270-283): when
+the frontier empties while Inpaint pixels remain (a Bystander moat), the
+stranded pixels take the colour of the nearest readable pixel via
+scipy's Euclidean distance transform, exactly as the reference does.
+"""
+
+from __future__ import annotations
+
+import math
+import time
+from dataclasses import asdict, dataclass, field
+
+import numpy as np
+
+from . import _native as N
+from . import grid
+from .grid import INPAINT, READABLE
+
+ORDERS = ("onion", "smart", "smart_with_data_term")
+NEIGHBORHOODS = ("rotated_ball", "axis_ball")
+G_SOURCES = ("guide_field", "modified_structure_tensor", "fixed")
+
+
+@dataclass
+class FillParams:
+    """Knobs of the fill engine; defaults are the guide-field configuration."""
+
+    r: int = 3
+    mu: float = 50.0
+    c: float = 0.05
+    c2: float = 0.0
+    order: str = "smart"
+    neighborhood: str = "rotated_ball"
+    g_source: str = "guide_field"
+    g_fixed: tuple | None = None
+    periodic_x: bool = False
+    sigma: float = 2.0
+    rho: float = 4.0
+    coherence_lambda: float = 1e-5
+
+    def __post_init__(self):
+        if self.r < 1:
+            raise ValueError("r must be >= 1")
+        if self.order not in ORDERS:
+            raise ValueError(f"order must be one of {ORDERS}")
+        if self.neighborhood not in NEIGHBORHOODS:
+            raise ValueError(f"neighborhood must be one of {NEIGHBORHOODS}")
+        if self.g_source not in G_SOURCES:
+            raise ValueError(f"g_source must be one of {G_SOURCES}")
+        if not (self.mu >= 0.0):
+            raise ValueError("mu must be >= 0 (inf allowed)")
+
+    @classmethod
+    def guidefill(cls, **kw) -> "FillParams":
+        return cls(**kw)
+
+    @classmethod
+    def coherence_transport(cls, **kw) -> "FillParams":
+        """Axis-ball transport steered by the boundary-aware structure tensor."""
+        defaults = dict(r=5, neighborhood="axis_ball", order="onion",
+                        g_source="modified_structure_tensor")
+        defaults.update(kw)
+        return cls(**defaults)
+
+    @classmethod
+    def telea(cls, **kw) -> "FillParams":
+        """Isotropic onion baseline: axis ball, g = 0."""
+        defaults = dict(neighborhood="axis_ball", order="onion", g_source="fixed",
+                        g_fixed=(0.0, 0.0))
+        defaults.update(kw)
+        return cls(**defaults)
+
+    def to_dict(self) -> dict:
+        d = asdict(self)
+        if math.isinf(d["mu"]):
+            d["mu"] = "inf"
+        return d
+
+
+@dataclass
+class FillReport:
+    iterations: int = 0
+    filled: int = 0
+    deadlock_fills: int = 0
+    unfillable: bool = False
+    unfillable_count: int = 0
+    wall_time_s: float = 0.0
+    # per-iteration rows: (iteration, frontier_size, candidates, threads_requested, filled)
+    rows: list = field(default_factory=list)
+
+    def to_dict(self) -> dict:
+        return {
+            "iterations": self.iterations,
+            "filled": self.filled,
+            "deadlock_fills": self.deadlock_fills,
+            "unfillable": self.unfillable,
+            "unfillable_count": self.unfillable_count,
+            "wall_time_s": self.wall_time_s,
+            "frontier_sizes": [r[1] for r in self.rows],
+            "filled_per_iteration": [r[4] for r in self.rows],
+        }
+
+
+def weight(x, y, g, mu: float, eps: float) -> float:
+    """Pairwise Eq. 3.2 weight for finite mu (engine.py:118-128); host scalar."""
+    dx = float(y[0]) - float(x[0])
+    dy = float(y[1]) - float(x[1])
+    dist = math.hypot(dx, dy)
+    if dist == 0.0:
+        raise ValueError("weight is undefined at y == x")
+    if math.isinf(mu):
+        raise ValueError("mu = inf weights are defined set-wise, not pairwise")
+    d = -float(g[1]) * dx + float(g[0]) * dy
+    return math.exp(-(mu * mu) / (2.0 * eps * eps) * d * d) / dist
+
+
+def _point_gather(point, image, labels, g, params):
+    import torch
+
+    dev = N.require_cuda()
+    from ._device import sample_points_device
+
+    img = np.ascontiguousarray(image, dtype=np.float64)
+    lab = np.ascontiguousarray(np.where(np.asarray(labels) == READABLE, READABLE, grid.BYSTANDER),
+                               dtype=np.uint8)
+    pts = torch.tensor([[float(point[0]), float(point[1])]], dtype=torch.float64, device=dev)
+    gv = np.asarray(g, dtype=np.float64).reshape(1, 2)
+    rw, tw, vals = sample_points_device(torch.from_numpy(img).to(dev), torch.from_numpy(lab).to(dev),
+                                        pts, torch.from_numpy(gv).to(dev), params)
+    return vals.cpu().numpy(), rw.cpu().numpy(), tw.cpu().numpy()
+
+
+
+def confidence(point, image, labels, g, params: FillParams) -> float:
+    """Readable over total ball weight mass at one pixel (Eq. 3.7, engine.py:202-209)."""
+    _, rw, tw = _point_gather(point, image, labels, g, params)
+    return float(rw[0] / tw[0])
+
+
+def fill_color(point, image, labels, g, params: FillParams):
+    """Weighted average of readable ball samples; (values, True) or (None, False)."""
+    vals, rw, _ = _point_gather(point, image, labels, g, params)
+    if rw[0] == 0.0:
+        return None, False
+    return vals[0], True
+
+
+def ready(conf: float, g, params: FillParams, data_term_live: bool = True) -> bool:
+    """Fill-readiness predicate for one pixel (engine.py:224-231)."""
+    if params.order == "onion":
+        return True
+    if params.order == "smart" or not data_term_live:
+        return conf > params.c
+    gnorm = math.hypot(float(g[0]), float(g[1]))
+    return gnorm > params.c2 and conf > params.c
+
+
+def _paint_unfillable(u, labels, fillshell):
+    """Nearest-readable colour for stranded Inpaint pixels (engine.py:270-283)."""
+    from scipy import ndimage
+
+    lab = np.asarray(labels)
+    stranded = (lab == INPAINT) & (fillshell < 0)
+    count = int(stranded.sum())
+    if count == 0:
+        return 0
+    readable = (lab == READABLE) | ((lab == INPAINT) & (fillshell >= 0))
+    if readable.any():
+        _, (jn, inn) = ndimage.distance_transform_edt(~readable, return_indices=True)
+        jr, ir = np.nonzero(stranded)
+        u[jr, ir] = u[jn[jr, ir], inn[jr, ir]]
+    else:
+        u[stranded] = 0.5
+    return count
+
+
+def _run_fill(image, labels, guide_vecs, params: FillParams, tracked: bool, order_log=False):
+    """Fill one frame on the GPU.  Returns (u float64 (H,W,C), FillReport, maps)."""
+    import torch
+
+    dev = N.require_cuda()
+    from ._device import fill_device
+
+    H, W = labels.shape
+    img = np.ascontiguousarray(image, dtype=np.float64)
+    C = img.shape[2]
+    t0 = time.perf_counter()
+    d_img = torch.from_numpy(img).to(dev, non_blocking=True).reshape(1, H, W, C)
+    d_lab = torch.from_numpy(np.ascontiguousarray(labels, dtype=np.uint8)).to(dev).reshape(1, H, W)
+    d_guide = None
+    if guide_vecs is not None and params.g_source == "guide_field":
+        d_guide = torch.from_numpy(np.ascontiguousarray(guide_vecs, dtype=np.float64)).to(dev)
+        d_guide = d_guide.reshape(1, H, W, 2)
+    res = fill_device(d_img, d_lab, d_guide, params, tracked=tracked, order_log=True,
+                      rows_cap=H * W + 1)
+    stats = res["stats"][0].cpu().numpy()
+    iters = int(stats[N.STAT_ITERATIONS])
+    rows_dev = res["rows"][0, :iters].cpu().numpy()
+    u = res["out"][0].cpu().numpy()
+    fillshell = res["fillshell"][0].cpu().numpy()
+    enter = res["enter"][0].cpu().numpy() if order_log else None
+    rep = FillReport()
+    rep.iterations = iters
+    rep.filled = int(stats[N.STAT_FILLED])
+    rep.deadlock_fills = int(stats[N.STAT_DEADLOCK])
+    rows = []
+    for k in range(iters):
+        F, filled = int(rows_dev[k, 0]), int(rows_dev[k, 1])
+        if tracked:
+            # candidates == next frontier size (the active filter never
+            # removes a candidate)
+            cand = int(rows_dev[k + 1, 0]) if k + 1 < iters else int(stats[N.STAT_LAST_FRONTIER])
+            rows.append((k, F, cand, F, filled))
+        else:
+            rows.append((k, F, W * H, W * H, filled))
+    rep.rows = rows
+    if stats[N.STAT_UNFILLABLE]:
+        rep.unfillable = True
+        rep.unfillable_count = _paint_unfillable(u, labels, fillshell)
+        fillshell = np.where((np.asarray(labels) == INPAINT) & (fillshell < 0), -2, fillshell)
+    rep.wall_time_s = time.perf_counter() - t0
+    return u, rep, dict(enter=enter, fillshell=fillshell)
+
+
+def inpaint(image, labels, guide=None, params: FillParams | None = None):
+    """Fill all Inpaint pixels of ``labels`` in ``image`` (engine.py:379-408).
+
+    Untracked variant: the GPU rescans the whole lattice for the frontier
+    after every shell (threads = W*H), like the reference's plain loop.
+    Returns (filled_image float64 (H, W, C), FillReport).
+    """
+    params = params or FillParams()
+    grid.validate_labels(labels)
+    if image.ndim != 3:
+        raise ValueError("image must be (H, W, C)")
+    if image.shape[:2] != labels.shape:
+        raise ValueError(
+            f"image {image.shape[:2]} and label mask {labels.shape} dimensions differ"
+        )
+    guide_vecs = None
+    if guide is not None:
+        guide_vecs = np.asarray(guide, dtype=np.float64)
+        if guide_vecs.shape != labels.shape + (2,):
+            raise ValueError("guide field shape must be (H, W, 2)")
+    u, report, _ = _run_fill(image, labels, guide_vecs, params, tracked=False)
+    return u, report
+
+
+def coherence_transport_mode(image, labels, **param_overrides):
+    """engine.py:411-414 -- the coherence g source is not on the B200 path yet."""
+    params = FillParams.coherence_transport(**param_overrides)
+    return inpaint(image, labels, None, params)
