@@ -45,57 +45,57 @@ def _peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    """SM clocks and throttle reasons polled through NVML during the timed region."""
 
-    def __init__(self, index=0):
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+               "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
+
+    def __init__(self, index=0, period_s=0.002):
         self.index = index
-        self.proc = None
-        self.lines = []
+        self.period = period_s
+        self.samples = []
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index),
-                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
+            import pynvml
+
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+
+            def poll():
+                while not self._stop.is_set():
+                    try:
+                        mhz = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                        rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        self.samples.append((mhz, rs))
+                    except Exception:
+                        pass
+                    time.sleep(self.period)
+
+            self._t = threading.Thread(target=poll, daemon=True)
+            self._t.start()
         except Exception:
-            self.proc = None
+            self._t = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
-
     def __exit__(self, *exc):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except Exception:
-                self.proc.kill()
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=2)
 
     def summary(self):
-        sm, mx, reasons = [], 0.0, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 6:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx = max(mx, float(parts[1]))
-            except ValueError:
-                continue
-            for n, v in zip(names, parts[2:]):
-                if v.lower() == "active":
-                    reasons.add(n)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        mhz = [m for m, _ in self.samples]
+        reasons = set()
+        for _, rs in self.samples:
+            for name, bit in self.REASONS.items():
+                if rs & bit:
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(mhz) if mhz else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(reasons), "samples": len(mhz)}
 
 
 def dist_env():
@@ -139,10 +139,15 @@ def run_reference(args):
 
     for _ in range(args.warmup):
         step()
+    # bounded sample: at most ~120 s of CPU work whatever --steps is
     t0 = time.perf_counter()
-    for _ in range(args.steps):
+    done = 0
+    while done < args.steps:
         step()
-    dt = (time.perf_counter() - t0) / args.steps
+        done += 1
+        if time.perf_counter() - t0 > 120.0:
+            break
+    dt = (time.perf_counter() - t0) / done
     D = sc.n_inpaint
     value = D / dt / 1e6
     line = {
@@ -155,8 +160,8 @@ def run_reference(args):
                                f"{'untracked' if args.untracked else 'tracked'}",
                    "global_batch": 1},
         "cpu_baseline": {"value": value, "unit": "Mpx/s", "cores": 1, "kind": "port",
-                         "sample": f"guide field + full fill of one {sc.name} frame per step "
-                                   f"(numpy restatement of the reference, single-threaded numpy)"},
+                         "sample": f"{done} steps x (guide field + full fill of one {sc.name} "
+                                   f"frame), numpy restatement of the reference, single-threaded"},
         "e2e": {"value": value, "unit": "Mpx/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -184,7 +189,7 @@ def run_ours(args):
 
     from paper_1611_05319_b200 import Spline, build_guide_field, tracker
     from paper_1611_05319_b200 import _native as N
-    from paper_1611_05319_b200._device import SegmentSet, fill_device, guide_field_device
+    from paper_1611_05319_b200._device import SegmentSet, fill_device
 
     ws, rank, local = dist_env()
     if ws > 1:
@@ -202,15 +207,23 @@ def run_ours(args):
     img = torch.from_numpy(sc.image.astype(np.float32)).to(dev).reshape(1, H, W, 3).contiguous()
     lab = torch.from_numpy(sc.labels).to(dev).reshape(1, H, W).contiguous()
     segs = SegmentSet(splines, dev)
-    field = torch.empty((1, H, W, 2), dtype=torch.float64, device=dev)
-    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    # L2 eviction between steps: write 256 MB, then read another 256 MB so the
+    # write-backs of the flush land outside the timed region
+    flush_w = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    flush_r = torch.ones(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    sink = torch.empty(1, dtype=torch.float32, device=dev)
+
+    def flush_l2():
+        flush_w.zero_()
+        torch.sum(flush_r, dim=0, keepdim=True, out=sink)
     ws_buf = None
 
-    def step():
+    def step(trace_cap=0):
+        # one gf_fill_splines call: the guide field is rastered inside the
+        # fill's first pass (same bits as gf_guide_field + gf_fill)
         nonlocal ws_buf
-        guide_field_device(lab[0], segs, 3.0, out=field[0])
-        res = fill_device(img, lab, field, params, tracked=not args.untracked,
-                          rows_cap=4096, workspace=ws_buf)
+        res = fill_device(img, lab, None, params, tracked=not args.untracked, rows_cap=4096,
+                          workspace=ws_buf, splines=segs, trace_cap=trace_cap)
         ws_buf = res["workspace"]
         return res
 
@@ -221,30 +234,30 @@ def run_ours(args):
     assert int(stats[N.STAT_FILLED]) == D, "fill incomplete"
     n_shells = int(stats[N.STAT_ITERATIONS])
 
+    # per-shell phase trace of one (untimed) step: fill phase, barrier, update
+    res = step(trace_cap=256)
+    torch.cuda.synchronize()
+    tr = res["trace"].cpu().numpy()[:n_shells]
+    shell_trace = [{"items": int(r[5]), "fill_us": (r[1] - r[0]) / 1e3,
+                    "sync_us": (r[2] - r[1]) / 1e3, "update_us": (r[3] - r[2]) / 1e3,
+                    "sync2_us": (r[4] - r[3]) / 1e3} for r in tr]
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    mids = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     if ws > 1:
         dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
         for k in range(args.steps):
-            flush.zero_()  # evict L2 (126 MB) between steps; not timed
+            flush_l2()  # evict L2 (126 MB) between steps; not timed
             starts[k].record()
-            guide_field_device(lab[0], segs, 3.0, out=field[0])
-            mids[k].record()
-            res = fill_device(img, lab, field, params, tracked=not args.untracked,
-                              rows_cap=4096, workspace=ws_buf)
+            res = step()
             ends[k].record()
         torch.cuda.synchronize()
     if ws > 1:
         dist.barrier()
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
-    fill_ms = [m.elapsed_time(e) for m, e in zip(mids, ends)]
-    gf_ms = [s.elapsed_time(m) for s, m in zip(starts, mids)]
     t_step = sum(step_ms) / len(step_ms)
-    t_fill = sum(fill_ms) / len(fill_ms)
-    t_gf = sum(gf_ms) / len(gf_ms)
+    t_fill = t_step
     if ws > 1:
         t = torch.tensor([t_step, float(D)], dtype=torch.float64, device=dev)
         tmax = t[:1].clone()
@@ -308,14 +321,15 @@ def run_ours(args):
             "shells": n_shells,
             "r": sc.params["r"], "mu": sc.params["mu"],
             "ms_per_frame": t_step,
-            "ms_fill": t_fill,
-            "ms_guide_field": t_gf,
-            "l2": "flushed between steps (512 MB write)",
+            "ms_step_min": min(step_ms),
+            "ms_step_max": max(step_ms),
+            "shell_trace": shell_trace,
+            "l2": "flushed between steps (256 MB write + 256 MB read, untimed)",
             "parallelism": f"frame-parallel x{ws}",
         },
         "roofline": {
             "bound": "hbm",
-            "kernel": "gf_fill (prep + hull + persistent shell loop + finalize)",
+            "kernel": "gf_fill_splines (prep+raster, persistent shell loop, finalize)",
             "achieved": achieved,
             "peak": peak,
             "peak_kind": peak_kind,
@@ -325,7 +339,7 @@ def run_ours(args):
             "algorithmic_bytes": b_frame,
         },
         "e2e": e2e,
-        "gpu_launches": 7 * args.steps,
+        "gpu_launches": 3 * args.steps,
         "clocks": clk.summary(),
         "cpu_baseline": cpu,
     }
@@ -337,7 +351,7 @@ def run_ours(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="C2")

@@ -103,10 +103,30 @@ typedef struct gf_fill_outputs {
                            pixel joined the frontier, -1 never (order log)     */
   int32_t* fillshell;   /* optional device [n_frames][H][W]: shell in which the
                            pixel was filled, -1 never                           */
+  uint64_t* shell_trace; /* optional device [trace_cap][6] profiling record per
+                           shell: globaltimer ns at shell start, end of the fill
+                           phase (latest block), after its grid barrier, end of
+                           the frontier update (latest block), after its
+                           barrier, and the number of frontier items          */
+  int32_t trace_cap;
 } gf_fill_outputs;
 
-/* Bytes of device workspace gf_fill needs for this batch. */
+/* Splines flattened to polylines on the host (Spline.polyline,
+ * splines.py:42-73), shared by every frame of a batch.  All device pointers. */
+typedef struct gf_splines {
+  int32_t n_seg;
+  const double* seg;         /* [n_seg][4] = (ax, ay, bx, by), polyline order */
+  const int32_t* seg_spline; /* [n_seg] owning spline index, non-decreasing  */
+  int32_t n_splines;
+  const double* dirs;        /* [n_splines][2] spline directions             */
+  double eta;                /* falloff scale, guide.py:28                   */
+} gf_splines;
+
+/* Bytes of device workspace gf_fill / gf_fill_splines need for this batch
+ * (splines may be NULL). */
 size_t gf_fill_workspace_bytes(const gf_frames* frames, const gf_fill_params* params);
+size_t gf_fill_splines_workspace_bytes(const gf_frames* frames, const gf_fill_params* params,
+                                       const gf_splines* splines);
 
 /*
  * Fill every Inpaint pixel of every frame: Algorithm 1 with Eq. 3.2 weights,
@@ -120,6 +140,17 @@ size_t gf_fill_workspace_bytes(const gf_frames* frames, const gf_fill_params* pa
 int gf_fill(const gf_frames* frames, const gf_fill_params* params,
             const gf_fill_outputs* outputs, void* workspace, size_t workspace_bytes,
             void* stream);
+
+/*
+ * gf_fill with the guide field rastered from splines inside the fill's
+ * first pass -- the CLI / project path build_guide_field + run_tracked
+ * (cli.py:106-112, project.py:193-202) as one call, without materialising
+ * the dense (H, W, 2) field.  g_mode is ignored (the rastered field is the
+ * guide).  Fill results are identical to gf_guide_field followed by gf_fill.
+ */
+int gf_fill_splines(const gf_frames* frames, const gf_fill_params* params,
+                    const gf_splines* splines, const gf_fill_outputs* outputs,
+                    void* workspace, size_t workspace_bytes, void* stream);
 
 /*
  * Guide-field rasteriser: g(x) = dir_s * exp(-d^2 / (2 eta^2)) for the

@@ -44,14 +44,16 @@ def resolve_g_mode(params, guide_present: bool) -> int:
 
 
 def fill_device(image, labels, guide, params, tracked=True, order_log=False, rows_cap=None,
-                workspace=None):
+                workspace=None, splines=None, eta=3.0, trace_cap=0):
     """Fill a batch of frames on the GPU.
 
     image: (N, H, W, C) float32/float64 CUDA tensor; labels: (N, H, W) uint8;
-    guide: (N, H, W, 2) float64 or None.  Returns a dict of CUDA tensors:
-    ``out`` (like image), ``stats`` (N, GF_STATS) int32, ``rows``
-    (N, rows_cap, 2) int32 and, with order_log, ``enter``/``fillshell``
-    (N, H, W) int32.
+    guide: (N, H, W, 2) float64 or None; splines: a SegmentSet to raster the
+    guide field inside the fill (gf_fill_splines) instead of ``guide``.
+    Returns a dict of CUDA tensors: ``out`` (like image), ``stats``
+    (N, GF_STATS) int32, ``rows`` (N, rows_cap, 2) int32, with order_log
+    ``enter``/``fillshell`` (N, H, W) int32, with trace_cap > 0 ``trace``
+    (trace_cap, 6) int64 per-shell phase timestamps.
     """
     import torch
 
@@ -59,8 +61,9 @@ def fill_device(image, labels, guide, params, tracked=True, order_log=False, row
     lib = N.load()
     assert image.is_cuda and image.is_contiguous() and image.dim() == 4
     nF, H, W, C = image.shape
-    g_mode = resolve_g_mode(params, guide is not None)
-    if g_mode != N.GF_G_FIELD:
+    raster = splines is not None and splines.n_seg > 0
+    g_mode = N.GF_G_FIELD if raster else resolve_g_mode(params, guide is not None)
+    if g_mode != N.GF_G_FIELD or raster:
         guide = None
     dev = image.device
     dtype = N.GF_F64 if image.dtype == torch.float64 else N.GF_F32
@@ -76,16 +79,30 @@ def fill_device(image, labels, guide, params, tracked=True, order_log=False, row
     fr = N.FramesC(nF, H, W, C, dtype, image.data_ptr(), labels.data_ptr(),
                    0 if guide is None else guide.data_ptr(), out.data_ptr())
     pc = params_to_c(params, tracked, g_mode)
+    trace = None
+    if trace_cap:
+        trace = torch.zeros((trace_cap, 6), dtype=torch.int64, device=dev)
     oc = N.FillOutputsC(stats.data_ptr(), rows.data_ptr(), rows_cap,
                         0 if enter is None else enter.data_ptr(),
-                        0 if fillshell is None else fillshell.data_ptr())
-    need = lib.gf_fill_workspace_bytes(ctypes.byref(fr), ctypes.byref(pc))
+                        0 if fillshell is None else fillshell.data_ptr(),
+                        0 if trace is None else trace.data_ptr(), int(trace_cap))
+    if raster:
+        sc = splines.as_c(eta)
+        need = lib.gf_fill_splines_workspace_bytes(ctypes.byref(fr), ctypes.byref(pc),
+                                                   ctypes.byref(sc))
+    else:
+        need = lib.gf_fill_workspace_bytes(ctypes.byref(fr), ctypes.byref(pc))
     if workspace is None or workspace.numel() < need:
         workspace = torch.empty(need, dtype=torch.uint8, device=dev)
-    N.check(lib.gf_fill(ctypes.byref(fr), ctypes.byref(pc), ctypes.byref(oc),
-                        ctypes.c_void_p(workspace.data_ptr()), need, N.stream_ptr()))
+    if raster:
+        N.check(lib.gf_fill_splines(ctypes.byref(fr), ctypes.byref(pc), ctypes.byref(sc),
+                                    ctypes.byref(oc), ctypes.c_void_p(workspace.data_ptr()), need,
+                                    N.stream_ptr()))
+    else:
+        N.check(lib.gf_fill(ctypes.byref(fr), ctypes.byref(pc), ctypes.byref(oc),
+                            ctypes.c_void_p(workspace.data_ptr()), need, N.stream_ptr()))
     return dict(out=out, stats=stats, rows=rows, enter=enter, fillshell=fillshell,
-                workspace=workspace, rows_cap=rows_cap)
+                workspace=workspace, rows_cap=rows_cap, trace=trace)
 
 
 def splines_to_segments(splines):
@@ -115,6 +132,10 @@ class SegmentSet:
         self.seg = torch.from_numpy(seg).to(device)
         self.owner = torch.from_numpy(own).to(device)
         self.dirs = torch.from_numpy(dv).to(device)
+
+    def as_c(self, eta=3.0):
+        return N.SplinesC(self.n_seg, self.seg.data_ptr(), self.owner.data_ptr(), self.n_splines,
+                          self.dirs.data_ptr(), float(eta))
 
 
 def guide_field_device(labels, segset: SegmentSet, eta: float = 3.0, out=None):

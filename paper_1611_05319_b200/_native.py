@@ -24,7 +24,8 @@ STAT_ITERATIONS, STAT_FILLED, STAT_DEADLOCK, STAT_UNFILLABLE = 0, 1, 2, 3
 STAT_REMAINING, STAT_INPAINT, STAT_ROWS_OVERFLOW, STAT_LAST_FRONTIER = 4, 5, 6, 7
 
 EXPORTS = (
-    "gf_fill_workspace_bytes", "gf_fill", "gf_guide_field", "gf_sample_points",
+    "gf_fill_workspace_bytes", "gf_fill_splines_workspace_bytes", "gf_fill", "gf_fill_splines",
+    "gf_guide_field", "gf_sample_points",
     "gf_bilinear_gather", "gf_boundary_masks", "gf_last_error", "gf_abi_version",
     "gf_host_exp", "gf_host_hypot", "gf_host_pairwise_sum",
 )
@@ -66,6 +67,19 @@ class FillOutputsC(ctypes.Structure):
         ("rows_cap", ctypes.c_int32),
         ("enter", ctypes.c_void_p),
         ("fillshell", ctypes.c_void_p),
+        ("shell_trace", ctypes.c_void_p),
+        ("trace_cap", ctypes.c_int32),
+    ]
+
+
+class SplinesC(ctypes.Structure):
+    _fields_ = [
+        ("n_seg", ctypes.c_int32),
+        ("seg", ctypes.c_void_p),
+        ("seg_spline", ctypes.c_void_p),
+        ("n_splines", ctypes.c_int32),
+        ("dirs", ctypes.c_void_p),
+        ("eta", ctypes.c_double),
     ]
 
 
@@ -94,6 +108,14 @@ def load(required: bool = True):
     lib.gf_fill.restype = ctypes.c_int
     lib.gf_fill.argtypes = [ctypes.POINTER(FramesC), ctypes.POINTER(FillParamsC),
                             ctypes.POINTER(FillOutputsC), P, ctypes.c_size_t, P]
+    lib.gf_fill_splines_workspace_bytes.restype = ctypes.c_size_t
+    lib.gf_fill_splines_workspace_bytes.argtypes = [ctypes.POINTER(FramesC),
+                                                    ctypes.POINTER(FillParamsC),
+                                                    ctypes.POINTER(SplinesC)]
+    lib.gf_fill_splines.restype = ctypes.c_int
+    lib.gf_fill_splines.argtypes = [ctypes.POINTER(FramesC), ctypes.POINTER(FillParamsC),
+                                    ctypes.POINTER(SplinesC), ctypes.POINTER(FillOutputsC), P,
+                                    ctypes.c_size_t, P]
     lib.gf_guide_field.restype = ctypes.c_int
     lib.gf_guide_field.argtypes = [ctypes.c_int32, ctypes.c_int32, P, ctypes.c_int32, P, P,
                                    ctypes.c_int32, P, ctypes.c_double, P, P]

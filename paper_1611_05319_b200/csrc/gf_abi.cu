@@ -81,20 +81,31 @@ const char* gf_last_error(void) { return g_last_error.c_str(); }
 
 int gf_abi_version(void) { return GF_ABI_VERSION; }
 
-size_t gf_fill_workspace_bytes(const gf_frames* frames, const gf_fill_params* params) {
+size_t gf_fill_splines_workspace_bytes(const gf_frames* frames, const gf_fill_params* params,
+                                       const gf_splines* splines) {
   (void)params;
   if (check_frames(frames) != GF_OK) return 0;
   const int nF = std::min(frames->n_frames, kMaxFramesPerLaunch);
-  return fill_workspace_bytes(nF, frames->height, frames->width, frames->channels);
+  return fill_workspace_bytes(nF, frames->height, frames->width, frames->channels,
+                              splines && splines->n_seg > 0);
 }
 
-int gf_fill(const gf_frames* frames, const gf_fill_params* params, const gf_fill_outputs* outputs,
-            void* workspace, size_t workspace_bytes, void* stream) {
+size_t gf_fill_workspace_bytes(const gf_frames* frames, const gf_fill_params* params) {
+  return gf_fill_splines_workspace_bytes(frames, params, nullptr);
+}
+
+static int fill_common(const gf_frames* frames, const gf_fill_params* params,
+                       const gf_splines* splines, const gf_fill_outputs* outputs,
+                       void* workspace, size_t workspace_bytes, void* stream) {
   int rc = check_frames(frames);
   if (rc != GF_OK) return rc;
   if (!params || !outputs) return set_error(GF_E_INVALID, "NULL params/outputs");
   if (frames->n_frames == 0) return GF_OK;
-  if (params->g_mode == GF_G_FIELD && !frames->guide)
+  const bool raster = splines && splines->n_seg > 0;
+  if (splines && splines->n_seg > 0 &&
+      (!splines->seg || !splines->seg_spline || !splines->dirs || splines->n_splines <= 0))
+    return set_error(GF_E_INVALID, "incomplete spline arrays");
+  if (!raster && params->g_mode == GF_G_FIELD && !frames->guide)
     return set_error(GF_E_INVALID, "g_mode field needs a guide pointer");
   if (!frames->image || !frames->labels || !frames->out || !outputs->frame_stats || !outputs->rows)
     return set_error(GF_E_INVALID, "NULL device pointer");
@@ -124,10 +135,24 @@ int gf_fill(const gf_frames* frames, const gf_fill_params* params, const gf_fill
     o.rows = outputs->rows + (size_t)f0 * outputs->rows_cap * 2;
     o.enter = outputs->enter ? outputs->enter + f0 * HW : nullptr;
     o.fillshell = outputs->fillshell ? outputs->fillshell + f0 * HW : nullptr;
-    rc = fill_launch(&sub, params, &o, workspace, workspace_bytes, s, P, *T);
+    if (f0 > 0) o.shell_trace = nullptr;
+    rc = fill_launch(&sub, params, &o, raster ? splines : nullptr, workspace, workspace_bytes, s,
+                     P, *T);
   }
   delete T;  // passed by value as a kernel parameter: safe to free now
   return rc;
+}
+
+int gf_fill(const gf_frames* frames, const gf_fill_params* params, const gf_fill_outputs* outputs,
+            void* workspace, size_t workspace_bytes, void* stream) {
+  return fill_common(frames, params, nullptr, outputs, workspace, workspace_bytes, stream);
+}
+
+int gf_fill_splines(const gf_frames* frames, const gf_fill_params* params,
+                    const gf_splines* splines, const gf_fill_outputs* outputs, void* workspace,
+                    size_t workspace_bytes, void* stream) {
+  if (!splines) return set_error(GF_E_INVALID, "NULL splines");
+  return fill_common(frames, params, splines, outputs, workspace, workspace_bytes, stream);
 }
 
 int gf_guide_field(int32_t height, int32_t width, const uint8_t* labels, int32_t n_seg,

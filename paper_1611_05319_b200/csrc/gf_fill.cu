@@ -57,31 +57,91 @@ __device__ __forceinline__ int* stamp_ptr(float4* work, int q) {
 }
 
 // ---------------------------------------------------------------- prep
+//
+// One pass over every pixel, frame-major grid (blockIdx.y = frame): builds
+// the working frame (fp32 colour + stamp), the initial frontier (Inpaint
+// with a Readable 8-neighbour, grid.py:104-106), |D|, the value hull
+// (min/max of the readable values over all channels, engine.py:291-296)
+// and, when splines are given, the guide field g of every Inpaint pixel
+// (guide.py:303-327) -- rastered in place, so the field never exists as a
+// dense array.  Segments are culled per 256-pixel tile against the tile's
+// bounding box inflated by 3 eta: a pixel's g is non-zero only if its
+// nearest segment lies within 3 eta, and then that segment (and every tied
+// one) survives the cull, so non-zero g values are bit-identical to the
+// dense rasteriser; pixels with no candidate get g = +0 (the reference's
+// +-0 there is indistinguishable to the fill: every use tests g == 0 or
+// |g|).
+
+constexpr int kMaxCand = 512;
+
+__device__ __forceinline__ double seg_dist(double px, double py, const double4 s) {
+  const double ax = s.x, ay = s.y, bx = s.z, by = s.w;
+  const double abx = bx - ax, aby = by - ay;
+  const double L2 = abx * abx + aby * aby;
+  if (L2 == 0.0) return hypot_np(px - ax, py - ay);
+  double t = ((px - ax) * abx + (py - ay) * aby) / L2;
+  t = (t < 0.0) ? 0.0 : t;
+  t = (t > 1.0) ? 1.0 : t;
+  return hypot_np(px - (ax + t * abx), py - (ay + t * aby));
+}
 
 template <typename T>
-__global__ void __launch_bounds__(kThreads) k_prep(FillArgs A) {
-  const long long total = (long long)A.nF * A.HW;
-  const int lane = threadIdx.x & 31;
-  for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-       g - threadIdx.x < total; g += (long long)gridDim.x * blockDim.x) {
-    const bool in = g < total;
-    const int f = in ? (int)(g / A.HW) : 0;
-    const int p = in ? (int)(g - (long long)f * A.HW) : 0;
-    bool active = false, inpaint = false;
+__global__ void __launch_bounds__(kThreads) k_prep(const __grid_constant__ FillArgs A) {
+  const int f = blockIdx.y;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __shared__ int s_cand[kMaxCand];
+  __shared__ int s_ncand;
+  __shared__ unsigned long long s_red[2][kThreads / 32];
+  __shared__ int s_cnt[kThreads / 32];
+  const uint8_t* lab = A.labels + (size_t)f * A.HW;
+  const T* img = reinterpret_cast<const T*>(A.image) + (size_t)f * A.HW * A.C;
+  float4* work = A.work + (size_t)f * A.HW;
+  unsigned long long emin_inv = 0ULL, emax = 0ULL;  // max(~enc) <=> min(enc)
+  int n_inp = 0;
+  bool anyg = false;
+  const bool raster = A.n_seg > 0;
+  for (int base = blockIdx.x * kThreads; base < A.HW; base += gridDim.x * kThreads) {
+    const int p = base + threadIdx.x;
+    const bool in = p < A.HW;
+    if (raster) {
+      // tile bounding box -> candidate segments (order-free: the fused
+      // raster takes the lexicographic min of (distance, spline index))
+      const int last = min(A.HW - 1, base + kThreads - 1);
+      const int j0 = base / A.W, j1 = last / A.W;
+      const double x0 = (j0 == j1) ? (double)(base % A.W) : 0.0;
+      const double x1 = (j0 == j1) ? (double)(last % A.W) : (double)(A.W - 1);
+      if (threadIdx.x == 0) s_ncand = 0;
+      __syncthreads();
+      for (int i = threadIdx.x; i < A.n_seg; i += kThreads) {
+        const double4 sg = A.seg[i];
+        const double lo_x = fmin(sg.x, sg.z) - A.cut, hi_x = fmax(sg.x, sg.z) + A.cut;
+        const double lo_y = fmin(sg.y, sg.w) - A.cut, hi_y = fmax(sg.y, sg.w) + A.cut;
+        if (hi_x >= x0 && lo_x <= x1 && hi_y >= (double)j0 && lo_y <= (double)j1) {
+          const int slot = atomicAdd(&s_ncand, 1);
+          if (slot < kMaxCand) s_cand[slot] = i;
+        }
+      }
+      __syncthreads();
+    }
+    bool active = false;
     if (in) {
-      const uint8_t* lab = A.labels + (size_t)f * A.HW;
       const uint8_t l = lab[p];
-      const T* img = reinterpret_cast<const T*>(A.image) + ((size_t)f * A.HW + p) * A.C;
+      const T* px_in = img + (size_t)p * A.C;
       float4 px;
-      px.x = A.C > 0 ? (float)img[0] : 0.f;
-      px.y = A.C > 1 ? (float)img[1] : 0.f;
-      px.z = A.C > 2 ? (float)img[2] : 0.f;
-      if (A.C > 3) A.c3[(size_t)f * A.HW + p] = (float)img[3];
+      px.x = (float)px_in[0];
+      px.y = A.C > 1 ? (float)px_in[1] : 0.f;
+      px.z = A.C > 2 ? (float)px_in[2] : 0.f;
+      if (A.C > 3) A.c3[(size_t)f * A.HW + p] = (float)px_in[3];
       int st;
       if (l == 0) {
         st = kStampReadable;
+        for (int c = 0; c < A.C; ++c) {
+          const unsigned long long e = enc_ordered((double)px_in[c]);
+          emin_inv = (~e > emin_inv) ? ~e : emin_inv;
+          emax = (e > emax) ? e : emax;
+        }
       } else if (l == 255) {
-        inpaint = true;
+        ++n_inp;
         const int i = p % A.W, j = p / A.W;
         for (int dj = -1; dj <= 1 && !active; ++dj) {
           const int jj = j + dj;
@@ -89,11 +149,8 @@ __global__ void __launch_bounds__(kThreads) k_prep(FillArgs A) {
           for (int di = -1; di <= 1; ++di) {
             if (di == 0 && dj == 0) continue;
             int ii = i + di;
-            if (A.periodic) {
-              ii = (ii + A.W) % A.W;
-            } else if (ii < 0 || ii >= A.W) {
-              continue;
-            }
+            if (A.periodic) ii = (ii + A.W) % A.W;
+            else if (ii < 0 || ii >= A.W) continue;
             if (lab[jj * A.W + ii] == 0) {
               active = true;
               break;
@@ -101,75 +158,84 @@ __global__ void __launch_bounds__(kThreads) k_prep(FillArgs A) {
           }
         }
         st = active ? kStampActive : kStampInactive;
+        double gx = 0.0, gy = 0.0;
+        if (raster) {
+          const bool exhaustive = s_ncand > kMaxCand;
+          const int n_eval = exhaustive ? A.n_seg : s_ncand;
+          double dmin = INFINITY;
+          int near = 0x7fffffff;
+          const double fx = (double)i, fy = (double)j;
+          for (int c = 0; c < n_eval; ++c) {
+            const int sidx = exhaustive ? c : s_cand[c];
+            const double d = seg_dist(fx, fy, A.seg[sidx]);
+            const int sp = A.seg_spline[sidx];
+            if (d < dmin || (d == dmin && sp < near)) {
+              dmin = d;
+              near = sp;
+            }
+          }
+          if (dmin <= A.cut) {
+            const double fall = exp_np((-(dmin * dmin)) / A.c2eta);
+            const double2 dir = A.dirs[near];
+            gx = dir.x * fall;
+            gy = dir.y * fall;
+          }
+          reinterpret_cast<double2*>(A.gfield)[(size_t)f * A.HW + p] = make_double2(gx, gy);
+        } else if (A.g_mode == 2) {
+          const double2 g = reinterpret_cast<const double2*>(A.gsrc)[(size_t)f * A.HW + p];
+          gx = g.x;
+          gy = g.y;
+        }
+        if (active && (gx != 0.0 || gy != 0.0)) anyg = true;
       } else {
         st = kStampBystander;
       }
       px.w = __int_as_float(st);
-      A.work[(size_t)f * A.HW + p] = px;
+      work[p] = px;
       if (A.enter) A.enter[(size_t)f * A.HW + p] = active ? 0 : -1;
-      if (active && A.order == 2 && A.g_mode == 2) {
-        const double* gp = A.guide + ((size_t)f * A.HW + p) * 2;
-        if (gp[0] != 0.0 || gp[1] != 0.0) A.anyg[f] = 1;
-      }
     }
-    // warp-aggregated |D| count and initial-frontier append (lanes may span frames)
-    const unsigned any_inp = __ballot_sync(0xffffffffu, inpaint);
-    if (any_inp) {
-      const unsigned peers = __match_any_sync(0xffffffffu, in ? f : -1);
-      const unsigned minp = any_inp & peers;
-      const unsigned mact = __ballot_sync(0xffffffffu, active) & peers;
-      if (inpaint && lane == __ffs(minp) - 1) atomicAdd(&A.remaining[f], __popc(minp));
-      if (active) {
-        const int leader = __ffs(mact) - 1;
-        int base = 0;
-        if (lane == leader) base = atomicAdd(&A.cnt[f], __popc(mact));
-        base = __shfl_sync(mact, base, leader);
-        A.list0[(size_t)f * A.cap + base + __popc(mact & ((1u << lane) - 1))] = (uint32_t)p;
-      }
+    // warp-aggregated append of the initial frontier
+    const unsigned mact = __ballot_sync(0xffffffffu, active);
+    if (mact) {
+      const int leader = __ffs(mact) - 1;
+      int b = 0;
+      if (lane == leader) b = atomicAdd(&A.cnt[f], __popc(mact));
+      b = __shfl_sync(0xffffffffu, b, leader);
+      if (active) A.list0[(size_t)f * A.cap + b + __popc(mact & ((1u << lane) - 1))] = (uint32_t)p;
     }
+    if (raster) __syncthreads();  // s_cand is rebuilt for the next tile
   }
-}
-
-// Exact per-frame hull: one block per (frame, slice); block reduction then
-// one atomic pair per block.
-template <typename T>
-__global__ void __launch_bounds__(kThreads) k_hull(FillArgs A, int slices) {
-  const int f = blockIdx.x / slices;
-  const int s = blockIdx.x % slices;
-  const int per = (A.HW + slices - 1) / slices;
-  const int p0 = s * per, p1 = min(A.HW, p0 + per);
-  const uint8_t* lab = A.labels + (size_t)f * A.HW;
-  const T* img = reinterpret_cast<const T*>(A.image) + (size_t)f * A.HW * A.C;
-  unsigned long long emin = ~0ULL, emax = 0ULL;
-  for (int p = p0 + threadIdx.x; p < p1; p += blockDim.x) {
-    if (lab[p] != 0) continue;
-    for (int c = 0; c < A.C; ++c) {
-      const unsigned long long e = enc_ordered((double)img[(size_t)p * A.C + c]);
-      emin = e < emin ? e : emin;
-      emax = e > emax ? e : emax;
-    }
-  }
-  __shared__ unsigned long long smin[kThreads / 32], smax[kThreads / 32];
+  // block reductions: hull, |D|, data-term flag -> one atomic each per block
   for (int o = 16; o > 0; o >>= 1) {
-    const unsigned long long a = __shfl_xor_sync(0xffffffffu, emin, o);
+    const unsigned long long a = __shfl_xor_sync(0xffffffffu, emin_inv, o);
     const unsigned long long b = __shfl_xor_sync(0xffffffffu, emax, o);
-    emin = a < emin ? a : emin;
+    emin_inv = a > emin_inv ? a : emin_inv;
     emax = b > emax ? b : emax;
+    n_inp += __shfl_xor_sync(0xffffffffu, n_inp, o);
   }
-  if ((threadIdx.x & 31) == 0) {
-    smin[threadIdx.x >> 5] = emin;
-    smax[threadIdx.x >> 5] = emax;
+  const bool blk_anyg = __syncthreads_or(anyg);
+  if (lane == 0) {
+    s_red[0][warp] = emin_inv;
+    s_red[1][warp] = emax;
+    s_cnt[warp] = n_inp;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    for (int w = 1; w < kThreads / 32; ++w) {
-      emin = smin[w] < emin ? smin[w] : emin;
-      emax = smax[w] > emax ? smax[w] : emax;
+    int tot = 0;
+    for (int w = 0; w < kThreads / 32; ++w) {
+      emin_inv = s_red[0][w] > emin_inv ? s_red[0][w] : emin_inv;
+      emax = s_red[1][w] > emax ? s_red[1][w] : emax;
+      tot += s_cnt[w];
     }
-    if (emin != ~0ULL) {
-      atomicMin(&A.hull[2 * f], emin);
+    if (emax != 0ULL) {
+      atomicMax(&A.hull[2 * f], emin_inv);
       atomicMax(&A.hull[2 * f + 1], emax);
     }
+    if (tot) {
+      atomicAdd(&A.remaining[f], tot);
+      atomicAdd(&A.inpaint[f], tot);
+    }
+    if (blk_anyg) A.anyg[f] = 1;
   }
 }
 
@@ -188,6 +254,20 @@ struct Smem {
   int any_dl;
   int total;
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// per-shell phase timestamps (profiling only, A.trace may be null)
+__device__ __forceinline__ void trace_set(const FillArgs& A, int k, int slot, unsigned long long v) {
+  if (A.trace && k < A.trace_cap && blockIdx.x == 0 && threadIdx.x == 0) A.trace[k * 6 + slot] = v;
+}
+__device__ __forceinline__ void trace_max(const FillArgs& A, int k, int slot) {
+  if (A.trace && k < A.trace_cap && threadIdx.x == 0) atomicMax(&A.trace[k * 6 + slot], gtimer());
+}
 
 __device__ __forceinline__ int find_frame(const int* pref, int nF, int t) {
   int lo = 0, hi = nF - 1;
@@ -229,7 +309,7 @@ __device__ __forceinline__ unsigned long long conf_key(double c) {
 __device__ __forceinline__ void frame_guide(const FillArgs& A, int f, int p, double& gx,
                                             double& gy) {
   if (A.g_mode == 2) {
-    const double2 g = reinterpret_cast<const double2*>(A.guide)[(size_t)f * A.HW + p];
+    const double2 g = reinterpret_cast<const double2*>(A.gsrc)[(size_t)f * A.HW + p];
     gx = g.x;
     gy = g.y;
   } else if (A.g_mode == 1) {
@@ -263,7 +343,7 @@ __device__ __forceinline__ void flush_appends(const FillArgs& A, Smem& S, int f,
       const uint32_t q = S.app[i];
       nxt_list[(size_t)f * A.cap + base + i] = q;
       if (A.order == 2 && A.g_mode == 2) {
-        const double2 g = reinterpret_cast<const double2*>(A.guide)[(size_t)f * A.HW + q];
+        const double2 g = reinterpret_cast<const double2*>(A.gsrc)[(size_t)f * A.HW + q];
         anyg |= (g.x != 0.0 || g.y != 0.0);
       }
     }
@@ -301,7 +381,7 @@ __device__ void bookkeep(const FillArgs& A, int k) {
       A.filled[f] += filled;
       A.remaining[f] -= filled;
       if (A.remaining[f] == 0) A.done[f] = 1;
-      if (A.dt_live[f] && !frontier_has_g(A, prev, f)) A.dt_live[f] = 0;
+      if (!A.dt_dead[f] && !frontier_has_g(A, prev, f)) A.dt_dead[f] = 1;
     }
   }
 }
@@ -359,6 +439,8 @@ __global__ void __launch_bounds__(kThreads) k_shells(const __grid_constant__ Fil
     __syncthreads();
     const int T = S.total;
     if (T == 0) break;
+    trace_set(A, k, 0, gtimer());
+    trace_set(A, k, 5, (unsigned long long)T);
     const int chunk = max(kGroupsPerBlock, (T + gridDim.x - 1) / gridDim.x);
     const int c_lo = min(T, blockIdx.x * chunk), c_hi = min(T, c_lo + chunk);
 
@@ -368,7 +450,7 @@ __global__ void __launch_bounds__(kThreads) k_shells(const __grid_constant__ Fil
       const int fe = min(c_hi, S.pref[f + 1]);
       const float4* fw = A.work + (size_t)f * A.HW;
       WorkSource src{fw, A.c3 ? A.c3 + (size_t)f * A.HW : nullptr, A.H, A.W, A.C, k};
-      const int dt_eff = (A.order == 2) && A.dt_live[f] && frontier_has_g(A, cur, f);
+      const int dt_eff = (A.order == 2) && !A.dt_dead[f] && frontier_has_g(A, cur, f);
       int my_fills = 0;
       for (int base = s; base < fe; base += kGroupsPerBlock) {
         const int t = base + group;
@@ -407,7 +489,9 @@ __global__ void __launch_bounds__(kThreads) k_shells(const __grid_constant__ Fil
       if (threadIdx.x == 0 && tot > 0) atomicAdd(&A.fills[cur * A.nF + f], tot);
       s = fe;
     }
+    trace_max(A, k, 1);
     grid.sync();
+    trace_set(A, k, 2, gtimer());
 
     // ---- G: deadlock guard (engine.py:334-348), only when some frame stalled
     if (threadIdx.x == 0) {
@@ -602,7 +686,9 @@ __global__ void __launch_bounds__(kThreads) k_shells(const __grid_constant__ Fil
         s = fe;
       }
     }
+    trace_max(A, k, 3);
     grid.sync();
+    trace_set(A, k, 4, gtimer());
   }
   // final bookkeeping: stats
   if (blockIdx.x == 0) {
@@ -631,8 +717,8 @@ __global__ void __launch_bounds__(kThreads) k_finalize(FillArgs A) {
     const float4 px = A.work[g];
     const int st = __float_as_int(px.w);
     const bool filled = st >= 1 && st < kStampInactive;
-    const unsigned long long elo = A.hull[2 * f], ehi = A.hull[2 * f + 1];
-    const bool has_hull = elo != ~0ULL;
+    const unsigned long long elo = ~A.hull[2 * f], ehi = A.hull[2 * f + 1];
+    const bool has_hull = ehi != 0ULL;
     const double lo = has_hull ? dec_ordered(elo) : 0.0;
     const double hi = has_hull ? dec_ordered(ehi) : 0.0;
     const T* in = reinterpret_cast<const T*>(A.image) + (size_t)g * A.C;
@@ -652,14 +738,15 @@ __global__ void __launch_bounds__(kThreads) k_finalize(FillArgs A) {
 static size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct Layout {
-  size_t work, c3, list0, list1, conf, ints, u64, total;
+  size_t work, c3, list0, list1, conf, gfield, ints, u64, total;
 };
 
-static Layout layout_for(int nF, int HW, int C) {
+static Layout layout_for(int nF, int HW, int C, bool raster) {
   Layout L;
   size_t off = 0;
   const size_t n = (size_t)nF * HW;
   L.work = off; off = align_up(off + n * sizeof(float4));
+  L.gfield = off; off = align_up(off + (raster ? n * 2 * sizeof(double) : 0));
   L.c3 = off; off = align_up(off + (C > 3 ? n * sizeof(float) : 0));
   L.list0 = off; off = align_up(off + n * sizeof(uint32_t));
   L.list1 = off; off = align_up(off + n * sizeof(uint32_t));
@@ -670,9 +757,9 @@ static Layout layout_for(int nF, int HW, int C) {
   return L;
 }
 
-size_t fill_workspace_bytes(int nF, int H, int W, int C) {
+size_t fill_workspace_bytes(int nF, int H, int W, int C, bool raster) {
   if (nF <= 0 || H <= 0 || W <= 0) return 0;
-  return layout_for(nF, H * W, C).total;
+  return layout_for(nF, H * W, C, raster).total;
 }
 
 static int coop_grid(const void* fn, size_t smem, int* out_grid) {
@@ -693,11 +780,12 @@ static int coop_grid(const void* fn, size_t smem, int* out_grid) {
 }
 
 int fill_launch(const gf_frames* fr, const gf_fill_params* prm, const gf_fill_outputs* out,
-                void* ws, size_t ws_bytes, cudaStream_t stream, const BallParams& P,
-                const BallTables& host_tab) {
+                const gf_splines* spl, void* ws, size_t ws_bytes, cudaStream_t stream,
+                const BallParams& P, const BallTables& host_tab) {
   const int nF = fr->n_frames, H = fr->height, W = fr->width, C = fr->channels;
   const int HW = H * W;
-  const Layout L = layout_for(nF, HW, C);
+  const bool raster = spl && spl->n_seg > 0;
+  const Layout L = layout_for(nF, HW, C, raster);
   if (ws_bytes < L.total) return set_error(GF_E_WORKSPACE, "workspace too small");
   unsigned char* base = static_cast<unsigned char*>(ws);
 
@@ -707,7 +795,20 @@ int fill_launch(const gf_frames* fr, const gf_fill_params* prm, const gf_fill_ou
   A.image = fr->image;
   A.labels = fr->labels;
   A.guide = fr->guide;
+  A.gsrc = fr->guide;
   A.out = fr->out;
+  if (raster) {
+    A.gfield = reinterpret_cast<double*>(base + L.gfield);
+    A.gsrc = A.gfield;
+    A.n_seg = spl->n_seg;
+    A.seg = reinterpret_cast<const double4*>(spl->seg);
+    A.seg_spline = spl->seg_spline;
+    A.dirs = reinterpret_cast<const double2*>(spl->dirs);
+    A.cut = 3.0 * spl->eta;
+    A.c2eta = 2.0 * spl->eta * spl->eta;
+  }
+  A.trace = reinterpret_cast<unsigned long long*>(out->shell_trace);
+  A.trace_cap = out->shell_trace ? out->trace_cap : 0;
   A.work = reinterpret_cast<float4*>(base + L.work);
   A.c3 = C > 3 ? reinterpret_cast<float*>(base + L.c3) : nullptr;
   A.list0 = reinterpret_cast<uint32_t*>(base + L.list0);
@@ -722,7 +823,7 @@ int fill_launch(const gf_frames* fr, const gf_fill_params* prm, const gf_fill_ou
   A.done = ints;             ints += nF;
   A.deadlocks = ints;        ints += nF;
   A.filled = ints;           ints += nF;
-  A.dt_live = ints;          ints += nF;
+  A.dt_dead = ints;          ints += nF;
   A.best_p = ints;           ints += nF;
   A.inpaint = ints;          ints += nF;
   A.overflow = ints;         ints += nF;
@@ -738,32 +839,32 @@ int fill_launch(const gf_frames* fr, const gf_fill_params* prm, const gf_fill_ou
   A.order = prm->order;
   A.c = prm->c;
   A.c2 = prm->c2;
-  A.g_mode = prm->g_mode;
+  A.g_mode = raster ? GF_G_FIELD : prm->g_mode;
   A.gfx = prm->g_fixed[0];
   A.gfy = prm->g_fixed[1];
   A.periodic = prm->periodic_x;
   A.dtype = fr->dtype;
 
-  // per-frame counters: zero, hull sentinels, data-term latch, fixed-g anyg
-  if (cudaMemsetAsync(base + L.ints, 0, (size_t)nF * kIntsPerFrame * sizeof(int), stream) != cudaSuccess)
+  // per-frame counters start at zero (the hull minimum is stored inverted
+  // and the data-term latch as a "dead" flag, so zero is the initial state)
+  if (cudaMemsetAsync(base + L.ints, 0, L.u64 + (size_t)nF * 4 * sizeof(unsigned long long) - L.ints,
+                      stream) != cudaSuccess)
     return set_error(GF_E_CUDA, "memset failed");
-  init_frames(A, prm, stream);
-
-  const long long total = (long long)nF * HW;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int pgrid = (int)std::min<long long>((total + kThreads - 1) / kThreads, (long long)sms * 16);
-  const int slices = std::max(1, std::min(64, HW / (kThreads * 16)));
-  if (fr->dtype == GF_F64) {
-    k_prep<double><<<pgrid, kThreads, 0, stream>>>(A);
-    k_hull<double><<<nF * slices, kThreads, 0, stream>>>(A, slices);
-  } else {
-    k_prep<float><<<pgrid, kThreads, 0, stream>>>(A);
-    k_hull<float><<<nF * slices, kThreads, 0, stream>>>(A, slices);
+  const long long total = (long long)nF * HW;
+  {
+    const int bpf = std::max(1, std::min((HW + kThreads - 1) / kThreads,
+                                         std::max(1, sms * 8 / std::max(1, nF))));
+    const dim3 pgrid(bpf, nF);
+    if (fr->dtype == GF_F64)
+      k_prep<double><<<pgrid, kThreads, 0, stream>>>(A);
+    else
+      k_prep<float><<<pgrid, kThreads, 0, stream>>>(A);
   }
-  if (cudaPeekAtLastError() != cudaSuccess) return set_error(GF_E_CUDA, cudaGetErrorString(cudaGetLastError()));
-  copy_inpaint_counts(A, stream);
+  if (cudaPeekAtLastError() != cudaSuccess)
+    return set_error(GF_E_CUDA, cudaGetErrorString(cudaGetLastError()));
 
   const size_t smem = sizeof(Smem);
   const bool multi = P.plan.n_leaves > 1;
@@ -787,33 +888,6 @@ int fill_launch(const gf_frames* fr, const gf_fill_params* prm, const gf_fill_ou
   e = cudaPeekAtLastError();
   if (e != cudaSuccess) return set_error(GF_E_CUDA, cudaGetErrorString(e));
   return GF_OK;
-}
-
-// small helper kernels --------------------------------------------------
-
-__global__ void k_init_frames(FillArgs A, int dt_live, int anyg_fixed) {
-  for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < A.nF; f += gridDim.x * blockDim.x) {
-    A.hull[2 * f] = ~0ULL;
-    A.hull[2 * f + 1] = 0ULL;
-    A.dt_live[f] = dt_live;
-    A.anyg[f] = anyg_fixed;
-  }
-}
-
-__global__ void k_copy_inpaint(FillArgs A) {
-  for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < A.nF; f += gridDim.x * blockDim.x)
-    A.inpaint[f] = A.remaining[f];
-}
-
-void init_frames(const FillArgs& A, const gf_fill_params* prm, cudaStream_t stream) {
-  const int dt = prm->order == GF_ORDER_SMART_DATA ? 1 : 0;
-  int anyg_fixed = 0;
-  if (prm->g_mode == GF_G_FIXED) anyg_fixed = (prm->g_fixed[0] != 0.0 || prm->g_fixed[1] != 0.0);
-  k_init_frames<<<(A.nF + 255) / 256, 256, 0, stream>>>(A, dt, anyg_fixed);
-}
-
-void copy_inpaint_counts(const FillArgs& A, cudaStream_t stream) {
-  k_copy_inpaint<<<(A.nF + 255) / 256, 256, 0, stream>>>(A);
 }
 
 }  // namespace gf

@@ -21,6 +21,8 @@ struct FillArgs {
   const void* image;
   const uint8_t* labels;
   const double* guide;
+  const double* gsrc;  // per-pixel guide read by the shell loop (guide or gfield)
+  double* gfield;      // fused-raster output (Inpaint pixels only), or nullptr
   void* out;
   float4* work;
   float* c3;
@@ -35,7 +37,7 @@ struct FillArgs {
   int* done;       // [nF] 0 running, 1 complete, 2 unfillable
   int* deadlocks;  // [nF]
   int* filled;     // [nF]
-  int* dt_live;    // [nF]
+  int* dt_dead;    // [nF] data-term latch released (engine.py:327-329)
   int* best_p;     // [nF]
   int* inpaint;    // [nF]
   int* overflow;   // [nF]
@@ -52,18 +54,26 @@ struct FillArgs {
   int g_mode;
   double gfx, gfy;
   int periodic;
+  // fused spline raster (guide.py:286-327), n_seg == 0 when off
+  int n_seg;
+  const double4* seg;
+  const int32_t* seg_spline;
+  const double2* dirs;
+  double cut;    // 3.0 * eta
+  double c2eta;  // 2.0 * eta * eta
+  // optional per-shell phase timestamps (globaltimer ns), [trace_cap][6]
+  unsigned long long* trace;
+  int trace_cap;
 };
 
 // thread-local error reporting (gf_abi.cu)
 int set_error(int code, const char* msg);
 
 // gf_fill.cu
-size_t fill_workspace_bytes(int nF, int H, int W, int C);
+size_t fill_workspace_bytes(int nF, int H, int W, int C, bool raster);
 int fill_launch(const gf_frames* fr, const gf_fill_params* prm, const gf_fill_outputs* out,
-                void* ws, size_t ws_bytes, cudaStream_t stream, const BallParams& P,
-                const BallTables& host_tab);
-void init_frames(const FillArgs& A, const gf_fill_params* prm, cudaStream_t stream);
-void copy_inpaint_counts(const FillArgs& A, cudaStream_t stream);
+                const gf_splines* spl, void* ws, size_t ws_bytes, cudaStream_t stream,
+                const BallParams& P, const BallTables& host_tab);
 
 // gf_points.cu
 int sample_points_launch(int H, int W, int C, const double* image, const uint8_t* labels, int n,
