@@ -238,9 +238,14 @@ def run_ours(args):
     res = step(trace_cap=256)
     torch.cuda.synchronize()
     tr = res["trace"].cpu().numpy()[:n_shells]
-    shell_trace = [{"items": int(r[5]), "fill_us": (r[1] - r[0]) / 1e3,
-                    "sync_us": (r[2] - r[1]) / 1e3, "update_us": (r[3] - r[2]) / 1e3,
-                    "sync2_us": (r[4] - r[3]) / 1e3} for r in tr]
+    shell_trace = []
+    for r in tr:
+        row = {"items": int(r[5]), "fill_us": (r[1] - r[0]) / 1e3,
+               "lattice_item_max_us": r[6] / 1e3, "rotated_item_max_us": r[7] / 1e3,
+               "sync_us": (r[2] - r[1]) / 1e3}
+        if args.untracked:
+            row.update(rescan_us=(r[3] - r[2]) / 1e3, sync2_us=(r[4] - r[3]) / 1e3)
+        shell_trace.append(row)
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     if ws > 1:

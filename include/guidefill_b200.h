@@ -103,11 +103,14 @@ typedef struct gf_fill_outputs {
                            pixel joined the frontier, -1 never (order log)     */
   int32_t* fillshell;   /* optional device [n_frames][H][W]: shell in which the
                            pixel was filled, -1 never                           */
-  uint64_t* shell_trace; /* optional device [trace_cap][6] profiling record per
-                           shell: globaltimer ns at shell start, end of the fill
-                           phase (latest block), after its grid barrier, end of
-                           the frontier update (latest block), after its
-                           barrier, and the number of frontier items          */
+  uint64_t* shell_trace; /* optional device [trace_cap][8], zero-initialised:
+                           profiling record per shell -- globaltimer ns at shell
+                           start, end of the fill phase (latest block), after
+                           its grid barrier, end of the frontier update (latest
+                           block), after its barrier; the number of frontier
+                           items; the longest single-item evaluation (ns) on
+                           the lattice (g = 0) path and on the rotated-ball
+                           path                                               */
   int32_t trace_cap;
 } gf_fill_outputs;
 

@@ -53,7 +53,7 @@ def fill_device(image, labels, guide, params, tracked=True, order_log=False, row
     Returns a dict of CUDA tensors: ``out`` (like image), ``stats``
     (N, GF_STATS) int32, ``rows`` (N, rows_cap, 2) int32, with order_log
     ``enter``/``fillshell`` (N, H, W) int32, with trace_cap > 0 ``trace``
-    (trace_cap, 6) int64 per-shell phase timestamps.
+    (trace_cap, 8) int64 per-shell phase timestamps.
     """
     import torch
 
@@ -81,7 +81,7 @@ def fill_device(image, labels, guide, params, tracked=True, order_log=False, row
     pc = params_to_c(params, tracked, g_mode)
     trace = None
     if trace_cap:
-        trace = torch.zeros((trace_cap, 6), dtype=torch.int64, device=dev)
+        trace = torch.zeros((trace_cap, 8), dtype=torch.int64, device=dev)
     oc = N.FillOutputsC(stats.data_ptr(), rows.data_ptr(), rows_cap,
                         0 if enter is None else enter.data_ptr(),
                         0 if fillshell is None else fillshell.data_ptr(),

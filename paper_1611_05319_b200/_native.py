@@ -11,7 +11,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgf_b200.so")
+LIB_PATH = os.environ.get("GF_B200_LIB", os.path.join(_HERE, "libgf_b200.so"))
 
 GF_OK = 0
 GF_F32, GF_F64 = 0, 1

@@ -123,7 +123,7 @@ __global__ void __launch_bounds__(kThreads) k_prep(const __grid_constant__ FillA
       }
       __syncthreads();
     }
-    bool active = false;
+    bool active = false, rot = false;
     if (in) {
       const uint8_t l = lab[p];
       const T* px_in = img + (size_t)p * A.C;
@@ -157,7 +157,6 @@ __global__ void __launch_bounds__(kThreads) k_prep(const __grid_constant__ FillA
             }
           }
         }
-        st = active ? kStampActive : kStampInactive;
         double gx = 0.0, gy = 0.0;
         if (raster) {
           const bool exhaustive = s_ncand > kMaxCand;
@@ -185,8 +184,13 @@ __global__ void __launch_bounds__(kThreads) k_prep(const __grid_constant__ FillA
           const double2 g = reinterpret_cast<const double2*>(A.gsrc)[(size_t)f * A.HW + p];
           gx = g.x;
           gy = g.y;
+        } else if (A.g_mode == 1) {
+          gx = A.gfx;
+          gy = A.gfy;
         }
-        if (active && (gx != 0.0 || gy != 0.0)) anyg = true;
+        rot = (gx != 0.0 || gy != 0.0);
+        st = (active ? kStampActive : kStampInactive) | (rot ? kRotBit : 0);
+        if (active && rot) anyg = true;
       } else {
         st = kStampBystander;
       }
@@ -194,15 +198,22 @@ __global__ void __launch_bounds__(kThreads) k_prep(const __grid_constant__ FillA
       work[p] = px;
       if (A.enter) A.enter[(size_t)f * A.HW + p] = active ? 0 : -1;
     }
-    // warp-aggregated append of the initial frontier
-    const unsigned mact = __ballot_sync(0xffffffffu, active);
-    if (mact) {
-      const int leader = __ffs(mact) - 1;
-      int b = 0;
-      if (lane == leader) b = atomicAdd(&A.cnt[f], __popc(mact));
-      b = __shfl_sync(0xffffffffu, b, leader);
-      if (active) A.list0[(size_t)f * A.cap + b + __popc(mact & ((1u << lane) - 1))] = (uint32_t)p;
+    // warp-aggregated append of the initial frontier: lattice entries to the
+    // front of the list, rotated-ball entries to the back (when split)
+    const bool back = active && rot && A.split;
+    const unsigned mL = __ballot_sync(0xffffffffu, active && !back);
+    const unsigned mR = __ballot_sync(0xffffffffu, back);
+    const unsigned lt = (1u << lane) - 1;
+    int bL = 0, bR = 0;
+    if (lane == 0) {
+      if (mL) bL = atomicAdd(&A.cnt[f], __popc(mL));
+      if (mR) bR = atomicAdd(&A.cntR[f], __popc(mR));
     }
+    bL = __shfl_sync(0xffffffffu, bL, 0);
+    bR = __shfl_sync(0xffffffffu, bR, 0);
+    const uint32_t e0 = (uint32_t)p | (rot ? kEntryRot : 0u);
+    if (back) A.list0[(size_t)f * A.cap + A.cap - 1 - (bR + __popc(mR & lt))] = e0;
+    else if (active) A.list0[(size_t)f * A.cap + bL + __popc(mL & lt)] = e0;
     if (raster) __syncthreads();  // s_cand is rebuilt for the next tile
   }
   // block reductions: hull, |D|, data-term flag -> one atomic each per block
@@ -240,19 +251,26 @@ __global__ void __launch_bounds__(kThreads) k_prep(const __grid_constant__ FillA
 }
 
 // ------------------------------------------------------- shell loop
+//
+// Frontier lists.  Each frame owns a list buffer of `cap` entries used from
+// both ends: lattice entries (g = 0, 8-lane sampler) grow from the front,
+// rotated-ball entries (g != 0, warp-per-item sampler) grow from the back,
+// with separate counters cnt / cntR.  An entry is pixel | kEntryRot.  The
+// per-frame item index j runs over [0, nL) for the front part and
+// [nL, nL + nR) for the back part (conf[] and the guard use it).
 
 struct Smem {
   BallTables tab;
-  int pref[kMaxFramesPerLaunch + 1];
+  int pref[kMaxFramesPerLaunch + 1];   // all items
+  int prefL[kMaxFramesPerLaunch + 1];  // lattice part
+  int prefR[kMaxFramesPerLaunch + 1];  // rotated part
   unsigned char act[kMaxFramesPerLaunch];
   unsigned char dl[kMaxFramesPerLaunch];
   uint32_t app[kAppendCap];
-  int napp;
-  int base;
   int red[kThreads / 32];
   unsigned long long redk[kThreads / 32];
   int any_dl;
-  int total;
+  int total, totalL, totalR;
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -262,13 +280,21 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 
 // per-shell phase timestamps (profiling only, A.trace may be null)
+constexpr int kTraceSlots = 8;
+__device__ __forceinline__ void trace_max_val(const FillArgs& A, int k, int slot,
+                                              unsigned long long v) {
+  if (A.trace && k < A.trace_cap) atomicMax(&A.trace[k * kTraceSlots + slot], v);
+}
 __device__ __forceinline__ void trace_set(const FillArgs& A, int k, int slot, unsigned long long v) {
-  if (A.trace && k < A.trace_cap && blockIdx.x == 0 && threadIdx.x == 0) A.trace[k * 6 + slot] = v;
+  if (A.trace && k < A.trace_cap && blockIdx.x == 0 && threadIdx.x == 0)
+    A.trace[k * kTraceSlots + slot] = v;
 }
 __device__ __forceinline__ void trace_max(const FillArgs& A, int k, int slot) {
-  if (A.trace && k < A.trace_cap && threadIdx.x == 0) atomicMax(&A.trace[k * 6 + slot], gtimer());
+  if (A.trace && k < A.trace_cap && threadIdx.x == 0)
+    atomicMax(&A.trace[k * kTraceSlots + slot], gtimer());
 }
 
+// largest f with pref[f] <= t
 __device__ __forceinline__ int find_frame(const int* pref, int nF, int t) {
   int lo = 0, hi = nF - 1;
   while (lo < hi) {
@@ -276,16 +302,6 @@ __device__ __forceinline__ int find_frame(const int* pref, int nF, int t) {
     if (pref[mid] <= t) lo = mid; else hi = mid - 1;
   }
   return lo;
-}
-
-__device__ __forceinline__ int block_sum(int v, Smem& S) {
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  __syncthreads();
-  if ((threadIdx.x & 31) == 0) S.red[threadIdx.x >> 5] = v;
-  __syncthreads();
-  int t = 0;
-  for (int w = 0; w < kThreads / 32; ++w) t += S.red[w];
-  return t;
 }
 
 __device__ __forceinline__ unsigned long long block_max_u64(unsigned long long v, Smem& S) {
@@ -329,45 +345,167 @@ __device__ __forceinline__ bool frontier_has_g(const FillArgs& A, int which, int
   return false;
 }
 
-// Append buffered pixels of frame f to the next list (one global atomic).
-__device__ __forceinline__ void flush_appends(const FillArgs& A, Smem& S, int f, uint32_t* nxt_list,
-                                              int nxt) {
-  __syncthreads();
-  const int n = S.napp;
-  if (threadIdx.x == 0 && n > 0) S.base = atomicAdd(&A.cnt[nxt * A.nF + f], n);
-  __syncthreads();
-  if (n > 0) {
-    const int base = S.base;
-    bool anyg = false;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-      const uint32_t q = S.app[i];
-      nxt_list[(size_t)f * A.cap + base + i] = q;
-      if (A.order == 2 && A.g_mode == 2) {
-        const double2 g = reinterpret_cast<const double2*>(A.gsrc)[(size_t)f * A.HW + q];
-        anyg |= (g.x != 0.0 || g.y != 0.0);
-      }
-    }
-    if (__syncthreads_or(anyg) && threadIdx.x == 0) A.anyg[nxt * A.nF + f] = 1;
-  }
-  if (threadIdx.x == 0) S.napp = 0;
-  __syncthreads();
+__device__ __forceinline__ int frontier_size(const FillArgs& A, int which, int f) {
+  return A.cnt[which * A.nF + f] + A.cntR[which * A.nF + f];
 }
 
-__device__ __forceinline__ void push_append(Smem& S, bool want, uint32_t q) {
+// entry j of frame f's list (front part first, then the back part)
+__device__ __forceinline__ uint32_t entry_at(const uint32_t* list, const FillArgs& A, int f, int j,
+                                             int nL) {
+  const uint32_t* l = list + (size_t)f * A.cap;
+  return j < nL ? l[j] : l[A.cap - 1 - (j - nL)];
+}
+
+__device__ __forceinline__ bool entry_back(const FillArgs& A, uint32_t e) {
+  return A.split && (e & kEntryRot) != 0;
+}
+
+// one entry straight into the global list (rare paths)
+__device__ __forceinline__ void append_direct(const FillArgs& A, uint32_t* list, int nxt, int f,
+                                              uint32_t e) {
+  if (entry_back(A, e)) {
+    const int r = atomicAdd(&A.cntR[nxt * A.nF + f], 1);
+    list[(size_t)f * A.cap + A.cap - 1 - r] = e;
+  } else {
+    list[(size_t)f * A.cap + atomicAdd(&A.cnt[nxt * A.nF + f], 1)] = e;
+  }
+  if (A.order == 2 && A.g_mode == 2 && (e & kEntryRot)) A.anyg[nxt * A.nF + f] = 1;
+}
+
+// Warp-private append staging: each warp owns a slice of S.app and a
+// warp-uniform count; a slice is published with one atomic per list part.
+constexpr int kWarpAppCap = kAppendCap / (kThreads / 32);
+
+__device__ __forceinline__ void warp_push(uint32_t* reg, int& n, bool want, uint32_t e) {
   const unsigned m = __ballot_sync(0xffffffffu, want);
-  if (!m) return;
   const int lane = threadIdx.x & 31;
-  int base = 0;
-  if (lane == __ffs(m) - 1) base = atomicAdd(&S.napp, __popc(m));
-  base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
-  if (want) S.app[base + __popc(m & ((1u << lane) - 1))] = q;
+  if (want) reg[n + __popc(m & ((1u << lane) - 1))] = e;
+  n += __popc(m);
+}
+
+__device__ __forceinline__ void warp_flush(const FillArgs& A, uint32_t* reg, int& n, int f,
+                                           uint32_t* nxt_list, int nxt) {
+  if (n == 0) return;
+  __syncwarp();
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1;
+  int nR = 0;
+  bool anyg = false;
+  for (int c0 = 0; c0 < n; c0 += 32) {
+    const bool in = c0 + lane < n;
+    const uint32_t e = in ? reg[c0 + lane] : 0u;
+    nR += __popc(__ballot_sync(0xffffffffu, in && entry_back(A, e)));
+    anyg |= in && (e & kEntryRot) != 0;
+  }
+  int bL = 0, bR = 0;
+  if (lane == 0) {
+    if (n - nR > 0) bL = atomicAdd(&A.cnt[nxt * A.nF + f], n - nR);
+    if (nR > 0) bR = atomicAdd(&A.cntR[nxt * A.nF + f], nR);
+  }
+  bL = __shfl_sync(0xffffffffu, bL, 0);
+  bR = __shfl_sync(0xffffffffu, bR, 0);
+  uint32_t* l = nxt_list + (size_t)f * A.cap;
+  for (int c0 = 0; c0 < n; c0 += 32) {
+    const bool in = c0 + lane < n;
+    const uint32_t e = in ? reg[c0 + lane] : 0u;
+    const bool back = in && entry_back(A, e);
+    const unsigned mR = __ballot_sync(0xffffffffu, back);
+    const unsigned mL = __ballot_sync(0xffffffffu, in && !back);
+    if (back) l[A.cap - 1 - (bR + __popc(mR & lt))] = e;
+    else if (in) l[bL + __popc(mL & lt)] = e;
+    bR += __popc(mR);
+    bL += __popc(mL);
+  }
+  if (A.order == 2 && A.g_mode == 2 && __any_sync(0xffffffffu, anyg) && lane == 0)
+    A.anyg[nxt * A.nF + f] = 1;
+  __syncwarp();
+  n = 0;
+}
+
+// ready / fill decision of one item (engine.py:317-333) and the in-place
+// write of its colour with the shell stamp (snapshot-safe: stamp k+1 is
+// unreadable for every other item of shell k).
+__device__ __forceinline__ bool decide_and_write(const FillArgs& A, int f, int j, uint32_t p, int k,
+                                                 bool dt_eff, double gx, double gy,
+                                                 const SampleResult& r) {
+  const double conf = r.rw / r.tw;
+  bool ready;
+  if (A.order == 0) {
+    ready = true;
+  } else if (!dt_eff) {
+    ready = conf > A.c;
+  } else {
+    ready = (hypot_np(gx, gy) > A.c2) && (conf > A.c);
+  }
+  const bool fill = ready && (r.rw > 0.0);
+  A.conf[(size_t)f * A.cap + j] = conf;
+  if (fill) {
+    float4 o;
+    o.x = (float)r.v[0];
+    o.y = (float)r.v[1];
+    o.z = (float)r.v[2];
+    o.w = __int_as_float(k + 1);
+    A.work[(size_t)f * A.HW + p] = o;
+    if (A.c3) A.c3[(size_t)f * A.HW + p] = (float)r.v[3];
+  }
+  return fill;
+}
+
+__device__ __forceinline__ int neighbor_of(const FillArgs& A, uint32_t p, int o, bool& in) {
+  const int di = (o < 3) ? o - 1 : (o == 3 ? -1 : (o == 4 ? 1 : o - 6));
+  const int dj = (o < 3) ? -1 : (o < 5 ? 0 : 1);
+  int ii = (int)p % A.W + di;
+  const int jj = (int)p / A.W + dj;
+  if (A.periodic) ii = pos_mod(ii, A.W);
+  in = ii >= 0 && ii < A.W && jj >= 0 && jj < A.H;
+  return in ? jj * A.W + ii : 0;
+}
+
+// Claim Inpaint neighbour q for the next frontier: INACTIVE -> ACTIVE (the
+// dedup of tracker.py:78).  One CAS in the common case, a second only when q
+// is an inactive rotated-ball pixel.  Returns the list entry or ~0u.
+__device__ __forceinline__ uint32_t claim(float4* fw, int q) {
+  int* sp = stamp_ptr(fw, q);
+  const int old = atomicCAS(sp, kStampInactive, kStampActive);
+  if (old == kStampInactive) return (uint32_t)q;
+  if (old == (kStampInactive | kRotBit) &&
+      atomicCAS(sp, kStampInactive | kRotBit, kStampActive | kRotBit) == (kStampInactive | kRotBit))
+    return (uint32_t)q | kEntryRot;
+  return 0xffffffffu;
+}
+
+// Tracked frontier maintenance fused into the fill (tracker.py:42-79): an
+// unfilled item re-enters the next list (entry e, flag kept), a filled
+// item's Inpaint 8-neighbours join it.  Lane `o` (0..7, -1 = idle) handles
+// neighbour o.  `staged`: warp-uniform; false -> direct global appends (the
+// items of this warp-round belong to different frames).  Every lane calls.
+__device__ __forceinline__ void activate(const FillArgs& A, uint32_t* reg, int& n, bool staged,
+                                         uint32_t* nxt_list, int nxt, float4* fw, int f, int k,
+                                         int o, bool filled, uint32_t e) {
+  const bool survive = o == 0 && !filled;
+  uint32_t qe = 0xffffffffu;
+  if (o >= 0 && filled) {
+    bool in;
+    const int q = neighbor_of(A, e & kEntryPix, o, in);
+    if (in) {
+      qe = claim(fw, q);
+      if (qe != 0xffffffffu && A.enter) A.enter[(size_t)f * A.HW + q] = k + 1;
+    }
+  }
+  if (staged) {
+    warp_push(reg, n, survive, e);
+    warp_push(reg, n, qe != 0xffffffffu, qe);
+  } else {
+    if (survive) append_direct(A, nxt_list, nxt, f, e);
+    if (qe != 0xffffffffu) append_direct(A, nxt_list, nxt, f, qe);
+  }
 }
 
 // Bookkeeping of shell k-1 (block 0 only): report row, remaining, latch.
 __device__ void bookkeep(const FillArgs& A, int k) {
   const int prev = (k - 1) & 1;
   for (int f = threadIdx.x; f < A.nF; f += blockDim.x) {
-    const int F = A.cnt[prev * A.nF + f];
+    const int F = frontier_size(A, prev, f);
     if (F > 0 && A.done[f] == 0) {
       const int filled = A.fills[prev * A.nF + f];
       const int it = A.iters[f];
@@ -386,10 +524,14 @@ __device__ void bookkeep(const FillArgs& A, int k) {
   }
 }
 
-template <int NL, bool kTracked>
-__global__ void __launch_bounds__(kThreads) k_shells(const __grid_constant__ FillArgs A,
-                                                     const __grid_constant__ BallParams P,
-                                                     const __grid_constant__ BallTables tables) {
+#ifndef GF_SHELL_MIN_BLOCKS
+#define GF_SHELL_MIN_BLOCKS 1
+#endif
+
+template <int NL, int KPL, bool kTracked>
+__global__ void __launch_bounds__(kThreads, GF_SHELL_MIN_BLOCKS)
+    k_shells(const __grid_constant__ FillArgs A, const __grid_constant__ BallParams P,
+             const __grid_constant__ BallTables tables) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Smem& S = *reinterpret_cast<Smem*>(smem_raw);
@@ -398,98 +540,155 @@ __global__ void __launch_bounds__(kThreads) k_shells(const __grid_constant__ Fil
     S.tab.m[i] = tables.m[i];
     S.tab.w0[i] = tables.w0[i];
   }
-  if (threadIdx.x == 0) S.napp = 0;
   __syncthreads();
 
+  constexpr int kWarps = kThreads / 32;
+  // rotated items take the warp-per-item path when the ball is one
+  // pairwise leaf (K <= 128; then A.split == 1); samples per lane there =
+  // ceil(K / 32)
+  constexpr bool kWarpRot = (NL == 1);
+  constexpr int KPW = KPL > 0 ? (KPL + 3) / 4 : 4;
   const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
   const int glane = lane & (kGroup - 1);
-  const int group = threadIdx.x / kGroup;
+  const int sub = lane / kGroup;  // 8-lane group within the warp
+  uint32_t* reg = S.app + warp * kWarpAppCap;
 
   for (int k = 0;; ++k) {
     const int cur = k & 1, nxt = cur ^ 1;
     uint32_t* cur_list = cur ? A.list1 : A.list0;
     uint32_t* nxt_list = cur ? A.list0 : A.list1;
-    // ---- P0: bookkeeping of shell k-1 (block 0), frame activity, prefix
+    // ---- P0: bookkeeping of shell k-1 (block 0), frame activity, prefixes
     if (blockIdx.x == 0) {
       if (k > 0) bookkeep(A, k);
       __syncthreads();
       for (int f = threadIdx.x; f < A.nF; f += blockDim.x) {
-        if (A.done[f] == 0 && A.cnt[cur * A.nF + f] == 0 && A.remaining[f] > 0) A.done[f] = 2;
+        if (A.done[f] == 0 && frontier_size(A, cur, f) == 0 && A.remaining[f] > 0) A.done[f] = 2;
         A.cnt[nxt * A.nF + f] = 0;
+        A.cntR[nxt * A.nF + f] = 0;
         A.fills[nxt * A.nF + f] = 0;
         A.anyg[nxt * A.nF + f] = 0;
         A.best_key[f] = 0ULL;
         A.best_p[f] = 0x7fffffff;
       }
     }
-    for (int f = threadIdx.x; f < A.nF; f += blockDim.x) {
-      const int c = A.cnt[cur * A.nF + f];
-      S.act[f] = (c > 0 && A.done[f] == 0) ? 1 : 0;
-    }
+    for (int f = threadIdx.x; f < A.nF; f += blockDim.x)
+      S.act[f] = (frontier_size(A, cur, f) > 0 && A.done[f] == 0) ? 1 : 0;
     __syncthreads();
     if (threadIdx.x == 0) {
-      int run = 0;
+      int run = 0, runL = 0, runR = 0;
       for (int f = 0; f < A.nF; ++f) {
         S.pref[f] = run;
-        if (S.act[f]) run += A.cnt[cur * A.nF + f];
+        S.prefL[f] = runL;
+        S.prefR[f] = runR;
+        if (S.act[f]) {
+          const int nL = A.cnt[cur * A.nF + f], nR = A.cntR[cur * A.nF + f];
+          run += nL + nR;
+          runL += nL;
+          runR += nR;
+        }
       }
       S.pref[A.nF] = run;
+      S.prefL[A.nF] = runL;
+      S.prefR[A.nF] = runR;
       S.total = run;
+      S.totalL = runL;
+      S.totalR = runR;
     }
     __syncthreads();
     const int T = S.total;
     if (T == 0) break;
     trace_set(A, k, 0, gtimer());
     trace_set(A, k, 5, (unsigned long long)T);
-    const int chunk = max(kGroupsPerBlock, (T + gridDim.x - 1) / gridDim.x);
-    const int c_lo = min(T, blockIdx.x * chunk), c_hi = min(T, c_lo + chunk);
 
-    // ---- A: fill
-    for (int s = c_lo; s < c_hi;) {
-      const int f = find_frame(S.pref, A.nF, s);
-      const int fe = min(c_hi, S.pref[f + 1]);
-      const float4* fw = A.work + (size_t)f * A.HW;
-      WorkSource src{fw, A.c3 ? A.c3 + (size_t)f * A.HW : nullptr, A.H, A.W, A.C, k};
-      const int dt_eff = (A.order == 2) && !A.dt_dead[f] && frontier_has_g(A, cur, f);
-      int my_fills = 0;
-      for (int base = s; base < fe; base += kGroupsPerBlock) {
-        const int t = base + group;
-        const bool valid = t < fe;
-        const int j = valid ? t - S.pref[f] : 0;
-        const uint32_t p = valid ? cur_list[(size_t)f * A.cap + j] : 0u;
-        double gx = 0.0, gy = 0.0;
-        if (valid) frame_guide(A, f, (int)p, gx, gy);
-        SampleResult r;
-        eval_item<NL>(P, S.tab, src, glane, valid, (double)((int)p % A.W), (double)((int)p / A.W), true, gx, gy, r);
-        if (valid && glane == 0) {
-          const double conf = r.rw / r.tw;
-          bool ready;
-          if (A.order == 0) {
-            ready = true;
-          } else if (!dt_eff) {
-            ready = conf > A.c;
-          } else {
-            ready = (hypot_np(gx, gy) > A.c2) && (conf > A.c);
+    // ---- A: fill (+ fused frontier update when tracked)
+    // Work units, dealt cyclically over every warp of the grid: a rotated
+    // item (whole warp) or a round of 4 consecutive lattice items (one per
+    // 8-lane group).  No block barrier.
+    {
+      const int TR = S.totalR, TL = S.totalL;
+      const int UL = (TL + 3) / 4;
+      const int U = TR + UL;
+      const int NW = gridDim.x * kWarps;
+      int wn = 0, wf = -1, wfills = 0;
+      for (int u = blockIdx.x * kWarps + warp; u < U; u += NW) {
+        if (kWarpRot && u < TR) {
+          // ---- rotated-ball item, one whole warp
+          const int f = find_frame(S.prefR, A.nF, u);
+          const int nL = A.cnt[cur * A.nF + f];
+          const int rr = u - S.prefR[f];
+          const int j = nL + rr;
+          const uint32_t e = cur_list[(size_t)f * A.cap + A.cap - 1 - rr];
+          const uint32_t p = e & kEntryPix;
+          if (f != wf) {
+            if (kTracked && wf >= 0) warp_flush(A, reg, wn, wf, nxt_list, nxt);
+            if (lane == 0 && wf >= 0 && wfills > 0) atomicAdd(&A.fills[cur * A.nF + wf], wfills);
+            wfills = 0;
+            wf = f;
           }
-          const bool fill = ready && (r.rw > 0.0);
-          A.conf[(size_t)f * A.cap + j] = conf;
-          if (fill) {
-            float4 o;
-            o.x = (float)r.v[0];
-            o.y = (float)r.v[1];
-            o.z = (float)r.v[2];
-            o.w = __int_as_float(k + 1);
-            A.work[(size_t)f * A.HW + p] = o;
-            if (A.c3) A.c3[(size_t)f * A.HW + p] = (float)r.v[3];
-            ++my_fills;
+          const bool dt_eff = (A.order == 2) && !A.dt_dead[f] && frontier_has_g(A, cur, f);
+          double gx, gy;
+          frame_guide(A, f, (int)p, gx, gy);
+          float4* fw = A.work + (size_t)f * A.HW;
+          WorkSource src{fw, A.c3 ? A.c3 + (size_t)f * A.HW : nullptr, A.H, A.W, A.C, k};
+          SampleResult res;
+          const unsigned long long tw0 = A.trace ? gtimer() : 0ULL;
+          eval_item_warp<KPW>(P, S.tab, src, lane, true, (double)((int)p % A.W),
+                              (double)((int)p / A.W), gx, gy, res);
+          if (A.trace && lane == 0) trace_max_val(A, k, 7, gtimer() - tw0);
+          bool filled = false;
+          if (lane == 0) filled = decide_and_write(A, f, j, p, k, dt_eff, gx, gy, res);
+          filled = __shfl_sync(0xffffffffu, filled, 0);
+          if (lane == 0 && filled) ++wfills;
+          if (kTracked)
+            activate(A, reg, wn, true, nxt_list, nxt, fw, f, k, lane < 8 ? lane : -1, filled, e);
+        } else {
+          // ---- lattice round: items 4q .. 4q+3 of the concatenated front parts
+          const int q = kWarpRot ? u - TR : u;
+          const int t = q * 4 + sub;
+          const int TLx = kWarpRot ? TL : T;  // NL > 1: everything lives in the front part
+          const bool valid = t < TLx;
+          const int* pf = kWarpRot ? S.prefL : S.pref;
+          const int f = valid ? find_frame(pf, A.nF, t) : -1;
+          const int f0 = __shfl_sync(0xffffffffu, f, 0);
+          const bool uniform = __all_sync(0xffffffffu, !valid || f == f0);
+          if (!uniform || f0 != wf) {
+            if (kTracked && wf >= 0) warp_flush(A, reg, wn, wf, nxt_list, nxt);
+            if (lane == 0 && wf >= 0 && wfills > 0) atomicAdd(&A.fills[cur * A.nF + wf], wfills);
+            wfills = 0;
+            wf = uniform ? f0 : -1;
           }
+          const int fs = valid ? f : 0;
+          const int j = valid ? t - pf[fs] : 0;
+          const uint32_t e = valid ? cur_list[(size_t)fs * A.cap + j] : 0u;
+          const uint32_t p = e & kEntryPix;
+          float4* fw = A.work + (size_t)fs * A.HW;
+          WorkSource src{fw, A.c3 ? A.c3 + (size_t)fs * A.HW : nullptr, A.H, A.W, A.C, k};
+          const bool dt_eff =
+              valid && (A.order == 2) && !A.dt_dead[fs] && frontier_has_g(A, cur, fs);
+          double gx = 0.0, gy = 0.0;
+          if (valid && (e & kEntryRot)) frame_guide(A, fs, (int)p, gx, gy);  // NL > 1 only
+          SampleResult res;
+          const unsigned long long te0 = A.trace ? gtimer() : 0ULL;
+          eval_item<NL, KPL>(P, S.tab, src, glane, valid, (double)((int)p % A.W),
+                             (double)((int)p / A.W), true, gx, gy, res);
+          if (A.trace && valid && glane == 0) trace_max_val(A, k, 6, gtimer() - te0);
+          bool filled = false;
+          if (valid && glane == 0) filled = decide_and_write(A, fs, j, p, k, dt_eff, gx, gy, res);
+          filled = __shfl_sync(0xffffffffu, filled, 0, kGroup);
+          if (kTracked)
+            activate(A, reg, wn, uniform, nxt_list, nxt, fw, fs, k, valid ? glane : -1, filled, e);
+          const int nf = (valid && glane == 0 && filled) ? 1 : 0;
+          if (uniform) wfills += __reduce_add_sync(0xffffffffu, (unsigned)nf);
+          else if (nf) atomicAdd(&A.fills[cur * A.nF + fs], 1);
         }
+        if (kTracked && wn > kWarpAppCap - 64) warp_flush(A, reg, wn, wf, nxt_list, nxt);
       }
-      const int tot = block_sum(my_fills, S);
-      if (threadIdx.x == 0 && tot > 0) atomicAdd(&A.fills[cur * A.nF + f], tot);
-      s = fe;
+      if (kTracked && wf >= 0) warp_flush(A, reg, wn, wf, nxt_list, nxt);
+      if (lane == 0 && wf >= 0 && wfills > 0) atomicAdd(&A.fills[cur * A.nF + wf], wfills);
+      if (A.trace && lane == 0 && k < A.trace_cap)
+        atomicMax(&A.trace[k * kTraceSlots + 1], gtimer());
     }
-    trace_max(A, k, 1);
     grid.sync();
     trace_set(A, k, 2, gtimer());
 
@@ -505,6 +704,8 @@ __global__ void __launch_bounds__(kThreads) k_shells(const __grid_constant__ Fil
     }
     __syncthreads();
     if (S.any_dl) {
+      const int chunk = max(kThreads, (T + gridDim.x - 1) / gridDim.x);
+      const int c_lo = min(T, blockIdx.x * chunk), c_hi = min(T, c_lo + chunk);
       // G1: max confidence key per stalled frame
       for (int s = c_lo; s < c_hi;) {
         const int f = find_frame(S.pref, A.nF, s);
@@ -527,54 +728,101 @@ __global__ void __launch_bounds__(kThreads) k_shells(const __grid_constant__ Fil
         const int fe = min(c_hi, S.pref[f + 1]);
         if (S.dl[f]) {
           const unsigned long long best = A.best_key[f];
+          const int nL = A.cnt[cur * A.nF + f];
           for (int t = s + threadIdx.x; t < fe; t += blockDim.x) {
             const int j = t - S.pref[f];
             if (conf_key(A.conf[(size_t)f * A.cap + j]) == best)
-              atomicMin(&A.best_p[f], (int)cur_list[(size_t)f * A.cap + j]);
+              atomicMin(&A.best_p[f], (int)(entry_at(cur_list, A, f, j, nL) & kEntryPix));
           }
         }
         s = fe;
       }
       grid.sync();
-      // G3: the guarded fill, one warp-group per stalled frame
-      for (int fb = blockIdx.x * kGroupsPerBlock; fb < A.nF; fb += gridDim.x * kGroupsPerBlock) {
-        const int f = fb + group;
-        const bool valid = f < A.nF && S.dl[f];
-        const int p = valid ? A.best_p[f] : 0;
-        const int fs = valid ? f : 0;
+      // G3: the guarded fill, one warp per stalled frame
+      for (int fb = blockIdx.x * kWarps; fb < A.nF; fb += gridDim.x * kWarps) {
+        const int f = fb + warp;
+        const bool fvalid = f < A.nF && S.dl[f];
+        const bool valid = fvalid && lane < kGroup;
+        const int p = fvalid ? A.best_p[f] : 0;
+        const int fs = fvalid ? f : 0;
         double gx = 0.0, gy = 0.0;
-        if (valid) frame_guide(A, f, p, gx, gy);
-        WorkSource src{A.work + (size_t)fs * A.HW, A.c3 ? A.c3 + (size_t)fs * A.HW : nullptr,
-                       A.H, A.W, A.C, k};
+        if (fvalid) frame_guide(A, f, p, gx, gy);
+        float4* fw = A.work + (size_t)fs * A.HW;
+        WorkSource src{fw, A.c3 ? A.c3 + (size_t)fs * A.HW : nullptr, A.H, A.W, A.C, k};
         SampleResult r;
-        eval_item<NL>(P, S.tab, src, glane, valid, (double)(p % A.W), (double)(p / A.W), true, gx, gy, r);
-        if (valid && glane == 0) {
-          double v[4] = {r.v[0], r.v[1], r.v[2], r.v[3]};
-          bool ok = r.rw > 0.0;
-          if (!ok) {
-            // mean of readable 8-neighbours, engine.py:252-267
-            double acc[4] = {0.0, 0.0, 0.0, 0.0};
-            int n = 0;
-            const int i = p % A.W, j = p / A.W;
-            const int offs[8][2] = {{-1, -1}, {0, -1}, {1, -1}, {-1, 0},
-                                    {1, 0},   {-1, 1}, {0, 1},  {1, 1}};
-            for (int o = 0; o < 8; ++o) {
-              int ii = i + offs[o][0];
-              const int jj = j + offs[o][1];
-              if (A.periodic) ii = pos_mod(ii, A.W);
-              if (ii < 0 || ii >= A.W || jj < 0 || jj >= A.H) continue;
-              double cv[4];
-              if (src.load(jj * A.W + ii, cv)) {
-                for (int c = 0; c < 4; ++c) acc[c] += cv[c];
-                ++n;
-              }
-            }
-            if (n > 0) {
-              for (int c = 0; c < 4; ++c) v[c] = acc[c] / n;
-              ok = true;
+        eval_item<NL, 0>(P, S.tab, src, glane, valid, (double)(p % A.W), (double)(p / A.W), true,
+                         gx, gy, r);
+        double v[4] = {r.v[0], r.v[1], r.v[2], r.v[3]};
+        bool ok = r.rw > 0.0;
+        if (fvalid && lane == 0 && !ok) {
+          // mean of readable 8-neighbours, engine.py:252-267
+          double acc[4] = {0.0, 0.0, 0.0, 0.0};
+          int n = 0;
+          for (int o = 0; o < 8; ++o) {
+            bool in;
+            const int q = neighbor_of(A, (uint32_t)p, o, in);
+            double cv[4];
+            if (in && src.load(q, cv)) {
+              for (int c = 0; c < 4; ++c) acc[c] += cv[c];
+              ++n;
             }
           }
-          if (ok) {
+          if (n > 0) {
+            for (int c = 0; c < 4; ++c) v[c] = acc[c] / n;
+            ok = true;
+          }
+        }
+        ok = __shfl_sync(0xffffffffu, ok, 0);
+        if (fvalid && !ok && lane == 0) {
+          A.done[f] = 2;  // unfillable: engine.py:342-345
+          A.last_f[f] = frontier_size(A, cur, f);
+        }
+        if (fvalid && ok) {
+          if (kTracked) {
+            // every item re-entered the next list as a survivor: drop p, add
+            // its Inpaint neighbours, refresh the data-term flag
+            uint32_t* lst = nxt_list + (size_t)f * A.cap;
+            const int nL = A.cnt[nxt * A.nF + f], nR = A.cntR[nxt * A.nF + f];
+            int pos = -1;
+            for (int i = lane; i < nL + nR; i += 32) {
+              const int at = i < nL ? i : A.cap - 1 - (i - nL);
+              if ((lst[at] & kEntryPix) == (uint32_t)p) pos = i;
+            }
+            for (int o = 16; o > 0; o >>= 1) pos = max(pos, __shfl_xor_sync(0xffffffffu, pos, o));
+            __syncwarp();
+            if (lane == 0 && pos >= 0) {
+              if (pos < nL) {
+                lst[pos] = lst[nL - 1];
+                A.cnt[nxt * A.nF + f] = nL - 1;
+              } else {
+                const int rr = pos - nL;
+                lst[A.cap - 1 - rr] = lst[A.cap - 1 - (nR - 1)];
+                A.cntR[nxt * A.nF + f] = nR - 1;
+              }
+            }
+            __syncwarp();
+            if (lane < 8) {
+              bool in;
+              const int q = neighbor_of(A, (uint32_t)p, lane, in);
+              const uint32_t qe = in ? claim(fw, q) : 0xffffffffu;
+              if (qe != 0xffffffffu) {
+                append_direct(A, nxt_list, nxt, f, qe);
+                if (A.enter) A.enter[(size_t)f * A.HW + q] = k + 1;
+              }
+            }
+            __syncwarp();
+            if (A.order == 2 && A.g_mode == 2) {
+              const int mL = A.cnt[nxt * A.nF + f], mR = A.cntR[nxt * A.nF + f];
+              bool any = false;
+              for (int i = lane; i < mL + mR; i += 32) {
+                const int at = i < mL ? i : A.cap - 1 - (i - mL);
+                any |= (lst[at] & kEntryRot) != 0;
+              }
+              any = __any_sync(0xffffffffu, any);
+              if (lane == 0) A.anyg[nxt * A.nF + f] = any ? 1 : 0;
+            }
+          }
+          if (lane == 0) {
             float4 o;
             o.x = (float)v[0];
             o.y = (float)v[1];
@@ -584,69 +832,30 @@ __global__ void __launch_bounds__(kThreads) k_shells(const __grid_constant__ Fil
             if (A.c3) A.c3[(size_t)f * A.HW + p] = (float)v[3];
             A.fills[cur * A.nF + f] = 1;
             A.deadlocks[f] += 1;
-          } else {
-            A.done[f] = 2;  // unfillable: engine.py:342-345
-            A.last_f[f] = A.cnt[cur * A.nF + f];
           }
         }
       }
       grid.sync();
     }
 
-    // ---- B: frontier update
-    if (kTracked) {
-      for (int s = c_lo; s < c_hi;) {
-        const int f = find_frame(S.pref, A.nF, s);
-        const int fe = min(c_hi, S.pref[f + 1]);
-        const bool live = A.done[f] == 0;
-        float4* fw = A.work + (size_t)f * A.HW;
-        for (int base = s; base < fe; base += kThreads) {
-          const int t = base + threadIdx.x;
-          const bool valid = live && t < fe;
-          const uint32_t p = valid ? cur_list[(size_t)f * A.cap + (t - S.pref[f])] : 0u;
-          const int st = valid ? stamp_of(fw, (int)p) : 0;
-          const bool filled = valid && st == k + 1;
-          // survivor keeps its slot
-          push_append(S, valid && !filled, p);
-          const int i = (int)p % A.W, j = (int)p / A.W;
-#pragma unroll
-          for (int o = 0; o < 8; ++o) {
-            const int di = (o < 3) ? o - 1 : (o == 3 ? -1 : (o == 4 ? 1 : o - 6));
-            const int dj = (o < 3) ? -1 : (o < 5 ? 0 : 1);
-            bool want = false;
-            int q = 0;
-            if (filled) {
-              int ii = i + di;
-              const int jj = j + dj;
-              if (A.periodic) ii = pos_mod(ii, A.W);
-              if (ii >= 0 && ii < A.W && jj >= 0 && jj < A.H) {
-                q = jj * A.W + ii;
-                if (stamp_of(fw, q) == kStampInactive &&
-                    atomicCAS(stamp_ptr(fw, q), kStampInactive, kStampActive) == kStampInactive) {
-                  want = true;
-                  if (A.enter) A.enter[(size_t)f * A.HW + q] = k + 1;
-                }
-              }
-            }
-            push_append(S, want, (uint32_t)q);
-          }
-          flush_appends(A, S, f, nxt_list, nxt);
-        }
-        s = fe;
-      }
-    } else {
-      // untracked: rescan every pixel of every active frame (engine.py:357-360)
+    // ---- B: untracked frontier = full-lattice rescan (engine.py:357-360)
+    if (!kTracked) {
       int nA = 0;
       for (int f = 0; f < A.nF; ++f) nA += S.act[f] && A.done[f] == 0;
       const long long TP = (long long)nA * A.HW;
-      const long long pchunk = ((TP + gridDim.x - 1) / gridDim.x + kThreads - 1) / kThreads * kThreads;
+      const long long pchunk =
+          ((TP + gridDim.x - 1) / gridDim.x + kThreads - 1) / kThreads * kThreads;
       const long long p_lo = min(TP, (long long)blockIdx.x * pchunk), p_hi = min(TP, p_lo + pchunk);
+      int wn = 0;
       for (long long s = p_lo; s < p_hi;) {
         const int a = (int)(s / A.HW);
         int f = -1;
         for (int ff = 0, seen = 0; ff < A.nF; ++ff)
           if (S.act[ff] && A.done[ff] == 0) {
-            if (seen == a) { f = ff; break; }
+            if (seen == a) {
+              f = ff;
+              break;
+            }
             ++seen;
           }
         const long long fe = min(p_hi, (long long)(a + 1) * A.HW);
@@ -654,41 +863,33 @@ __global__ void __launch_bounds__(kThreads) k_shells(const __grid_constant__ Fil
         for (long long base = s; base < fe; base += kThreads) {
           const long long t = base + threadIdx.x;
           bool want = false;
-          int p = 0;
+          uint32_t e = 0;
           if (t < fe) {
-            p = (int)(t - (long long)a * A.HW);
+            const int p = (int)(t - (long long)a * A.HW);
             const int st = stamp_of(fw, p);
-            if (st == kStampInactive || st == kStampActive) {
-              const int i = p % A.W, j = p / A.W;
-              for (int dj = -1; dj <= 1 && !want; ++dj) {
-                const int jj = j + dj;
-                if (jj < 0 || jj >= A.H) continue;
-                for (int di = -1; di <= 1; ++di) {
-                  if (di == 0 && dj == 0) continue;
-                  int ii = i + di;
-                  if (A.periodic) ii = pos_mod(ii, A.W);
-                  else if (ii < 0 || ii >= A.W) continue;
-                  if (stamp_of(fw, jj * A.W + ii) <= k + 1) {
-                    want = true;
-                    break;
-                  }
-                }
+            if (stamp_unfilled(st)) {
+              for (int o = 0; o < 8 && !want; ++o) {
+                bool in;
+                const int q = neighbor_of(A, (uint32_t)p, o, in);
+                if (in && stamp_of(fw, q) <= k + 1) want = true;
               }
-              if (want && st == kStampInactive) {
-                *stamp_ptr(fw, p) = kStampActive;
+              if (want && (st & ~kRotBit) == kStampInactive) {
+                *stamp_ptr(fw, p) = st | 2;  // INACTIVE -> ACTIVE, rot bit kept
                 if (A.enter) A.enter[(size_t)f * A.HW + p] = k + 1;
               }
+              e = (uint32_t)p | ((st & kRotBit) ? kEntryRot : 0u);
             }
           }
-          push_append(S, want, (uint32_t)p);
-          flush_appends(A, S, f, nxt_list, nxt);
+          warp_push(reg, wn, want, e);
+          if (wn > kWarpAppCap - 32) warp_flush(A, reg, wn, f, nxt_list, nxt);
         }
+        warp_flush(A, reg, wn, f, nxt_list, nxt);
         s = fe;
       }
+      trace_max(A, k, 3);
+      grid.sync();
+      trace_set(A, k, 4, gtimer());
     }
-    trace_max(A, k, 3);
-    grid.sync();
-    trace_set(A, k, 4, gtimer());
   }
   // final bookkeeping: stats
   if (blockIdx.x == 0) {
@@ -762,6 +963,21 @@ size_t fill_workspace_bytes(int nF, int H, int W, int C, bool raster) {
   return layout_for(nF, H * W, C, raster).total;
 }
 
+// kernel specialised on the ball size: samples per lane = ceil(K / 8)
+template <bool kTracked>
+static const void* shell_kernel(const BallParams& P) {
+  if (P.plan.n_leaves > 1) return (const void*)k_shells<kMaxLeaves, 0, kTracked>;
+  switch ((P.K + kGroup - 1) / kGroup) {
+    case 1: return (const void*)k_shells<1, 1, kTracked>;
+    case 2: return (const void*)k_shells<1, 2, kTracked>;
+    case 4: return (const void*)k_shells<1, 4, kTracked>;
+    case 6: return (const void*)k_shells<1, 6, kTracked>;
+    case 10: return (const void*)k_shells<1, 10, kTracked>;
+    case 14: return (const void*)k_shells<1, 14, kTracked>;
+    default: return (const void*)k_shells<1, 0, kTracked>;
+  }
+}
+
 static int coop_grid(const void* fn, size_t smem, int* out_grid) {
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return GF_E_CUDA;
@@ -816,6 +1032,7 @@ int fill_launch(const gf_frames* fr, const gf_fill_params* prm, const gf_fill_ou
   A.conf = reinterpret_cast<double*>(base + L.conf);
   int* ints = reinterpret_cast<int*>(base + L.ints);
   A.cnt = ints;              ints += 2 * nF;
+  A.cntR = ints;             ints += 2 * nF;
   A.fills = ints;            ints += 2 * nF;
   A.anyg = ints;             ints += 2 * nF;
   A.remaining = ints;        ints += nF;
@@ -843,6 +1060,7 @@ int fill_launch(const gf_frames* fr, const gf_fill_params* prm, const gf_fill_ou
   A.gfx = prm->g_fixed[0];
   A.gfy = prm->g_fixed[1];
   A.periodic = prm->periodic_x;
+  A.split = P.plan.n_leaves == 1 ? 1 : 0;
   A.dtype = fr->dtype;
 
   // per-frame counters start at zero (the hull minimum is stored inverted
@@ -867,12 +1085,7 @@ int fill_launch(const gf_frames* fr, const gf_fill_params* prm, const gf_fill_ou
     return set_error(GF_E_CUDA, cudaGetErrorString(cudaGetLastError()));
 
   const size_t smem = sizeof(Smem);
-  const bool multi = P.plan.n_leaves > 1;
-  const void* fn;
-  if (prm->tracked)
-    fn = multi ? (const void*)k_shells<kMaxLeaves, true> : (const void*)k_shells<1, true>;
-  else
-    fn = multi ? (const void*)k_shells<kMaxLeaves, false> : (const void*)k_shells<1, false>;
+  const void* fn = prm->tracked ? shell_kernel<true>(P) : shell_kernel<false>(P);
   int grid = 0;
   int rc = coop_grid(fn, smem, &grid);
   if (rc != GF_OK) return rc;

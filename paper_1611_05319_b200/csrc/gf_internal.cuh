@@ -12,7 +12,7 @@
 namespace gf {
 
 constexpr int kMaxFramesPerLaunch = 1024;
-constexpr int kIntsPerFrame = 16;  // cnt[2] fills[2] anyg[2] + 10 scalars
+constexpr int kIntsPerFrame = 18;  // cnt[2] cntR[2] fills[2] anyg[2] + 10 scalars
 
 // Everything the fill kernels need, passed by value (__grid_constant__).
 struct FillArgs {
@@ -29,7 +29,8 @@ struct FillArgs {
   uint32_t* list0;
   uint32_t* list1;
   double* conf;
-  int* cnt;        // [2][nF] frontier sizes (ping-pong)
+  int* cnt;        // [2][nF] frontier list front part (lattice entries)
+  int* cntR;       // [2][nF] frontier list back part (rotated-ball entries)
   int* fills;      // [2][nF] pixels filled in the shell
   int* anyg;       // [2][nF] frontier holds a g != 0 pixel (data-term latch)
   int* remaining;  // [nF]
@@ -54,6 +55,7 @@ struct FillArgs {
   int g_mode;
   double gfx, gfy;
   int periodic;
+  int split;       // rotated-ball entries kept in the back part (K <= 128)
   // fused spline raster (guide.py:286-327), n_seg == 0 when off
   int n_seg;
   const double4* seg;

@@ -20,11 +20,22 @@ namespace gf {
 constexpr int kMaxK = 440;  // disk of radius 12, centre excluded
 constexpr int kGroup = 8;   // lanes per item
 
-// stamp encoding (int32, one per pixel): readable at shell k <=> stamp <= k
+// stamp encoding (int32, one per pixel): readable at shell k <=> stamp <= k.
+// Unfilled Inpaint pixels carry a marker whose bit 0 (kRotBit) records
+// g != 0 (the item takes the rotated-ball path), so frontier entries know
+// their path without reading the guide field.
 constexpr int kStampReadable = 0;
-constexpr int kStampInactive = 0x7ffffffd;  // Inpaint, not in the frontier
-constexpr int kStampActive = 0x7ffffffe;    // Inpaint, in the frontier
+constexpr int kRotBit = 1;
+constexpr int kStampInactive = 0x7ffffff8;  // Inpaint, not in the frontier (| kRotBit)
+constexpr int kStampActive = 0x7ffffffa;    // Inpaint, in the frontier (| kRotBit)
 constexpr int kStampBystander = 0x7fffffff;
+// frontier list entries: pixel index | kEntryRot when g != 0
+constexpr uint32_t kEntryRot = 0x80000000u;
+constexpr uint32_t kEntryPix = 0x7fffffffu;
+
+__host__ __device__ __forceinline__ bool stamp_unfilled(int st) {
+  return st >= kStampInactive && st < kStampBystander;
+}
 
 struct BallParams {
   int r, K;
@@ -53,11 +64,31 @@ struct SampleResult {
 
 // Working frame of the fill engine: float4 (c0, c1, c2, stamp bits) per
 // pixel plus an optional 4th channel plane.
+struct Px {
+  float4 v;  // c0, c1, c2, stamp bits (WorkSource) / c0..c2, unused (RawSource)
+  float c3;
+};
+
 struct WorkSource {
   const float4* work;  // frame base
   const float* c3;     // frame base or nullptr
   int H, W, C;
   int shell;
+  __device__ __forceinline__ Px fetch(int q) const {
+    Px r;
+    r.v = work[q];
+    r.c3 = c3 ? c3[q] : 0.f;
+    return r;
+  }
+  __device__ __forceinline__ bool readable(const Px& x) const {
+    return __float_as_int(x.v.w) <= shell;
+  }
+  __device__ __forceinline__ void accumulate(const Px& x, double wc, double* sv) const {
+    sv[0] += wc * (double)x.v.x;
+    sv[1] += wc * (double)x.v.y;
+    sv[2] += wc * (double)x.v.z;
+    sv[3] += wc * (double)x.c3;
+  }
   __device__ __forceinline__ bool load(int q, double* v) const {
     const float4 px = work[q];
     if (__float_as_int(px.w) > shell) return false;
@@ -74,6 +105,21 @@ struct RawSource {
   const double* img;
   const uint8_t* lab;
   int H, W, C;
+  struct RawPx {
+    double c[4];
+    bool ok;
+  };
+  __device__ __forceinline__ RawPx fetch(int q) const {
+    RawPx r;
+    r.ok = lab[q] == 0;
+    const double* p = img + (size_t)q * C;
+    for (int c = 0; c < 4; ++c) r.c[c] = c < C ? p[c] : 0.0;
+    return r;
+  }
+  __device__ __forceinline__ bool readable(const RawPx& x) const { return x.ok; }
+  __device__ __forceinline__ void accumulate(const RawPx& x, double wc, double* sv) const {
+    for (int c = 0; c < 4; ++c) sv[c] += wc * x.c[c];
+  }
   __device__ __forceinline__ bool load(int q, double* v) const {
     if (lab[q] != 0) return false;
     const double* p = img + (size_t)q * C;
@@ -159,12 +205,108 @@ __device__ __forceinline__ double min_prop(double a, double b) {
   return (a != a || b != b) ? (a + b) : fmin(a, b);
 }
 
+// Corner set of one ghost sample (grid.py:186-209): index of each corner to
+// fetch (-1: not live, nothing to read) and whether a live corner falls
+// outside the lattice (the sample is then unreadable).  No loads here, so
+// the fetches of all corners of all samples can be issued back to back.
+struct Corners {
+  int q[4];
+  double w[4];
+  bool outside;
+};
+
+__device__ __forceinline__ void ghost_corners(double X, double Y, int H, int W, int periodic,
+                                              Corners& c) {
+  const double fx0 = floor(X), fy0 = floor(Y);
+  const double tx = X - fx0, ty = Y - fy0;
+  const long long x0 = (long long)fx0, y0 = (long long)fy0;
+  const double wxs[2] = {1.0 - tx, tx};
+  const double wys[2] = {1.0 - ty, ty};
+  c.outside = false;
+#pragma unroll
+  for (int a = 0; a < 2; ++a) {
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      const int i = 2 * a + b;  // reference corner order (x0,y0),(x0,y0+1),(x0+1,y0),(x0+1,y0+1)
+      const double wc = wxs[a] * wys[b];
+      c.w[i] = wc;
+      c.q[i] = -1;
+      if (wc != 0.0) {
+        const long long cx = x0 + a, cy = y0 + b;
+        bool inside;
+        int col;
+        if (periodic) {
+          inside = (cy >= 0) && (cy < H);
+          col = pos_mod(cx, W);
+        } else {
+          inside = (cx >= 0) && (cx < W) && (cy >= 0) && (cy < H);
+          col = (int)cx;
+        }
+        if (inside) c.q[i] = (int)cy * W + col;
+        else c.outside = true;
+      }
+    }
+  }
+}
+
+// Lattice sample index for g = 0 at an integer centre: -1 when out of lattice.
+__device__ __forceinline__ int lattice_index(int x, int y, int H, int W, int periodic) {
+  if (y < 0 || y >= H) return -1;
+  if (periodic) x = pos_mod(x, W);
+  else if (x < 0 || x >= W) return -1;
+  return y * W + x;
+}
+
+// numpy pairwise accumulation of sample k (lane-local part)
+template <int NL>
+__device__ __forceinline__ void acc_sample(const BallParams& P, int k, double w, double wr,
+                                           double* acc_rw, double* acc_tw, double* tl_rw,
+                                           double* tl_tw) {
+#pragma unroll
+  for (int L = 0; L < NL; ++L) {
+    const int lo = NL == 1 ? 0 : P.plan.leaf_lo[L];
+    const int n = P.plan.leaf_n[L];
+    const int kk = k - lo;
+    if ((NL == 1 || (L < P.plan.n_leaves && kk >= 0)) && kk < n) {
+      if (kk < n - (n % 8)) {
+        acc_rw[L] += wr;
+        acc_tw[L] += w;
+      } else {
+        tl_rw[L] = wr;
+        tl_tw[L] = w;
+      }
+    }
+  }
+}
+
+// Weight of ball sample k for a g != 0 guide (engine.py:131-164); also
+// returns the rotated offset.
+__device__ __forceinline__ double sample_weight(const BallParams& P, const BallTables& T, int k,
+                                                double gx, double gy, double ux, double uy,
+                                                double safe, double thr, double& px, double& py) {
+  px = T.n[k];
+  py = T.m[k];
+  if (P.rotated) {
+    px = T.n[k] * uy + T.m[k] * ux;
+    py = (-T.n[k]) * ux + T.m[k] * uy;
+  }
+  const double dist = hypot_np(px, py);
+  if (P.mu_inf) {
+    const double d = ((-gy) * px + gx * py) / safe;
+    return (d * d <= thr) ? 1.0 / dist : 0.0;
+  }
+  const double d = (-gy) * px + gx * py;
+  return exp_np((P.coef * d) * d) / dist;
+}
+
 // Evaluate one item.  Must be called by all 32 lanes of the warp
 // (groups with valid == false compute on dummy data and never write).
-// NL = number of pairwise leaves the kernel was specialised for: 1 covers
-// K <= 128 (r <= 6); kMaxLeaves covers every supported radius.
+// NL  = pairwise leaves the kernel was specialised for (1 covers K <= 128);
+// KPL = samples per lane (ceil(K / 8)) as a compile-time bound so every
+//       fetch of a lane is issued before the first one is consumed, or 0
+//       for a runtime loop (large radii).
 // The result is valid in every lane of the group.
-template <int NL, class Src>
+template <int NL, int KPL, class Src>
 __device__ __forceinline__ void eval_item(const BallParams& P, const BallTables& T,
                                           const Src& src, int lane, bool valid, double fi,
                                           double fj, bool integral, double gx, double gy,
@@ -201,52 +343,95 @@ __device__ __forceinline__ void eval_item(const BallParams& P, const BallTables&
 #pragma unroll
   for (int L = 0; L < NL; ++L) acc_rw[L] = acc_tw[L] = tl_rw[L] = tl_tw[L] = 0.0;
   double num[4] = {0.0, 0.0, 0.0, 0.0};
-
   const int pi = (int)fi, pj = (int)fj;
-#pragma unroll 1
-  for (int k = lane; k < K; k += kGroup) {
-    double w;
-    double sv[4] = {0.0, 0.0, 0.0, 0.0};
-    bool ok;
-    if (gzero) {
-      w = T.w0[k];
-      ok = integral ? lattice_sample(src, pi + (int)T.n[k], pj + (int)T.m[k], P.periodic, sv)
-                    : ghost_sample(src, fi + T.n[k], fj + T.m[k], P.periodic, sv);
-    } else {
-      double px = T.n[k], py = T.m[k];
-      if (P.rotated) {
-        px = T.n[k] * uy + T.m[k] * ux;
-        py = (-T.n[k]) * ux + T.m[k] * uy;
-      }
-      const double dist = hypot_np(px, py);
-      if (P.mu_inf) {
-        const double d = ((-gy) * px + gx * py) / safe;
-        w = (d * d <= thr) ? 1.0 / dist : 0.0;
-      } else {
-        const double d = (-gy) * px + gx * py;
-        w = exp_np((P.coef * d) * d) / dist;
-      }
-      ok = ghost_sample(src, fi + px, fj + py, P.periodic, sv);
-    }
-    if (!valid) ok = false;
-    const double wr = ok ? w : 0.0;
-    if (ok) {
+
+  if (gzero && integral) {
+    // lattice path (most Inpaint pixels): weights are the host's
+    // 1/hypot(n, m); one fetch per sample, all issued up front
+    if constexpr (KPL > 0) {
+      int q[KPL];
+      decltype(src.fetch(0)) v[KPL];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) num[c] += wr * sv[c];
-    }
+      for (int t = 0; t < KPL; ++t) {
+        const int k = lane + kGroup * t;
+        q[t] = (valid && k < K)
+                   ? lattice_index(pi + (int)T.n[k], pj + (int)T.m[k], src.H, src.W, P.periodic)
+                   : -1;
+      }
 #pragma unroll
-    for (int L = 0; L < NL; ++L) {
-      const int lo = P.plan.leaf_lo[L], n = P.plan.leaf_n[L];
-      const int kk = k - lo;
-      if (L < P.plan.n_leaves && kk >= 0 && kk < n) {
-        if (kk < n - (n % 8)) {
-          acc_rw[L] += wr;
-          acc_tw[L] += w;
-        } else {
-          tl_rw[L] = wr;
-          tl_tw[L] = w;
+      for (int t = 0; t < KPL; ++t)
+        if (q[t] >= 0) v[t] = src.fetch(q[t]);
+#pragma unroll
+      for (int t = 0; t < KPL; ++t) {
+        const int k = lane + kGroup * t;
+        if (k < K) {
+          const double w = T.w0[k];
+          const bool ok = q[t] >= 0 && src.readable(v[t]);
+          const double wr = ok ? w : 0.0;
+          if (ok) {
+            double sv[4] = {0.0, 0.0, 0.0, 0.0};
+            src.accumulate(v[t], 1.0, sv);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) num[c] += wr * sv[c];
+          }
+          acc_sample<NL>(P, k, w, wr, acc_rw, acc_tw, tl_rw, tl_tw);
         }
       }
+    } else {
+#pragma unroll 1
+      for (int k = lane; k < K; k += kGroup) {
+        const int q = valid ? lattice_index(pi + (int)T.n[k], pj + (int)T.m[k], src.H, src.W,
+                                            P.periodic)
+                            : -1;
+        const double w = T.w0[k];
+        bool ok = false;
+        double sv[4] = {0.0, 0.0, 0.0, 0.0};
+        if (q >= 0) {
+          const auto v = src.fetch(q);
+          ok = src.readable(v);
+          if (ok) src.accumulate(v, 1.0, sv);
+        }
+        const double wr = ok ? w : 0.0;
+        if (ok) {
+#pragma unroll
+          for (int c = 0; c < 4; ++c) num[c] += wr * sv[c];
+        }
+        acc_sample<NL>(P, k, w, wr, acc_rw, acc_tw, tl_rw, tl_tw);
+      }
+    }
+  } else {
+    // ghost-pixel path: rotated ball at g, or g = 0 at a non-lattice point
+#pragma unroll 1
+    for (int k = lane; k < K; k += kGroup) {
+      double px, py, w;
+      if (gzero) {
+        px = T.n[k];
+        py = T.m[k];
+        w = T.w0[k];
+      } else {
+        w = sample_weight(P, T, k, gx, gy, ux, uy, safe, thr, px, py);
+      }
+      Corners cn;
+      ghost_corners(fi + px, fj + py, src.H, src.W, P.periodic, cn);
+      decltype(src.fetch(0)) v[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        if (valid && cn.q[c] >= 0) v[c] = src.fetch(cn.q[c]);
+      bool ok = valid && !cn.outside;
+      double sv[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        if (cn.q[c] >= 0 && valid) {
+          ok = ok && src.readable(v[c]);
+          src.accumulate(v[c], cn.w[c], sv);
+        }
+      }
+      const double wr = ok ? w : 0.0;
+      if (ok) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) num[c] += wr * sv[c];
+      }
+      acc_sample<NL>(P, k, w, wr, acc_rw, acc_tw, tl_rw, tl_tw);
     }
   }
 
@@ -316,6 +501,128 @@ __device__ __forceinline__ void eval_item(const BallParams& P, const BallTables&
     s += __shfl_xor_sync(0xffffffffu, s, 2, kGroup);
     s += __shfl_xor_sync(0xffffffffu, s, 4, kGroup);
     out.v[c] = (rw != 0.0) ? s / rw : 0.0;
+  }
+  out.rw = rw;
+  out.tw = tw;
+}
+
+// One item per warp (32 lanes) for the rotated-ball path, single pairwise
+// leaf (K <= 128).  Sample k lives in lane k % 32, slot k / 32, so a lane
+// evaluates ceil(K/32) samples instead of ceil(K/8): the long fp64 chains
+// (glibc hypot, SVML exp, two divisions) of a ghost sample run 4x wider.
+// numpy's accumulator j = a_j + a_{j+8} + ... is rebuilt exactly by lane j
+// pulling a_{j+8t} from lane (j + 8t) % 32, slot t / 4 (uniform across
+// lanes for a given t).  Result valid in every lane.
+template <int KPW, class Src>
+__device__ __forceinline__ void eval_item_warp(const BallParams& P, const BallTables& T,
+                                               const Src& src, int lane, bool valid, double fi,
+                                               double fj, double gx, double gy,
+                                               SampleResult& out) {
+  const int K = P.K;
+  const bool gzero = (gx == 0.0) && (gy == 0.0);
+  double ux = 0.0, uy = 1.0;
+  if (P.rotated && !gzero) {
+    const double nr = hypot_np(gx, gy);
+    ux = gx / nr;
+    uy = gy / nr;
+  }
+  double safe = 1.0, thr = 0.0;
+  if (P.mu_inf) {
+    const double nr2 = sqrt(gx * gx + gy * gy);
+    safe = (nr2 == 0.0) ? 1.0 : nr2;
+    double mloc = INFINITY;
+#pragma unroll
+    for (int s = 0; s < KPW; ++s) {
+      const int k = lane + 32 * s;
+      if (k < K) {
+        double px = T.n[k], py = T.m[k];
+        if (P.rotated && !gzero) {
+          px = T.n[k] * uy + T.m[k] * ux;
+          py = (-T.n[k]) * ux + T.m[k] * uy;
+        }
+        const double d = ((-gy) * px + gx * py) / safe;
+        mloc = min_prop(mloc, d * d);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mloc = min_prop(mloc, __shfl_xor_sync(0xffffffffu, mloc, o));
+    thr = mloc + P.tol_inf;
+  }
+  double w[KPW], wr[KPW];
+  double num[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+  for (int s = 0; s < KPW; ++s) {
+    const int k = lane + 32 * s;
+    w[s] = 0.0;
+    wr[s] = 0.0;
+    if (k < K) {
+      double px, py;
+      if (gzero) {
+        px = T.n[k];
+        py = T.m[k];
+        w[s] = T.w0[k];
+      } else {
+        w[s] = sample_weight(P, T, k, gx, gy, ux, uy, safe, thr, px, py);
+      }
+      Corners cn;
+      ghost_corners(fi + px, fj + py, src.H, src.W, P.periodic, cn);
+      decltype(src.fetch(0)) v[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        if (valid && cn.q[c] >= 0) v[c] = src.fetch(cn.q[c]);
+      bool ok = valid && !cn.outside;
+      double sv[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        if (valid && cn.q[c] >= 0) {
+          ok = ok && src.readable(v[c]);
+          src.accumulate(v[c], cn.w[c], sv);
+        }
+      }
+      wr[s] = ok ? w[s] : 0.0;
+      if (ok) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) num[c] += wr[s] * sv[c];
+      }
+    }
+  }
+  // accumulator j (lanes 0..7): a_j, a_{j+8}, ... in order
+  const int n = K, n8 = n - (n % 8);
+  double acc_rw = 0.0, acc_tw = 0.0;
+  for (int t = 0; t < n8 / 8; ++t) {
+    const int src_lane = (lane & 7) + 8 * (t & 3);
+    const int slot = t >> 2;
+    double a = 0.0, b = 0.0;
+#pragma unroll
+    for (int s = 0; s < KPW; ++s)
+      if (s == slot) {
+        a = wr[s];
+        b = w[s];
+      }
+    acc_rw += __shfl_sync(0xffffffffu, a, src_lane);
+    acc_tw += __shfl_sync(0xffffffffu, b, src_lane);
+  }
+  double rw = group_sum_tree(acc_rw);
+  double tw = group_sum_tree(acc_tw);
+  for (int e = n8; e < n; ++e) {
+    double a = 0.0, b = 0.0;
+#pragma unroll
+    for (int s = 0; s < KPW; ++s)
+      if (s == e / 32) {
+        a = wr[s];
+        b = w[s];
+      }
+    rw = rw + __shfl_sync(0xffffffffu, a, e % 32);
+    tw = tw + __shfl_sync(0xffffffffu, b, e % 32);
+  }
+  rw = __shfl_sync(0xffffffffu, rw, 0);
+  tw = __shfl_sync(0xffffffffu, tw, 0);
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    double sacc = num[c];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, o);
+    out.v[c] = (rw != 0.0) ? sacc / rw : 0.0;
   }
   out.rw = rw;
   out.tw = tw;
