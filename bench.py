@@ -237,7 +237,14 @@ def run_ours(args):
     # per-shell phase trace of one (untimed) step: fill phase, barrier, update
     res = step(trace_cap=256)
     torch.cuda.synchronize()
-    tr = res["trace"].cpu().numpy()[:n_shells]
+    trace_all = res["trace"].cpu().numpy()
+    tl = trace_all[-1].astype(np.uint64)
+    t_start = [int(~np.uint64(tl[2 * i])) for i in range(3)]
+    t_end = [int(tl[2 * i + 1]) for i in range(3)]
+    timeline = {name: {"start_us": (t_start[i] - t_start[0]) / 1e3,
+                       "end_us": (t_end[i] - t_start[0]) / 1e3}
+                for i, name in enumerate(["prep", "shells", "finalize"])}
+    tr = trace_all[:n_shells]
     shell_trace = []
     for r in tr:
         row = {"items": int(r[5]), "fill_us": (r[1] - r[0]) / 1e3,
@@ -328,6 +335,7 @@ def run_ours(args):
             "ms_per_frame": t_step,
             "ms_step_min": min(step_ms),
             "ms_step_max": max(step_ms),
+            "timeline": timeline,
             "shell_trace": shell_trace,
             "l2": "flushed between steps (256 MB write + 256 MB read, untimed)",
             "parallelism": f"frame-parallel x{ws}",

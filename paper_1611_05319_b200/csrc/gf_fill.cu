@@ -58,21 +58,42 @@ __device__ __forceinline__ int* stamp_ptr(float4* work, int q) {
 
 // ---------------------------------------------------------------- prep
 //
-// One pass over every pixel, frame-major grid (blockIdx.y = frame): builds
-// the working frame (fp32 colour + stamp), the initial frontier (Inpaint
-// with a Readable 8-neighbour, grid.py:104-106), |D|, the value hull
-// (min/max of the readable values over all channels, engine.py:291-296)
-// and, when splines are given, the guide field g of every Inpaint pixel
-// (guide.py:303-327) -- rastered in place, so the field never exists as a
-// dense array.  Segments are culled per 256-pixel tile against the tile's
-// bounding box inflated by 3 eta: a pixel's g is non-zero only if its
-// nearest segment lies within 3 eta, and then that segment (and every tied
-// one) survives the cull, so non-zero g values are bit-identical to the
-// dense rasteriser; pixels with no candidate get g = +0 (the reference's
-// +-0 there is indistinguishable to the fill: every use tests g == 0 or
-// |g|).
+// One pass over every pixel in 32x32 tiles, frame-major grid
+// (blockIdx.y = frame).  Labels of the tile plus an (r+1)-pixel halo are
+// staged in shared memory; from them the block derives
+//   * which pixels can ever be read by the shell loop -- those within
+//     Chebyshev distance r+1 of an Inpaint pixel (a ball sample lies within
+//     r of its centre, its bilinear corners within r+1), found with a
+//     ballot bitmask dilation -- only these get a working-buffer entry;
+//   * the initial frontier (Inpaint with a Readable 8-neighbour,
+//     grid.py:104-106), |D|, the value hull (engine.py:291-296);
+//   * the guide field g of every Inpaint pixel (guide.py:303-327), rastered
+//     in place from the splines when given -- segments are culled against
+//     the tile's box inflated by 3 eta; a non-zero g needs its nearest
+//     segment within 3 eta, which then survives the cull, so non-zero g
+//     are bit-identical to the dense rasteriser (pixels with no candidate
+//     get +0; the reference's -0 there is indistinguishable to the fill).
+// Readable pixels are copied straight to the output: the final hull clip
+// (engine.py:372-375) is the identity on them.  k_finalize writes the rest.
+
+__device__ __forceinline__ unsigned long long gtimer0() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// pipeline timeline in the last trace row: slots 2i = ~start (max of ~t =
+// earliest start), 2i+1 = latest end; i = 0 prep, 1 shell loop, 2 finalize
+__device__ __forceinline__ void timeline_mark(const FillArgs& A, int stage, bool start) {
+  if (!A.trace || A.trace_cap < 2 || threadIdx.x != 0) return;
+  unsigned long long* row = A.trace + (size_t)(A.trace_cap - 1) * 8;
+  const unsigned long long t = gtimer0();
+  atomicMax(&row[2 * stage + (start ? 0 : 1)], start ? ~t : t);
+}
 
 constexpr int kMaxCand = 512;
+constexpr int kTile = 32;
+constexpr int kMaxHalo = GF_MAX_RADIUS + 1;
+constexpr int kTileExt = kTile + 2 * kMaxHalo;  // 58 <= 64: one 64-bit row mask
 
 __device__ __forceinline__ double seg_dist(double px, double py, const double4 s) {
   const double ax = s.x, ay = s.y, bx = s.z, by = s.w;
@@ -85,169 +106,356 @@ __device__ __forceinline__ double seg_dist(double px, double py, const double4 s
   return hypot_np(px - (ax + t * abx), py - (ay + t * aby));
 }
 
-template <typename T>
-__global__ void __launch_bounds__(kThreads) k_prep(const __grid_constant__ FillArgs A) {
+// Streaming pass over every pixel: Readable pixels are copied to the
+// output (the final hull clip is the identity on them, engine.py:372-375),
+// the value hull of the Readable values is reduced (engine.py:291-296), and
+// every 32x32 tile holding an Inpaint pixel is flagged for k_prep.  Four
+// consecutive pixels per thread; 16-byte loads/stores when the row pitch
+// allows (then non-Readable pixels get their input too; k_finalize
+// overwrites them).
+template <typename T, int C>
+__global__ void __launch_bounds__(kThreads) k_copy(const __grid_constant__ FillArgs A) {
   const int f = blockIdx.y;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  __shared__ int s_cand[kMaxCand];
-  __shared__ int s_ncand;
   __shared__ unsigned long long s_red[2][kThreads / 32];
-  __shared__ int s_cnt[kThreads / 32];
   const uint8_t* lab = A.labels + (size_t)f * A.HW;
-  const T* img = reinterpret_cast<const T*>(A.image) + (size_t)f * A.HW * A.C;
-  float4* work = A.work + (size_t)f * A.HW;
-  unsigned long long emin_inv = 0ULL, emax = 0ULL;  // max(~enc) <=> min(enc)
-  int n_inp = 0;
-  bool anyg = false;
-  const bool raster = A.n_seg > 0;
-  for (int base = blockIdx.x * kThreads; base < A.HW; base += gridDim.x * kThreads) {
-    const int p = base + threadIdx.x;
-    const bool in = p < A.HW;
-    if (raster) {
-      // tile bounding box -> candidate segments (order-free: the fused
-      // raster takes the lexicographic min of (distance, spline index))
-      const int last = min(A.HW - 1, base + kThreads - 1);
-      const int j0 = base / A.W, j1 = last / A.W;
-      const double x0 = (j0 == j1) ? (double)(base % A.W) : 0.0;
-      const double x1 = (j0 == j1) ? (double)(last % A.W) : (double)(A.W - 1);
-      if (threadIdx.x == 0) s_ncand = 0;
-      __syncthreads();
-      for (int i = threadIdx.x; i < A.n_seg; i += kThreads) {
-        const double4 sg = A.seg[i];
-        const double lo_x = fmin(sg.x, sg.z) - A.cut, hi_x = fmax(sg.x, sg.z) + A.cut;
-        const double lo_y = fmin(sg.y, sg.w) - A.cut, hi_y = fmax(sg.y, sg.w) + A.cut;
-        if (hi_x >= x0 && lo_x <= x1 && hi_y >= (double)j0 && lo_y <= (double)j1) {
-          const int slot = atomicAdd(&s_ncand, 1);
-          if (slot < kMaxCand) s_cand[slot] = i;
+  const T* img = reinterpret_cast<const T*>(A.image) + (size_t)f * A.HW * C;
+  T* out = reinterpret_cast<T*>(A.out) + (size_t)f * A.HW * C;
+  int* dtile = A.dtile + (size_t)f * A.ntiles;
+  const int tiles_x = (A.W + kTile - 1) / kTile;
+  constexpr int nv = (4 * C * (int)sizeof(T)) / 16;
+  constexpr bool vec_ok = (4 * C * (int)sizeof(T)) % 16 == 0;
+  const bool vec = vec_ok && (A.W % 4 == 0);
+  timeline_mark(A, 0, true);
+  T vlo = T(INFINITY), vhi = T(-INFINITY);
+  const int units = (A.HW + 3) / 4;
+  for (int u = blockIdx.x * kThreads + threadIdx.x; u < units; u += gridDim.x * kThreads) {
+    const int p0 = 4 * u;
+    if (vec) {
+      const uchar4 l4 = *reinterpret_cast<const uchar4*>(lab + p0);
+      const uint8_t l[4] = {l4.x, l4.y, l4.z, l4.w};
+      union {
+        T t[4 * C];
+        uint4 q[nv > 0 ? nv : 1];
+      } v;
+      const uint4* src = reinterpret_cast<const uint4*>(img + (size_t)p0 * C);
+#pragma unroll
+      for (int i = 0; i < nv; ++i) v.q[i] = __ldg(src + i);
+      uint4* dst = reinterpret_cast<uint4*>(out + (size_t)p0 * C);
+#pragma unroll
+      for (int i = 0; i < nv; ++i) dst[i] = v.q[i];
+      bool inp = false;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        inp |= l[q] == 255;
+        if (l[q] == 0) {
+#pragma unroll
+          for (int ch = 0; ch < C; ++ch) {
+            const T x = v.t[q * C + ch];
+            vlo = x < vlo ? x : vlo;
+            vhi = x > vhi ? x : vhi;
+          }
         }
       }
-      __syncthreads();
-    }
-    bool active = false, rot = false;
-    if (in) {
-      const uint8_t l = lab[p];
-      const T* px_in = img + (size_t)p * A.C;
-      float4 px;
-      px.x = (float)px_in[0];
-      px.y = A.C > 1 ? (float)px_in[1] : 0.f;
-      px.z = A.C > 2 ? (float)px_in[2] : 0.f;
-      if (A.C > 3) A.c3[(size_t)f * A.HW + p] = (float)px_in[3];
-      int st;
-      if (l == 0) {
-        st = kStampReadable;
-        for (int c = 0; c < A.C; ++c) {
-          const unsigned long long e = enc_ordered((double)px_in[c]);
-          emin_inv = (~e > emin_inv) ? ~e : emin_inv;
-          emax = (e > emax) ? e : emax;
+      if (inp) dtile[((p0 / A.W) / kTile) * tiles_x + (p0 % A.W) / kTile] = 1;
+      if (A.enter) *reinterpret_cast<int4*>(A.enter + (size_t)f * A.HW + p0) = make_int4(-1, -1, -1, -1);
+    } else {
+      for (int q = 0; q < 4; ++q) {
+        const int p = p0 + q;
+        if (p >= A.HW) break;
+        const uint8_t l = lab[p];
+        if (A.enter) A.enter[(size_t)f * A.HW + p] = -1;
+        if (l == 255) dtile[((p / A.W) / kTile) * tiles_x + (p % A.W) / kTile] = 1;
+        if (l != 0) continue;
+#pragma unroll
+        for (int ch = 0; ch < C; ++ch) {
+          const T x = img[(size_t)p * C + ch];
+          out[(size_t)p * C + ch] = x;
+          vlo = x < vlo ? x : vlo;
+          vhi = x > vhi ? x : vhi;
         }
-      } else if (l == 255) {
-        ++n_inp;
-        const int i = p % A.W, j = p / A.W;
-        for (int dj = -1; dj <= 1 && !active; ++dj) {
-          const int jj = j + dj;
-          if (jj < 0 || jj >= A.H) continue;
-          for (int di = -1; di <= 1; ++di) {
-            if (di == 0 && dj == 0) continue;
-            int ii = i + di;
-            if (A.periodic) ii = (ii + A.W) % A.W;
-            else if (ii < 0 || ii >= A.W) continue;
-            if (lab[jj * A.W + ii] == 0) {
-              active = true;
-              break;
-            }
-          }
-        }
-        double gx = 0.0, gy = 0.0;
-        if (raster) {
-          const bool exhaustive = s_ncand > kMaxCand;
-          const int n_eval = exhaustive ? A.n_seg : s_ncand;
-          double dmin = INFINITY;
-          int near = 0x7fffffff;
-          const double fx = (double)i, fy = (double)j;
-          for (int c = 0; c < n_eval; ++c) {
-            const int sidx = exhaustive ? c : s_cand[c];
-            const double d = seg_dist(fx, fy, A.seg[sidx]);
-            const int sp = A.seg_spline[sidx];
-            if (d < dmin || (d == dmin && sp < near)) {
-              dmin = d;
-              near = sp;
-            }
-          }
-          if (dmin <= A.cut) {
-            const double fall = exp_np((-(dmin * dmin)) / A.c2eta);
-            const double2 dir = A.dirs[near];
-            gx = dir.x * fall;
-            gy = dir.y * fall;
-          }
-          reinterpret_cast<double2*>(A.gfield)[(size_t)f * A.HW + p] = make_double2(gx, gy);
-        } else if (A.g_mode == 2) {
-          const double2 g = reinterpret_cast<const double2*>(A.gsrc)[(size_t)f * A.HW + p];
-          gx = g.x;
-          gy = g.y;
-        } else if (A.g_mode == 1) {
-          gx = A.gfx;
-          gy = A.gfy;
-        }
-        rot = (gx != 0.0 || gy != 0.0);
-        st = (active ? kStampActive : kStampInactive) | (rot ? kRotBit : 0);
-        if (active && rot) anyg = true;
-      } else {
-        st = kStampBystander;
       }
-      px.w = __int_as_float(st);
-      work[p] = px;
-      if (A.enter) A.enter[(size_t)f * A.HW + p] = active ? 0 : -1;
     }
-    // warp-aggregated append of the initial frontier: lattice entries to the
-    // front of the list, rotated-ball entries to the back (when split)
-    const bool back = active && rot && A.split;
-    const unsigned mL = __ballot_sync(0xffffffffu, active && !back);
-    const unsigned mR = __ballot_sync(0xffffffffu, back);
-    const unsigned lt = (1u << lane) - 1;
-    int bL = 0, bR = 0;
-    if (lane == 0) {
-      if (mL) bL = atomicAdd(&A.cnt[f], __popc(mL));
-      if (mR) bR = atomicAdd(&A.cntR[f], __popc(mR));
-    }
-    bL = __shfl_sync(0xffffffffu, bL, 0);
-    bR = __shfl_sync(0xffffffffu, bR, 0);
-    const uint32_t e0 = (uint32_t)p | (rot ? kEntryRot : 0u);
-    if (back) A.list0[(size_t)f * A.cap + A.cap - 1 - (bR + __popc(mR & lt))] = e0;
-    else if (active) A.list0[(size_t)f * A.cap + bL + __popc(mL & lt)] = e0;
-    if (raster) __syncthreads();  // s_cand is rebuilt for the next tile
   }
-  // block reductions: hull, |D|, data-term flag -> one atomic each per block
+  unsigned long long emin_inv = 0ULL, emax = 0ULL;  // max(~enc) <=> min(enc)
+  if (vlo <= vhi) {
+    emin_inv = ~enc_ordered((double)vlo);
+    emax = enc_ordered((double)vhi);
+  }
   for (int o = 16; o > 0; o >>= 1) {
     const unsigned long long a = __shfl_xor_sync(0xffffffffu, emin_inv, o);
     const unsigned long long b = __shfl_xor_sync(0xffffffffu, emax, o);
     emin_inv = a > emin_inv ? a : emin_inv;
     emax = b > emax ? b : emax;
-    n_inp += __shfl_xor_sync(0xffffffffu, n_inp, o);
   }
-  const bool blk_anyg = __syncthreads_or(anyg);
   if (lane == 0) {
     s_red[0][warp] = emin_inv;
     s_red[1][warp] = emax;
-    s_cnt[warp] = n_inp;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    int tot = 0;
     for (int w = 0; w < kThreads / 32; ++w) {
       emin_inv = s_red[0][w] > emin_inv ? s_red[0][w] : emin_inv;
       emax = s_red[1][w] > emax ? s_red[1][w] : emax;
-      tot += s_cnt[w];
     }
+    // most blocks cannot move the frame's hull any more: skip their atomics
     if (emax != 0ULL) {
-      atomicMax(&A.hull[2 * f], emin_inv);
-      atomicMax(&A.hull[2 * f + 1], emax);
+      if (emin_inv > *(volatile unsigned long long*)&A.hull[2 * f]) atomicMax(&A.hull[2 * f], emin_inv);
+      if (emax > *(volatile unsigned long long*)&A.hull[2 * f + 1]) atomicMax(&A.hull[2 * f + 1], emax);
     }
+  }
+  timeline_mark(A, 0, false);
+}
+
+template <typename T, int C>
+__global__ void __launch_bounds__(kThreads) k_prep(const __grid_constant__ FillArgs A) {
+  const int f = blockIdx.y;
+  const int tiles_x = (A.W + kTile - 1) / kTile;
+  const int tiles_y = (A.H + kTile - 1) / kTile;
+  const int tix = (int)(blockIdx.x % tiles_x), tiy = (int)(blockIdx.x / tiles_x);
+  const int tx0 = tix * kTile;
+  const int ty0 = tiy * kTile;
+  // only tiles within one tile of an Inpaint pixel (r + 1 <= 13 < 32) work
+  {
+    const int* dtile = A.dtile + (size_t)f * A.ntiles;
+    bool any = false;
+    for (int dy = -1; dy <= 1; ++dy) {
+      const int ty = tiy + dy;
+      if (ty < 0 || ty >= tiles_y) continue;
+      for (int dx = -1; dx <= 1; ++dx) {
+        int tx = tix + dx;
+        if (A.periodic) tx = (tx + tiles_x) % tiles_x;
+        else if (tx < 0 || tx >= tiles_x) continue;
+        any |= dtile[ty * tiles_x + tx] != 0;
+      }
+    }
+    if (!any) return;
+  }
+  const int R = A.halo;
+  const int ext = kTile + 2 * R;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __shared__ uint8_t s_lab[kTileExt][kTileExt + 6];
+  __shared__ unsigned int s_hrow[kTileExt];
+  __shared__ unsigned long long s_hrow64[kTileExt];
+  __shared__ unsigned long long s_rrow64[kTileExt];
+  __shared__ int s_cand[kMaxCand];
+  __shared__ int s_ncand;
+  __shared__ int s_cnt[kThreads / 32];
+  __shared__ int s_wl[kThreads / 32], s_wr[kThreads / 32];
+  __shared__ int s_bL, s_bR;
+  const uint8_t* lab = A.labels + (size_t)f * A.HW;
+  const T* img = reinterpret_cast<const T*>(A.image) + (size_t)f * A.HW * C;
+  float4* work = A.work + (size_t)f * A.HW;
+  const bool raster = A.n_seg > 0;
+  const int ry = threadIdx.x >> 3;
+  const int c0 = (threadIdx.x & 7) * 4;
+  const int gy = ty0 + ry;
+
+  // 1. labels of the tile + halo, one warp per halo row (out of lattice ->
+  //    128: neither readable nor Inpaint; x wraps when periodic), with the
+  //    row's Inpaint bitmask from two ballots
+  if (threadIdx.x == 0) s_ncand = 0;
+  bool any_inp = false;
+  constexpr int kRowsPerWarp = (kTileExt + kThreads / 32 - 1) / (kThreads / 32);
+  uint8_t l2[kRowsPerWarp][2];
+  // every label load of the warp is issued before the first one is used
+#pragma unroll
+  for (int i = 0; i < kRowsPerWarp; ++i) {
+    const int y = warp + i * (kThreads / 32);
+    const int gyy = ty0 - R + y;
+    const bool row_in = y < ext && gyy >= 0 && gyy < A.H;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int x = lane + 32 * h;
+      int gxx = tx0 - R + x;
+      if (A.periodic) gxx = gxx < 0 ? gxx + A.W : (gxx >= A.W ? gxx - A.W : gxx);
+      const bool in = x < ext && row_in && gxx >= 0 && gxx < A.W;
+      l2[i][h] = in ? __ldg(lab + gyy * A.W + gxx) : (uint8_t)128;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < kRowsPerWarp; ++i) {
+    const int y = warp + i * (kThreads / 32);
+    if (y < ext) {
+      if (lane < ext) s_lab[y][lane] = l2[i][0];
+      if (lane + 32 < ext) s_lab[y][lane + 32] = l2[i][1];
+    }
+    const unsigned lo = __ballot_sync(0xffffffffu, y < ext && l2[i][0] == 255);
+    const unsigned hi = __ballot_sync(0xffffffffu, y < ext && l2[i][1] == 255);
+    const unsigned rlo = __ballot_sync(0xffffffffu, y < ext && l2[i][0] == 0);
+    const unsigned rhi = __ballot_sync(0xffffffffu, y < ext && l2[i][1] == 0);
+    any_inp |= (lo | hi) != 0;
+    if (lane == 0 && y < ext) {
+      s_hrow64[y] = ((unsigned long long)hi << 32) | lo;
+      s_rrow64[y] = ((unsigned long long)rhi << 32) | rlo;
+    }
+  }
+  // a tile with no Inpaint pixel in reach only copies its Readable pixels
+  const bool tile_d = __syncthreads_or(any_inp);
+  if (tile_d && raster) {
+    const double x0 = (double)tx0, x1 = (double)min(A.W - 1, tx0 + kTile - 1);
+    const double y0 = (double)ty0, y1 = (double)min(A.H - 1, ty0 + kTile - 1);
+    for (int i = threadIdx.x; i < A.n_seg; i += kThreads) {
+      const double4 sg = A.seg[i];
+      const double lo_x = fmin(sg.x, sg.z) - A.cut, hi_x = fmax(sg.x, sg.z) + A.cut;
+      const double lo_y = fmin(sg.y, sg.w) - A.cut, hi_y = fmax(sg.y, sg.w) + A.cut;
+      if (hi_x >= x0 && lo_x <= x1 && hi_y >= y0 && lo_y <= y1) {
+        const int slot = atomicAdd(&s_ncand, 1);
+        if (slot < kMaxCand) s_cand[slot] = i;
+      }
+    }
+  }
+  // 2. horizontal dilation of the Inpaint indicator: bit c of s_hrow[y] <=>
+  //    an Inpaint pixel in ext columns [c, c + 2R]
+  if (tile_d) {
+    for (int y = threadIdx.x; y < ext; y += kThreads) {
+      const unsigned long long m = s_hrow64[y];
+      unsigned long long h = m;
+      int w = 1;  // h covers a window of w columns
+      while (2 * w <= 2 * R + 1) {
+        h |= h >> w;
+        w *= 2;
+      }
+      if (w < 2 * R + 1) h |= h >> (2 * R + 1 - w);
+      s_hrow[y] = (unsigned int)h;
+    }
+  }
+  __syncthreads();
+
+  // 3. four consecutive pixels per thread: row ry, columns c0 .. c0+3
+  unsigned int vmask = 0;
+  if (tile_d)
+    for (int dy = 0; dy <= 2 * R; ++dy) vmask |= s_hrow[ry + dy];
+  int n_inp = 0;
+  bool anyg = false;
+  uint32_t ent[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int c = c0 + u;
+    const int gx = tx0 + c;
+    const bool in = gy < A.H && gx < A.W;
+    const int p = gy * A.W + gx;
+    const uint8_t l = s_lab[ry + R][c + R];
+    const bool near = (vmask >> c) & 1u;
+    bool active = false, rot = false;
+    if (in) {
+      if (l == 0) {
+        if (near) {
+          T cv[4] = {T(0), T(0), T(0), T(0)};
+#pragma unroll
+          for (int ch = 0; ch < C; ++ch) cv[ch] = __ldg(img + (size_t)p * C + ch);
+          work[p] = make_float4((float)cv[0], (float)cv[1], (float)cv[2],
+                                __int_as_float(kStampReadable));
+          if (C > 3) A.c3[(size_t)f * A.HW + p] = (float)cv[3];
+        }
+      } else if (l == 255) {
+        ++n_inp;
+        // a Readable 8-neighbour (the pixel itself is not Readable): the
+        // three ext columns c+R-1 .. c+R+1 of the rows above, at and below
+        const unsigned long long nb = s_rrow64[ry + R - 1] | s_rrow64[ry + R] | s_rrow64[ry + R + 1];
+        active = ((nb >> (c + R - 1)) & 7ull) != 0;
+        double gxv = 0.0, gyv = 0.0;
+        if (raster) {
+          const bool exhaustive = s_ncand > kMaxCand;
+          const int n_eval = exhaustive ? A.n_seg : s_ncand;
+          double dmin = INFINITY;
+          int nearest = 0x7fffffff;
+          const double fx = (double)gx, fy = (double)gy;
+          for (int cc = 0; cc < n_eval; ++cc) {
+            const int sidx = exhaustive ? cc : s_cand[cc];
+            const double d = seg_dist(fx, fy, A.seg[sidx]);
+            const int sp = A.seg_spline[sidx];
+            if (d < dmin || (d == dmin && sp < nearest)) {
+              dmin = d;
+              nearest = sp;
+            }
+          }
+          if (dmin <= A.cut) {
+            const double fall = exp_np((-(dmin * dmin)) / A.c2eta);
+            const double2 dir = A.dirs[nearest];
+            gxv = dir.x * fall;
+            gyv = dir.y * fall;
+          }
+          reinterpret_cast<double2*>(A.gfield)[(size_t)f * A.HW + p] = make_double2(gxv, gyv);
+        } else if (A.g_mode == 2) {
+          const double2 g = reinterpret_cast<const double2*>(A.gsrc)[(size_t)f * A.HW + p];
+          gxv = g.x;
+          gyv = g.y;
+        } else if (A.g_mode == 1) {
+          gxv = A.gfx;
+          gyv = A.gfy;
+        }
+        rot = (gxv != 0.0 || gyv != 0.0);
+        if (active && rot) anyg = true;
+        const int st = (active ? kStampActive : kStampInactive) | (rot ? kRotBit : 0);
+        work[p] = make_float4(0.f, 0.f, 0.f, __int_as_float(st));
+      } else if (near) {
+        work[p] = make_float4(0.f, 0.f, 0.f, __int_as_float(kStampBystander));
+      }
+      if (A.enter) A.enter[(size_t)f * A.HW + p] = active ? 0 : -1;
+    }
+    // initial frontier entry of this pixel (published per block below)
+    ent[u] = active ? ((uint32_t)p | (rot ? kEntryRot : 0u)) : 0xffffffffu;
+  }
+  // block-aggregated append of the initial frontier: lattice entries to the
+  // front of the list, rotated-ball entries to the back (when split); one
+  // atomic per part per block
+  {
+    const unsigned lt = (1u << lane) - 1;
+    int wL = 0, wR = 0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const bool act = ent[u] != 0xffffffffu;
+      const bool back = act && (ent[u] & kEntryRot) && A.split;
+      wL += __popc(__ballot_sync(0xffffffffu, act && !back));
+      wR += __popc(__ballot_sync(0xffffffffu, back));
+    }
+    if (lane == 0) {
+      s_wl[warp] = wL;
+      s_wr[warp] = wR;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int tL = 0, tR = 0;
+      for (int w = 0; w < kThreads / 32; ++w) {
+        const int a = s_wl[w], b = s_wr[w];
+        s_wl[w] = tL;
+        s_wr[w] = tR;
+        tL += a;
+        tR += b;
+      }
+      s_bL = tL > 0 ? atomicAdd(&A.cnt[f], tL) : 0;
+      s_bR = tR > 0 ? atomicAdd(&A.cntR[f], tR) : 0;
+    }
+    __syncthreads();
+    int bL = s_bL + s_wl[warp], bR = s_bR + s_wr[warp];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const bool act = ent[u] != 0xffffffffu;
+      const bool back = act && (ent[u] & kEntryRot) && A.split;
+      const unsigned mL = __ballot_sync(0xffffffffu, act && !back);
+      const unsigned mR = __ballot_sync(0xffffffffu, back);
+      if (back) A.list0[(size_t)f * A.cap + A.cap - 1 - (bR + __popc(mR & lt))] = ent[u];
+      else if (act) A.list0[(size_t)f * A.cap + bL + __popc(mL & lt)] = ent[u];
+      bL += __popc(mL);
+      bR += __popc(mR);
+    }
+  }
+  // block reductions: |D| and the data-term flag -> one atomic each per block
+  for (int o = 16; o > 0; o >>= 1) n_inp += __shfl_xor_sync(0xffffffffu, n_inp, o);
+  const bool blk_anyg = __syncthreads_or(anyg);
+  if (lane == 0) s_cnt[warp] = n_inp;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int tot = 0;
+    for (int w = 0; w < kThreads / 32; ++w) tot += s_cnt[w];
     if (tot) {
       atomicAdd(&A.remaining[f], tot);
       atomicAdd(&A.inpaint[f], tot);
     }
     if (blk_anyg) A.anyg[f] = 1;
   }
+  timeline_mark(A, 0, false);
 }
 
 // ------------------------------------------------------- shell loop
@@ -271,6 +479,9 @@ struct Smem {
   unsigned long long redk[kThreads / 32];
   int any_dl;
   int total, totalL, totalR;
+  // block-level flush of the warps' staged appends
+  int bf_frame[kThreads / 32], bf_nL[kThreads / 32], bf_nR[kThreads / 32];
+  int bf_fill[kThreads / 32], bf_anyg[kThreads / 32], bf_bL[kThreads / 32], bf_bR[kThreads / 32];
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -383,27 +594,26 @@ __device__ __forceinline__ void warp_push(uint32_t* reg, int& n, bool want, uint
   n += __popc(m);
 }
 
-__device__ __forceinline__ void warp_flush(const FillArgs& A, uint32_t* reg, int& n, int f,
-                                           uint32_t* nxt_list, int nxt) {
-  if (n == 0) return;
-  __syncwarp();
+// staged entries of one warp: how many go to the back part, any g != 0
+__device__ __forceinline__ void warp_count(const FillArgs& A, const uint32_t* reg, int n, int& nR,
+                                           bool& anyg) {
   const int lane = threadIdx.x & 31;
-  const unsigned lt = (1u << lane) - 1;
-  int nR = 0;
-  bool anyg = false;
+  nR = 0;
+  anyg = false;
   for (int c0 = 0; c0 < n; c0 += 32) {
     const bool in = c0 + lane < n;
     const uint32_t e = in ? reg[c0 + lane] : 0u;
     nR += __popc(__ballot_sync(0xffffffffu, in && entry_back(A, e)));
     anyg |= in && (e & kEntryRot) != 0;
   }
-  int bL = 0, bR = 0;
-  if (lane == 0) {
-    if (n - nR > 0) bL = atomicAdd(&A.cnt[nxt * A.nF + f], n - nR);
-    if (nR > 0) bR = atomicAdd(&A.cntR[nxt * A.nF + f], nR);
-  }
-  bL = __shfl_sync(0xffffffffu, bL, 0);
-  bR = __shfl_sync(0xffffffffu, bR, 0);
+  anyg = __any_sync(0xffffffffu, anyg);
+}
+
+// copy staged entries to frame f's next list at reserved bases bL / bR
+__device__ __forceinline__ void warp_copy(const FillArgs& A, const uint32_t* reg, int n, int f,
+                                          uint32_t* nxt_list, int bL, int bR) {
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1;
   uint32_t* l = nxt_list + (size_t)f * A.cap;
   for (int c0 = 0; c0 < n; c0 += 32) {
     const bool in = c0 + lane < n;
@@ -416,8 +626,26 @@ __device__ __forceinline__ void warp_flush(const FillArgs& A, uint32_t* reg, int
     bR += __popc(mR);
     bL += __popc(mL);
   }
-  if (A.order == 2 && A.g_mode == 2 && __any_sync(0xffffffffu, anyg) && lane == 0)
-    A.anyg[nxt * A.nF + f] = 1;
+}
+
+// warp-level publish (frame switches, full staging slices -- rare)
+__device__ __forceinline__ void warp_flush(const FillArgs& A, uint32_t* reg, int& n, int f,
+                                           uint32_t* nxt_list, int nxt) {
+  if (n == 0) return;
+  __syncwarp();
+  const int lane = threadIdx.x & 31;
+  int nR;
+  bool anyg;
+  warp_count(A, reg, n, nR, anyg);
+  int bL = 0, bR = 0;
+  if (lane == 0) {
+    if (n - nR > 0) bL = atomicAdd(&A.cnt[nxt * A.nF + f], n - nR);
+    if (nR > 0) bR = atomicAdd(&A.cntR[nxt * A.nF + f], nR);
+    if (A.order == 2 && A.g_mode == 2 && anyg) A.anyg[nxt * A.nF + f] = 1;
+  }
+  bL = __shfl_sync(0xffffffffu, bL, 0);
+  bR = __shfl_sync(0xffffffffu, bR, 0);
+  warp_copy(A, reg, n, f, nxt_list, bL, bR);
   __syncwarp();
   n = 0;
 }
@@ -501,6 +729,57 @@ __device__ __forceinline__ void activate(const FillArgs& A, uint32_t* reg, int& 
   }
 }
 
+// End of the fill phase: every warp's pending appends and fill count are
+// published with one atomic per list part and per frame for the whole block
+// (same-address atomics from every warp of the grid would serialise in L2).
+// All threads of the block call.
+__device__ void block_flush(const FillArgs& A, Smem& S, const uint32_t* reg, int wn, int wf,
+                            int wfills, uint32_t* nxt_list, int nxt, int cur, bool tracked) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int nR = 0;
+  bool anyg = false;
+  if (tracked) warp_count(A, reg, wn, nR, anyg);
+  if (lane == 0) {
+    S.bf_frame[warp] = wf;
+    S.bf_nL[warp] = tracked ? wn - nR : 0;
+    S.bf_nR[warp] = nR;
+    S.bf_fill[warp] = wfills;
+    S.bf_anyg[warp] = anyg ? 1 : 0;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    constexpr int NW = kThreads / 32;
+    bool done[NW];
+    for (int w = 0; w < NW; ++w) done[w] = S.bf_frame[w] < 0;
+    for (int w = 0; w < NW; ++w) {
+      if (done[w]) continue;
+      const int f = S.bf_frame[w];
+      int nL = 0, nRt = 0, fl = 0, ag = 0;
+      for (int v = w; v < NW; ++v)
+        if (!done[v] && S.bf_frame[v] == f) {
+          nL += S.bf_nL[v];
+          nRt += S.bf_nR[v];
+          fl += S.bf_fill[v];
+          ag |= S.bf_anyg[v];
+        }
+      int bL = nL > 0 ? atomicAdd(&A.cnt[nxt * A.nF + f], nL) : 0;
+      int bR = nRt > 0 ? atomicAdd(&A.cntR[nxt * A.nF + f], nRt) : 0;
+      if (fl > 0) atomicAdd(&A.fills[cur * A.nF + f], fl);
+      if (ag && A.order == 2 && A.g_mode == 2) A.anyg[nxt * A.nF + f] = 1;
+      for (int v = w; v < NW; ++v)
+        if (!done[v] && S.bf_frame[v] == f) {
+          S.bf_bL[v] = bL;
+          S.bf_bR[v] = bR;
+          bL += S.bf_nL[v];
+          bR += S.bf_nR[v];
+          done[v] = true;
+        }
+    }
+  }
+  __syncthreads();
+  if (tracked && wf >= 0 && wn > 0) warp_copy(A, reg, wn, wf, nxt_list, S.bf_bL[warp], S.bf_bR[warp]);
+}
+
 // Bookkeeping of shell k-1 (block 0 only): report row, remaining, latch.
 __device__ void bookkeep(const FillArgs& A, int k) {
   const int prev = (k - 1) & 1;
@@ -533,6 +812,7 @@ __global__ void __launch_bounds__(kThreads, GF_SHELL_MIN_BLOCKS)
     k_shells(const __grid_constant__ FillArgs A, const __grid_constant__ BallParams P,
              const __grid_constant__ BallTables tables) {
   cg::grid_group grid = cg::this_grid();
+  timeline_mark(A, 1, true);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Smem& S = *reinterpret_cast<Smem*>(smem_raw);
   for (int i = threadIdx.x; i < P.K; i += blockDim.x) {
@@ -866,7 +1146,8 @@ __global__ void __launch_bounds__(kThreads, GF_SHELL_MIN_BLOCKS)
           uint32_t e = 0;
           if (t < fe) {
             const int p = (int)(t - (long long)a * A.HW);
-            const int st = stamp_of(fw, p);
+            // only Inpaint pixels have a working-buffer entry far from D
+            const int st = A.labels[(size_t)f * A.HW + p] == 255 ? stamp_of(fw, p) : 0;
             if (stamp_unfilled(st)) {
               for (int o = 0; o < 8 && !want; ++o) {
                 bool in;
@@ -891,6 +1172,7 @@ __global__ void __launch_bounds__(kThreads, GF_SHELL_MIN_BLOCKS)
       trace_set(A, k, 4, gtimer());
     }
   }
+  timeline_mark(A, 1, false);
   // final bookkeeping: stats
   if (blockIdx.x == 0) {
     for (int f = threadIdx.x; f < A.nF; f += blockDim.x) {
@@ -908,23 +1190,43 @@ __global__ void __launch_bounds__(kThreads, GF_SHELL_MIN_BLOCKS)
 }
 
 // ------------------------------------------------------------ finalize
-
+//
+// Writes the output for every non-Readable pixel (Readable ones were copied
+// by k_prep): Bystanders are clipped to the value hull of the initially
+// Readable values, filled pixels take their fp32 fill value clipped to the
+// same hull (engine.py:372-375), stranded Inpaint pixels keep their input
+// (the caller's unfillable fallback paints them).  Optionally emits the
+// per-pixel fill shell (order log).
 template <typename T>
-__global__ void __launch_bounds__(kThreads) k_finalize(FillArgs A) {
+__global__ void __launch_bounds__(kThreads) k_finalize(const __grid_constant__ FillArgs A) {
+  timeline_mark(A, 2, true);
   const long long total = (long long)A.nF * A.HW;
   for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < total;
        g += (long long)gridDim.x * blockDim.x) {
+    const uint8_t l = A.labels[g];
+    if (l == 0) {
+      if (A.fillshell) A.fillshell[g] = -1;
+      continue;
+    }
     const int f = (int)(g / A.HW);
-    const float4 px = A.work[g];
-    const int st = __float_as_int(px.w);
-    const bool filled = st >= 1 && st < kStampInactive;
     const unsigned long long elo = ~A.hull[2 * f], ehi = A.hull[2 * f + 1];
     const bool has_hull = ehi != 0ULL;
     const double lo = has_hull ? dec_ordered(elo) : 0.0;
     const double hi = has_hull ? dec_ordered(ehi) : 0.0;
     const T* in = reinterpret_cast<const T*>(A.image) + (size_t)g * A.C;
     T* out = reinterpret_cast<T*>(A.out) + (size_t)g * A.C;
-    const float fv[4] = {px.x, px.y, px.z, A.c3 ? A.c3[g] : 0.f};
+    bool filled = false;
+    int st = 0;
+    float fv[4] = {0.f, 0.f, 0.f, 0.f};
+    if (l == 255) {
+      const float4 px = A.work[g];
+      st = __float_as_int(px.w);
+      filled = st >= 1 && st < kStampInactive;
+      fv[0] = px.x;
+      fv[1] = px.y;
+      fv[2] = px.z;
+      if (A.c3 && filled) fv[3] = A.c3[g];
+    }
     for (int c = 0; c < A.C; ++c) {
       double v = filled ? (double)fv[c] : (double)in[c];
       if (has_hull) v = (v < lo) ? lo : ((v > hi) ? hi : v);
@@ -932,17 +1234,48 @@ __global__ void __launch_bounds__(kThreads) k_finalize(FillArgs A) {
     }
     if (A.fillshell) A.fillshell[g] = filled ? st - 1 : -1;
   }
+  timeline_mark(A, 2, false);
 }
 
 // ---------------------------------------------------------------- host
 
+static void launch_prep(bool f64, int C, dim3 cgrid, dim3 grid, cudaStream_t stream,
+                        const FillArgs& A) {
+#define GF_PREP(T, CC)                                   \
+  do {                                                   \
+    k_copy<T, CC><<<cgrid, kThreads, 0, stream>>>(A);    \
+    k_prep<T, CC><<<grid, kThreads, 0, stream>>>(A);     \
+  } while (0)
+  if (f64) {
+    switch (C) {
+      case 1: GF_PREP(double, 1); break;
+      case 2: GF_PREP(double, 2); break;
+      case 3: GF_PREP(double, 3); break;
+      default: GF_PREP(double, 4); break;
+    }
+  } else {
+    switch (C) {
+      case 1: GF_PREP(float, 1); break;
+      case 2: GF_PREP(float, 2); break;
+      case 3: GF_PREP(float, 3); break;
+      default: GF_PREP(float, 4); break;
+    }
+  }
+#undef GF_PREP
+}
+
 static size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct Layout {
-  size_t work, c3, list0, list1, conf, gfield, ints, u64, total;
+  size_t work, c3, list0, list1, conf, gfield, ints, dtile, u64, total;
 };
 
-static Layout layout_for(int nF, int HW, int C, bool raster) {
+static int tiles_of(int H, int W) {
+  return ((W + kTile - 1) / kTile) * ((H + kTile - 1) / kTile);
+}
+
+static Layout layout_for(int nF, int H, int W, int C, bool raster) {
+  const int HW = H * W;
   Layout L;
   size_t off = 0;
   const size_t n = (size_t)nF * HW;
@@ -953,6 +1286,7 @@ static Layout layout_for(int nF, int HW, int C, bool raster) {
   L.list1 = off; off = align_up(off + n * sizeof(uint32_t));
   L.conf = off; off = align_up(off + n * sizeof(double));
   L.ints = off; off = align_up(off + (size_t)nF * kIntsPerFrame * sizeof(int));
+  L.dtile = off; off = align_up(off + (size_t)nF * tiles_of(H, W) * sizeof(int));
   L.u64 = off; off = align_up(off + (size_t)nF * 4 * sizeof(unsigned long long));
   L.total = off;
   return L;
@@ -960,7 +1294,7 @@ static Layout layout_for(int nF, int HW, int C, bool raster) {
 
 size_t fill_workspace_bytes(int nF, int H, int W, int C, bool raster) {
   if (nF <= 0 || H <= 0 || W <= 0) return 0;
-  return layout_for(nF, H * W, C, raster).total;
+  return layout_for(nF, H, W, C, raster).total;
 }
 
 // kernel specialised on the ball size: samples per lane = ceil(K / 8)
@@ -1001,7 +1335,7 @@ int fill_launch(const gf_frames* fr, const gf_fill_params* prm, const gf_fill_ou
   const int nF = fr->n_frames, H = fr->height, W = fr->width, C = fr->channels;
   const int HW = H * W;
   const bool raster = spl && spl->n_seg > 0;
-  const Layout L = layout_for(nF, HW, C, raster);
+  const Layout L = layout_for(nF, H, W, C, raster);
   if (ws_bytes < L.total) return set_error(GF_E_WORKSPACE, "workspace too small");
   unsigned char* base = static_cast<unsigned char*>(ws);
 
@@ -1045,6 +1379,8 @@ int fill_launch(const gf_frames* fr, const gf_fill_params* prm, const gf_fill_ou
   A.inpaint = ints;          ints += nF;
   A.overflow = ints;         ints += nF;
   A.last_f = ints;           ints += nF;
+  A.dtile = reinterpret_cast<int*>(base + L.dtile);
+  A.ntiles = tiles_of(H, W);
   unsigned long long* u64 = reinterpret_cast<unsigned long long*>(base + L.u64);
   A.best_key = u64;
   A.hull = u64 + nF;
@@ -1061,6 +1397,7 @@ int fill_launch(const gf_frames* fr, const gf_fill_params* prm, const gf_fill_ou
   A.gfy = prm->g_fixed[1];
   A.periodic = prm->periodic_x;
   A.split = P.plan.n_leaves == 1 ? 1 : 0;
+  A.halo = P.r + 1;
   A.dtype = fr->dtype;
 
   // per-frame counters start at zero (the hull minimum is stored inverted
@@ -1073,13 +1410,10 @@ int fill_launch(const gf_frames* fr, const gf_fill_params* prm, const gf_fill_ou
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const long long total = (long long)nF * HW;
   {
-    const int bpf = std::max(1, std::min((HW + kThreads - 1) / kThreads,
-                                         std::max(1, sms * 8 / std::max(1, nF))));
-    const dim3 pgrid(bpf, nF);
-    if (fr->dtype == GF_F64)
-      k_prep<double><<<pgrid, kThreads, 0, stream>>>(A);
-    else
-      k_prep<float><<<pgrid, kThreads, 0, stream>>>(A);
+    const int units = (HW + 3) / 4;
+    const int cblocks = std::max(1, std::min((units + kThreads - 1) / kThreads,
+                                             std::max(1, sms * 8 / std::max(1, nF))));
+    launch_prep(fr->dtype == GF_F64, C, dim3(cblocks, nF), dim3(tiles_of(H, W), nF), stream, A);
   }
   if (cudaPeekAtLastError() != cudaSuccess)
     return set_error(GF_E_CUDA, cudaGetErrorString(cudaGetLastError()));

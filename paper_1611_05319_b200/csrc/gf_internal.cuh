@@ -56,6 +56,9 @@ struct FillArgs {
   double gfx, gfy;
   int periodic;
   int split;       // rotated-ball entries kept in the back part (K <= 128)
+  int halo;        // r + 1: farthest pixel a ball sample's corners can touch
+  int* dtile;      // [nF][ntiles] 32x32 tile holds an Inpaint pixel
+  int ntiles;
   // fused spline raster (guide.py:286-327), n_seg == 0 when off
   int n_seg;
   const double4* seg;

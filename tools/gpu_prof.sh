@@ -1,6 +1,5 @@
 mkdir -p gpurun_out
 CMD="python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu"
-timeout -s KILL 300 python bench.py --steps 300 --warmup 5 --no-cpu > gpurun_out/bench.log 2>&1; echo "bench rc=$?"; tail -2 gpurun_out/bench.log
 timeout -s KILL 300 $CMD > gpurun_out/plain.log 2>&1 && \
-timeout -s KILL 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 80 --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launch.log 2>&1; echo "ncu launches rc=$?"
-timeout -s KILL 900 ncu --set full --clock-control none --import-source on -k regex:"k_shells|k_prep|k_finalize|k_guide" -s 4 -c 4 -o gpurun_out/prof_r1 $CMD > gpurun_out/ncu_full.log 2>&1; echo "ncu full rc=$?"; tail -5 gpurun_out/ncu_full.log
+timeout -s KILL 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 40 --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launch.log 2>&1; echo "ncu launches rc=$?"
+timeout -s KILL 900 ncu --set full --clock-control none --import-source on -k regex:"k_shells|k_prep|k_finalize" -s 3 -c 3 -o gpurun_out/prof_r1b $CMD > gpurun_out/ncu_full.log 2>&1; echo "ncu full rc=$?"; tail -3 gpurun_out/ncu_full.log
