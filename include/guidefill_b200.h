@@ -115,7 +115,7 @@ typedef struct gf_fill_outputs {
 } gf_fill_outputs;
 
 /* Splines flattened to polylines on the host (Spline.polyline,
- * splines.py:42-73), shared by every frame of a batch.  All device pointers. */
+ * splines.py:42-73), for every frame of a batch.  All device pointers. */
 typedef struct gf_splines {
   int32_t n_seg;
   const double* seg;         /* [n_seg][4] = (ax, ay, bx, by), polyline order */
@@ -123,6 +123,9 @@ typedef struct gf_splines {
   int32_t n_splines;
   const double* dirs;        /* [n_splines][2] spline directions             */
   double eta;                /* falloff scale, guide.py:28                   */
+  const int32_t* frame_seg;  /* optional [n_frames + 1]: frame f uses segments
+                                [frame_seg[f], frame_seg[f+1]); NULL = every
+                                frame uses all segments                      */
 } gf_splines;
 
 /* Bytes of device workspace gf_fill / gf_fill_splines need for this batch

@@ -121,21 +121,42 @@ def splines_to_segments(splines):
 
 
 class SegmentSet:
-    """Flattened splines resident on the device (reused across frames)."""
+    """Flattened splines resident on the device (reused across steps).
 
-    def __init__(self, splines, device):
+    ``splines`` is one spline list shared by every frame, or, with
+    ``per_frame=True``, a list of spline lists (one per frame of a batch).
+    """
+
+    def __init__(self, splines, device, per_frame=False):
         import torch
 
-        seg, own, dv = splines_to_segments(list(splines))
+        if per_frame:
+            segs, owns, dirs, offs = [], [], [], [0]
+            base = 0
+            for frame_splines in splines:
+                seg, own, dv = splines_to_segments(list(frame_splines))
+                segs.append(seg)
+                owns.append(own + base)
+                dirs.append(dv)
+                base += len(dv)
+                offs.append(offs[-1] + len(seg))
+            seg = np.concatenate(segs) if segs else np.zeros((0, 4))
+            own = np.concatenate(owns).astype(np.int32) if owns else np.zeros(0, np.int32)
+            dv = np.concatenate(dirs) if dirs else np.zeros((0, 2))
+            self.frame_seg = torch.tensor(offs, dtype=torch.int32, device=device)
+        else:
+            seg, own, dv = splines_to_segments(list(splines))
+            self.frame_seg = None
         self.n_splines = len(dv)
         self.n_seg = len(seg)
-        self.seg = torch.from_numpy(seg).to(device)
-        self.owner = torch.from_numpy(own).to(device)
-        self.dirs = torch.from_numpy(dv).to(device)
+        self.seg = torch.from_numpy(np.ascontiguousarray(seg)).to(device)
+        self.owner = torch.from_numpy(np.ascontiguousarray(own, dtype=np.int32)).to(device)
+        self.dirs = torch.from_numpy(np.ascontiguousarray(dv)).to(device)
 
     def as_c(self, eta=3.0):
         return N.SplinesC(self.n_seg, self.seg.data_ptr(), self.owner.data_ptr(), self.n_splines,
-                          self.dirs.data_ptr(), float(eta))
+                          self.dirs.data_ptr(), float(eta),
+                          0 if self.frame_seg is None else self.frame_seg.data_ptr())
 
 
 def guide_field_device(labels, segset: SegmentSet, eta: float = 3.0, out=None):

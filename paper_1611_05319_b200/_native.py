@@ -80,6 +80,7 @@ class SplinesC(ctypes.Structure):
         ("n_splines", ctypes.c_int32),
         ("dirs", ctypes.c_void_p),
         ("eta", ctypes.c_double),
+        ("frame_seg", ctypes.c_void_p),
     ]
 
 

@@ -136,8 +136,13 @@ static int fill_common(const gf_frames* frames, const gf_fill_params* params,
     o.enter = outputs->enter ? outputs->enter + f0 * HW : nullptr;
     o.fillshell = outputs->fillshell ? outputs->fillshell + f0 * HW : nullptr;
     if (f0 > 0) o.shell_trace = nullptr;
-    rc = fill_launch(&sub, params, &o, raster ? splines : nullptr, workspace, workspace_bytes, s,
-                     P, *T);
+    gf_splines sp;
+    if (raster) {
+      sp = *splines;
+      if (sp.frame_seg) sp.frame_seg += f0;
+    }
+    rc = fill_launch(&sub, params, &o, raster ? &sp : nullptr, workspace, workspace_bytes, s, P,
+                     *T);
   }
   delete T;  // passed by value as a kernel parameter: safe to free now
   return rc;

@@ -295,7 +295,9 @@ __global__ void __launch_bounds__(kThreads) k_prep(const __grid_constant__ FillA
   if (tile_d && raster) {
     const double x0 = (double)tx0, x1 = (double)min(A.W - 1, tx0 + kTile - 1);
     const double y0 = (double)ty0, y1 = (double)min(A.H - 1, ty0 + kTile - 1);
-    for (int i = threadIdx.x; i < A.n_seg; i += kThreads) {
+    const int s0 = A.frame_seg ? A.frame_seg[f] : 0;
+    const int s1 = A.frame_seg ? A.frame_seg[f + 1] : A.n_seg;
+    for (int i = s0 + threadIdx.x; i < s1; i += kThreads) {
       const double4 sg = A.seg[i];
       const double lo_x = fmin(sg.x, sg.z) - A.cut, hi_x = fmax(sg.x, sg.z) + A.cut;
       const double lo_y = fmin(sg.y, sg.w) - A.cut, hi_y = fmax(sg.y, sg.w) + A.cut;
@@ -357,12 +359,13 @@ __global__ void __launch_bounds__(kThreads) k_prep(const __grid_constant__ FillA
         double gxv = 0.0, gyv = 0.0;
         if (raster) {
           const bool exhaustive = s_ncand > kMaxCand;
-          const int n_eval = exhaustive ? A.n_seg : s_ncand;
+          const int e0 = (exhaustive && A.frame_seg) ? A.frame_seg[f] : 0;
+          const int n_eval = exhaustive ? (A.frame_seg ? A.frame_seg[f + 1] - e0 : A.n_seg) : s_ncand;
           double dmin = INFINITY;
           int nearest = 0x7fffffff;
           const double fx = (double)gx, fy = (double)gy;
           for (int cc = 0; cc < n_eval; ++cc) {
-            const int sidx = exhaustive ? cc : s_cand[cc];
+            const int sidx = exhaustive ? e0 + cc : s_cand[cc];
             const double d = seg_dist(fx, fy, A.seg[sidx]);
             const int sp = A.seg_spline[sidx];
             if (d < dmin || (d == dmin && sp < nearest)) {
@@ -1351,6 +1354,7 @@ int fill_launch(const gf_frames* fr, const gf_fill_params* prm, const gf_fill_ou
     A.gfield = reinterpret_cast<double*>(base + L.gfield);
     A.gsrc = A.gfield;
     A.n_seg = spl->n_seg;
+    A.frame_seg = spl->frame_seg;
     A.seg = reinterpret_cast<const double4*>(spl->seg);
     A.seg_spline = spl->seg_spline;
     A.dirs = reinterpret_cast<const double2*>(spl->dirs);

@@ -61,6 +61,7 @@ struct FillArgs {
   int ntiles;
   // fused spline raster (guide.py:286-327), n_seg == 0 when off
   int n_seg;
+  const int32_t* frame_seg;  // per-frame segment ranges or nullptr
   const double4* seg;
   const int32_t* seg_spline;
   const double2* dirs;
