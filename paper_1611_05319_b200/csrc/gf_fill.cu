@@ -807,7 +807,7 @@ __device__ void bookkeep(const FillArgs& A, int k) {
 }
 
 #ifndef GF_SHELL_MIN_BLOCKS
-#define GF_SHELL_MIN_BLOCKS 1
+#define GF_SHELL_MIN_BLOCKS 3
 #endif
 
 template <int NL, int KPL, bool kTracked>
