@@ -44,7 +44,7 @@ def resolve_g_mode(params, guide_present: bool) -> int:
 
 
 def fill_device(image, labels, guide, params, tracked=True, order_log=False, rows_cap=None,
-                workspace=None, splines=None, eta=3.0, trace_cap=0):
+                workspace=None, splines=None, eta=3.0, trace_cap=0, want_fillshell=False):
     """Fill a batch of frames on the GPU.
 
     image: (N, H, W, C) float32/float64 CUDA tensor; labels: (N, H, W) uint8;
@@ -75,6 +75,7 @@ def fill_device(image, labels, guide, params, tracked=True, order_log=False, row
     enter = fillshell = None
     if order_log:
         enter = torch.empty((nF, H, W), dtype=torch.int32, device=dev)
+    if order_log or want_fillshell:
         fillshell = torch.empty((nF, H, W), dtype=torch.int32, device=dev)
     fr = N.FramesC(nF, H, W, C, dtype, image.data_ptr(), labels.data_ptr(),
                    0 if guide is None else guide.data_ptr(), out.data_ptr())

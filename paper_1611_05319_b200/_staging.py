@@ -1,0 +1,124 @@
+"""Host <-> device transfers for the numpy drop-in API.
+
+The reference API takes and returns host float64 arrays (1080p RGB = 50 MB
+each way).  Pageable copies are slow (measured on the B200 box: H2D 3.5 ms,
+D2H 23.5 ms for 50 MB), pinned ones ~0.9 ms.  The stager keeps cached
+pinned staging buffers and moves data in chunks: host threads copy chunk i
+into / out of pinned memory while the DMA engine moves chunk i-1 (numpy's
+copyto releases the GIL, so the host copies run in parallel).
+"""
+
+from __future__ import annotations
+
+import os
+import threading
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+
+_CHUNK = 8 << 20
+_lock = threading.Lock()
+_pool = None
+_pinned = {}
+
+
+def _executor():
+    global _pool
+    if _pool is None:
+        _pool = ThreadPoolExecutor(max_workers=max(1, min(16, os.cpu_count() or 1)))
+    return _pool
+
+
+def _staging(nbytes: int, slot: str):
+    """Cached pinned uint8 buffer of at least nbytes (one per slot)."""
+    import torch
+
+    with _lock:
+        buf = _pinned.get(slot)
+        if buf is None or buf.numel() < nbytes:
+            buf = torch.empty(max(nbytes, 1), dtype=torch.uint8, pin_memory=True)
+            _pinned[slot] = buf
+        return buf
+
+
+def _chunks(n: int):
+    return [(o, min(n, o + _CHUNK)) for o in range(0, n, _CHUNK)]
+
+
+def upload(arr: np.ndarray, device, slot: str = "up"):
+    """numpy array -> CUDA tensor of the same dtype/shape (stream-ordered)."""
+    import torch
+
+    a = np.ascontiguousarray(arr)
+    n = a.nbytes
+    dst = torch.empty(a.shape, dtype=torch.from_numpy(a[:0].reshape(-1)).dtype, device=device)
+    if n == 0:
+        return dst
+    if n < (1 << 20):
+        return torch.from_numpy(a).to(device)
+    stage = _staging(n, slot)
+    src = a.reshape(-1).view(np.uint8)
+    host = stage.numpy()
+    dflat = dst.view(-1).view(torch.uint8)
+    stream = torch.cuda.current_stream()
+    futs = [_executor().submit(np.copyto, host[lo:hi], src[lo:hi]) for lo, hi in _chunks(n)]
+    for (lo, hi), fut in zip(_chunks(n), futs):
+        fut.result()
+        dflat[lo:hi].copy_(stage[lo:hi], non_blocking=True)
+    # the staging buffer is reused by the next call: wait for the DMA
+    stream.synchronize()
+    return dst
+
+
+class _PinnedPool:
+    """Recycled pinned host buffers for returned arrays.
+
+    ``take`` hands out a numpy array backed by pinned, already-touched memory;
+    the buffer returns to the pool when that array (and every view of it) is
+    garbage-collected, so steady-state calls pay neither page faults nor
+    pinned allocation, and the D2H lands in it at full DMA speed.
+    """
+
+    def __init__(self):
+        self.free = {}
+        self.lock = threading.Lock()
+
+    def take(self, shape, dtype):
+        import weakref
+
+        import torch
+
+        dtype = np.dtype(dtype)
+        n = int(np.prod(shape)) * dtype.itemsize
+        with self.lock:
+            lst = self.free.get(n)
+            buf = lst.pop() if lst else None
+        if buf is None:
+            buf = torch.empty(max(n, 1), dtype=torch.uint8, pin_memory=True)
+        arr = buf.numpy()[:n].view(dtype).reshape(shape)
+        weakref.finalize(arr, self._give, n, buf)
+        return arr, buf
+
+    def _give(self, n, buf):
+        with self.lock:
+            lst = self.free.setdefault(n, [])
+            if len(lst) < 4:
+                lst.append(buf)
+
+
+_pool_out = _PinnedPool()
+
+
+def download(t) -> np.ndarray:
+    """CUDA tensor -> new numpy array (synchronous), DMA'd straight into a
+    recycled pinned buffer."""
+    import torch
+
+    t = t.contiguous()
+    dtype = torch.empty(0, dtype=t.dtype).numpy().dtype
+    if t.numel() * dtype.itemsize < (1 << 20):
+        return t.cpu().numpy()
+    out, buf = _pool_out.take(tuple(t.shape), dtype)
+    buf[: out.nbytes].copy_(t.view(-1).view(torch.uint8), non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    return out

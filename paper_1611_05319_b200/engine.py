@@ -184,31 +184,46 @@ def _paint_unfillable(u, labels, fillshell):
     return count
 
 
-def _run_fill(image, labels, guide_vecs, params: FillParams, tracked: bool, order_log=False):
-    """Fill one frame on the GPU.  Returns (u float64 (H,W,C), FillReport, maps)."""
+def _is_spline_list(guide) -> bool:
+    return isinstance(guide, (list, tuple)) and all(hasattr(s, "polyline") for s in guide)
+
+
+def _run_fill(image, labels, guide_vecs, params: FillParams, tracked: bool, order_log=False,
+              splines=None, eta=3.0, validate=False):
+    """Fill one frame on the GPU.  Returns (u float64 (H,W,C), FillReport, maps).
+
+    ``splines`` (a list of Spline) rasters the guide field inside the fill
+    (gf_fill_splines) instead of uploading a dense ``guide_vecs``.
+    """
     import torch
 
+    if validate and not torch.cuda.is_available():
+        grid.validate_labels(labels)  # same ValueError without a device
     dev = N.require_cuda()
-    from ._device import fill_device
+    from . import _staging
+    from ._device import SegmentSet, fill_device
 
     H, W = labels.shape
     img = np.ascontiguousarray(image, dtype=np.float64)
     C = img.shape[2]
     t0 = time.perf_counter()
-    d_img = torch.from_numpy(img).to(dev, non_blocking=True).reshape(1, H, W, C)
-    d_lab = torch.from_numpy(np.ascontiguousarray(labels, dtype=np.uint8)).to(dev).reshape(1, H, W)
+    d_img = _staging.upload(img, dev, "img").reshape(1, H, W, C)
+    d_lab = _staging.upload(np.ascontiguousarray(labels, dtype=np.uint8), dev, "lab").reshape(1, H, W)
+    if validate:
+        grid.validate_labels(labels, d_lab)
     d_guide = None
-    if guide_vecs is not None and params.g_source == "guide_field":
-        d_guide = torch.from_numpy(np.ascontiguousarray(guide_vecs, dtype=np.float64)).to(dev)
-        d_guide = d_guide.reshape(1, H, W, 2)
-    res = fill_device(d_img, d_lab, d_guide, params, tracked=tracked, order_log=True,
-                      rows_cap=H * W + 1)
+    segs = None
+    if splines is not None and params.g_source == "guide_field":
+        segs = SegmentSet(list(splines), dev) if len(splines) else None
+    elif guide_vecs is not None and params.g_source == "guide_field":
+        d_guide = _staging.upload(np.ascontiguousarray(guide_vecs, dtype=np.float64), dev,
+                                  "guide").reshape(1, H, W, 2)
+    res = fill_device(d_img, d_lab, d_guide, params, tracked=tracked, order_log=order_log,
+                      rows_cap=H * W + 1, splines=segs, eta=eta, want_fillshell=True)
     stats = res["stats"][0].cpu().numpy()
     iters = int(stats[N.STAT_ITERATIONS])
-    rows_dev = res["rows"][0, :iters].cpu().numpy()
-    u = res["out"][0].cpu().numpy()
-    fillshell = res["fillshell"][0].cpu().numpy()
-    enter = res["enter"][0].cpu().numpy() if order_log else None
+    rows_dev = res["rows"][0, :iters + 1].cpu().numpy()
+    u = _staging.download(res["out"][0])
     rep = FillReport()
     rep.iterations = iters
     rep.filled = int(stats[N.STAT_FILLED])
@@ -224,10 +239,14 @@ def _run_fill(image, labels, guide_vecs, params: FillParams, tracked: bool, orde
         else:
             rows.append((k, F, W * H, W * H, filled))
     rep.rows = rows
+    fillshell = None
+    if order_log or stats[N.STAT_UNFILLABLE]:
+        fillshell = res["fillshell"][0].cpu().numpy()
     if stats[N.STAT_UNFILLABLE]:
         rep.unfillable = True
         rep.unfillable_count = _paint_unfillable(u, labels, fillshell)
         fillshell = np.where((np.asarray(labels) == INPAINT) & (fillshell < 0), -2, fillshell)
+    enter = res["enter"][0].cpu().numpy() if order_log else None
     rep.wall_time_s = time.perf_counter() - t0
     return u, rep, dict(enter=enter, fillshell=fillshell)
 
@@ -240,19 +259,28 @@ def inpaint(image, labels, guide=None, params: FillParams | None = None):
     Returns (filled_image float64 (H, W, C), FillReport).
     """
     params = params or FillParams()
-    grid.validate_labels(labels)
+    labels = np.asarray(labels)
+    if labels.ndim != 2:
+        grid.validate_labels(labels)
+    if labels.dtype != np.uint8:
+        grid.validate_labels(labels)  # values are scanned on the GPU for uint8 masks
     if image.ndim != 3:
         raise ValueError("image must be (H, W, C)")
     if image.shape[:2] != labels.shape:
         raise ValueError(
             f"image {image.shape[:2]} and label mask {labels.shape} dimensions differ"
         )
+    if _is_spline_list(guide):
+        # extension: splines instead of a field -> rastered inside the fill
+        u, report, _ = _run_fill(image, labels, None, params, tracked=False, splines=guide,
+                                 validate=True)
+        return u, report
     guide_vecs = None
     if guide is not None:
         guide_vecs = np.asarray(guide, dtype=np.float64)
         if guide_vecs.shape != labels.shape + (2,):
             raise ValueError("guide field shape must be (H, W, 2)")
-    u, report, _ = _run_fill(image, labels, guide_vecs, params, tracked=False)
+    u, report, _ = _run_fill(image, labels, guide_vecs, params, tracked=False, validate=True)
     return u, report
 
 

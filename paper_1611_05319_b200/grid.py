@@ -27,12 +27,27 @@ NEIGHBOR_OFFSETS = (
 )
 
 
-def validate_labels(labels) -> None:
-    """ValueError unless labels is 2-D over the three label values (grid.py:36-46)."""
+_LUT = np.ones(256, dtype=bool)
+_LUT[list(_LABEL_VALUES)] = False
+
+
+def validate_labels(labels, device_labels=None) -> None:
+    """ValueError unless labels is 2-D over the three label values (grid.py:36-46).
+
+    With ``device_labels`` (the same mask already on the GPU) the scan runs
+    on the device; the host only locates the first bad value for the message.
+    """
     labels = np.asarray(labels)
     if labels.ndim != 2:
         raise ValueError(f"label mask must be 2-D, got shape {labels.shape}")
-    bad = ~np.isin(labels, _LABEL_VALUES)
+    if device_labels is not None and labels.dtype == np.uint8:
+        d = device_labels
+        if not bool(((d != READABLE) & (d != BYSTANDER) & (d != INPAINT)).any()):
+            return
+    if labels.dtype == np.uint8:
+        bad = _LUT[labels]
+    else:
+        bad = ~np.isin(labels, _LABEL_VALUES)
     if bad.any():
         j, i = np.nonzero(bad)
         raise ValueError(

@@ -34,10 +34,12 @@ def build_guide_field(splines, labels, eta: float = DEFAULT_ETA) -> np.ndarray:
     splines = list(splines)
     if not splines or not (labels == INPAINT).any():
         return np.zeros((H, W, 2))
+    from . import _staging
+
     dev = N.require_cuda()
     segs = SegmentSet(splines, dev)
-    d_lab = torch.from_numpy(np.ascontiguousarray(labels, dtype=np.uint8)).to(dev)
-    return guide_field_device(d_lab, segs, eta).cpu().numpy()
+    d_lab = _staging.upload(np.ascontiguousarray(labels, dtype=np.uint8), dev, "lab")
+    return _staging.download(guide_field_device(d_lab, segs, eta))
 
 
 def detect_splines(image, labels, *args, **kwargs):

@@ -161,3 +161,20 @@ def test_bilinear_gather_matches_oracle():
         v0, ok0 = orc.ghost_gather(img, read, X, Y, periodic)
         assert np.array_equal(ok, ok0)
         assert np.abs(v - v0).max() <= 1e-12
+
+
+def test_spline_guide_extension_equals_field():
+    """run_tracked / inpaint accept splines in place of the dense field."""
+    from paper_1611_05319_b200 import scenes
+
+    sc = scenes.small_scene(120, 200, band=6, gx=4, gy=3, n_spl=3, seed=21)
+    spl = [Spline(id=s["id"], source="user", direction=s["direction"], points=s["points"],
+                  kind=s["kind"]) for s in sc.splines]
+    p = FillParams(**sc.params)
+    field = build_guide_field(spl, sc.labels)
+    u1, wm1 = tracker.run_tracked(sc.image, sc.labels, field, p)
+    u2, wm2 = tracker.run_tracked(sc.image, sc.labels, spl, p)
+    assert np.array_equal(u1, u2) and wm1.rows == wm2.rows
+    v1, r1 = engine.inpaint(sc.image, sc.labels, field, p)
+    v2, r2 = engine.inpaint(sc.image, sc.labels, spl, p)
+    assert np.array_equal(v1, v2) and r1.rows == r2.rows
