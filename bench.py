@@ -35,6 +35,15 @@ sys.path.insert(0, ROOT)
 METRIC = "Mpixels inpainted/s and ms per 1080p frame; fill-kernel HBM GB/s vs peak"
 
 
+def _ncu_traffic():
+    """DRAM bytes of one fill launch from the committed ncu capture (profiles/)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "round1_ncu_summary.json")) as f:
+            return float(json.load(f)["fill_dram_bytes_per_launch"])
+    except Exception:
+        return None
+
+
 def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -386,11 +395,11 @@ def run_ours(args):
             "peak_kind": peak_kind,
             "unit": "GB/s",
             "frac": achieved / peak,
-            "traffic": None,
+            "traffic": _ncu_traffic(),
             "algorithmic_bytes": b_frame,
         },
         "e2e": e2e,
-        "gpu_launches": 3 * args.steps,
+        "gpu_launches": 4 * args.steps,  # k_copy, k_prep, k_shells, k_finalize
         "clocks": clk.summary(),
         "cpu_baseline": cpu,
     }
