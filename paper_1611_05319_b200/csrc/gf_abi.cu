@@ -46,6 +46,8 @@ static int build_ball(const gf_fill_params* p, BallParams& P, BallTables& T) {
       T.n[K] = (double)n;
       T.m[K] = (double)m;
       T.w0[K] = 1.0 / hypot_np((double)n, (double)m);
+      T.ni[K] = n;
+      T.mi[K] = m;
       ++K;
     }
   P.r = r;
@@ -58,6 +60,7 @@ static int build_ball(const gf_fill_params* p, BallParams& P, BallTables& T) {
   P.tol_inf = 1e-12 * std::max(1.0, (double)(r * r));
   P.plan = make_plan(K);
   if (P.plan.n_leaves > kMaxLeaves) return set_error(GF_E_UNSUPPORTED, "pairwise plan too deep");
+  P.tw0 = plan_sum(P.plan, T.w0);  // tw of every g = 0 item (engine.py:193)
   return GF_OK;
 }
 
@@ -83,11 +86,11 @@ int gf_abi_version(void) { return GF_ABI_VERSION; }
 
 size_t gf_fill_splines_workspace_bytes(const gf_frames* frames, const gf_fill_params* params,
                                        const gf_splines* splines) {
-  (void)params;
   if (check_frames(frames) != GF_OK) return 0;
   const int nF = std::min(frames->n_frames, kMaxFramesPerLaunch);
-  return fill_workspace_bytes(nF, frames->height, frames->width, frames->channels,
-                              splines && splines->n_seg > 0);
+  // the per-pixel guide buffer exists whenever a guide can be non-zero
+  const bool need_g = (splines && splines->n_seg > 0) || !params || params->g_mode != GF_G_ZERO;
+  return fill_workspace_bytes(nF, frames->height, frames->width, frames->channels, need_g);
 }
 
 size_t gf_fill_workspace_bytes(const gf_frames* frames, const gf_fill_params* params) {

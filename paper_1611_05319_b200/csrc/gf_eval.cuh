@@ -1,0 +1,241 @@
+// Radius-specialised ball evaluators for the shell loop (r <= 6, K <= 128:
+// one numpy pairwise leaf).  With K a compile-time constant every loop is
+// unrolled, so the fetches of an item are issued before any of them is
+// consumed and the weight arithmetic overlaps their latency.
+//
+// Both produce exactly engine._BallSampler.gather's rw / tw bits
+// (engine.py:175-199); colours are weighted averages in fp64 (stored fp32).
+#pragma once
+
+#include "gf_sampler.cuh"
+
+namespace gf {
+
+__host__ __device__ constexpr int disk_count(int r) {
+  int k = 0;
+  for (int m = -r; m <= r; ++m)
+    for (int n = -r; n <= r; ++n)
+      if (n * n + m * m <= r * r && (n != 0 || m != 0)) ++k;
+  return k;
+}
+
+template <int R>
+struct Ball {
+  static constexpr int K = disk_count(R);
+  static constexpr int KPL = (K + kGroup - 1) / kGroup;  // samples per lane, 8-lane item
+  static constexpr int KPW = (K + 31) / 32;              // samples per lane, warp item
+  static constexpr int N8 = K - K % 8;                   // pairwise: 8-accumulator part
+  static constexpr int NT = K % 8;                       // pairwise: sequential tail
+  static_assert(K <= 128, "one pairwise leaf");
+};
+
+// Lattice item (g = 0, integral centre) on an 8-lane group.  Lane j of the
+// group owns samples j, j+8, j+16, ... = numpy accumulator j, so its
+// readable mass is summed in registers; the accumulator tree is three xor
+// shuffles, the tail samples (k >= N8, owned by slot KPL-1) are added from
+// a ballot of their readability.  tw is the host's constant P.tw0.
+template <int R>
+__device__ __forceinline__ void eval_lattice(const BallParams& P, const BallTables& T,
+                                             const WorkSource& src, int glane, int sub, bool valid,
+                                             int pi, int pj, SampleResult& out) {
+  using B = Ball<R>;
+  int q[B::KPL];
+  float4 v[B::KPL];
+#pragma unroll
+  for (int t = 0; t < B::KPL; ++t) {
+    const int k = glane + kGroup * t;
+    q[t] = (valid && k < B::K) ? lattice_index(pi + T.ni[k], pj + T.mi[k], src.H, src.W, P.periodic)
+                               : -1;
+  }
+#pragma unroll
+  for (int t = 0; t < B::KPL; ++t)
+    if (q[t] >= 0) v[t] = src.work[q[t]];
+  unsigned okm = 0;  // bit t: sample glane + 8t readable
+#pragma unroll
+  for (int t = 0; t < B::KPL; ++t)
+    if (q[t] >= 0 && __float_as_int(v[t].w) <= src.shell) okm |= 1u << t;
+  double acc = 0.0;
+#pragma unroll
+  for (int t = 0; t < B::N8 / kGroup; ++t)
+    if ((okm >> t) & 1u) acc += T.w0[glane + kGroup * t];  // + 0.0 would be the identity
+  acc = group_sum_tree(acc);
+  if constexpr (B::NT > 0) {
+    const unsigned tb =
+        (__ballot_sync(0xffffffffu, (okm >> (B::KPL - 1)) & 1u) >> (kGroup * sub)) & 0xffu;
+#pragma unroll
+    for (int e = 0; e < B::NT; ++e)
+      if ((tb >> e) & 1u) acc = acc + T.w0[B::N8 + e];
+  }
+  double num[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+  for (int t = 0; t < B::KPL; ++t)
+    if ((okm >> t) & 1u) {
+      const double w = T.w0[glane + kGroup * t];
+      num[0] += w * (double)v[t].x;
+      num[1] += w * (double)v[t].y;
+      num[2] += w * (double)v[t].z;
+    }
+  if (src.c3) {
+#pragma unroll
+    for (int t = 0; t < B::KPL; ++t)
+      if ((okm >> t) & 1u) num[3] += T.w0[glane + kGroup * t] * (double)src.c3[q[t]];
+  }
+  const double inv = (acc != 0.0) ? 1.0 / acc : 0.0;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    double s = 0.0;
+    if (c < 3 || src.c3) {
+      s = num[c];
+      s += __shfl_xor_sync(0xffffffffu, s, 1, kGroup);
+      s += __shfl_xor_sync(0xffffffffu, s, 2, kGroup);
+      s += __shfl_xor_sync(0xffffffffu, s, 4, kGroup);
+    }
+    out.v[c] = s * inv;
+  }
+  out.rw = acc;
+  out.tw = P.tw0;
+}
+
+// Column wrap for the fill's ghost corners: |x| stays within r + 1 of the
+// lattice, so a couple of conditional adds replace the 64-bit modulo.
+__device__ __forceinline__ int wrap_col(int x, int W) {
+  while (x < 0) x += W;
+  while (x >= W) x -= W;
+  return x;
+}
+
+// Rotated-ball item (g != 0) on a whole warp.  Sample k lives in lane
+// k % 32, slot k / 32.  (ux, uy) = g / hypot(g) comes precomputed with g.
+// Per slot: rotated offset -> ghost corners -> corner fetches issued ->
+// weight (glibc hypot, SVML exp, division) computed while they fly.
+// numpy's accumulator j = a_j + a_{j+8} + ... is rebuilt by lane j pulling
+// a_{j+8t} from lane j + 8 (t % 4), slot t / 4.
+template <int R>
+__device__ __forceinline__ void eval_rot_warp(const BallParams& P, const BallTables& T,
+                                              const WorkSource& src, int lane, double fi, double fj,
+                                              double gx, double gy, double ux, double uy,
+                                              SampleResult& out) {
+  using B = Ball<R>;
+  constexpr int KPW = B::KPW;
+  double safe = 1.0, thr = 0.0;
+  if (P.mu_inf) {
+    const double nr2 = sqrt(gx * gx + gy * gy);
+    safe = (nr2 == 0.0) ? 1.0 : nr2;
+    double mloc = INFINITY;
+#pragma unroll
+    for (int s = 0; s < KPW; ++s) {
+      const int k = lane + 32 * s;
+      if (k < B::K) {
+        double px = T.n[k], py = T.m[k];
+        if (P.rotated) {
+          px = T.n[k] * uy + T.m[k] * ux;
+          py = (-T.n[k]) * ux + T.m[k] * uy;
+        }
+        const double d = ((-gy) * px + gx * py) / safe;
+        mloc = min_prop(mloc, d * d);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mloc = min_prop(mloc, __shfl_xor_sync(0xffffffffu, mloc, o));
+    thr = mloc + P.tol_inf;
+  }
+  double w[KPW], wr[KPW];
+  double num[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+  for (int s = 0; s < KPW; ++s) {
+    const int k = lane + 32 * s;
+    w[s] = 0.0;
+    wr[s] = 0.0;
+    if (k < B::K) {
+      double px = T.n[k], py = T.m[k];
+      if (P.rotated) {
+        px = T.n[k] * uy + T.m[k] * ux;
+        py = (-T.n[k]) * ux + T.m[k] * uy;
+      }
+      // ghost corners (grid.py:186-209), fetches issued before the weight
+      const double X = fi + px, Y = fj + py;
+      const double fx0 = floor(X), fy0 = floor(Y);
+      const double tx = X - fx0, ty = Y - fy0;
+      const int x0 = (int)fx0, y0 = (int)fy0;
+      int cq[4];
+      bool outside = false;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int a = c >> 1, b = c & 1;  // (x0,y0),(x0,y0+1),(x0+1,y0),(x0+1,y0+1)
+        const double wc = (a ? tx : 1.0 - tx) * (b ? ty : 1.0 - ty);
+        cq[c] = -1;
+        if (wc != 0.0) {
+          const int cy = y0 + b;
+          int cx = x0 + a;
+          bool inside = cy >= 0 && cy < src.H;
+          if (P.periodic) cx = wrap_col(cx, src.W);
+          else inside = inside && cx >= 0 && cx < src.W;
+          if (inside) cq[c] = cy * src.W + cx;
+          else outside = true;
+        }
+      }
+      float4 v[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        if (cq[c] >= 0) v[c] = src.work[cq[c]];
+      const double dist = hypot_np(px, py);
+      double ws;
+      if (P.mu_inf) {
+        const double d = ((-gy) * px + gx * py) / safe;
+        ws = (d * d <= thr) ? 1.0 / dist : 0.0;
+      } else {
+        const double d = (-gy) * px + gx * py;
+        ws = exp_np((P.coef * d) * d) / dist;
+      }
+      w[s] = ws;
+      bool ok = !outside;
+      double sv[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        if (cq[c] >= 0) {
+          const int a = c >> 1, b = c & 1;
+          const double wc = (a ? tx : 1.0 - tx) * (b ? ty : 1.0 - ty);
+          ok = ok && __float_as_int(v[c].w) <= src.shell;
+          sv[0] += wc * (double)v[c].x;
+          sv[1] += wc * (double)v[c].y;
+          sv[2] += wc * (double)v[c].z;
+          if (src.c3) sv[3] += wc * (double)src.c3[cq[c]];
+        }
+      wr[s] = ok ? ws : 0.0;
+      if (ok) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) num[c] += ws * sv[c];
+      }
+    }
+  }
+  double acc_rw = 0.0, acc_tw = 0.0;
+#pragma unroll
+  for (int t = 0; t < B::N8 / 8; ++t) {
+    const int src_lane = (lane & 7) + 8 * (t & 3);
+    acc_rw += __shfl_sync(0xffffffffu, wr[t >> 2], src_lane);
+    acc_tw += __shfl_sync(0xffffffffu, w[t >> 2], src_lane);
+  }
+  double rw = group_sum_tree(acc_rw);
+  double tw = group_sum_tree(acc_tw);
+#pragma unroll
+  for (int e = 0; e < B::NT; ++e) {
+    const int i = B::N8 + e;
+    rw = rw + __shfl_sync(0xffffffffu, wr[i >> 5], i & 31);
+    tw = tw + __shfl_sync(0xffffffffu, w[i >> 5], i & 31);
+  }
+  const double inv = (rw != 0.0) ? 1.0 / rw : 0.0;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    double sacc = 0.0;
+    if (c < 3 || src.c3) {
+      sacc = num[c];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, o);
+    }
+    out.v[c] = sacc * inv;
+  }
+  out.rw = rw;
+  out.tw = tw;
+}
+
+}  // namespace gf

@@ -28,6 +28,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "gf_eval.cuh"
 #include "gf_internal.cuh"
 
 namespace cg = cooperative_groups;
@@ -379,7 +380,6 @@ __global__ void __launch_bounds__(kThreads) k_prep(const __grid_constant__ FillA
             gxv = dir.x * fall;
             gyv = dir.y * fall;
           }
-          reinterpret_cast<double2*>(A.gfield)[(size_t)f * A.HW + p] = make_double2(gxv, gyv);
         } else if (A.g_mode == 2) {
           const double2 g = reinterpret_cast<const double2*>(A.gsrc)[(size_t)f * A.HW + p];
           gxv = g.x;
@@ -390,6 +390,16 @@ __global__ void __launch_bounds__(kThreads) k_prep(const __grid_constant__ FillA
         }
         rot = (gxv != 0.0 || gyv != 0.0);
         if (active && rot) anyg = true;
+        if (A.gbuf) {
+          // the unit guide of the rotated ball (engine.py:155-158), once per pixel
+          double ux = 0.0, uy = 1.0;
+          if (rot) {
+            const double nr = hypot_np(gxv, gyv);
+            ux = gxv / nr;
+            uy = gyv / nr;
+          }
+          A.gbuf[(size_t)f * A.HW + p] = make_double4(gxv, gyv, ux, uy);
+        }
         const int st = (active ? kStampActive : kStampInactive) | (rot ? kRotBit : 0);
         work[p] = make_float4(0.f, 0.f, 0.f, __int_as_float(st));
       } else if (near) {
@@ -508,6 +518,27 @@ __device__ __forceinline__ void trace_max(const FillArgs& A, int k, int slot) {
     atomicMax(&A.trace[k * kTraceSlots + slot], gtimer());
 }
 
+// Fine phase trace (experiment builds only, -DGF_FINE_TRACE): per-shell
+// maxima of the phases of one work unit in trace row 128 + k; slots 0-3
+// lattice units (entry load, eval, decide, activate), 4-7 rotated units.
+#ifdef GF_FINE_TRACE
+__device__ __forceinline__ unsigned long long fine_after(unsigned v) {
+  if (v == 0xfffffffeu) asm volatile("trap;");
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void fine_put(const FillArgs& A, int k, int slot, unsigned long long d) {
+  if (A.trace && 128 + k < A.trace_cap - 1) atomicMax(&A.trace[(128 + k) * kTraceSlots + slot], d);
+}
+__device__ __forceinline__ void fine_add(const FillArgs& A, int k, int slot, unsigned long long d) {
+  if (A.trace && 128 + k < A.trace_cap - 1) atomicAdd(&A.trace[(128 + k) * kTraceSlots + slot], d);
+}
+#define GF_FINE(x) x
+#else
+#define GF_FINE(x)
+#endif
+
 // largest f with pref[f] <= t
 __device__ __forceinline__ int find_frame(const int* pref, int nF, int t) {
   int lo = 0, hi = nF - 1;
@@ -538,13 +569,10 @@ __device__ __forceinline__ unsigned long long conf_key(double c) {
 
 __device__ __forceinline__ void frame_guide(const FillArgs& A, int f, int p, double& gx,
                                             double& gy) {
-  if (A.g_mode == 2) {
-    const double2 g = reinterpret_cast<const double2*>(A.gsrc)[(size_t)f * A.HW + p];
+  if (A.gbuf) {
+    const double4 g = A.gbuf[(size_t)f * A.HW + p];
     gx = g.x;
     gy = g.y;
-  } else if (A.g_mode == 1) {
-    gx = A.gfx;
-    gy = A.gfy;
   } else {
     gx = 0.0;
     gy = 0.0;
@@ -807,11 +835,17 @@ __device__ void bookkeep(const FillArgs& A, int k) {
 }
 
 #ifndef GF_SHELL_MIN_BLOCKS
-#define GF_SHELL_MIN_BLOCKS 3
+#define GF_SHELL_MIN_BLOCKS 2
 #endif
 
-template <int NL, int KPL, bool kTracked>
+// R in 1..6: radius-specialised evaluators (K <= 128, one pairwise leaf);
+// R == 0: the generic multi-leaf evaluator for larger balls.
+template <int R, bool kTracked>
+#ifdef GF_SHELL_MAXNREG
+__global__ void __maxnreg__(GF_SHELL_MAXNREG)
+#else
 __global__ void __launch_bounds__(kThreads, GF_SHELL_MIN_BLOCKS)
+#endif
     k_shells(const __grid_constant__ FillArgs A, const __grid_constant__ BallParams P,
              const __grid_constant__ BallTables tables) {
   cg::grid_group grid = cg::this_grid();
@@ -822,15 +856,16 @@ __global__ void __launch_bounds__(kThreads, GF_SHELL_MIN_BLOCKS)
     S.tab.n[i] = tables.n[i];
     S.tab.m[i] = tables.m[i];
     S.tab.w0[i] = tables.w0[i];
+    S.tab.ni[i] = tables.ni[i];
+    S.tab.mi[i] = tables.mi[i];
   }
   __syncthreads();
 
   constexpr int kWarps = kThreads / 32;
   // rotated items take the warp-per-item path when the ball is one
-  // pairwise leaf (K <= 128; then A.split == 1); samples per lane there =
-  // ceil(K / 32)
-  constexpr bool kWarpRot = (NL == 1);
-  constexpr int KPW = KPL > 0 ? (KPL + 3) / 4 : 4;
+  // pairwise leaf (K <= 128; then A.split == 1)
+  constexpr int NL = R > 0 ? 1 : kMaxLeaves;
+  constexpr bool kWarpRot = R > 0;
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int glane = lane & (kGroup - 1);
@@ -901,8 +936,10 @@ __global__ void __launch_bounds__(kThreads, GF_SHELL_MIN_BLOCKS)
           const int nL = A.cnt[cur * A.nF + f];
           const int rr = u - S.prefR[f];
           const int j = nL + rr;
+          GF_FINE(const unsigned long long fr0 = fine_after(0u);)
           const uint32_t e = cur_list[(size_t)f * A.cap + A.cap - 1 - rr];
           const uint32_t p = e & kEntryPix;
+          GF_FINE(const unsigned long long fr1 = fine_after(e);)
           if (f != wf) {
             if (kTracked && wf >= 0) warp_flush(A, reg, wn, wf, nxt_list, nxt);
             if (lane == 0 && wf >= 0 && wfills > 0) atomicAdd(&A.fills[cur * A.nF + wf], wfills);
@@ -910,23 +947,33 @@ __global__ void __launch_bounds__(kThreads, GF_SHELL_MIN_BLOCKS)
             wf = f;
           }
           const bool dt_eff = (A.order == 2) && !A.dt_dead[f] && frontier_has_g(A, cur, f);
-          double gx, gy;
-          frame_guide(A, f, (int)p, gx, gy);
+          const double4 g4 = A.gbuf[(size_t)f * A.HW + p];
+          const double gx = g4.x, gy = g4.y;
           float4* fw = A.work + (size_t)f * A.HW;
           WorkSource src{fw, A.c3 ? A.c3 + (size_t)f * A.HW : nullptr, A.H, A.W, A.C, k};
           SampleResult res;
           const unsigned long long tw0 = A.trace ? gtimer() : 0ULL;
-          eval_item_warp<KPW>(P, S.tab, src, lane, true, (double)((int)p % A.W),
-                              (double)((int)p / A.W), gx, gy, res);
+          if constexpr (R > 0)
+            eval_rot_warp<R>(P, S.tab, src, lane, (double)((int)p % A.W), (double)((int)p / A.W),
+                             gx, gy, g4.z, g4.w, res);
           if (A.trace && lane == 0) trace_max_val(A, k, 7, gtimer() - tw0);
+          GF_FINE(const unsigned long long fr2 = fine_after((unsigned)(__double_as_longlong(res.rw) >> 32));)
           bool filled = false;
           if (lane == 0) filled = decide_and_write(A, f, j, p, k, dt_eff, gx, gy, res);
           filled = __shfl_sync(0xffffffffu, filled, 0);
+          GF_FINE(const unsigned long long fr3 = fine_after(filled ? 1u : 0u);)
           if (lane == 0 && filled) ++wfills;
           if (kTracked)
             activate(A, reg, wn, true, nxt_list, nxt, fw, f, k, lane < 8 ? lane : -1, filled, e);
+          GF_FINE(const unsigned long long fr4 = fine_after((unsigned)wn);
+                  if (lane == 0) {
+                    fine_put(A, k, 4, fr2 - fr1); fine_add(A, k, 5, fr2 - fr1);
+                    fine_add(A, k, 6, 1); fine_put(A, k, 7, fr4 - fr3);
+                    (void)fr0;
+                  })
         } else {
           // ---- lattice round: items 4q .. 4q+3 of the concatenated front parts
+          GF_FINE(const unsigned long long fl0 = fine_after(0u);)
           const int q = kWarpRot ? u - TR : u;
           const int t = q * 4 + sub;
           const int TLx = kWarpRot ? TL : T;  // NL > 1: everything lives in the front part
@@ -945,22 +992,35 @@ __global__ void __launch_bounds__(kThreads, GF_SHELL_MIN_BLOCKS)
           const int j = valid ? t - pf[fs] : 0;
           const uint32_t e = valid ? cur_list[(size_t)fs * A.cap + j] : 0u;
           const uint32_t p = e & kEntryPix;
+          GF_FINE(const unsigned long long fl1 = fine_after(e);)
           float4* fw = A.work + (size_t)fs * A.HW;
           WorkSource src{fw, A.c3 ? A.c3 + (size_t)fs * A.HW : nullptr, A.H, A.W, A.C, k};
           const bool dt_eff =
               valid && (A.order == 2) && !A.dt_dead[fs] && frontier_has_g(A, cur, fs);
           double gx = 0.0, gy = 0.0;
-          if (valid && (e & kEntryRot)) frame_guide(A, fs, (int)p, gx, gy);  // NL > 1 only
           SampleResult res;
           const unsigned long long te0 = A.trace ? gtimer() : 0ULL;
-          eval_item<NL, KPL>(P, S.tab, src, glane, valid, (double)((int)p % A.W),
+          if constexpr (R > 0) {
+            eval_lattice<R>(P, S.tab, src, glane, sub, valid, (int)p % A.W, (int)p / A.W, res);
+          } else {
+            if (valid && (e & kEntryRot)) frame_guide(A, fs, (int)p, gx, gy);
+            eval_item<NL, 0>(P, S.tab, src, glane, valid, (double)((int)p % A.W),
                              (double)((int)p / A.W), true, gx, gy, res);
+          }
           if (A.trace && valid && glane == 0) trace_max_val(A, k, 6, gtimer() - te0);
+          GF_FINE(const unsigned long long fl2 = fine_after((unsigned)(__double_as_longlong(res.rw) >> 32));)
           bool filled = false;
           if (valid && glane == 0) filled = decide_and_write(A, fs, j, p, k, dt_eff, gx, gy, res);
           filled = __shfl_sync(0xffffffffu, filled, 0, kGroup);
+          GF_FINE(const unsigned long long fl3 = fine_after(filled ? 1u : 0u);)
           if (kTracked)
             activate(A, reg, wn, uniform, nxt_list, nxt, fw, fs, k, valid ? glane : -1, filled, e);
+          GF_FINE(const unsigned long long fl4 = fine_after((unsigned)wn);
+                  if (valid && glane == 0) {
+                    fine_put(A, k, 0, fl1 - fl0); fine_put(A, k, 1, fl2 - fl1);
+                    fine_add(A, k, 2, fl2 - fl1); fine_add(A, k, 3, 1);
+                    (void)fl3; (void)fl4;
+                  })
           const int nf = (valid && glane == 0 && filled) ? 1 : 0;
           if (uniform) wfills += __reduce_add_sync(0xffffffffu, (unsigned)nf);
           else if (nf) atomicAdd(&A.fills[cur * A.nF + fs], 1);
@@ -1270,20 +1330,20 @@ static void launch_prep(bool f64, int C, dim3 cgrid, dim3 grid, cudaStream_t str
 static size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct Layout {
-  size_t work, c3, list0, list1, conf, gfield, ints, dtile, u64, total;
+  size_t work, c3, list0, list1, conf, gbuf, ints, dtile, u64, total;
 };
 
 static int tiles_of(int H, int W) {
   return ((W + kTile - 1) / kTile) * ((H + kTile - 1) / kTile);
 }
 
-static Layout layout_for(int nF, int H, int W, int C, bool raster) {
+static Layout layout_for(int nF, int H, int W, int C, bool need_g) {
   const int HW = H * W;
   Layout L;
   size_t off = 0;
   const size_t n = (size_t)nF * HW;
   L.work = off; off = align_up(off + n * sizeof(float4));
-  L.gfield = off; off = align_up(off + (raster ? n * 2 * sizeof(double) : 0));
+  L.gbuf = off; off = align_up(off + (need_g ? n * sizeof(double4) : 0));
   L.c3 = off; off = align_up(off + (C > 3 ? n * sizeof(float) : 0));
   L.list0 = off; off = align_up(off + n * sizeof(uint32_t));
   L.list1 = off; off = align_up(off + n * sizeof(uint32_t));
@@ -1295,24 +1355,26 @@ static Layout layout_for(int nF, int H, int W, int C, bool raster) {
   return L;
 }
 
-size_t fill_workspace_bytes(int nF, int H, int W, int C, bool raster) {
+size_t fill_workspace_bytes(int nF, int H, int W, int C, bool need_g) {
   if (nF <= 0 || H <= 0 || W <= 0) return 0;
-  return layout_for(nF, H, W, C, raster).total;
+  return layout_for(nF, H, W, C, need_g).total;
 }
 
 // kernel specialised on the ball size: samples per lane = ceil(K / 8)
 template <bool kTracked>
 static const void* shell_kernel(const BallParams& P) {
-  if (P.plan.n_leaves > 1) return (const void*)k_shells<kMaxLeaves, 0, kTracked>;
-  switch ((P.K + kGroup - 1) / kGroup) {
-    case 1: return (const void*)k_shells<1, 1, kTracked>;
-    case 2: return (const void*)k_shells<1, 2, kTracked>;
-    case 4: return (const void*)k_shells<1, 4, kTracked>;
-    case 6: return (const void*)k_shells<1, 6, kTracked>;
-    case 10: return (const void*)k_shells<1, 10, kTracked>;
-    case 14: return (const void*)k_shells<1, 14, kTracked>;
-    default: return (const void*)k_shells<1, 0, kTracked>;
+  if (P.plan.n_leaves == 1) {
+    switch (P.r) {
+      case 1: return (const void*)k_shells<1, kTracked>;
+      case 2: return (const void*)k_shells<2, kTracked>;
+      case 3: return (const void*)k_shells<3, kTracked>;
+      case 4: return (const void*)k_shells<4, kTracked>;
+      case 5: return (const void*)k_shells<5, kTracked>;
+      case 6: return (const void*)k_shells<6, kTracked>;
+      default: break;
+    }
   }
+  return (const void*)k_shells<0, kTracked>;
 }
 
 static int coop_grid(const void* fn, size_t smem, int* out_grid) {
@@ -1338,7 +1400,8 @@ int fill_launch(const gf_frames* fr, const gf_fill_params* prm, const gf_fill_ou
   const int nF = fr->n_frames, H = fr->height, W = fr->width, C = fr->channels;
   const int HW = H * W;
   const bool raster = spl && spl->n_seg > 0;
-  const Layout L = layout_for(nF, H, W, C, raster);
+  const bool need_g = raster || prm->g_mode != GF_G_ZERO;
+  const Layout L = layout_for(nF, H, W, C, need_g);
   if (ws_bytes < L.total) return set_error(GF_E_WORKSPACE, "workspace too small");
   unsigned char* base = static_cast<unsigned char*>(ws);
 
@@ -1351,8 +1414,6 @@ int fill_launch(const gf_frames* fr, const gf_fill_params* prm, const gf_fill_ou
   A.gsrc = fr->guide;
   A.out = fr->out;
   if (raster) {
-    A.gfield = reinterpret_cast<double*>(base + L.gfield);
-    A.gsrc = A.gfield;
     A.n_seg = spl->n_seg;
     A.frame_seg = spl->frame_seg;
     A.seg = reinterpret_cast<const double4*>(spl->seg);
@@ -1361,6 +1422,7 @@ int fill_launch(const gf_frames* fr, const gf_fill_params* prm, const gf_fill_ou
     A.cut = 3.0 * spl->eta;
     A.c2eta = 2.0 * spl->eta * spl->eta;
   }
+  A.gbuf = need_g ? reinterpret_cast<double4*>(base + L.gbuf) : nullptr;
   A.trace = reinterpret_cast<unsigned long long*>(out->shell_trace);
   A.trace_cap = out->shell_trace ? out->trace_cap : 0;
   A.work = reinterpret_cast<float4*>(base + L.work);

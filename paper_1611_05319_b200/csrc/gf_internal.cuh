@@ -21,8 +21,8 @@ struct FillArgs {
   const void* image;
   const uint8_t* labels;
   const double* guide;
-  const double* gsrc;  // per-pixel guide read by the shell loop (guide or gfield)
-  double* gfield;      // fused-raster output (Inpaint pixels only), or nullptr
+  const double* gsrc;  // caller's per-pixel guide (g_mode 2 without splines)
+  double4* gbuf;       // per Inpaint pixel (gx, gy, ux, uy), written by k_prep, or nullptr
   void* out;
   float4* work;
   float* c3;
@@ -76,7 +76,7 @@ struct FillArgs {
 int set_error(int code, const char* msg);
 
 // gf_fill.cu
-size_t fill_workspace_bytes(int nF, int H, int W, int C, bool raster);
+size_t fill_workspace_bytes(int nF, int H, int W, int C, bool need_g);
 int fill_launch(const gf_frames* fr, const gf_fill_params* prm, const gf_fill_outputs* out,
                 const gf_splines* spl, void* ws, size_t ws_bytes, cudaStream_t stream,
                 const BallParams& P, const BallTables& host_tab);

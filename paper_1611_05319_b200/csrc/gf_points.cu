@@ -21,6 +21,8 @@ __global__ void __launch_bounds__(kPtThreads)
     T.n[i] = tab.n[i];
     T.m[i] = tab.m[i];
     T.w0[i] = tab.w0[i];
+    T.ni[i] = tab.ni[i];
+    T.mi[i] = tab.mi[i];
   }
   __syncthreads();
   const int lane = threadIdx.x & (kGroup - 1);

@@ -39,6 +39,7 @@ __host__ __device__ __forceinline__ bool stamp_unfilled(int st) {
 
 struct BallParams {
   int r, K;
+  double tw0;      // numpy pairwise sum of the g = 0 weights (the lattice-path tw)
   int rotated;   // rotated_ball (engine.py:150-164) vs axis_ball
   int periodic;  // periodic_x
   int mu_inf;
@@ -53,6 +54,8 @@ struct BallTables {
   double n[kMaxK];
   double m[kMaxK];
   double w0[kMaxK];
+  int ni[kMaxK];  // the same offsets as integers (lattice path)
+  int mi[kMaxK];
 };
 
 struct SampleResult {
@@ -131,6 +134,10 @@ struct RawSource {
 __device__ __forceinline__ int pos_mod(long long a, int W) {
   long long r = a % W;
   return (int)(r < 0 ? r + W : r);
+}
+__device__ __forceinline__ int pos_mod32(int a, int W) {
+  const int r = a % W;
+  return r < 0 ? r + W : r;
 }
 
 // Strict bilinear ghost sample at (X, Y), grid.py:186-210.  Returns ok; adds
@@ -252,7 +259,7 @@ __device__ __forceinline__ void ghost_corners(double X, double Y, int H, int W, 
 // Lattice sample index for g = 0 at an integer centre: -1 when out of lattice.
 __device__ __forceinline__ int lattice_index(int x, int y, int H, int W, int periodic) {
   if (y < 0 || y >= H) return -1;
-  if (periodic) x = pos_mod(x, W);
+  if (periodic) x = pos_mod32(x, W);
   else if (x < 0 || x >= W) return -1;
   return y * W + x;
 }
@@ -501,128 +508,6 @@ __device__ __forceinline__ void eval_item(const BallParams& P, const BallTables&
     s += __shfl_xor_sync(0xffffffffu, s, 2, kGroup);
     s += __shfl_xor_sync(0xffffffffu, s, 4, kGroup);
     out.v[c] = (rw != 0.0) ? s / rw : 0.0;
-  }
-  out.rw = rw;
-  out.tw = tw;
-}
-
-// One item per warp (32 lanes) for the rotated-ball path, single pairwise
-// leaf (K <= 128).  Sample k lives in lane k % 32, slot k / 32, so a lane
-// evaluates ceil(K/32) samples instead of ceil(K/8): the long fp64 chains
-// (glibc hypot, SVML exp, two divisions) of a ghost sample run 4x wider.
-// numpy's accumulator j = a_j + a_{j+8} + ... is rebuilt exactly by lane j
-// pulling a_{j+8t} from lane (j + 8t) % 32, slot t / 4 (uniform across
-// lanes for a given t).  Result valid in every lane.
-template <int KPW, class Src>
-__device__ __forceinline__ void eval_item_warp(const BallParams& P, const BallTables& T,
-                                               const Src& src, int lane, bool valid, double fi,
-                                               double fj, double gx, double gy,
-                                               SampleResult& out) {
-  const int K = P.K;
-  const bool gzero = (gx == 0.0) && (gy == 0.0);
-  double ux = 0.0, uy = 1.0;
-  if (P.rotated && !gzero) {
-    const double nr = hypot_np(gx, gy);
-    ux = gx / nr;
-    uy = gy / nr;
-  }
-  double safe = 1.0, thr = 0.0;
-  if (P.mu_inf) {
-    const double nr2 = sqrt(gx * gx + gy * gy);
-    safe = (nr2 == 0.0) ? 1.0 : nr2;
-    double mloc = INFINITY;
-#pragma unroll
-    for (int s = 0; s < KPW; ++s) {
-      const int k = lane + 32 * s;
-      if (k < K) {
-        double px = T.n[k], py = T.m[k];
-        if (P.rotated && !gzero) {
-          px = T.n[k] * uy + T.m[k] * ux;
-          py = (-T.n[k]) * ux + T.m[k] * uy;
-        }
-        const double d = ((-gy) * px + gx * py) / safe;
-        mloc = min_prop(mloc, d * d);
-      }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mloc = min_prop(mloc, __shfl_xor_sync(0xffffffffu, mloc, o));
-    thr = mloc + P.tol_inf;
-  }
-  double w[KPW], wr[KPW];
-  double num[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-  for (int s = 0; s < KPW; ++s) {
-    const int k = lane + 32 * s;
-    w[s] = 0.0;
-    wr[s] = 0.0;
-    if (k < K) {
-      double px, py;
-      if (gzero) {
-        px = T.n[k];
-        py = T.m[k];
-        w[s] = T.w0[k];
-      } else {
-        w[s] = sample_weight(P, T, k, gx, gy, ux, uy, safe, thr, px, py);
-      }
-      Corners cn;
-      ghost_corners(fi + px, fj + py, src.H, src.W, P.periodic, cn);
-      decltype(src.fetch(0)) v[4];
-#pragma unroll
-      for (int c = 0; c < 4; ++c)
-        if (valid && cn.q[c] >= 0) v[c] = src.fetch(cn.q[c]);
-      bool ok = valid && !cn.outside;
-      double sv[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        if (valid && cn.q[c] >= 0) {
-          ok = ok && src.readable(v[c]);
-          src.accumulate(v[c], cn.w[c], sv);
-        }
-      }
-      wr[s] = ok ? w[s] : 0.0;
-      if (ok) {
-#pragma unroll
-        for (int c = 0; c < 4; ++c) num[c] += wr[s] * sv[c];
-      }
-    }
-  }
-  // accumulator j (lanes 0..7): a_j, a_{j+8}, ... in order
-  const int n = K, n8 = n - (n % 8);
-  double acc_rw = 0.0, acc_tw = 0.0;
-  for (int t = 0; t < n8 / 8; ++t) {
-    const int src_lane = (lane & 7) + 8 * (t & 3);
-    const int slot = t >> 2;
-    double a = 0.0, b = 0.0;
-#pragma unroll
-    for (int s = 0; s < KPW; ++s)
-      if (s == slot) {
-        a = wr[s];
-        b = w[s];
-      }
-    acc_rw += __shfl_sync(0xffffffffu, a, src_lane);
-    acc_tw += __shfl_sync(0xffffffffu, b, src_lane);
-  }
-  double rw = group_sum_tree(acc_rw);
-  double tw = group_sum_tree(acc_tw);
-  for (int e = n8; e < n; ++e) {
-    double a = 0.0, b = 0.0;
-#pragma unroll
-    for (int s = 0; s < KPW; ++s)
-      if (s == e / 32) {
-        a = wr[s];
-        b = w[s];
-      }
-    rw = rw + __shfl_sync(0xffffffffu, a, e % 32);
-    tw = tw + __shfl_sync(0xffffffffu, b, e % 32);
-  }
-  rw = __shfl_sync(0xffffffffu, rw, 0);
-  tw = __shfl_sync(0xffffffffu, tw, 0);
-#pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    double sacc = num[c];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, o);
-    out.v[c] = (rw != 0.0) ? sacc / rw : 0.0;
   }
   out.rw = rw;
   out.tw = tw;

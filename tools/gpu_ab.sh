@@ -1,6 +1,5 @@
 mkdir -p gpurun_out
-
-for lib in libgf_b200.so; do
+for lib in ${LIBS:-libgf_b200.so}; do
   GF_B200_LIB=$PWD/paper_1611_05319_b200/$lib timeout -s KILL 300 python bench.py --no-cpu --no-e2e > gpurun_out/bench_$lib.log 2>&1; echo "$lib rc=$?"
   python - "$lib" <<'PY'
 import json,sys
