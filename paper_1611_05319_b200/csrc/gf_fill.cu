@@ -37,7 +37,11 @@ namespace gf {
 
 constexpr int kThreads = 256;
 constexpr int kGroupsPerBlock = kThreads / kGroup;
-constexpr int kAppendCap = kThreads * 9;
+#ifndef GF_SHELL_THREADS
+#define GF_SHELL_THREADS 256
+#endif
+constexpr int kShellThreads = GF_SHELL_THREADS;  // block size of the shell loop
+constexpr int kAppendCap = kShellThreads * 9;
 
 __device__ __forceinline__ unsigned long long enc_ordered(double d) {
   const unsigned long long b = (unsigned long long)__double_as_longlong(d);
@@ -107,131 +111,20 @@ __device__ __forceinline__ double seg_dist(double px, double py, const double4 s
   return hypot_np(px - (ax + t * abx), py - (ay + t * aby));
 }
 
-// Streaming pass over every pixel: Readable pixels are copied to the
-// output (the final hull clip is the identity on them, engine.py:372-375),
-// the value hull of the Readable values is reduced (engine.py:291-296), and
-// every 32x32 tile holding an Inpaint pixel is flagged for k_prep.  Four
-// consecutive pixels per thread; 16-byte loads/stores when the row pitch
-// allows (then non-Readable pixels get their input too; k_finalize
-// overwrites them).
-template <typename T, int C>
-__global__ void __launch_bounds__(kThreads) k_copy(const __grid_constant__ FillArgs A) {
-  const int f = blockIdx.y;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  __shared__ unsigned long long s_red[2][kThreads / 32];
-  const uint8_t* lab = A.labels + (size_t)f * A.HW;
-  const T* img = reinterpret_cast<const T*>(A.image) + (size_t)f * A.HW * C;
-  T* out = reinterpret_cast<T*>(A.out) + (size_t)f * A.HW * C;
-  int* dtile = A.dtile + (size_t)f * A.ntiles;
-  const int tiles_x = (A.W + kTile - 1) / kTile;
-  constexpr int nv = (4 * C * (int)sizeof(T)) / 16;
-  constexpr bool vec_ok = (4 * C * (int)sizeof(T)) % 16 == 0;
-  const bool vec = vec_ok && (A.W % 4 == 0);
-  timeline_mark(A, 0, true);
-  T vlo = T(INFINITY), vhi = T(-INFINITY);
-  const int units = (A.HW + 3) / 4;
-  for (int u = blockIdx.x * kThreads + threadIdx.x; u < units; u += gridDim.x * kThreads) {
-    const int p0 = 4 * u;
-    if (vec) {
-      const uchar4 l4 = *reinterpret_cast<const uchar4*>(lab + p0);
-      const uint8_t l[4] = {l4.x, l4.y, l4.z, l4.w};
-      union {
-        T t[4 * C];
-        uint4 q[nv > 0 ? nv : 1];
-      } v;
-      const uint4* src = reinterpret_cast<const uint4*>(img + (size_t)p0 * C);
-#pragma unroll
-      for (int i = 0; i < nv; ++i) v.q[i] = __ldg(src + i);
-      uint4* dst = reinterpret_cast<uint4*>(out + (size_t)p0 * C);
-#pragma unroll
-      for (int i = 0; i < nv; ++i) dst[i] = v.q[i];
-      bool inp = false;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        inp |= l[q] == 255;
-        if (l[q] == 0) {
-#pragma unroll
-          for (int ch = 0; ch < C; ++ch) {
-            const T x = v.t[q * C + ch];
-            vlo = x < vlo ? x : vlo;
-            vhi = x > vhi ? x : vhi;
-          }
-        }
-      }
-      if (inp) dtile[((p0 / A.W) / kTile) * tiles_x + (p0 % A.W) / kTile] = 1;
-      if (A.enter) *reinterpret_cast<int4*>(A.enter + (size_t)f * A.HW + p0) = make_int4(-1, -1, -1, -1);
-    } else {
-      for (int q = 0; q < 4; ++q) {
-        const int p = p0 + q;
-        if (p >= A.HW) break;
-        const uint8_t l = lab[p];
-        if (A.enter) A.enter[(size_t)f * A.HW + p] = -1;
-        if (l == 255) dtile[((p / A.W) / kTile) * tiles_x + (p % A.W) / kTile] = 1;
-        if (l != 0) continue;
-#pragma unroll
-        for (int ch = 0; ch < C; ++ch) {
-          const T x = img[(size_t)p * C + ch];
-          out[(size_t)p * C + ch] = x;
-          vlo = x < vlo ? x : vlo;
-          vhi = x > vhi ? x : vhi;
-        }
-      }
-    }
-  }
-  unsigned long long emin_inv = 0ULL, emax = 0ULL;  // max(~enc) <=> min(enc)
-  if (vlo <= vhi) {
-    emin_inv = ~enc_ordered((double)vlo);
-    emax = enc_ordered((double)vhi);
-  }
-  for (int o = 16; o > 0; o >>= 1) {
-    const unsigned long long a = __shfl_xor_sync(0xffffffffu, emin_inv, o);
-    const unsigned long long b = __shfl_xor_sync(0xffffffffu, emax, o);
-    emin_inv = a > emin_inv ? a : emin_inv;
-    emax = b > emax ? b : emax;
-  }
-  if (lane == 0) {
-    s_red[0][warp] = emin_inv;
-    s_red[1][warp] = emax;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int w = 0; w < kThreads / 32; ++w) {
-      emin_inv = s_red[0][w] > emin_inv ? s_red[0][w] : emin_inv;
-      emax = s_red[1][w] > emax ? s_red[1][w] : emax;
-    }
-    // most blocks cannot move the frame's hull any more: skip their atomics
-    if (emax != 0ULL) {
-      if (emin_inv > *(volatile unsigned long long*)&A.hull[2 * f]) atomicMax(&A.hull[2 * f], emin_inv);
-      if (emax > *(volatile unsigned long long*)&A.hull[2 * f + 1]) atomicMax(&A.hull[2 * f + 1], emax);
-    }
-  }
-  timeline_mark(A, 0, false);
-}
-
+// One pass over every pixel in 32x32 tiles, frame-major grid (blockIdx.y =
+// frame).  Every tile copies its pixels to the output (Readable pixels are
+// final: the closing hull clip, engine.py:372-375, is the identity on them;
+// fills and the Bystander clip overwrite the others later) and reduces the
+// value hull of its Readable values (engine.py:291-296).  Tiles with an
+// Inpaint pixel within reach go on to the D-tile work below.
 template <typename T, int C>
 __global__ void __launch_bounds__(kThreads) k_prep(const __grid_constant__ FillArgs A) {
   const int f = blockIdx.y;
   const int tiles_x = (A.W + kTile - 1) / kTile;
-  const int tiles_y = (A.H + kTile - 1) / kTile;
   const int tix = (int)(blockIdx.x % tiles_x), tiy = (int)(blockIdx.x / tiles_x);
   const int tx0 = tix * kTile;
   const int ty0 = tiy * kTile;
-  // only tiles within one tile of an Inpaint pixel (r + 1 <= 13 < 32) work
-  {
-    const int* dtile = A.dtile + (size_t)f * A.ntiles;
-    bool any = false;
-    for (int dy = -1; dy <= 1; ++dy) {
-      const int ty = tiy + dy;
-      if (ty < 0 || ty >= tiles_y) continue;
-      for (int dx = -1; dx <= 1; ++dx) {
-        int tx = tix + dx;
-        if (A.periodic) tx = (tx + tiles_x) % tiles_x;
-        else if (tx < 0 || tx >= tiles_x) continue;
-        any |= dtile[ty * tiles_x + tx] != 0;
-      }
-    }
-    if (!any) return;
-  }
+  timeline_mark(A, 0, true);
   const int R = A.halo;
   const int ext = kTile + 2 * R;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -244,6 +137,7 @@ __global__ void __launch_bounds__(kThreads) k_prep(const __grid_constant__ FillA
   __shared__ int s_cnt[kThreads / 32];
   __shared__ int s_wl[kThreads / 32], s_wr[kThreads / 32];
   __shared__ int s_bL, s_bR;
+  __shared__ unsigned long long s_red[4][kThreads / 32];
   const uint8_t* lab = A.labels + (size_t)f * A.HW;
   const T* img = reinterpret_cast<const T*>(A.image) + (size_t)f * A.HW * C;
   float4* work = A.work + (size_t)f * A.HW;
@@ -291,9 +185,102 @@ __global__ void __launch_bounds__(kThreads) k_prep(const __grid_constant__ FillA
       s_rrow64[y] = ((unsigned long long)rhi << 32) | rlo;
     }
   }
-  // a tile with no Inpaint pixel in reach only copies its Readable pixels
+  // the thread's 4 pixels: loads issued before the label sync
+  const int gx0 = tx0 + c0;
+  constexpr int nv = (4 * C * (int)sizeof(T)) / 16;
+  constexpr bool vec_ok = (4 * C * (int)sizeof(T)) % 16 == 0;
+  const bool row_in = gy < A.H;
+  const bool vec = vec_ok && (A.W % 4 == 0) && row_in && gx0 < A.W;
+  union {
+    T t[4 * C];
+    uint4 q[nv > 0 ? nv : 1];
+  } px;
+  if (vec) {
+    const uint4* src = reinterpret_cast<const uint4*>(img + ((size_t)gy * A.W + gx0) * C);
+#pragma unroll
+    for (int i = 0; i < nv; ++i) px.q[i] = __ldg(src + i);
+  } else {
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int ch = 0; ch < C; ++ch)
+        px.t[u * C + ch] = (row_in && gx0 + u < A.W) ? __ldg(img + ((size_t)gy * A.W + gx0 + u) * C + ch) : T(0);
+  }
   const bool tile_d = __syncthreads_or(any_inp);
-  if (tile_d && raster) {
+  // copy to the output + value hull of the Readable pixels
+  {
+    T* out = reinterpret_cast<T*>(A.out) + (size_t)f * A.HW * C;
+    if (vec) {
+      uint4* dst = reinterpret_cast<uint4*>(out + ((size_t)gy * A.W + gx0) * C);
+#pragma unroll
+      for (int i = 0; i < nv; ++i) dst[i] = px.q[i];
+    } else {
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (row_in && gx0 + u < A.W)
+#pragma unroll
+          for (int ch = 0; ch < C; ++ch) out[((size_t)gy * A.W + gx0 + u) * C + ch] = px.t[u * C + ch];
+    }
+    // [0] value hull of the Readable pixels, [1] range of the Bystanders
+    T vlo[2] = {T(INFINITY), T(INFINITY)}, vhi[2] = {T(-INFINITY), T(-INFINITY)};
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint8_t l = s_lab[ry + R][c0 + u + R];
+      if (row_in && gx0 + u < A.W && (l == 0 || l == 128)) {
+        const int b = l == 0 ? 0 : 1;
+#pragma unroll
+        for (int ch = 0; ch < C; ++ch) {
+          const T x = px.t[u * C + ch];
+          vlo[b] = x < vlo[b] ? x : vlo[b];
+          vhi[b] = x > vhi[b] ? x : vhi[b];
+        }
+      }
+    }
+    unsigned long long ered[4];  // max(~enc) <=> min(enc)
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      ered[2 * b] = vlo[b] <= vhi[b] ? ~enc_ordered((double)vlo[b]) : 0ULL;
+      ered[2 * b + 1] = vlo[b] <= vhi[b] ? enc_ordered((double)vhi[b]) : 0ULL;
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long a = __shfl_xor_sync(0xffffffffu, ered[i], o);
+        ered[i] = a > ered[i] ? a : ered[i];
+      }
+      if (lane == 0) s_red[i][warp] = ered[i];
+    }
+    if (A.fillshell && row_in) {
+      int* fsh = A.fillshell + (size_t)f * A.HW + (size_t)gy * A.W + gx0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (gx0 + u < A.W) fsh[u] = -1;
+    }
+    __syncthreads();
+    if (threadIdx.x < 4) {
+      const int i = threadIdx.x;
+      unsigned long long e = 0ULL;
+      for (int w = 0; w < kThreads / 32; ++w) e = s_red[i][w] > e ? s_red[i][w] : e;
+      // i < 2: the frame's hull (most tiles cannot move it any more: skip
+      // their atomics); i >= 2: the tile's Bystander range, read by the
+      // shell loop's clip, and the frame's
+      unsigned long long* fr = i < 2 ? &A.hull[2 * f + i] : &A.bys_frame[2 * f + i - 2];
+      if (e != 0ULL && e > *(volatile unsigned long long*)fr) atomicMax(fr, e);
+      if (i >= 2) A.bys[((size_t)f * A.ntiles + blockIdx.x) * 2 + i - 2] = e;
+    }
+  }
+  if (!tile_d) {
+    // no Inpaint pixel within reach: nothing of this tile is ever sampled
+    if (A.enter && row_in) {
+      int* en = A.enter + (size_t)f * A.HW + (size_t)gy * A.W + gx0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (gx0 + u < A.W) en[u] = -1;
+    }
+    timeline_mark(A, 0, false);
+    return;
+  }
+  if (raster) {
     const double x0 = (double)tx0, x1 = (double)min(A.W - 1, tx0 + kTile - 1);
     const double y0 = (double)ty0, y1 = (double)min(A.H - 1, ty0 + kTile - 1);
     const int s0 = A.frame_seg ? A.frame_seg[f] : 0;
@@ -310,7 +297,7 @@ __global__ void __launch_bounds__(kThreads) k_prep(const __grid_constant__ FillA
   }
   // 2. horizontal dilation of the Inpaint indicator: bit c of s_hrow[y] <=>
   //    an Inpaint pixel in ext columns [c, c + 2R]
-  if (tile_d) {
+  {
     for (int y = threadIdx.x; y < ext; y += kThreads) {
       const unsigned long long m = s_hrow64[y];
       unsigned long long h = m;
@@ -327,8 +314,7 @@ __global__ void __launch_bounds__(kThreads) k_prep(const __grid_constant__ FillA
 
   // 3. four consecutive pixels per thread: row ry, columns c0 .. c0+3
   unsigned int vmask = 0;
-  if (tile_d)
-    for (int dy = 0; dy <= 2 * R; ++dy) vmask |= s_hrow[ry + dy];
+  for (int dy = 0; dy <= 2 * R; ++dy) vmask |= s_hrow[ry + dy];
   int n_inp = 0;
   bool anyg = false;
   uint32_t ent[4];
@@ -344,12 +330,11 @@ __global__ void __launch_bounds__(kThreads) k_prep(const __grid_constant__ FillA
     if (in) {
       if (l == 0) {
         if (near) {
-          T cv[4] = {T(0), T(0), T(0), T(0)};
+          float cv[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-          for (int ch = 0; ch < C; ++ch) cv[ch] = __ldg(img + (size_t)p * C + ch);
-          work[p] = make_float4((float)cv[0], (float)cv[1], (float)cv[2],
-                                __int_as_float(kStampReadable));
-          if (C > 3) A.c3[(size_t)f * A.HW + p] = (float)cv[3];
+          for (int ch = 0; ch < C; ++ch) cv[ch] = (float)px.t[u * C + ch];
+          work[p] = make_float4(cv[0], cv[1], cv[2], __int_as_float(kStampReadable));
+          if (C > 3) A.c3[(size_t)f * A.HW + p] = cv[3];
         }
       } else if (l == 255) {
         ++n_inp;
@@ -488,13 +473,13 @@ struct Smem {
   unsigned char act[kMaxFramesPerLaunch];
   unsigned char dl[kMaxFramesPerLaunch];
   uint32_t app[kAppendCap];
-  int red[kThreads / 32];
-  unsigned long long redk[kThreads / 32];
-  int any_dl;
+  int red[kShellThreads / 32];
+  unsigned long long redk[kShellThreads / 32];
+  int any_dl, any_clip;
   int total, totalL, totalR;
   // block-level flush of the warps' staged appends
-  int bf_frame[kThreads / 32], bf_nL[kThreads / 32], bf_nR[kThreads / 32];
-  int bf_fill[kThreads / 32], bf_anyg[kThreads / 32], bf_bL[kThreads / 32], bf_bR[kThreads / 32];
+  int bf_frame[kShellThreads / 32], bf_nL[kShellThreads / 32], bf_nR[kShellThreads / 32];
+  int bf_fill[kShellThreads / 32], bf_anyg[kShellThreads / 32], bf_bL[kShellThreads / 32], bf_bR[kShellThreads / 32];
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -558,7 +543,7 @@ __device__ __forceinline__ unsigned long long block_max_u64(unsigned long long v
   if ((threadIdx.x & 31) == 0) S.redk[threadIdx.x >> 5] = v;
   __syncthreads();
   unsigned long long t = 0;
-  for (int w = 0; w < kThreads / 32; ++w) t = S.redk[w] > t ? S.redk[w] : t;
+  for (int w = 0; w < kShellThreads / 32; ++w) t = S.redk[w] > t ? S.redk[w] : t;
   return t;
 }
 
@@ -616,7 +601,7 @@ __device__ __forceinline__ void append_direct(const FillArgs& A, uint32_t* list,
 
 // Warp-private append staging: each warp owns a slice of S.app and a
 // warp-uniform count; a slice is published with one atomic per list part.
-constexpr int kWarpAppCap = kAppendCap / (kThreads / 32);
+constexpr int kWarpAppCap = kAppendCap / (kShellThreads / 32);
 
 __device__ __forceinline__ void warp_push(uint32_t* reg, int& n, bool want, uint32_t e) {
   const unsigned m = __ballot_sync(0xffffffffu, want);
@@ -681,6 +666,82 @@ __device__ __forceinline__ void warp_flush(const FillArgs& A, uint32_t* reg, int
   n = 0;
 }
 
+// Output of a filled pixel: its fp32 fill value clipped to the frame's value
+// hull of the initially Readable values (engine.py:372-375), stored in the
+// caller's dtype.
+__device__ __forceinline__ void write_out(const FillArgs& A, int f, uint32_t p, const float* v) {
+  const unsigned long long elo = ~A.hull[2 * f], ehi = A.hull[2 * f + 1];
+  const bool has_hull = ehi != 0ULL;
+  const double lo = has_hull ? dec_ordered(elo) : 0.0;
+  const double hi = has_hull ? dec_ordered(ehi) : 0.0;
+  const size_t o = ((size_t)f * A.HW + p) * A.C;
+  for (int c = 0; c < A.C; ++c) {
+    double x = (double)v[c];
+    if (has_hull) x = (x < lo) ? lo : ((x > hi) ? hi : x);
+    if (A.dtype == GF_F64) reinterpret_cast<double*>(A.out)[o + c] = x;
+    else reinterpret_cast<float*>(A.out)[o + c] = (float)x;
+  }
+}
+
+// Bystander clip (engine.py:372-375), one 32x32 tile per warp.  k_prep
+// recorded each tile's Bystander value range: a tile whose range lies in
+// the frame's hull is already final (the clip is the identity), so only
+// tiles holding out-of-hull Bystanders are touched.  Tiles are handed out by
+// an atomic counter to warps with no fill work in a shell, the rest after
+// the last shell.
+__device__ __forceinline__ bool range_inside(const FillArgs& A, int f, const unsigned long long* r) {
+  const unsigned long long hl = A.hull[2 * f], hh = A.hull[2 * f + 1];
+  if (hh == 0ULL || r[1] == 0ULL) return true;  // no hull (no clip) or no Bystander
+  return r[0] <= hl && r[1] <= hh;              // ~enc(min) <= ~enc(lo), enc(max) <= enc(hi)
+}
+
+template <typename T>
+__device__ __forceinline__ void clip_tile_rows(const FillArgs& A, int f, int tx0, int ty0, double lo,
+                                               double hi) {
+  const int lane = threadIdx.x & 31;
+  const int x = tx0 + lane;
+  if (x >= A.W) return;
+  const uint8_t* lab = A.labels + (size_t)f * A.HW;
+  const T* in = reinterpret_cast<const T*>(A.image) + (size_t)f * A.HW * A.C;
+  T* out = reinterpret_cast<T*>(A.out) + (size_t)f * A.HW * A.C;
+  for (int y0 = ty0; y0 < min(A.H, ty0 + kTile); y0 += 8) {
+    uint8_t l[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) l[i] = (y0 + i < A.H) ? lab[(size_t)(y0 + i) * A.W + x] : 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      if (l[i] == 128) {
+        const size_t g = ((size_t)(y0 + i) * A.W + x) * A.C;
+        for (int c = 0; c < A.C; ++c) {
+          double v = (double)in[g + c];
+          v = (v < lo) ? lo : ((v > hi) ? hi : v);
+          out[g + c] = (T)v;
+        }
+      }
+  }
+}
+
+__device__ __noinline__ void clip_tile(const FillArgs& A, int chunk) {
+  const int f = chunk / A.ntiles, t = chunk - f * A.ntiles;
+  const unsigned long long* r = A.bys + ((size_t)f * A.ntiles + t) * 2;
+  if (range_inside(A, f, r)) return;
+  const double lo = dec_ordered(~A.hull[2 * f]), hi = dec_ordered(A.hull[2 * f + 1]);
+  const int tiles_x = (A.W + kTile - 1) / kTile;
+  const int tx0 = (t % tiles_x) * kTile, ty0 = (t / tiles_x) * kTile;
+  if (A.dtype == GF_F64) clip_tile_rows<double>(A, f, tx0, ty0, lo, hi);
+  else clip_tile_rows<float>(A, f, tx0, ty0, lo, hi);
+}
+
+// one tile for the calling warp; false once every tile is taken
+__device__ __forceinline__ bool clip_claim(const FillArgs& A) {
+  int c = A.clip_total;
+  if ((threadIdx.x & 31) == 0 && *(volatile int*)A.clip_next < A.clip_total) c = atomicAdd(A.clip_next, 1);
+  c = __shfl_sync(0xffffffffu, c, 0);
+  if (c >= A.clip_total) return false;
+  clip_tile(A, c);
+  return true;
+}
+
 // ready / fill decision of one item (engine.py:317-333) and the in-place
 // write of its colour with the shell stamp (snapshot-safe: stamp k+1 is
 // unreadable for every other item of shell k).
@@ -705,7 +766,10 @@ __device__ __forceinline__ bool decide_and_write(const FillArgs& A, int f, int j
     o.z = (float)r.v[2];
     o.w = __int_as_float(k + 1);
     A.work[(size_t)f * A.HW + p] = o;
-    if (A.c3) A.c3[(size_t)f * A.HW + p] = (float)r.v[3];
+    const float v[4] = {o.x, o.y, o.z, (float)r.v[3]};
+    if (A.c3) A.c3[(size_t)f * A.HW + p] = v[3];
+    write_out(A, f, p, v);
+    if (A.fillshell) A.fillshell[(size_t)f * A.HW + p] = k;
   }
   return fill;
 }
@@ -779,7 +843,7 @@ __device__ void block_flush(const FillArgs& A, Smem& S, const uint32_t* reg, int
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    constexpr int NW = kThreads / 32;
+    constexpr int NW = kShellThreads / 32;
     bool done[NW];
     for (int w = 0; w < NW; ++w) done[w] = S.bf_frame[w] < 0;
     for (int w = 0; w < NW; ++w) {
@@ -844,7 +908,7 @@ template <int R, bool kTracked>
 #ifdef GF_SHELL_MAXNREG
 __global__ void __maxnreg__(GF_SHELL_MAXNREG)
 #else
-__global__ void __launch_bounds__(kThreads, GF_SHELL_MIN_BLOCKS)
+__global__ void __launch_bounds__(kShellThreads, GF_SHELL_MIN_BLOCKS)
 #endif
     k_shells(const __grid_constant__ FillArgs A, const __grid_constant__ BallParams P,
              const __grid_constant__ BallTables tables) {
@@ -861,7 +925,15 @@ __global__ void __launch_bounds__(kThreads, GF_SHELL_MIN_BLOCKS)
   }
   __syncthreads();
 
-  constexpr int kWarps = kThreads / 32;
+  // does any frame hold a Bystander outside its hull?  (else no clip work)
+  if (threadIdx.x == 0) {
+    int need = 0;
+    for (int f = 0; f < A.nF && !need; ++f) need = !range_inside(A, f, A.bys_frame + 2 * f);
+    S.any_clip = need;
+  }
+  __syncthreads();
+  const bool clip_work = S.any_clip != 0;
+  constexpr int kWarps = kShellThreads / 32;
   // rotated items take the warp-per-item path when the ball is one
   // pairwise leaf (K <= 128; then A.split == 1)
   constexpr int NL = R > 0 ? 1 : kMaxLeaves;
@@ -1029,6 +1101,8 @@ __global__ void __launch_bounds__(kThreads, GF_SHELL_MIN_BLOCKS)
       }
       if (kTracked && wf >= 0) warp_flush(A, reg, wn, wf, nxt_list, nxt);
       if (lane == 0 && wf >= 0 && wfills > 0) atomicAdd(&A.fills[cur * A.nF + wf], wfills);
+      // a warp without fill work this shell clips one chunk of Bystanders
+      if (clip_work && blockIdx.x * kWarps + warp >= U) clip_claim(A);
       if (A.trace && lane == 0 && k < A.trace_cap)
         atomicMax(&A.trace[k * kTraceSlots + 1], gtimer());
     }
@@ -1047,7 +1121,7 @@ __global__ void __launch_bounds__(kThreads, GF_SHELL_MIN_BLOCKS)
     }
     __syncthreads();
     if (S.any_dl) {
-      const int chunk = max(kThreads, (T + gridDim.x - 1) / gridDim.x);
+      const int chunk = max(kShellThreads, (T + gridDim.x - 1) / gridDim.x);
       const int c_lo = min(T, blockIdx.x * chunk), c_hi = min(T, c_lo + chunk);
       // G1: max confidence key per stalled frame
       for (int s = c_lo; s < c_hi;) {
@@ -1172,7 +1246,10 @@ __global__ void __launch_bounds__(kThreads, GF_SHELL_MIN_BLOCKS)
             o.z = (float)v[2];
             o.w = __int_as_float(k + 1);
             A.work[(size_t)f * A.HW + p] = o;
-            if (A.c3) A.c3[(size_t)f * A.HW + p] = (float)v[3];
+            const float fv[4] = {o.x, o.y, o.z, (float)v[3]};
+            if (A.c3) A.c3[(size_t)f * A.HW + p] = fv[3];
+            write_out(A, f, (uint32_t)p, fv);
+            if (A.fillshell) A.fillshell[(size_t)f * A.HW + p] = k;
             A.fills[cur * A.nF + f] = 1;
             A.deadlocks[f] += 1;
           }
@@ -1187,7 +1264,7 @@ __global__ void __launch_bounds__(kThreads, GF_SHELL_MIN_BLOCKS)
       for (int f = 0; f < A.nF; ++f) nA += S.act[f] && A.done[f] == 0;
       const long long TP = (long long)nA * A.HW;
       const long long pchunk =
-          ((TP + gridDim.x - 1) / gridDim.x + kThreads - 1) / kThreads * kThreads;
+          ((TP + gridDim.x - 1) / gridDim.x + kShellThreads - 1) / kShellThreads * kShellThreads;
       const long long p_lo = min(TP, (long long)blockIdx.x * pchunk), p_hi = min(TP, p_lo + pchunk);
       int wn = 0;
       for (long long s = p_lo; s < p_hi;) {
@@ -1203,7 +1280,7 @@ __global__ void __launch_bounds__(kThreads, GF_SHELL_MIN_BLOCKS)
           }
         const long long fe = min(p_hi, (long long)(a + 1) * A.HW);
         float4* fw = A.work + (size_t)f * A.HW;
-        for (long long base = s; base < fe; base += kThreads) {
+        for (long long base = s; base < fe; base += kShellThreads) {
           const long long t = base + threadIdx.x;
           bool want = false;
           uint32_t e = 0;
@@ -1235,6 +1312,9 @@ __global__ void __launch_bounds__(kThreads, GF_SHELL_MIN_BLOCKS)
       trace_set(A, k, 4, gtimer());
     }
   }
+  // the Bystander chunks no idle warp took
+  while (clip_work && clip_claim(A)) {
+  }
   timeline_mark(A, 1, false);
   // final bookkeeping: stats
   if (blockIdx.x == 0) {
@@ -1252,61 +1332,11 @@ __global__ void __launch_bounds__(kThreads, GF_SHELL_MIN_BLOCKS)
   }
 }
 
-// ------------------------------------------------------------ finalize
-//
-// Writes the output for every non-Readable pixel (Readable ones were copied
-// by k_prep): Bystanders are clipped to the value hull of the initially
-// Readable values, filled pixels take their fp32 fill value clipped to the
-// same hull (engine.py:372-375), stranded Inpaint pixels keep their input
-// (the caller's unfillable fallback paints them).  Optionally emits the
-// per-pixel fill shell (order log).
-template <typename T>
-__global__ void __launch_bounds__(kThreads) k_finalize(const __grid_constant__ FillArgs A) {
-  timeline_mark(A, 2, true);
-  const long long total = (long long)A.nF * A.HW;
-  for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < total;
-       g += (long long)gridDim.x * blockDim.x) {
-    const uint8_t l = A.labels[g];
-    if (l == 0) {
-      if (A.fillshell) A.fillshell[g] = -1;
-      continue;
-    }
-    const int f = (int)(g / A.HW);
-    const unsigned long long elo = ~A.hull[2 * f], ehi = A.hull[2 * f + 1];
-    const bool has_hull = ehi != 0ULL;
-    const double lo = has_hull ? dec_ordered(elo) : 0.0;
-    const double hi = has_hull ? dec_ordered(ehi) : 0.0;
-    const T* in = reinterpret_cast<const T*>(A.image) + (size_t)g * A.C;
-    T* out = reinterpret_cast<T*>(A.out) + (size_t)g * A.C;
-    bool filled = false;
-    int st = 0;
-    float fv[4] = {0.f, 0.f, 0.f, 0.f};
-    if (l == 255) {
-      const float4 px = A.work[g];
-      st = __float_as_int(px.w);
-      filled = st >= 1 && st < kStampInactive;
-      fv[0] = px.x;
-      fv[1] = px.y;
-      fv[2] = px.z;
-      if (A.c3 && filled) fv[3] = A.c3[g];
-    }
-    for (int c = 0; c < A.C; ++c) {
-      double v = filled ? (double)fv[c] : (double)in[c];
-      if (has_hull) v = (v < lo) ? lo : ((v > hi) ? hi : v);
-      out[c] = (T)v;
-    }
-    if (A.fillshell) A.fillshell[g] = filled ? st - 1 : -1;
-  }
-  timeline_mark(A, 2, false);
-}
-
 // ---------------------------------------------------------------- host
 
-static void launch_prep(bool f64, int C, dim3 cgrid, dim3 grid, cudaStream_t stream,
-                        const FillArgs& A) {
+static void launch_prep(bool f64, int C, dim3 grid, cudaStream_t stream, const FillArgs& A) {
 #define GF_PREP(T, CC)                                   \
   do {                                                   \
-    k_copy<T, CC><<<cgrid, kThreads, 0, stream>>>(A);    \
     k_prep<T, CC><<<grid, kThreads, 0, stream>>>(A);     \
   } while (0)
   if (f64) {
@@ -1330,7 +1360,7 @@ static void launch_prep(bool f64, int C, dim3 cgrid, dim3 grid, cudaStream_t str
 static size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct Layout {
-  size_t work, c3, list0, list1, conf, gbuf, ints, dtile, u64, total;
+  size_t work, c3, list0, list1, conf, gbuf, bys, ints, u64, total;
 };
 
 static int tiles_of(int H, int W) {
@@ -1348,9 +1378,9 @@ static Layout layout_for(int nF, int H, int W, int C, bool need_g) {
   L.list0 = off; off = align_up(off + n * sizeof(uint32_t));
   L.list1 = off; off = align_up(off + n * sizeof(uint32_t));
   L.conf = off; off = align_up(off + n * sizeof(double));
+  L.bys = off; off = align_up(off + (size_t)nF * tiles_of(H, W) * 2 * sizeof(unsigned long long));
   L.ints = off; off = align_up(off + (size_t)nF * kIntsPerFrame * sizeof(int));
-  L.dtile = off; off = align_up(off + (size_t)nF * tiles_of(H, W) * sizeof(int));
-  L.u64 = off; off = align_up(off + (size_t)nF * 4 * sizeof(unsigned long long));
+  L.u64 = off; off = align_up(off + (size_t)nF * 6 * sizeof(unsigned long long));
   L.total = off;
   return L;
 }
@@ -1387,7 +1417,7 @@ static int coop_grid(const void* fn, size_t smem, int* out_grid) {
   if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return set_error(GF_E_CUDA, "cudaFuncSetAttribute failed");
   int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, smem) != cudaSuccess ||
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kShellThreads, smem) != cudaSuccess ||
       per_sm <= 0)
     return set_error(GF_E_CUDA, "occupancy query failed");
   *out_grid = sms * per_sm;
@@ -1445,11 +1475,14 @@ int fill_launch(const gf_frames* fr, const gf_fill_params* prm, const gf_fill_ou
   A.inpaint = ints;          ints += nF;
   A.overflow = ints;         ints += nF;
   A.last_f = ints;           ints += nF;
-  A.dtile = reinterpret_cast<int*>(base + L.dtile);
+  A.clip_next = ints;         ints += 1;
   A.ntiles = tiles_of(H, W);
+  A.clip_total = nF * A.ntiles;
+  A.bys = reinterpret_cast<unsigned long long*>(base + L.bys);
   unsigned long long* u64 = reinterpret_cast<unsigned long long*>(base + L.u64);
   A.best_key = u64;
   A.hull = u64 + nF;
+  A.bys_frame = u64 + 3 * nF;
   A.stats = out->frame_stats;
   A.rows = out->rows;
   A.rows_cap = out->rows_cap;
@@ -1468,19 +1501,14 @@ int fill_launch(const gf_frames* fr, const gf_fill_params* prm, const gf_fill_ou
 
   // per-frame counters start at zero (the hull minimum is stored inverted
   // and the data-term latch as a "dead" flag, so zero is the initial state)
-  if (cudaMemsetAsync(base + L.ints, 0, L.u64 + (size_t)nF * 4 * sizeof(unsigned long long) - L.ints,
+  if (cudaMemsetAsync(base + L.ints, 0, L.u64 + (size_t)nF * 6 * sizeof(unsigned long long) - L.ints,
                       stream) != cudaSuccess)
     return set_error(GF_E_CUDA, "memset failed");
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const long long total = (long long)nF * HW;
-  {
-    const int units = (HW + 3) / 4;
-    const int cblocks = std::max(1, std::min((units + kThreads - 1) / kThreads,
-                                             std::max(1, sms * 8 / std::max(1, nF))));
-    launch_prep(fr->dtype == GF_F64, C, dim3(cblocks, nF), dim3(tiles_of(H, W), nF), stream, A);
-  }
+  launch_prep(fr->dtype == GF_F64, C, dim3(tiles_of(H, W), nF), stream, A);
   if (cudaPeekAtLastError() != cudaSuccess)
     return set_error(GF_E_CUDA, cudaGetErrorString(cudaGetLastError()));
 
@@ -1490,14 +1518,9 @@ int fill_launch(const gf_frames* fr, const gf_fill_params* prm, const gf_fill_ou
   int rc = coop_grid(fn, smem, &grid);
   if (rc != GF_OK) return rc;
   void* args[] = {(void*)&A, (void*)&P, (void*)&host_tab};
-  cudaError_t e = cudaLaunchCooperativeKernel(fn, grid, kThreads, args, smem, stream);
+  cudaError_t e = cudaLaunchCooperativeKernel(fn, grid, kShellThreads, args, smem, stream);
   if (e != cudaSuccess) return set_error(GF_E_CUDA, cudaGetErrorString(e));
 
-  const int fgrid = (int)std::min<long long>((total + kThreads - 1) / kThreads, (long long)sms * 16);
-  if (fr->dtype == GF_F64)
-    k_finalize<double><<<fgrid, kThreads, 0, stream>>>(A);
-  else
-    k_finalize<float><<<fgrid, kThreads, 0, stream>>>(A);
   e = cudaPeekAtLastError();
   if (e != cudaSuccess) return set_error(GF_E_CUDA, cudaGetErrorString(e));
   return GF_OK;

@@ -12,7 +12,7 @@
 namespace gf {
 
 constexpr int kMaxFramesPerLaunch = 1024;
-constexpr int kIntsPerFrame = 18;  // cnt[2] cntR[2] fills[2] anyg[2] + 10 scalars
+constexpr int kIntsPerFrame = 19;  // cnt[2] cntR[2] fills[2] anyg[2] + 10 scalars (+ 1 shared)
 
 // Everything the fill kernels need, passed by value (__grid_constant__).
 struct FillArgs {
@@ -57,8 +57,11 @@ struct FillArgs {
   int periodic;
   int split;       // rotated-ball entries kept in the back part (K <= 128)
   int halo;        // r + 1: farthest pixel a ball sample's corners can touch
-  int* dtile;      // [nF][ntiles] 32x32 tile holds an Inpaint pixel
-  int ntiles;
+  int* clip_next;  // Bystander-clip tile counter (shell loop)
+  int clip_total;  // tiles over all frames
+  int ntiles;      // 32x32 tiles per frame
+  unsigned long long* bys;        // [nF][ntiles][2] Bystander value range per tile (encoded)
+  unsigned long long* bys_frame;  // [nF][2] the same per frame
   // fused spline raster (guide.py:286-327), n_seg == 0 when off
   int n_seg;
   const int32_t* frame_seg;  // per-frame segment ranges or nullptr
