@@ -95,6 +95,12 @@ __device__ __forceinline__ void timeline_mark(const FillArgs& A, int stage, bool
   atomicMax(&row[2 * stage + (start ? 0 : 1)], start ? ~t : t);
 }
 
+// Programmatic dependent launch: each k_prep block signals at its end, so
+// the shell kernel's launch overlaps the last prep wave; the shell kernel
+// waits for k_prep's completion (and memory) before its first read.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 constexpr int kMaxCand = 512;
 constexpr int kTile = 32;
 constexpr int kMaxHalo = GF_MAX_RADIUS + 1;
@@ -278,6 +284,7 @@ __global__ void __launch_bounds__(kThreads) k_prep(const __grid_constant__ FillA
         if (gx0 + u < A.W) en[u] = -1;
     }
     timeline_mark(A, 0, false);
+    pdl_trigger();
     return;
   }
   if (raster) {
@@ -454,6 +461,7 @@ __global__ void __launch_bounds__(kThreads) k_prep(const __grid_constant__ FillA
     if (blk_anyg) A.anyg[f] = 1;
   }
   timeline_mark(A, 0, false);
+  pdl_trigger();
 }
 
 // ------------------------------------------------------- shell loop
@@ -470,6 +478,8 @@ struct Smem {
   int pref[kMaxFramesPerLaunch + 1];   // all items
   int prefL[kMaxFramesPerLaunch + 1];  // lattice part
   int prefR[kMaxFramesPerLaunch + 1];  // rotated part
+  int nLf[kMaxFramesPerLaunch];  // frame's lattice / rotated items (0 if inactive)
+  int nRf[kMaxFramesPerLaunch];
   unsigned char act[kMaxFramesPerLaunch];
   unsigned char dl[kMaxFramesPerLaunch];
   uint32_t app[kAppendCap];
@@ -570,6 +580,15 @@ __device__ __forceinline__ bool frontier_has_g(const FillArgs& A, int which, int
   if (A.g_mode == 2) return A.anyg[which * A.nF + f] != 0;
   if (A.g_mode == 1) return A.gfx != 0.0 || A.gfy != 0.0;
   return false;
+}
+
+// Data-term latch (engine.py:327-329) as of shell k: released once some
+// earlier frontier held no g != 0 pixel.  dt_dead covers the shells block 0
+// has booked (it may lag one shell behind), the previous frontier's own flag
+// the rest, so every block sees the same answer.
+__device__ __forceinline__ bool frontier_has_g(const FillArgs& A, int which, int f);
+__device__ __forceinline__ bool dt_dead_at(const FillArgs& A, int f, int k, int prv) {
+  return A.dt_dead[f] != 0 || (k > 0 && !frontier_has_g(A, prv, f));
 }
 
 __device__ __forceinline__ int frontier_size(const FillArgs& A, int which, int f) {
@@ -877,7 +896,7 @@ __device__ void block_flush(const FillArgs& A, Smem& S, const uint32_t* reg, int
 
 // Bookkeeping of shell k-1 (block 0 only): report row, remaining, latch.
 __device__ void bookkeep(const FillArgs& A, int k) {
-  const int prev = (k - 1) & 1;
+  const int prev = (k + 3) % 4;  // counter slot of shell k-1
   for (int f = threadIdx.x; f < A.nF; f += blockDim.x) {
     const int F = frontier_size(A, prev, f);
     if (F > 0 && A.done[f] == 0) {
@@ -898,6 +917,61 @@ __device__ void bookkeep(const FillArgs& A, int k) {
   }
 }
 
+// Shell prologue (every block): the frame table of the frontier in slot
+// `slot` -- which frames are active and the prefix sums that deal their
+// items over the grid.
+__device__ __forceinline__ void build_prefix(const FillArgs& A, Smem& S) {
+  if (threadIdx.x == 0) {
+    int run = 0, runL = 0, runR = 0;
+    for (int f = 0; f < A.nF; ++f) {
+      S.pref[f] = run;
+      S.prefL[f] = runL;
+      S.prefR[f] = runR;
+      run += S.nLf[f] + S.nRf[f];
+      runL += S.nLf[f];
+      runR += S.nRf[f];
+    }
+    S.pref[A.nF] = run;
+    S.prefL[A.nF] = runL;
+    S.prefR[A.nF] = runR;
+    S.total = run;
+    S.totalL = runL;
+    S.totalR = runR;
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void stage_frame(Smem& S, int f, int nL, int nR, int done) {
+  const bool act = nL + nR > 0 && done == 0;
+  S.act[f] = act ? 1 : 0;
+  S.nLf[f] = act ? nL : 0;
+  S.nRf[f] = act ? nR : 0;
+}
+
+__device__ void load_p0(const FillArgs& A, Smem& S, int slot) {
+  for (int f = threadIdx.x; f < A.nF; f += blockDim.x)
+    stage_frame(S, f, A.cnt[slot * A.nF + f], A.cntR[slot * A.nF + f], A.done[f]);
+  __syncthreads();
+  build_prefix(A, S);
+}
+
+// Book-keeping done by one block while the others fill shell k: the report
+// row of shell k-1, the unfillable mark of shell k's frames, and the
+// clearing of the counter slot shell k+1 will append to (no block touches
+// it in shell k).  Ordered before the shell-end barrier.
+__device__ void book_shell(const FillArgs& A, int k, int cur, int clr) {
+  if (k > 0) bookkeep(A, k);
+  for (int f = threadIdx.x; f < A.nF; f += blockDim.x) {
+    if (A.done[f] == 0 && frontier_size(A, cur, f) == 0 && A.remaining[f] > 0) A.done[f] = 2;
+    A.cnt[clr * A.nF + f] = 0;
+    A.cntR[clr * A.nF + f] = 0;
+    A.anyg[clr * A.nF + f] = 0;
+    A.fills[clr * A.nF + f] = 0;
+    A.best_key[f] = 0ULL;
+    A.best_p[f] = 0x7fffffff;
+  }
+}
+
 #ifndef GF_SHELL_MIN_BLOCKS
 #define GF_SHELL_MIN_BLOCKS 2
 #endif
@@ -913,7 +987,6 @@ __global__ void __launch_bounds__(kShellThreads, GF_SHELL_MIN_BLOCKS)
     k_shells(const __grid_constant__ FillArgs A, const __grid_constant__ BallParams P,
              const __grid_constant__ BallTables tables) {
   cg::grid_group grid = cg::this_grid();
-  timeline_mark(A, 1, true);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Smem& S = *reinterpret_cast<Smem*>(smem_raw);
   for (int i = threadIdx.x; i < P.K; i += blockDim.x) {
@@ -923,6 +996,8 @@ __global__ void __launch_bounds__(kShellThreads, GF_SHELL_MIN_BLOCKS)
     S.tab.ni[i] = tables.ni[i];
     S.tab.mi[i] = tables.mi[i];
   }
+  pdl_wait();
+  timeline_mark(A, 1, true);
   __syncthreads();
 
   // does any frame hold a Bystander outside its hull?  (else no clip work)
@@ -943,49 +1018,20 @@ __global__ void __launch_bounds__(kShellThreads, GF_SHELL_MIN_BLOCKS)
   const int glane = lane & (kGroup - 1);
   const int sub = lane / kGroup;  // 8-lane group within the warp
   uint32_t* reg = S.app + warp * kWarpAppCap;
+  const bool booker = blockIdx.x == gridDim.x - 1;  // last block: fewest fill units
 
-  for (int k = 0;; ++k) {
-    const int cur = k & 1, nxt = cur ^ 1;
-    uint32_t* cur_list = cur ? A.list1 : A.list0;
-    uint32_t* nxt_list = cur ? A.list0 : A.list1;
-    // ---- P0: bookkeeping of shell k-1 (block 0), frame activity, prefixes
-    if (blockIdx.x == 0) {
-      if (k > 0) bookkeep(A, k);
-      __syncthreads();
-      for (int f = threadIdx.x; f < A.nF; f += blockDim.x) {
-        if (A.done[f] == 0 && frontier_size(A, cur, f) == 0 && A.remaining[f] > 0) A.done[f] = 2;
-        A.cnt[nxt * A.nF + f] = 0;
-        A.cntR[nxt * A.nF + f] = 0;
-        A.fills[nxt * A.nF + f] = 0;
-        A.anyg[nxt * A.nF + f] = 0;
-        A.best_key[f] = 0ULL;
-        A.best_p[f] = 0x7fffffff;
-      }
-    }
-    for (int f = threadIdx.x; f < A.nF; f += blockDim.x)
-      S.act[f] = (frontier_size(A, cur, f) > 0 && A.done[f] == 0) ? 1 : 0;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      int run = 0, runL = 0, runR = 0;
-      for (int f = 0; f < A.nF; ++f) {
-        S.pref[f] = run;
-        S.prefL[f] = runL;
-        S.prefR[f] = runR;
-        if (S.act[f]) {
-          const int nL = A.cnt[cur * A.nF + f], nR = A.cntR[cur * A.nF + f];
-          run += nL + nR;
-          runL += nL;
-          runR += nR;
-        }
-      }
-      S.pref[A.nF] = run;
-      S.prefL[A.nF] = runL;
-      S.prefR[A.nF] = runR;
-      S.total = run;
-      S.totalL = runL;
-      S.totalR = runR;
-    }
-    __syncthreads();
+  load_p0(A, S, 0);
+  int k = 0;
+  for (;; ++k) {
+    // Frontier lists alternate between two buffers; their counters (cnt,
+    // cntR, anyg) and the fill counts rotate through four slots: cur = this
+    // shell's frontier, nxt = the one being built, prv = shell k-1's (its
+    // report row is booked in this shell, its g flag read by the data-term
+    // latch), clr = shell k-2's, cleared by the booking block for shell k+1
+    // -- a slot no other block reads or writes in this shell.
+    const int cur = k % 4, nxt = (k + 1) % 4, prv = (k + 3) % 4, clr = (k + 2) % 4;
+    uint32_t* cur_list = (k & 1) ? A.list1 : A.list0;
+    uint32_t* nxt_list = (k & 1) ? A.list0 : A.list1;
     const int T = S.total;
     if (T == 0) break;
     trace_set(A, k, 0, gtimer());
@@ -1005,7 +1051,7 @@ __global__ void __launch_bounds__(kShellThreads, GF_SHELL_MIN_BLOCKS)
         if (kWarpRot && u < TR) {
           // ---- rotated-ball item, one whole warp
           const int f = find_frame(S.prefR, A.nF, u);
-          const int nL = A.cnt[cur * A.nF + f];
+          const int nL = S.prefL[f + 1] - S.prefL[f];
           const int rr = u - S.prefR[f];
           const int j = nL + rr;
           GF_FINE(const unsigned long long fr0 = fine_after(0u);)
@@ -1018,7 +1064,7 @@ __global__ void __launch_bounds__(kShellThreads, GF_SHELL_MIN_BLOCKS)
             wfills = 0;
             wf = f;
           }
-          const bool dt_eff = (A.order == 2) && !A.dt_dead[f] && frontier_has_g(A, cur, f);
+          const bool dt_eff = (A.order == 2) && !dt_dead_at(A, f, k, prv) && frontier_has_g(A, cur, f);
           const double4 g4 = A.gbuf[(size_t)f * A.HW + p];
           const double gx = g4.x, gy = g4.y;
           float4* fw = A.work + (size_t)f * A.HW;
@@ -1068,7 +1114,7 @@ __global__ void __launch_bounds__(kShellThreads, GF_SHELL_MIN_BLOCKS)
           float4* fw = A.work + (size_t)fs * A.HW;
           WorkSource src{fw, A.c3 ? A.c3 + (size_t)fs * A.HW : nullptr, A.H, A.W, A.C, k};
           const bool dt_eff =
-              valid && (A.order == 2) && !A.dt_dead[fs] && frontier_has_g(A, cur, fs);
+              valid && (A.order == 2) && !dt_dead_at(A, fs, k, prv) && frontier_has_g(A, cur, fs);
           double gx = 0.0, gy = 0.0;
           SampleResult res;
           const unsigned long long te0 = A.trace ? gtimer() : 0ULL;
@@ -1106,21 +1152,23 @@ __global__ void __launch_bounds__(kShellThreads, GF_SHELL_MIN_BLOCKS)
       if (A.trace && lane == 0 && k < A.trace_cap)
         atomicMax(&A.trace[k * kTraceSlots + 1], gtimer());
     }
+    if (booker) book_shell(A, k, cur, clr);
     grid.sync();
     trace_set(A, k, 2, gtimer());
 
-    // ---- G: deadlock guard (engine.py:334-348), only when some frame stalled
-    if (threadIdx.x == 0) {
-      int any = 0;
-      for (int f = 0; f < A.nF; ++f) {
-        const int d = S.act[f] && A.fills[cur * A.nF + f] == 0;
-        S.dl[f] = (unsigned char)d;
-        any |= d;
-      }
-      S.any_dl = any;
+    // ---- G: deadlock guard (engine.py:334-348), only when some frame
+    // stalled.  The stall test and the next shell's frame table come from
+    // one round of loads (tracked: the next frontier is complete here).
+    int any = 0;
+    for (int f = threadIdx.x; f < A.nF; f += blockDim.x) {
+      const int d = S.act[f] && A.fills[cur * A.nF + f] == 0;
+      S.dl[f] = (unsigned char)d;
+      any |= d;
+      if (kTracked) stage_frame(S, f, A.cnt[nxt * A.nF + f], A.cntR[nxt * A.nF + f], A.done[f]);
     }
-    __syncthreads();
-    if (S.any_dl) {
+    any = __syncthreads_or(any);
+    if (kTracked && !any) build_prefix(A, S);
+    if (any) {
       const int chunk = max(kShellThreads, (T + gridDim.x - 1) / gridDim.x);
       const int c_lo = min(T, blockIdx.x * chunk), c_hi = min(T, c_lo + chunk);
       // G1: max confidence key per stalled frame
@@ -1256,6 +1304,7 @@ __global__ void __launch_bounds__(kShellThreads, GF_SHELL_MIN_BLOCKS)
         }
       }
       grid.sync();
+      if (kTracked) load_p0(A, S, nxt);
     }
 
     // ---- B: untracked frontier = full-lattice rescan (engine.py:357-360)
@@ -1310,14 +1359,16 @@ __global__ void __launch_bounds__(kShellThreads, GF_SHELL_MIN_BLOCKS)
       trace_max(A, k, 3);
       grid.sync();
       trace_set(A, k, 4, gtimer());
+      load_p0(A, S, nxt);
     }
   }
   // the Bystander chunks no idle warp took
   while (clip_work && clip_claim(A)) {
   }
   timeline_mark(A, 1, false);
-  // final bookkeeping: stats
-  if (blockIdx.x == 0) {
+  // the last shell's row, then the stats
+  if (booker) {
+    if (k > 0) bookkeep(A, k);
     for (int f = threadIdx.x; f < A.nF; f += blockDim.x) {
       int* st = A.stats + (size_t)f * GF_STATS;
       st[GF_STAT_ITERATIONS] = A.iters[f];
@@ -1461,10 +1512,10 @@ int fill_launch(const gf_frames* fr, const gf_fill_params* prm, const gf_fill_ou
   A.list1 = reinterpret_cast<uint32_t*>(base + L.list1);
   A.conf = reinterpret_cast<double*>(base + L.conf);
   int* ints = reinterpret_cast<int*>(base + L.ints);
-  A.cnt = ints;              ints += 2 * nF;
-  A.cntR = ints;             ints += 2 * nF;
-  A.fills = ints;            ints += 2 * nF;
-  A.anyg = ints;             ints += 2 * nF;
+  A.cnt = ints;              ints += 4 * nF;
+  A.cntR = ints;             ints += 4 * nF;
+  A.fills = ints;            ints += 4 * nF;
+  A.anyg = ints;             ints += 4 * nF;
   A.remaining = ints;        ints += nF;
   A.iters = ints;            ints += nF;
   A.done = ints;             ints += nF;
@@ -1518,7 +1569,24 @@ int fill_launch(const gf_frames* fr, const gf_fill_params* prm, const gf_fill_ou
   int rc = coop_grid(fn, smem, &grid);
   if (rc != GF_OK) return rc;
   void* args[] = {(void*)&A, (void*)&P, (void*)&host_tab};
-  cudaError_t e = cudaLaunchCooperativeKernel(fn, grid, kShellThreads, args, smem, stream);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kShellThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  cudaError_t e = cudaLaunchKernelExC(&cfg, fn, args);
+  if (e != cudaSuccess) {
+    // without programmatic serialisation: a plain cooperative launch
+    (void)cudaGetLastError();
+    e = cudaLaunchCooperativeKernel(fn, grid, kShellThreads, args, smem, stream);
+  }
   if (e != cudaSuccess) return set_error(GF_E_CUDA, cudaGetErrorString(e));
 
   e = cudaPeekAtLastError();

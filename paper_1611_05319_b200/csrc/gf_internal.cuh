@@ -12,7 +12,7 @@
 namespace gf {
 
 constexpr int kMaxFramesPerLaunch = 1024;
-constexpr int kIntsPerFrame = 19;  // cnt[2] cntR[2] fills[2] anyg[2] + 10 scalars (+ 1 shared)
+constexpr int kIntsPerFrame = 27;  // cnt[4] cntR[4] fills[4] anyg[4] + 10 scalars (+ 1 shared)
 
 // Everything the fill kernels need, passed by value (__grid_constant__).
 struct FillArgs {
@@ -29,10 +29,10 @@ struct FillArgs {
   uint32_t* list0;
   uint32_t* list1;
   double* conf;
-  int* cnt;        // [2][nF] frontier list front part (lattice entries)
-  int* cntR;       // [2][nF] frontier list back part (rotated-ball entries)
-  int* fills;      // [2][nF] pixels filled in the shell
-  int* anyg;       // [2][nF] frontier holds a g != 0 pixel (data-term latch)
+  int* cnt;        // [4][nF] frontier list front part (lattice entries)
+  int* cntR;       // [4][nF] frontier list back part (rotated-ball entries)
+  int* fills;      // [4][nF] pixels filled in the shell
+  int* anyg;       // [4][nF] frontier holds a g != 0 pixel (data-term latch)
   int* remaining;  // [nF]
   int* iters;      // [nF]
   int* done;       // [nF] 0 running, 1 complete, 2 unfillable
