@@ -43,18 +43,9 @@ def resolve_g_mode(params, guide_present: bool) -> int:
         "B200 fill path yet (SURVEY.md section 8f-2)")
 
 
-def fill_device(image, labels, guide, params, tracked=True, order_log=False, rows_cap=None,
+def _fill_setup(image, labels, guide, params, tracked=True, order_log=False, rows_cap=None,
                 workspace=None, splines=None, eta=3.0, trace_cap=0, want_fillshell=False):
-    """Fill a batch of frames on the GPU.
-
-    image: (N, H, W, C) float32/float64 CUDA tensor; labels: (N, H, W) uint8;
-    guide: (N, H, W, 2) float64 or None; splines: a SegmentSet to raster the
-    guide field inside the fill (gf_fill_splines) instead of ``guide``.
-    Returns a dict of CUDA tensors: ``out`` (like image), ``stats``
-    (N, GF_STATS) int32, ``rows`` (N, rows_cap, 2) int32, with order_log
-    ``enter``/``fillshell`` (N, H, W) int32, with trace_cap > 0 ``trace``
-    (trace_cap, 8) int64 per-shell phase timestamps.
-    """
+    """Output buffers, workspace and the C-ABI argument structs of one fill."""
     import torch
 
     N.require_cuda()
@@ -68,7 +59,7 @@ def fill_device(image, labels, guide, params, tracked=True, order_log=False, row
     dev = image.device
     dtype = N.GF_F64 if image.dtype == torch.float64 else N.GF_F32
     out = torch.empty_like(image)
-    stats = torch.zeros((nF, N.GF_STATS), dtype=torch.int32, device=dev)
+    stats = torch.empty((nF, N.GF_STATS), dtype=torch.int32, device=dev)  # every field is written
     if rows_cap is None:
         rows_cap = min(H * W + 1, max(1024, (1 << 24) // max(1, nF)))
     rows = torch.empty((nF, rows_cap, 2), dtype=torch.int32, device=dev)
@@ -87,23 +78,78 @@ def fill_device(image, labels, guide, params, tracked=True, order_log=False, row
                         0 if enter is None else enter.data_ptr(),
                         0 if fillshell is None else fillshell.data_ptr(),
                         0 if trace is None else trace.data_ptr(), int(trace_cap))
+    sc = splines.as_c(eta) if raster else None
     if raster:
-        sc = splines.as_c(eta)
         need = lib.gf_fill_splines_workspace_bytes(ctypes.byref(fr), ctypes.byref(pc),
                                                    ctypes.byref(sc))
     else:
         need = lib.gf_fill_workspace_bytes(ctypes.byref(fr), ctypes.byref(pc))
     if workspace is None or workspace.numel() < need:
         workspace = torch.empty(need, dtype=torch.uint8, device=dev)
-    if raster:
-        N.check(lib.gf_fill_splines(ctypes.byref(fr), ctypes.byref(pc), ctypes.byref(sc),
-                                    ctypes.byref(oc), ctypes.c_void_p(workspace.data_ptr()), need,
-                                    N.stream_ptr()))
+    res = dict(out=out, stats=stats, rows=rows, enter=enter, fillshell=fillshell,
+               workspace=workspace, rows_cap=rows_cap, trace=trace)
+    # the structs keep raw pointers: hold the tensors they point into
+    call = dict(fr=fr, pc=pc, oc=oc, sc=sc, need=need, keep=(image, labels, guide, splines))
+    return res, call
+
+
+def _fill_launch(res, call):
+    """The C-ABI fill call on the current stream (memset + k_prep + k_shells)."""
+    lib = N.load()
+    ws = ctypes.c_void_p(res["workspace"].data_ptr())
+    if call["sc"] is not None:
+        N.check(lib.gf_fill_splines(ctypes.byref(call["fr"]), ctypes.byref(call["pc"]),
+                                    ctypes.byref(call["sc"]), ctypes.byref(call["oc"]), ws,
+                                    call["need"], N.stream_ptr()))
     else:
-        N.check(lib.gf_fill(ctypes.byref(fr), ctypes.byref(pc), ctypes.byref(oc),
-                            ctypes.c_void_p(workspace.data_ptr()), need, N.stream_ptr()))
-    return dict(out=out, stats=stats, rows=rows, enter=enter, fillshell=fillshell,
-                workspace=workspace, rows_cap=rows_cap, trace=trace)
+        N.check(lib.gf_fill(ctypes.byref(call["fr"]), ctypes.byref(call["pc"]),
+                            ctypes.byref(call["oc"]), ws, call["need"], N.stream_ptr()))
+
+
+def fill_device(image, labels, guide, params, tracked=True, order_log=False, rows_cap=None,
+                workspace=None, splines=None, eta=3.0, trace_cap=0, want_fillshell=False):
+    """Fill a batch of frames on the GPU.
+
+    image: (N, H, W, C) float32/float64 CUDA tensor; labels: (N, H, W) uint8;
+    guide: (N, H, W, 2) float64 or None; splines: a SegmentSet to raster the
+    guide field inside the fill (gf_fill_splines) instead of ``guide``.
+    Returns a dict of CUDA tensors: ``out`` (like image), ``stats``
+    (N, GF_STATS) int32, ``rows`` (N, rows_cap, 2) int32, with order_log
+    ``enter``/``fillshell`` (N, H, W) int32, with trace_cap > 0 ``trace``
+    (trace_cap, 8) int64 per-shell phase timestamps.
+    """
+    res, call = _fill_setup(image, labels, guide, params, tracked, order_log, rows_cap, workspace,
+                            splines, eta, trace_cap, want_fillshell)
+    _fill_launch(res, call)
+    return res
+
+
+class FillGraph:
+    """One fill captured as a CUDA graph for fixed device buffers.
+
+    For streams of same-shaped frames (video, serving): the memset, k_prep
+    and the cooperative shell kernel replay without any host launch work.
+    New frames are written into the ``image`` / ``labels`` tensors given
+    here (``copy_``); ``replay()`` refills ``self.res`` (the fill_device
+    outputs) on the current stream.
+    """
+
+    def __init__(self, image, labels, guide, params, tracked=True, rows_cap=4096, splines=None,
+                 eta=3.0, want_fillshell=False):
+        import torch
+
+        self.res, self.call = _fill_setup(image, labels, guide, params, tracked, False, rows_cap,
+                                          None, splines, eta, 0, want_fillshell)
+        _fill_launch(self.res, self.call)  # warm-up: function attributes, occupancy
+        torch.cuda.synchronize()
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            _fill_launch(self.res, self.call)
+        torch.cuda.synchronize()
+
+    def replay(self):
+        self.graph.replay()
+        return self.res
 
 
 def splines_to_segments(splines):

@@ -29,56 +29,80 @@ struct Ball {
   static_assert(K <= 128, "one pairwise leaf");
 };
 
-// Lattice item (g = 0, integral centre) on an 8-lane group.  Lane j of the
-// group owns samples j, j+8, j+16, ... = numpy accumulator j, so its
-// readable mass is summed in registers; the accumulator tree is three xor
-// shuffles, the tail samples (k >= N8, owned by slot KPL-1) are added from
-// a ballot of their readability.  tw is the host's constant P.tw0.
-template <int R>
+// Lattice item (g = 0, integral centre) on a group of LG = 8 or 4 lanes.
+// Lane j owns samples j, j+LG, j+2LG, ...; numpy's accumulator of sample k
+// is k % 8, so with LG = 8 a lane holds accumulator j, with LG = 4 it holds
+// accumulators j (even slots) and j+4 (odd slots), each summed in sample
+// order in registers.  The accumulator tree ((r0+r1)+(r2+r3))+((r4+r5)+
+// (r6+r7)) is three xor levels (LG = 8) or two plus the lane-local pair
+// (LG = 4); the tail samples (k >= N8) are added in order from ballots of
+// their readability.  tw is the host's constant P.tw0.
+template <int R, int LG>
 __device__ __forceinline__ void eval_lattice(const BallParams& P, const BallTables& T,
                                              const WorkSource& src, int glane, int sub, bool valid,
                                              int pi, int pj, SampleResult& out) {
   using B = Ball<R>;
-  int q[B::KPL];
-  float4 v[B::KPL];
+  static_assert(LG == 8 || LG == 4, "8 or 4 lanes per item");
+  constexpr int KPL = (B::K + LG - 1) / LG;
+  int q[KPL];
+  float4 v[KPL];
 #pragma unroll
-  for (int t = 0; t < B::KPL; ++t) {
-    const int k = glane + kGroup * t;
+  for (int t = 0; t < KPL; ++t) {
+    const int k = glane + LG * t;
     q[t] = (valid && k < B::K) ? lattice_index(pi + T.ni[k], pj + T.mi[k], src.H, src.W, P.periodic)
                                : -1;
   }
 #pragma unroll
-  for (int t = 0; t < B::KPL; ++t)
+  for (int t = 0; t < KPL; ++t)
     if (q[t] >= 0) v[t] = src.work[q[t]];
-  unsigned okm = 0;  // bit t: sample glane + 8t readable
+  unsigned okm = 0;  // bit t: sample glane + LG t readable
 #pragma unroll
-  for (int t = 0; t < B::KPL; ++t)
+  for (int t = 0; t < KPL; ++t)
     if (q[t] >= 0 && __float_as_int(v[t].w) <= src.shell) okm |= 1u << t;
-  double acc = 0.0;
+  double acc0 = 0.0, acc1 = 0.0;  // accumulators glane (and glane + 4 when LG == 4)
 #pragma unroll
-  for (int t = 0; t < B::N8 / kGroup; ++t)
-    if ((okm >> t) & 1u) acc += T.w0[glane + kGroup * t];  // + 0.0 would be the identity
-  acc = group_sum_tree(acc);
+  for (int t = 0; t < B::N8 / LG; ++t)
+    if ((okm >> t) & 1u) {  // + 0.0 for an unreadable sample would be the identity
+      const double w = T.w0[glane + LG * t];
+      if (LG == 8 || (t & 1) == 0) acc0 += w;
+      else acc1 += w;
+    }
+  double acc;
+  if constexpr (LG == 8) {
+    acc = group_sum_tree(acc0);
+  } else {
+    acc0 = acc0 + __shfl_xor_sync(0xffffffffu, acc0, 1, LG);
+    acc1 = acc1 + __shfl_xor_sync(0xffffffffu, acc1, 1, LG);
+    acc0 = acc0 + __shfl_xor_sync(0xffffffffu, acc0, 2, LG);
+    acc1 = acc1 + __shfl_xor_sync(0xffffffffu, acc1, 2, LG);
+    acc = acc0 + acc1;
+  }
   if constexpr (B::NT > 0) {
-    const unsigned tb =
-        (__ballot_sync(0xffffffffu, (okm >> (B::KPL - 1)) & 1u) >> (kGroup * sub)) & 0xffu;
+    constexpr int ts0 = B::N8 / LG, ts1 = (B::K - 1) / LG;  // slots holding the tail
+    unsigned tb0 = (__ballot_sync(0xffffffffu, (okm >> ts0) & 1u) >> (LG * sub)) & ((1u << LG) - 1);
+    unsigned tb1 = tb0;
+    if constexpr (ts1 != ts0)
+      tb1 = (__ballot_sync(0xffffffffu, (okm >> ts1) & 1u) >> (LG * sub)) & ((1u << LG) - 1);
 #pragma unroll
-    for (int e = 0; e < B::NT; ++e)
-      if ((tb >> e) & 1u) acc = acc + T.w0[B::N8 + e];
+    for (int e = 0; e < B::NT; ++e) {
+      const int k = B::N8 + e;
+      const unsigned tb = (k / LG == ts0) ? tb0 : tb1;
+      if ((tb >> (k % LG)) & 1u) acc = acc + T.w0[k];
+    }
   }
   double num[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-  for (int t = 0; t < B::KPL; ++t)
+  for (int t = 0; t < KPL; ++t)
     if ((okm >> t) & 1u) {
-      const double w = T.w0[glane + kGroup * t];
+      const double w = T.w0[glane + LG * t];
       num[0] += w * (double)v[t].x;
       num[1] += w * (double)v[t].y;
       num[2] += w * (double)v[t].z;
     }
   if (src.c3) {
 #pragma unroll
-    for (int t = 0; t < B::KPL; ++t)
-      if ((okm >> t) & 1u) num[3] += T.w0[glane + kGroup * t] * (double)src.c3[q[t]];
+    for (int t = 0; t < KPL; ++t)
+      if ((okm >> t) & 1u) num[3] += T.w0[glane + LG * t] * (double)src.c3[q[t]];
   }
   const double inv = (acc != 0.0) ? 1.0 / acc : 0.0;
 #pragma unroll
@@ -86,9 +110,8 @@ __device__ __forceinline__ void eval_lattice(const BallParams& P, const BallTabl
     double s = 0.0;
     if (c < 3 || src.c3) {
       s = num[c];
-      s += __shfl_xor_sync(0xffffffffu, s, 1, kGroup);
-      s += __shfl_xor_sync(0xffffffffu, s, 2, kGroup);
-      s += __shfl_xor_sync(0xffffffffu, s, 4, kGroup);
+#pragma unroll
+      for (int o = 1; o < LG; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o, LG);
     }
     out.v[c] = s * inv;
   }

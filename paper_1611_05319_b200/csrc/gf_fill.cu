@@ -28,6 +28,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <mutex>
+#include <vector>
+
 #include "gf_eval.cuh"
 #include "gf_internal.cuh"
 
@@ -818,28 +821,38 @@ __device__ __forceinline__ uint32_t claim(float4* fw, int q) {
 
 // Tracked frontier maintenance fused into the fill (tracker.py:42-79): an
 // unfilled item re-enters the next list (entry e, flag kept), a filled
-// item's Inpaint 8-neighbours join it.  Lane `o` (0..7, -1 = idle) handles
-// neighbour o.  `staged`: warp-uniform; false -> direct global appends (the
-// items of this warp-round belong to different frames).  Every lane calls.
+// item's Inpaint 8-neighbours join it.  Lane gl (0..LG-1, -1 = idle) of the
+// item's group handles neighbours gl, gl + LG, ...  `staged`: warp-uniform;
+// false -> direct global appends (the items of this warp-round belong to
+// different frames).  Every lane calls.
+template <int LG>
 __device__ __forceinline__ void activate(const FillArgs& A, uint32_t* reg, int& n, bool staged,
                                          uint32_t* nxt_list, int nxt, float4* fw, int f, int k,
-                                         int o, bool filled, uint32_t e) {
-  const bool survive = o == 0 && !filled;
-  uint32_t qe = 0xffffffffu;
-  if (o >= 0 && filled) {
-    bool in;
-    const int q = neighbor_of(A, e & kEntryPix, o, in);
-    if (in) {
-      qe = claim(fw, q);
-      if (qe != 0xffffffffu && A.enter) A.enter[(size_t)f * A.HW + q] = k + 1;
+                                         int gl, bool filled, uint32_t e) {
+  constexpr int NPL = 8 / LG;  // neighbours per lane
+  const bool survive = gl == 0 && !filled;
+  uint32_t qe[NPL];
+#pragma unroll
+  for (int r = 0; r < NPL; ++r) {
+    qe[r] = 0xffffffffu;
+    if (gl >= 0 && filled) {
+      bool in;
+      const int q = neighbor_of(A, e & kEntryPix, gl + LG * r, in);
+      if (in) {
+        qe[r] = claim(fw, q);
+        if (qe[r] != 0xffffffffu && A.enter) A.enter[(size_t)f * A.HW + q] = k + 1;
+      }
     }
   }
   if (staged) {
     warp_push(reg, n, survive, e);
-    warp_push(reg, n, qe != 0xffffffffu, qe);
+#pragma unroll
+    for (int r = 0; r < NPL; ++r) warp_push(reg, n, qe[r] != 0xffffffffu, qe[r]);
   } else {
     if (survive) append_direct(A, nxt_list, nxt, f, e);
-    if (qe != 0xffffffffu) append_direct(A, nxt_list, nxt, f, qe);
+#pragma unroll
+    for (int r = 0; r < NPL; ++r)
+      if (qe[r] != 0xffffffffu) append_direct(A, nxt_list, nxt, f, qe[r]);
   }
 }
 
@@ -1016,7 +1029,15 @@ __global__ void __launch_bounds__(kShellThreads, GF_SHELL_MIN_BLOCKS)
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int glane = lane & (kGroup - 1);
-  const int sub = lane / kGroup;  // 8-lane group within the warp
+  // lattice items: LG lanes each (4 for the r <= 3 balls: K <= 28 samples,
+  // 7 per lane), IPU = 32 / LG items per warp round
+#ifndef GF_LATTICE_LANES
+#define GF_LATTICE_LANES 4
+#endif
+  constexpr int LG = (R > 0 && R <= 3) ? GF_LATTICE_LANES : 8;
+  constexpr int IPU = 32 / LG;
+  const int lglane = lane & (LG - 1);
+  const int lsub = lane / LG;
   uint32_t* reg = S.app + warp * kWarpAppCap;
   const bool booker = blockIdx.x == gridDim.x - 1;  // last block: fewest fill units
 
@@ -1043,7 +1064,7 @@ __global__ void __launch_bounds__(kShellThreads, GF_SHELL_MIN_BLOCKS)
     // 8-lane group).  No block barrier.
     {
       const int TR = S.totalR, TL = S.totalL;
-      const int UL = (TL + 3) / 4;
+      const int UL = (TL + IPU - 1) / IPU;
       const int U = TR + UL;
       const int NW = gridDim.x * kWarps;
       int wn = 0, wf = -1, wfills = 0;
@@ -1070,11 +1091,11 @@ __global__ void __launch_bounds__(kShellThreads, GF_SHELL_MIN_BLOCKS)
           float4* fw = A.work + (size_t)f * A.HW;
           WorkSource src{fw, A.c3 ? A.c3 + (size_t)f * A.HW : nullptr, A.H, A.W, A.C, k};
           SampleResult res;
-          const unsigned long long tw0 = A.trace ? gtimer() : 0ULL;
+          GF_FINE(const unsigned long long tw0 = A.trace ? gtimer() : 0ULL;)
           if constexpr (R > 0)
             eval_rot_warp<R>(P, S.tab, src, lane, (double)((int)p % A.W), (double)((int)p / A.W),
                              gx, gy, g4.z, g4.w, res);
-          if (A.trace && lane == 0) trace_max_val(A, k, 7, gtimer() - tw0);
+          GF_FINE(if (A.trace && lane == 0) trace_max_val(A, k, 7, gtimer() - tw0);)
           GF_FINE(const unsigned long long fr2 = fine_after((unsigned)(__double_as_longlong(res.rw) >> 32));)
           bool filled = false;
           if (lane == 0) filled = decide_and_write(A, f, j, p, k, dt_eff, gx, gy, res);
@@ -1082,7 +1103,7 @@ __global__ void __launch_bounds__(kShellThreads, GF_SHELL_MIN_BLOCKS)
           GF_FINE(const unsigned long long fr3 = fine_after(filled ? 1u : 0u);)
           if (lane == 0 && filled) ++wfills;
           if (kTracked)
-            activate(A, reg, wn, true, nxt_list, nxt, fw, f, k, lane < 8 ? lane : -1, filled, e);
+            activate<8>(A, reg, wn, true, nxt_list, nxt, fw, f, k, lane < 8 ? lane : -1, filled, e);
           GF_FINE(const unsigned long long fr4 = fine_after((unsigned)wn);
                   if (lane == 0) {
                     fine_put(A, k, 4, fr2 - fr1); fine_add(A, k, 5, fr2 - fr1);
@@ -1090,10 +1111,11 @@ __global__ void __launch_bounds__(kShellThreads, GF_SHELL_MIN_BLOCKS)
                     (void)fr0;
                   })
         } else {
-          // ---- lattice round: items 4q .. 4q+3 of the concatenated front parts
+          // ---- lattice round: items IPU q .. IPU q + IPU-1 of the concatenated
+          // front parts, one per LG-lane group
           GF_FINE(const unsigned long long fl0 = fine_after(0u);)
           const int q = kWarpRot ? u - TR : u;
-          const int t = q * 4 + sub;
+          const int t = q * IPU + lsub;
           const int TLx = kWarpRot ? TL : T;  // NL > 1: everything lives in the front part
           const bool valid = t < TLx;
           const int* pf = kWarpRot ? S.prefL : S.pref;
@@ -1117,33 +1139,33 @@ __global__ void __launch_bounds__(kShellThreads, GF_SHELL_MIN_BLOCKS)
               valid && (A.order == 2) && !dt_dead_at(A, fs, k, prv) && frontier_has_g(A, cur, fs);
           double gx = 0.0, gy = 0.0;
           SampleResult res;
-          const unsigned long long te0 = A.trace ? gtimer() : 0ULL;
+          GF_FINE(const unsigned long long te0 = A.trace ? gtimer() : 0ULL;)
           if constexpr (R > 0) {
-            eval_lattice<R>(P, S.tab, src, glane, sub, valid, (int)p % A.W, (int)p / A.W, res);
+            eval_lattice<R, LG>(P, S.tab, src, lglane, lsub, valid, (int)p % A.W, (int)p / A.W, res);
           } else {
             if (valid && (e & kEntryRot)) frame_guide(A, fs, (int)p, gx, gy);
             eval_item<NL, 0>(P, S.tab, src, glane, valid, (double)((int)p % A.W),
                              (double)((int)p / A.W), true, gx, gy, res);
           }
-          if (A.trace && valid && glane == 0) trace_max_val(A, k, 6, gtimer() - te0);
+          GF_FINE(if (A.trace && valid && lglane == 0) trace_max_val(A, k, 6, gtimer() - te0);)
           GF_FINE(const unsigned long long fl2 = fine_after((unsigned)(__double_as_longlong(res.rw) >> 32));)
           bool filled = false;
-          if (valid && glane == 0) filled = decide_and_write(A, fs, j, p, k, dt_eff, gx, gy, res);
-          filled = __shfl_sync(0xffffffffu, filled, 0, kGroup);
+          if (valid && lglane == 0) filled = decide_and_write(A, fs, j, p, k, dt_eff, gx, gy, res);
+          filled = __shfl_sync(0xffffffffu, filled, 0, LG);
           GF_FINE(const unsigned long long fl3 = fine_after(filled ? 1u : 0u);)
           if (kTracked)
-            activate(A, reg, wn, uniform, nxt_list, nxt, fw, fs, k, valid ? glane : -1, filled, e);
+            activate<LG>(A, reg, wn, uniform, nxt_list, nxt, fw, fs, k, valid ? lglane : -1, filled, e);
           GF_FINE(const unsigned long long fl4 = fine_after((unsigned)wn);
-                  if (valid && glane == 0) {
+                  if (valid && lglane == 0) {
                     fine_put(A, k, 0, fl1 - fl0); fine_put(A, k, 1, fl2 - fl1);
                     fine_add(A, k, 2, fl2 - fl1); fine_add(A, k, 3, 1);
                     (void)fl3; (void)fl4;
                   })
-          const int nf = (valid && glane == 0 && filled) ? 1 : 0;
+          const int nf = (valid && lglane == 0 && filled) ? 1 : 0;
           if (uniform) wfills += __reduce_add_sync(0xffffffffu, (unsigned)nf);
           else if (nf) atomicAdd(&A.fills[cur * A.nF + fs], 1);
         }
-        if (kTracked && wn > kWarpAppCap - 64) warp_flush(A, reg, wn, wf, nxt_list, nxt);
+        if (kTracked && wn > kWarpAppCap - 80) warp_flush(A, reg, wn, wf, nxt_list, nxt);
       }
       if (kTracked && wf >= 0) warp_flush(A, reg, wn, wf, nxt_list, nxt);
       if (lane == 0 && wf >= 0 && wfills > 0) atomicAdd(&A.fills[cur * A.nF + wf], wfills);
@@ -1458,9 +1480,28 @@ static const void* shell_kernel(const BallParams& P) {
   return (const void*)k_shells<0, kTracked>;
 }
 
+// Cooperative grid size of a shell kernel on the current device, cached per
+// (device, kernel): the attribute call and the occupancy query cost host
+// microseconds on every fill otherwise.
 static int coop_grid(const void* fn, size_t smem, int* out_grid) {
+  struct Entry {
+    int dev;
+    const void* fn;
+    size_t smem;
+    int grid;
+  };
+  static std::mutex mu;
+  static std::vector<Entry> cache;
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return GF_E_CUDA;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    for (const Entry& e : cache)
+      if (e.dev == dev && e.fn == fn && e.smem == smem) {
+        *out_grid = e.grid;
+        return GF_OK;
+      }
+  }
   int sms = 0, coop = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
@@ -1472,6 +1513,8 @@ static int coop_grid(const void* fn, size_t smem, int* out_grid) {
       per_sm <= 0)
     return set_error(GF_E_CUDA, "occupancy query failed");
   *out_grid = sms * per_sm;
+  std::lock_guard<std::mutex> lock(mu);
+  cache.push_back(Entry{dev, fn, smem, *out_grid});
   return GF_OK;
 }
 
@@ -1555,10 +1598,6 @@ int fill_launch(const gf_frames* fr, const gf_fill_params* prm, const gf_fill_ou
   if (cudaMemsetAsync(base + L.ints, 0, L.u64 + (size_t)nF * 6 * sizeof(unsigned long long) - L.ints,
                       stream) != cudaSuccess)
     return set_error(GF_E_CUDA, "memset failed");
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const long long total = (long long)nF * HW;
   launch_prep(fr->dtype == GF_F64, C, dim3(tiles_of(H, W), nF), stream, A);
   if (cudaPeekAtLastError() != cudaSuccess)
     return set_error(GF_E_CUDA, cudaGetErrorString(cudaGetLastError()));
