@@ -57,6 +57,17 @@ __host__ __device__ inline double dec_ordered(unsigned long long e) {
   return d;
 }
 
+// order-preserving 32-bit code of a float (larger value -> larger code)
+__device__ __forceinline__ unsigned enc32(float x) {
+  const unsigned b = __float_as_uint(x);
+  return (b >> 31) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ float dec32(unsigned e) {
+  return __uint_as_float((e >> 31) ? (e & 0x7fffffffu) : ~e);
+}
+// 4 byte-wise test results (0xff / 0x00 per byte) -> 4 bits, byte i -> bit i
+__device__ __forceinline__ unsigned nib4(unsigned m) { return ((m & 0x01010101u) * 0x01020408u) >> 24; }
+
 __device__ __forceinline__ int stamp_of(const float4* work, int q) {
   return __float_as_int(work[q].w);
 }
@@ -137,7 +148,6 @@ __global__ void __launch_bounds__(kThreads) k_prep(const __grid_constant__ FillA
   const int R = A.halo;
   const int ext = kTile + 2 * R;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  __shared__ uint8_t s_lab[kTileExt][kTileExt + 6];
   __shared__ unsigned int s_hrow[kTileExt];
   __shared__ unsigned long long s_hrow64[kTileExt];
   __shared__ unsigned long long s_rrow64[kTileExt];
@@ -155,43 +165,81 @@ __global__ void __launch_bounds__(kThreads) k_prep(const __grid_constant__ FillA
   const int c0 = (threadIdx.x & 7) * 4;
   const int gy = ty0 + ry;
 
-  // 1. labels of the tile + halo, one warp per halo row (out of lattice ->
-  //    128: neither readable nor Inpaint; x wraps when periodic), with the
-  //    row's Inpaint bitmask from two ballots
+  // 1. Inpaint / Readable bitmasks of the tile + halo rows (bit x <=> ext
+  //    column x; out of lattice = neither, x wraps when periodic).  Interior
+  //    tiles read 32-bit words, two rows per warp instruction, and pack each
+  //    word's 4 byte tests into a nibble (one multiply); the OR of 16 lanes'
+  //    nibbles is one redux.  Edge tiles fall back to byte loads + ballots.
   if (threadIdx.x == 0) s_ncand = 0;
   bool any_inp = false;
-  constexpr int kRowsPerWarp = (kTileExt + kThreads / 32 - 1) / (kThreads / 32);
-  uint8_t l2[kRowsPerWarp][2];
-  // every label load of the warp is issued before the first one is used
-#pragma unroll
-  for (int i = 0; i < kRowsPerWarp; ++i) {
-    const int y = warp + i * (kThreads / 32);
+  const int sh = (tx0 - R) & 3;       // ext column 0 within its aligned word
+  const int ws = tx0 - R - sh;        // first word's global column
+  const int nw = (ext + sh + 3) >> 2;  // words per row (<= 16)
+  const unsigned long long ext_mask = ext >= 64 ? ~0ULL : ((1ULL << ext) - 1);
+  if ((A.W & 3) == 0 && ws >= 0 && ws + 4 * nw <= A.W) {
+    // one thread per ext row: up to 16 aligned words, all loads in flight
+    const int y = threadIdx.x;
     const int gyy = ty0 - R + y;
-    const bool row_in = y < ext && gyy >= 0 && gyy < A.H;
+    if (y < ext) {
+      unsigned long long im = 0ULL, rm = 0ULL;
+      if (gyy >= 0 && gyy < A.H) {
+        const unsigned* row = reinterpret_cast<const unsigned*>(lab + (size_t)gyy * A.W + ws);
+        unsigned w[16];
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int x = lane + 32 * h;
-      int gxx = tx0 - R + x;
-      if (A.periodic) gxx = gxx < 0 ? gxx + A.W : (gxx >= A.W ? gxx - A.W : gxx);
-      const bool in = x < ext && row_in && gxx >= 0 && gxx < A.W;
-      l2[i][h] = in ? __ldg(lab + gyy * A.W + gxx) : (uint8_t)128;
+        for (int i = 0; i < 16; ++i) w[i] = i < nw ? __ldg(row + i) : 0x80808080u;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          im |= (unsigned long long)nib4(__vcmpeq4(w[i], 0xffffffffu)) << (4 * i);
+          rm |= (unsigned long long)nib4(__vcmpeq4(w[i], 0u)) << (4 * i);
+        }
+        im = (im >> sh) & ext_mask;
+        rm = (rm >> sh) & ext_mask;
+      }
+      s_hrow64[y] = im;
+      s_rrow64[y] = rm;
+      any_inp = im != 0ULL;
+    }
+  } else {
+    constexpr int kRowsPerWarp = (kTileExt + kThreads / 32 - 1) / (kThreads / 32);
+    uint8_t l2[kRowsPerWarp][2];
+#pragma unroll
+    for (int i = 0; i < kRowsPerWarp; ++i) {
+      const int y = warp + i * (kThreads / 32);
+      const int gyy = ty0 - R + y;
+      const bool row_ok = y < ext && gyy >= 0 && gyy < A.H;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int x = lane + 32 * h;
+        int gxx = tx0 - R + x;
+        if (A.periodic) gxx = gxx < 0 ? gxx + A.W : (gxx >= A.W ? gxx - A.W : gxx);
+        const bool in = x < ext && row_ok && gxx >= 0 && gxx < A.W;
+        l2[i][h] = in ? __ldg(lab + gyy * A.W + gxx) : (uint8_t)128;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < kRowsPerWarp; ++i) {
+      const int y = warp + i * (kThreads / 32);
+      const unsigned lo = __ballot_sync(0xffffffffu, y < ext && l2[i][0] == 255);
+      const unsigned hi = __ballot_sync(0xffffffffu, y < ext && l2[i][1] == 255);
+      const unsigned rlo = __ballot_sync(0xffffffffu, y < ext && l2[i][0] == 0);
+      const unsigned rhi = __ballot_sync(0xffffffffu, y < ext && l2[i][1] == 0);
+      any_inp |= (lo | hi) != 0;
+      if (lane == 0 && y < ext) {
+        s_hrow64[y] = ((unsigned long long)hi << 32) | lo;
+        s_rrow64[y] = ((unsigned long long)rhi << 32) | rlo;
+      }
     }
   }
+  // labels of the thread's own 4 pixels (byte u = column c0 + u)
+  uint32_t own4 = 0x80808080u;
+  if (gy < A.H) {
+    if ((A.W & 3) == 0 && tx0 + c0 < A.W) {
+      own4 = __ldg(reinterpret_cast<const uint32_t*>(lab + (size_t)gy * A.W + tx0 + c0));
+    } else {
 #pragma unroll
-  for (int i = 0; i < kRowsPerWarp; ++i) {
-    const int y = warp + i * (kThreads / 32);
-    if (y < ext) {
-      if (lane < ext) s_lab[y][lane] = l2[i][0];
-      if (lane + 32 < ext) s_lab[y][lane + 32] = l2[i][1];
-    }
-    const unsigned lo = __ballot_sync(0xffffffffu, y < ext && l2[i][0] == 255);
-    const unsigned hi = __ballot_sync(0xffffffffu, y < ext && l2[i][1] == 255);
-    const unsigned rlo = __ballot_sync(0xffffffffu, y < ext && l2[i][0] == 0);
-    const unsigned rhi = __ballot_sync(0xffffffffu, y < ext && l2[i][1] == 0);
-    any_inp |= (lo | hi) != 0;
-    if (lane == 0 && y < ext) {
-      s_hrow64[y] = ((unsigned long long)hi << 32) | lo;
-      s_rrow64[y] = ((unsigned long long)rhi << 32) | rlo;
+      for (int u = 0; u < 4; ++u)
+        if (tx0 + c0 + u < A.W)
+          own4 = (own4 & ~(0xffu << (8 * u))) | ((uint32_t)lab[(size_t)gy * A.W + tx0 + c0 + u] << (8 * u));
     }
   }
   // the thread's 4 pixels: loads issued before the label sync
@@ -234,7 +282,7 @@ __global__ void __launch_bounds__(kThreads) k_prep(const __grid_constant__ FillA
     T vlo[2] = {T(INFINITY), T(INFINITY)}, vhi[2] = {T(-INFINITY), T(-INFINITY)};
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      const uint8_t l = s_lab[ry + R][c0 + u + R];
+      const uint8_t l = (uint8_t)(own4 >> (8 * u));
       if (row_in && gx0 + u < A.W && (l == 0 || l == 128)) {
         const int b = l == 0 ? 0 : 1;
 #pragma unroll
@@ -246,19 +294,32 @@ __global__ void __launch_bounds__(kThreads) k_prep(const __grid_constant__ FillA
       }
     }
     unsigned long long ered[4];  // max(~enc) <=> min(enc)
+    if constexpr (sizeof(T) == 4) {
+      // fp32 values: order-preserving 32-bit codes, one redux per quantity
 #pragma unroll
-    for (int b = 0; b < 2; ++b) {
-      ered[2 * b] = vlo[b] <= vhi[b] ? ~enc_ordered((double)vlo[b]) : 0ULL;
-      ered[2 * b + 1] = vlo[b] <= vhi[b] ? enc_ordered((double)vhi[b]) : 0ULL;
-    }
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      for (int o = 16; o > 0; o >>= 1) {
-        const unsigned long long a = __shfl_xor_sync(0xffffffffu, ered[i], o);
-        ered[i] = a > ered[i] ? a : ered[i];
+      for (int b = 0; b < 2; ++b) {
+        const bool any = vlo[b] <= vhi[b];
+        const unsigned mlo = __reduce_max_sync(0xffffffffu, any ? ~enc32((float)vlo[b]) : 0u);
+        const unsigned mhi = __reduce_max_sync(0xffffffffu, any ? enc32((float)vhi[b]) : 0u);
+        ered[2 * b] = mlo ? ~enc_ordered((double)dec32(~mlo)) : 0ULL;
+        ered[2 * b + 1] = mhi ? enc_ordered((double)dec32(mhi)) : 0ULL;
       }
-      if (lane == 0) s_red[i][warp] = ered[i];
+    } else {
+#pragma unroll
+      for (int b = 0; b < 2; ++b) {
+        ered[2 * b] = vlo[b] <= vhi[b] ? ~enc_ordered((double)vlo[b]) : 0ULL;
+        ered[2 * b + 1] = vlo[b] <= vhi[b] ? enc_ordered((double)vhi[b]) : 0ULL;
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        for (int o = 16; o > 0; o >>= 1) {
+          const unsigned long long a = __shfl_xor_sync(0xffffffffu, ered[i], o);
+          ered[i] = a > ered[i] ? a : ered[i];
+        }
     }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (lane == 0) s_red[i][warp] = ered[i];
     if (A.fillshell && row_in) {
       int* fsh = A.fillshell + (size_t)f * A.HW + (size_t)gy * A.W + gx0;
 #pragma unroll
@@ -334,7 +395,7 @@ __global__ void __launch_bounds__(kThreads) k_prep(const __grid_constant__ FillA
     const int gx = tx0 + c;
     const bool in = gy < A.H && gx < A.W;
     const int p = gy * A.W + gx;
-    const uint8_t l = s_lab[ry + R][c + R];
+    const uint8_t l = (uint8_t)(own4 >> (8 * u));
     const bool near = (vmask >> c) & 1u;
     bool active = false, rot = false;
     if (in) {

@@ -1,5 +1,6 @@
+# Full ncu capture of one k_prep and one k_shells launch of the bench step.
 mkdir -p gpurun_out
 CMD="python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu"
-timeout -s KILL 300 $CMD > gpurun_out/plain.log 2>&1 && \
-timeout -s KILL 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 40 --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launch.log 2>&1; echo "ncu launches rc=$?"
-timeout -s KILL 900 ncu --set full --clock-control none --import-source on -k regex:"k_shells|k_prep|k_finalize" -s 3 -c 3 -o gpurun_out/prof_r1b $CMD > gpurun_out/ncu_full.log 2>&1; echo "ncu full rc=$?"; tail -3 gpurun_out/ncu_full.log
+timeout -s KILL 300 $CMD > gpurun_out/plain.log 2>&1; echo "plain rc=$?"
+timeout -s KILL 900 ncu --set full --clock-control none --import-source on -k regex:"k_shells|k_prep" -s 6 -c 2 -o gpurun_out/prof_${TAG:-cur} $CMD > gpurun_out/ncu_full.log 2>&1; echo "full rc=$?"
+tail -3 gpurun_out/ncu_full.log
