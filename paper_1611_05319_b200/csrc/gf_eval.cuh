@@ -180,27 +180,30 @@ __device__ __forceinline__ void eval_rot_warp(const BallParams& P, const BallTab
       const double fx0 = floor(X), fy0 = floor(Y);
       const double tx = X - fx0, ty = Y - fy0;
       const int x0 = (int)fx0, y0 = (int)fy0;
-      int cq[4];
+      unsigned live = 0;  // bit c: corner c has weight and lies in the lattice
       bool outside = false;
+      float4 v[4];
+      float c3v[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         const int a = c >> 1, b = c & 1;  // (x0,y0),(x0,y0+1),(x0+1,y0),(x0+1,y0+1)
         const double wc = (a ? tx : 1.0 - tx) * (b ? ty : 1.0 - ty);
-        cq[c] = -1;
         if (wc != 0.0) {
           const int cy = y0 + b;
           int cx = x0 + a;
           bool inside = cy >= 0 && cy < src.H;
           if (P.periodic) cx = wrap_col(cx, src.W);
           else inside = inside && cx >= 0 && cx < src.W;
-          if (inside) cq[c] = cy * src.W + cx;
-          else outside = true;
+          if (inside) {
+            const int q = cy * src.W + cx;
+            v[c] = src.work[q];
+            if (src.c3) c3v[c] = src.c3[q];
+            live |= 1u << c;
+          } else {
+            outside = true;
+          }
         }
       }
-      float4 v[4];
-#pragma unroll
-      for (int c = 0; c < 4; ++c)
-        if (cq[c] >= 0) v[c] = src.work[cq[c]];
       const double dist = hypot_np(px, py);
       double ws;
       if (P.mu_inf) {
@@ -215,14 +218,14 @@ __device__ __forceinline__ void eval_rot_warp(const BallParams& P, const BallTab
       double sv[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
       for (int c = 0; c < 4; ++c)
-        if (cq[c] >= 0) {
+        if ((live >> c) & 1u) {
           const int a = c >> 1, b = c & 1;
           const double wc = (a ? tx : 1.0 - tx) * (b ? ty : 1.0 - ty);
           ok = ok && __float_as_int(v[c].w) <= src.shell;
           sv[0] += wc * (double)v[c].x;
           sv[1] += wc * (double)v[c].y;
           sv[2] += wc * (double)v[c].z;
-          if (src.c3) sv[3] += wc * (double)src.c3[cq[c]];
+          sv[3] += wc * (double)c3v[c];
         }
       wr[s] = ok ? ws : 0.0;
       if (ok) {

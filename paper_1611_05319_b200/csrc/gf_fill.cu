@@ -109,9 +109,10 @@ __device__ __forceinline__ void timeline_mark(const FillArgs& A, int stage, bool
   atomicMax(&row[2 * stage + (start ? 0 : 1)], start ? ~t : t);
 }
 
-// Programmatic dependent launch: each k_prep block signals at its end, so
-// the shell kernel's launch overlaps the last prep wave; the shell kernel
-// waits for k_prep's completion (and memory) before its first read.
+// Programmatic dependent launch: each k_prep block signals at its start, so
+// the shell kernel's launch and block set-up overlap the last prep wave; the
+// shell kernel waits for k_prep's completion (and memory) before its first
+// read.
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
@@ -138,13 +139,19 @@ __device__ __forceinline__ double seg_dist(double px, double py, const double4 s
 // value hull of its Readable values (engine.py:291-296).  Tiles with an
 // Inpaint pixel within reach go on to the D-tile work below.
 template <typename T, int C>
-__global__ void __launch_bounds__(kThreads) k_prep(const __grid_constant__ FillArgs A) {
+#ifndef GF_PREP_MIN_BLOCKS
+#define GF_PREP_MIN_BLOCKS 4
+#endif
+__global__ void __launch_bounds__(kThreads, GF_PREP_MIN_BLOCKS) k_prep(const __grid_constant__ FillArgs A) {
   const int f = blockIdx.y;
   const int tiles_x = (A.W + kTile - 1) / kTile;
   const int tix = (int)(blockIdx.x % tiles_x), tiy = (int)(blockIdx.x / tiles_x);
   const int tx0 = tix * kTile;
   const int ty0 = tiy * kTile;
   timeline_mark(A, 0, true);
+  // every prep block is resident once all have passed here: the shell
+  // kernel may start launching (it waits for this grid's completion)
+  pdl_trigger();
   const int R = A.halo;
   const int ext = kTile + 2 * R;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -348,7 +355,6 @@ __global__ void __launch_bounds__(kThreads) k_prep(const __grid_constant__ FillA
         if (gx0 + u < A.W) en[u] = -1;
     }
     timeline_mark(A, 0, false);
-    pdl_trigger();
     return;
   }
   if (raster) {
@@ -525,7 +531,6 @@ __global__ void __launch_bounds__(kThreads) k_prep(const __grid_constant__ FillA
     if (blk_anyg) A.anyg[f] = 1;
   }
   timeline_mark(A, 0, false);
-  pdl_trigger();
 }
 
 // ------------------------------------------------------- shell loop
@@ -758,7 +763,9 @@ __device__ __forceinline__ void write_out(const FillArgs& A, int f, uint32_t p, 
   const double lo = has_hull ? dec_ordered(elo) : 0.0;
   const double hi = has_hull ? dec_ordered(ehi) : 0.0;
   const size_t o = ((size_t)f * A.HW + p) * A.C;
-  for (int c = 0; c < A.C; ++c) {
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {  // compile-time indices: v stays in registers
+    if (c >= A.C) break;
     double x = (double)v[c];
     if (has_hull) x = (x < lo) ? lo : ((x > hi) ? hi : x);
     if (A.dtype == GF_F64) reinterpret_cast<double*>(A.out)[o + c] = x;
@@ -1093,7 +1100,7 @@ __global__ void __launch_bounds__(kShellThreads, GF_SHELL_MIN_BLOCKS)
   // lattice items: LG lanes each (4 for the r <= 3 balls: K <= 28 samples,
   // 7 per lane), IPU = 32 / LG items per warp round
 #ifndef GF_LATTICE_LANES
-#define GF_LATTICE_LANES 4
+#define GF_LATTICE_LANES 8
 #endif
   constexpr int LG = (R > 0 && R <= 3) ? GF_LATTICE_LANES : 8;
   constexpr int IPU = 32 / LG;
@@ -1129,6 +1136,7 @@ __global__ void __launch_bounds__(kShellThreads, GF_SHELL_MIN_BLOCKS)
       const int U = TR + UL;
       const int NW = gridDim.x * kWarps;
       int wn = 0, wf = -1, wfills = 0;
+      GF_FINE(if (lane == 0 && blockIdx.x * kWarps + warp < U) fine_put(A, k, 6, ~gtimer());)
       for (int u = blockIdx.x * kWarps + warp; u < U; u += NW) {
         if (kWarpRot && u < TR) {
           // ---- rotated-ball item, one whole warp
@@ -1165,12 +1173,7 @@ __global__ void __launch_bounds__(kShellThreads, GF_SHELL_MIN_BLOCKS)
           if (lane == 0 && filled) ++wfills;
           if (kTracked)
             activate<8>(A, reg, wn, true, nxt_list, nxt, fw, f, k, lane < 8 ? lane : -1, filled, e);
-          GF_FINE(const unsigned long long fr4 = fine_after((unsigned)wn);
-                  if (lane == 0) {
-                    fine_put(A, k, 4, fr2 - fr1); fine_add(A, k, 5, fr2 - fr1);
-                    fine_add(A, k, 6, 1); fine_put(A, k, 7, fr4 - fr3);
-                    (void)fr0;
-                  })
+          GF_FINE(if (lane == 0) fine_put(A, k, 7, fr2 - fr1); (void)fr0; (void)fr3;)
         } else {
           // ---- lattice round: items IPU q .. IPU q + IPU-1 of the concatenated
           // front parts, one per LG-lane group
@@ -1220,7 +1223,7 @@ __global__ void __launch_bounds__(kShellThreads, GF_SHELL_MIN_BLOCKS)
                   if (valid && lglane == 0) {
                     fine_put(A, k, 0, fl1 - fl0); fine_put(A, k, 1, fl2 - fl1);
                     fine_add(A, k, 2, fl2 - fl1); fine_add(A, k, 3, 1);
-                    (void)fl3; (void)fl4;
+                    fine_put(A, k, 4, fl4 - fl2); (void)fl3;
                   })
           const int nf = (valid && lglane == 0 && filled) ? 1 : 0;
           if (uniform) wfills += __reduce_add_sync(0xffffffffu, (unsigned)nf);
@@ -1228,8 +1231,11 @@ __global__ void __launch_bounds__(kShellThreads, GF_SHELL_MIN_BLOCKS)
         }
         if (kTracked && wn > kWarpAppCap - 80) warp_flush(A, reg, wn, wf, nxt_list, nxt);
       }
+      GF_FINE(const unsigned long long ff0 = fine_after((unsigned)wn);)
       if (kTracked && wf >= 0) warp_flush(A, reg, wn, wf, nxt_list, nxt);
       if (lane == 0 && wf >= 0 && wfills > 0) atomicAdd(&A.fills[cur * A.nF + wf], wfills);
+      GF_FINE(const unsigned long long ff1 = fine_after((unsigned)wn);
+              if (lane == 0 && wf >= 0) fine_put(A, k, 5, ff1 - ff0);)
       // a warp without fill work this shell clips one chunk of Bystanders
       if (clip_work && blockIdx.x * kWarps + warp >= U) clip_claim(A);
       if (A.trace && lane == 0 && k < A.trace_cap)
@@ -1682,6 +1688,9 @@ int fill_launch(const gf_frames* fr, const gf_fill_params* prm, const gf_fill_ou
   cfg.attrs = attr;
   cfg.numAttrs = 2;
   cudaError_t e = cudaLaunchKernelExC(&cfg, fn, args);
+#ifdef GF_PDL_STRICT
+  if (e != cudaSuccess) return set_error(GF_E_CUDA, cudaGetErrorString(e));
+#endif
   if (e != cudaSuccess) {
     // without programmatic serialisation: a plain cooperative launch
     (void)cudaGetLastError();
