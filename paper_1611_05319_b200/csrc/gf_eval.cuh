@@ -52,9 +52,21 @@ __device__ __forceinline__ void eval_lattice(const BallParams& P, const BallTabl
     q[t] = (valid && k < B::K) ? lattice_index(pi + T.ni[k], pj + T.mi[k], src.H, src.W, P.periodic)
                                : -1;
   }
+#ifdef GF_FINE_TRACE
+  {
+    if (q[0] == -2) asm volatile("trap;");
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(out.t0));
+  }
+#endif
 #pragma unroll
   for (int t = 0; t < KPL; ++t)
     if (q[t] >= 0) v[t] = src.work[q[t]];
+#ifdef GF_FINE_TRACE
+  {
+    if (__float_as_int(v[0].w) == -2 && q[0] >= 0) asm volatile("trap;");
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(out.t1));
+  }
+#endif
   unsigned okm = 0;  // bit t: sample glane + LG t readable
 #pragma unroll
   for (int t = 0; t < KPL; ++t)

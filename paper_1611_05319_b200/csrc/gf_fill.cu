@@ -1127,7 +1127,7 @@ __global__ void __launch_bounds__(kShellThreads, GF_SHELL_MIN_BLOCKS)
     trace_set(A, k, 5, (unsigned long long)T);
 
     // ---- A: fill (+ fused frontier update when tracked)
-    // Work units, dealt cyclically over every warp of the grid: a rotated
+    // Work units, dealt over every warp of the grid: a rotated
     // item (whole warp) or a round of 4 consecutive lattice items (one per
     // 8-lane group).  No block barrier.
     {
@@ -1136,8 +1136,14 @@ __global__ void __launch_bounds__(kShellThreads, GF_SHELL_MIN_BLOCKS)
       const int U = TR + UL;
       const int NW = gridDim.x * kWarps;
       int wn = 0, wf = -1, wfills = 0;
-      GF_FINE(if (lane == 0 && blockIdx.x * kWarps + warp < U) fine_put(A, k, 6, ~gtimer());)
-      for (int u = blockIdx.x * kWarps + warp; u < U; u += NW) {
+      // unit u -> block u % G, warp u / G: a small shell's units land on as
+      // many SMs as possible (each SM's L1/LSU serves few gathers), not on
+      // the first few blocks
+#ifndef GF_UNIT_SPREAD
+#define GF_UNIT_SPREAD 0
+#endif
+      const int u0 = GF_UNIT_SPREAD ? warp * (int)gridDim.x + blockIdx.x : blockIdx.x * kWarps + warp;
+      for (int u = u0; u < U; u += NW) {
         if (kWarpRot && u < TR) {
           // ---- rotated-ball item, one whole warp
           const int f = find_frame(S.prefR, A.nF, u);
@@ -1237,7 +1243,7 @@ __global__ void __launch_bounds__(kShellThreads, GF_SHELL_MIN_BLOCKS)
       GF_FINE(const unsigned long long ff1 = fine_after((unsigned)wn);
               if (lane == 0 && wf >= 0) fine_put(A, k, 5, ff1 - ff0);)
       // a warp without fill work this shell clips one chunk of Bystanders
-      if (clip_work && blockIdx.x * kWarps + warp >= U) clip_claim(A);
+      if (clip_work && u0 >= U) clip_claim(A);
       if (A.trace && lane == 0 && k < A.trace_cap)
         atomicMax(&A.trace[k * kTraceSlots + 1], gtimer());
     }

@@ -61,6 +61,9 @@ struct BallTables {
 struct SampleResult {
   double rw, tw;  // readable / total weight mass (exact numpy bits)
   double v[4];    // weighted average colour, 0 where rw == 0
+#ifdef GF_FINE_TRACE
+  unsigned long long t0, t1;  // fetch issued / first fetch arrived (phase trace)
+#endif
 };
 
 // --------------------------------------------------------------- sources

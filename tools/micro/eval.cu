@@ -3,7 +3,7 @@
 #include <cstdio>
 #include <cmath>
 #include <vector>
-#include "../../paper_1611_05319_b200/csrc/gf_sampler.cuh"
+#include "../../paper_1611_05319_b200/csrc/gf_eval.cuh"
 using namespace gf;
 __device__ __forceinline__ long long clk() { long long t; asm volatile("mov.u64 %0, %%clock64;" : "=l"(t)); return t; }
 
@@ -22,7 +22,7 @@ __global__ void k_prims(double* out, long long* cyc, double a0, double b0) {
 __global__ void k_eval(const __grid_constant__ BallParams P, const __grid_constant__ BallTables T,
                        const float4* work, int H, int W, long long* cyc, double* out, double gx, double gy) {
   __shared__ BallTables S;
-  for (int i = threadIdx.x; i < P.K; i += blockDim.x) { S.n[i] = T.n[i]; S.m[i] = T.m[i]; S.w0[i] = T.w0[i]; }
+  for (int i = threadIdx.x; i < P.K; i += blockDim.x) { S.n[i] = T.n[i]; S.m[i] = T.m[i]; S.w0[i] = T.w0[i]; S.ni[i] = T.ni[i]; S.mi[i] = T.mi[i]; }
   __syncthreads();
   const int lane = threadIdx.x & 31;
   WorkSource src{work, nullptr, H, W, 3, 5};
@@ -32,7 +32,7 @@ __global__ void k_eval(const __grid_constant__ BallParams P, const __grid_consta
   long long t0 = clk();
   for (int i = 0; i < N; ++i) {
     SampleResult r;
-    eval_item<1, 4>(P, S, src, lane & 7, true, (double)(p % W), (double)(p / W), true, 0.0, 0.0, r);
+    eval_lattice<3, 8>(P, S, src, lane & 7, lane >> 3, true, p % W, p / W, r);
     accum += r.rw;
     p += 7919 + ((int)r.v[0] & 1);  // dependent: next item waits for this one
     if (p >= H * W - 10 * W) p -= (H - 40) * W;
@@ -41,7 +41,7 @@ __global__ void k_eval(const __grid_constant__ BallParams P, const __grid_consta
   t0 = clk();
   for (int i = 0; i < N; ++i) {
     SampleResult r;
-    eval_item_warp<1>(P, S, src, lane, true, (double)(p % W), (double)(p / W), gx, gy, r);
+    eval_rot_warp<3>(P, S, src, lane, (double)(p % W), (double)(p / W), gx, gy, gx / 0.5, gy / 0.5, r);
     accum += r.rw;
     p += 7919 + ((int)r.v[0] & 1);
     if (p >= H * W - 10 * W) p -= (H - 40) * W;
@@ -65,7 +65,7 @@ int main() {
   int K = 0;
   for (int m = -r; m <= r; ++m)
     for (int n = -r; n <= r; ++n)
-      if (n * n + m * m <= r * r && !(n == 0 && m == 0)) { T.n[K] = n; T.m[K] = m; T.w0[K] = 1.0 / std::hypot((double)n, (double)m); ++K; }
+      if (n * n + m * m <= r * r && !(n == 0 && m == 0)) { T.n[K] = n; T.m[K] = m; T.ni[K] = n; T.mi[K] = m; T.w0[K] = 1.0 / std::hypot((double)n, (double)m); ++K; }
   P.r = r; P.K = K; P.rotated = 1; P.periodic = 0; P.mu_inf = 0;
   P.coef = -(50.0 * 50.0) / (2.0 * r * r);
   P.plan.n_leaves = 1; P.plan.leaf_lo[0] = 0; P.plan.leaf_n[0] = K; P.plan.n_prog = 1; P.plan.prog[0] = 0;
