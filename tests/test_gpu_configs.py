@@ -98,3 +98,70 @@ def test_fused_raster_fill_equals_two_pass(name):
     assert torch.equal(one["enter"], two["enter"])
     assert torch.equal(one["out"], two["out"])
     assert torch.equal(one["stats"], two["stats"])
+
+
+def _clip_scene(seed, H=150, W=230):
+    """Readable values in [0.3, 0.6]; Bystanders hold 0.0 / 1.0 / in-hull
+    values spread over many 32x32 tiles, so the shell loop's tile clip runs."""
+    rng = np.random.default_rng(seed)
+    img = 0.3 + 0.3 * rng.random((H, W, 3))
+    lab = np.zeros((H, W), np.uint8)
+    lab[40:48, 20:200] = 255
+    lab[90:130, 100:108] = 255
+    bys = rng.random((H, W)) < 0.08
+    bys &= lab == 0
+    lab[bys] = 128
+    vals = rng.choice([0.0, 1.0, 0.45], size=(int(bys.sum()), 3))
+    img[bys] = vals
+    img[lab == 255] = 0.0
+    return img, lab
+
+
+@pytest.mark.parametrize("seed", [1, 2])
+def test_bystander_clip_outside_hull(seed):
+    img, lab = _clip_scene(seed)
+    p = FillParams(r=3, mu=50.0, order="smart", neighborhood="rotated_ball")
+    ref = orc.fill(img, lab, None, orc.Params.of(p), tracked=True)
+    assert float(np.abs(ref["u"][lab == 128] - img[lab == 128]).max()) > 0.1  # clip does work
+    for tracked in (True, False):
+        u, rep, maps = engine._run_fill(img, lab, None, p, tracked=tracked, order_log=True)
+        assert np.array_equal(maps["fillshell"], ref["fillshell"])
+        assert np.array_equal(u[lab == 128], ref["u"][lab == 128])  # clip is exact
+        assert np.array_equal(u[lab == 0], img[lab == 0])
+        assert float(np.abs(u - ref["u"]).max()) <= 1e-4
+
+
+def test_bystander_clip_batched_frames_own_hulls():
+    scenes_ = [_clip_scene(s) for s in (3, 4, 5)]
+    p = FillParams(r=3, mu=50.0, order="smart", neighborhood="rotated_ball")
+    dev = torch.device("cuda")
+    # frame 1 gets a wider hull: its Bystanders need no clip, the others do
+    scenes_[1][0][0, 0] = (0.0, 1.0, 0.5)
+    img = torch.from_numpy(np.stack([s[0] for s in scenes_])).to(dev)
+    lab = torch.from_numpy(np.stack([s[1] for s in scenes_])).to(dev)
+    res = fill_device(img, lab, None, p, order_log=True)
+    for f, (im, lb) in enumerate(scenes_):
+        ref = orc.fill(im, lb, None, orc.Params.of(p), tracked=True)
+        out = res["out"][f].cpu().numpy()
+        assert np.array_equal(res["fillshell"][f].cpu().numpy(), ref["fillshell"])
+        assert np.array_equal(out[lb == 128], ref["u"][lb == 128])
+
+
+def test_fill_graph_replay_matches_eager():
+    from paper_1611_05319_b200._device import FillGraph, SegmentSet
+
+    sc = scenes.config("C1")
+    dev = torch.device("cuda")
+    p = FillParams(**sc.params)
+    img = torch.from_numpy(sc.image.astype(np.float32))[None].to(dev).contiguous()
+    lab = torch.from_numpy(sc.labels)[None].to(dev).contiguous()
+    segs = SegmentSet(_splines(sc), dev)
+    g = FillGraph(img, lab, None, p, splines=segs, want_fillshell=True)
+    for scale in (1.0, 0.5):  # a new frame written into the captured input
+        img.copy_(torch.from_numpy((sc.image * scale).astype(np.float32))[None].to(dev))
+        out = g.replay()
+        eager = fill_device(img, lab, None, p, splines=segs, want_fillshell=True, rows_cap=4096)
+        torch.cuda.synchronize()
+        assert torch.equal(out["out"], eager["out"])
+        assert torch.equal(out["fillshell"], eager["fillshell"])
+        assert torch.equal(out["stats"], eager["stats"])
