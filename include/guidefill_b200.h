@@ -23,7 +23,7 @@
 extern "C" {
 #endif
 
-#define GF_ABI_VERSION 1
+#define GF_ABI_VERSION 2
 
 /* status codes */
 #define GF_OK 0
@@ -64,7 +64,10 @@ extern "C" {
 #define GF_STAT_ROWS_OVERFLOW 6 /* 1 if iterations > rows_cap */
 #define GF_STAT_LAST_FRONTIER 7 /* frontier size of the shell that ended the
                                    loop unfilled (0 when the fill completed) */
-#define GF_STATS 8
+#define GF_STAT_BAD_LABELS 8    /* 1 if a label is not 0 / 128 / 255 (the
+                                   caller raises grid.py:36-46's ValueError;
+                                   the fill result is then meaningless) */
+#define GF_STATS 9
 
 /* FillParams (engine.py:33-60), minus the coherence-transport knobs */
 typedef struct gf_fill_params {

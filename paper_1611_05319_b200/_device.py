@@ -200,6 +200,28 @@ class SegmentSet:
         self.owner = torch.from_numpy(np.ascontiguousarray(own, dtype=np.int32)).to(device)
         self.dirs = torch.from_numpy(np.ascontiguousarray(dv)).to(device)
 
+    _cache = {}
+    _cache_order = []
+
+    @classmethod
+    def cached(cls, splines, device, max_entries=8):
+        """A SegmentSet for ``splines`` reused across calls: keyed on the
+        splines' content (control points, kind, direction), so repeated
+        fills with the same guide curves skip the host flattening and upload."""
+        key = (str(device), tuple((tuple(np.asarray(s.points, dtype=np.float64).ravel().tolist()),
+                                   str(getattr(s, "kind", "")),
+                                   tuple(np.asarray(s.direction, dtype=np.float64).tolist()))
+                                  for s in splines))
+        hit = cls._cache.get(key)
+        if hit is not None:
+            return hit
+        seg = cls(splines, device)
+        cls._cache[key] = seg
+        cls._cache_order.append(key)
+        if len(cls._cache_order) > max_entries:
+            cls._cache.pop(cls._cache_order.pop(0), None)
+        return seg
+
     def as_c(self, eta=3.0):
         return N.SplinesC(self.n_seg, self.seg.data_ptr(), self.owner.data_ptr(), self.n_splines,
                           self.dirs.data_ptr(), float(eta),

@@ -19,9 +19,10 @@ GF_ORDER = {"onion": 0, "smart": 1, "smart_with_data_term": 2}
 GF_BALL = {"rotated_ball": 0, "axis_ball": 1}
 GF_G_ZERO, GF_G_FIXED, GF_G_FIELD = 0, 1, 2
 GF_MAX_RADIUS = 12
-GF_STATS = 8
+GF_STATS = 9
 STAT_ITERATIONS, STAT_FILLED, STAT_DEADLOCK, STAT_UNFILLABLE = 0, 1, 2, 3
 STAT_REMAINING, STAT_INPAINT, STAT_ROWS_OVERFLOW, STAT_LAST_FRONTIER = 4, 5, 6, 7
+STAT_BAD_LABELS = 8
 
 EXPORTS = (
     "gf_fill_workspace_bytes", "gf_fill_splines_workspace_bytes", "gf_fill", "gf_fill_splines",

@@ -122,3 +122,25 @@ def download(t) -> np.ndarray:
     buf[: out.nbytes].copy_(t.view(-1).view(torch.uint8), non_blocking=True)
     torch.cuda.current_stream().synchronize()
     return out
+
+
+_report_buf = {}
+
+
+def read_report(stats, rows, max_rows=4096):
+    """One pinned read-back of a frame's stats and its first report rows
+    (a single synchronisation instead of two)."""
+    import torch
+
+    n_rows = min(rows.shape[0], max_rows)
+    key = (stats.numel(), n_rows)
+    with _lock:
+        buf = _report_buf.get(key)
+        if buf is None:
+            buf = (torch.empty(stats.numel(), dtype=torch.int32, pin_memory=True),
+                   torch.empty((n_rows, 2), dtype=torch.int32, pin_memory=True))
+            _report_buf[key] = buf
+    buf[0].copy_(stats.reshape(-1), non_blocking=True)
+    buf[1].copy_(rows[:n_rows], non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    return buf[0].numpy().copy(), buf[1].numpy().copy()

@@ -270,6 +270,19 @@ __global__ void __launch_bounds__(kThreads, GF_PREP_MIN_BLOCKS) k_prep(const __g
       for (int ch = 0; ch < C; ++ch)
         px.t[u * C + ch] = (row_in && gx0 + u < A.W) ? __ldg(img + ((size_t)gy * A.W + gx0 + u) * C + ch) : T(0);
   }
+  // label validation (grid.py:36-46) rides on the own-pixel load: any byte
+  // outside {0, 128, 255} flags the frame
+  {
+    const unsigned bad = ~(__vcmpeq4(own4, 0u) | __vcmpeq4(own4, 0x80808080u) |
+                           __vcmpeq4(own4, 0xffffffffu));
+    if (bad && gy < A.H) {
+      unsigned valid = 0;  // bytes of in-lattice columns
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (tx0 + c0 + u < A.W) valid |= 0xffu << (8 * u);
+      if (bad & valid) A.badlab[f] = 1;
+    }
+  }
   const bool tile_d = __syncthreads_or(any_inp);
   // copy to the output + value hull of the Readable pixels
   {
@@ -1474,6 +1487,7 @@ __global__ void __launch_bounds__(kShellThreads, GF_SHELL_MIN_BLOCKS)
       st[GF_STAT_INPAINT] = A.inpaint[f];
       st[GF_STAT_ROWS_OVERFLOW] = A.overflow[f];
       st[GF_STAT_LAST_FRONTIER] = A.last_f[f];
+      st[GF_STAT_BAD_LABELS] = A.badlab[f];
     }
   }
 }
@@ -1642,6 +1656,7 @@ int fill_launch(const gf_frames* fr, const gf_fill_params* prm, const gf_fill_ou
   A.inpaint = ints;          ints += nF;
   A.overflow = ints;         ints += nF;
   A.last_f = ints;           ints += nF;
+  A.badlab = ints;           ints += nF;
   A.clip_next = ints;         ints += 1;
   A.ntiles = tiles_of(H, W);
   A.clip_total = nF * A.ntiles;

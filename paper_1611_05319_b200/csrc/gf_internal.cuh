@@ -12,7 +12,7 @@
 namespace gf {
 
 constexpr int kMaxFramesPerLaunch = 1024;
-constexpr int kIntsPerFrame = 27;  // cnt[4] cntR[4] fills[4] anyg[4] + 10 scalars (+ 1 shared)
+constexpr int kIntsPerFrame = 28;  // cnt[4] cntR[4] fills[4] anyg[4] + 11 scalars (+ 1 shared)
 
 // Everything the fill kernels need, passed by value (__grid_constant__).
 struct FillArgs {
@@ -43,6 +43,7 @@ struct FillArgs {
   int* inpaint;    // [nF]
   int* overflow;   // [nF]
   int* last_f;     // [nF] frontier size of a shell that ended unfilled
+  int* badlab;     // [nF] a label outside {0, 128, 255} was seen
   unsigned long long* best_key;  // [nF]
   unsigned long long* hull;      // [nF][2] order-preserving encoded min/max
   int* stats;

@@ -207,22 +207,26 @@ def _run_fill(image, labels, guide_vecs, params: FillParams, tracked: bool, orde
     img = np.ascontiguousarray(image, dtype=np.float64)
     C = img.shape[2]
     t0 = time.perf_counter()
-    d_img = _staging.upload(img, dev, "img").reshape(1, H, W, C)
-    d_lab = _staging.upload(np.ascontiguousarray(labels, dtype=np.uint8), dev, "lab").reshape(1, H, W)
-    if validate:
-        grid.validate_labels(labels, d_lab)
+    # labels first (small, direct), then the image through the chunked pinned
+    # stager; the spline segments come from a content-keyed device cache
+    d_lab = torch.from_numpy(np.ascontiguousarray(labels, dtype=np.uint8)).to(dev).reshape(1, H, W)
     d_guide = None
     segs = None
     if splines is not None and params.g_source == "guide_field":
-        segs = SegmentSet(list(splines), dev) if len(splines) else None
-    elif guide_vecs is not None and params.g_source == "guide_field":
+        segs = SegmentSet.cached(list(splines), dev) if len(splines) else None
+    d_img = _staging.upload(img, dev, "img").reshape(1, H, W, C)
+    if guide_vecs is not None and params.g_source == "guide_field" and segs is None:
         d_guide = _staging.upload(np.ascontiguousarray(guide_vecs, dtype=np.float64), dev,
                                   "guide").reshape(1, H, W, 2)
     res = fill_device(d_img, d_lab, d_guide, params, tracked=tracked, order_log=order_log,
                       rows_cap=H * W + 1, splines=segs, eta=eta, want_fillshell=True)
-    stats = res["stats"][0].cpu().numpy()
+    stats, rows_dev = _staging.read_report(res["stats"][0], res["rows"][0])
+    if validate and stats[N.STAT_BAD_LABELS]:
+        grid.validate_labels(labels)  # k_prep saw a bad label: the reference's message
+        raise ValueError("label mask holds values outside {0, 128, 255}")
     iters = int(stats[N.STAT_ITERATIONS])
-    rows_dev = res["rows"][0, :iters + 1].cpu().numpy()
+    if iters + 1 > rows_dev.shape[0]:
+        rows_dev = res["rows"][0, :iters + 1].cpu().numpy()
     u = _staging.download(res["out"][0])
     rep = FillReport()
     rep.iterations = iters
