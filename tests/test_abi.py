@@ -25,7 +25,7 @@ def test_library_exports_every_declared_symbol():
     lib = _native.load()
     for name in declared_functions():
         assert hasattr(lib, name), name
-    assert lib.gf_abi_version() == 1
+    assert lib.gf_abi_version() == 2
 
 
 def test_struct_layouts_match_the_header(tmp_path):
