@@ -1113,7 +1113,7 @@ __global__ void __launch_bounds__(kShellThreads, GF_SHELL_MIN_BLOCKS)
   // lattice items: LG lanes each (4 for the r <= 3 balls: K <= 28 samples,
   // 7 per lane), IPU = 32 / LG items per warp round
 #ifndef GF_LATTICE_LANES
-#define GF_LATTICE_LANES 8
+#define GF_LATTICE_LANES 4
 #endif
   constexpr int LG = (R > 0 && R <= 3) ? GF_LATTICE_LANES : 8;
   constexpr int IPU = 32 / LG;

@@ -22,9 +22,9 @@ for rep in range(4):
 t = res["trace"].cpu().numpy()
 n = int(res["stats"][0, 0].item())
 print(f"{cfg}: shells {n}")
-print("k  items  fill  sync | first_unit_after_start | lat: entry eval_max eval_mean n dec+act | flush_max | rot eval_max (us)")
+print("k  items  fill  sync | entry_max eval_max eval_mean n | fetch rest | decide activate  (means, us)")
 for k in range(n):
     r, f = t[k], t[128 + k]
-    first = (int(~np.uint64(f[6])) - int(r[0])) / 1e3 if f[6] else float('nan')
-    print(f"{k:2d} {r[5]:6d} {(r[1]-r[0])/1e3:5.2f} {(r[2]-r[1])/1e3:5.2f} | {first:6.2f} | "
-          f"{f[0]/1e3:5.2f} {f[1]/1e3:5.2f} {f[2]/max(1,f[3])/1e3:5.2f} {f[3]:6d} {f[4]/1e3:5.2f} | {f[5]/1e3:5.2f} | {f[7]/1e3:5.2f}")
+    c = max(1, f[3])
+    print(f"{k:2d} {r[5]:6d} {(r[1]-r[0])/1e3:5.2f} {(r[2]-r[1])/1e3:5.2f} | "
+          f"{f[0]/1e3:5.2f} {f[1]/1e3:5.2f} {f[2]/c/1e3:5.2f} {f[3]:6d} | {f[4]/c/1e3:5.2f} {f[5]/c/1e3:5.2f} | {f[6]/c/1e3:5.2f} {f[7]/c/1e3:5.2f}")

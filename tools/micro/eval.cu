@@ -47,6 +47,24 @@ __global__ void k_eval(const __grid_constant__ BallParams P, const __grid_consta
     if (p >= H * W - 10 * W) p -= (H - 40) * W;
   }
   cyc[1] = (clk() - t0) / N;
+  // lattice eval timed alone, with a rotated eval (other code) between timings
+  long long lat_sum = 0;
+  for (int i = 0; i < N; ++i) {
+    SampleResult r2;
+    eval_rot_warp<3>(P, S, src, lane, (double)(p % W), (double)(p / W), gx, gy, gx / 0.5, gy / 0.5, r2);
+    accum += r2.rw;
+    p += 7919 + ((int)r2.v[0] & 1);
+    if (p >= H * W - 10 * W) p -= (H - 40) * W;
+    const long long ta = clk();
+    SampleResult r;
+    eval_lattice<3, 8>(P, S, src, lane & 7, lane >> 3, true, p % W, p / W, r);
+    if (r.rw == -1.0) asm volatile("trap;");
+    lat_sum += clk() - ta;
+    accum += r.rw;
+    p += 7919 + ((int)r.v[0] & 1);
+    if (p >= H * W - 10 * W) p -= (H - 40) * W;
+  }
+  cyc[3] = lat_sum / N;
   // loads only: 4 independent float4 fetches per lane, dependent across iterations
   t0 = clk();
   for (int i = 0; i < N; ++i) {
@@ -86,5 +104,6 @@ int main() {
   printf("%-16s %lld cycles\n", "eval lattice", hc[16]);
   printf("%-16s %lld cycles\n", "eval rotated", hc[17]);
   printf("%-16s %lld cycles\n", "4 fetches", hc[18]);
+  printf("%-16s %lld cycles\n", "lattice after rot", hc[19]);
   printf("err: %s\n", cudaGetErrorString(cudaGetLastError()));
 }
