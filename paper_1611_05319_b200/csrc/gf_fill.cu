@@ -156,6 +156,7 @@ __global__ void __launch_bounds__(kThreads, GF_PREP_MIN_BLOCKS) k_prep(const __g
   const int ext = kTile + 2 * R;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   __shared__ unsigned int s_hrow[kTileExt];
+  __shared__ unsigned int s_vrow[kTile];
   __shared__ unsigned long long s_hrow64[kTileExt];
   __shared__ unsigned long long s_rrow64[kTileExt];
   __shared__ int s_cand[kMaxCand];
@@ -299,19 +300,23 @@ __global__ void __launch_bounds__(kThreads, GF_PREP_MIN_BLOCKS) k_prep(const __g
           for (int ch = 0; ch < C; ++ch) out[((size_t)gy * A.W + gx0 + u) * C + ch] = px.t[u * C + ch];
     }
     // [0] value hull of the Readable pixels, [1] range of the Bystanders
+    // per pixel: channel min / max, then merged into its class (branch-free)
     T vlo[2] = {T(INFINITY), T(INFINITY)}, vhi[2] = {T(-INFINITY), T(-INFINITY)};
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const uint8_t l = (uint8_t)(own4 >> (8 * u));
-      if (row_in && gx0 + u < A.W && (l == 0 || l == 128)) {
-        const int b = l == 0 ? 0 : 1;
+      T mn = px.t[u * C], mx = px.t[u * C];
 #pragma unroll
-        for (int ch = 0; ch < C; ++ch) {
-          const T x = px.t[u * C + ch];
-          vlo[b] = x < vlo[b] ? x : vlo[b];
-          vhi[b] = x > vhi[b] ? x : vhi[b];
-        }
+      for (int ch = 1; ch < C; ++ch) {
+        mn = fmin(mn, px.t[u * C + ch]);
+        mx = fmax(mx, px.t[u * C + ch]);
       }
+      const bool in = row_in && gx0 + u < A.W;
+      const bool rd = in && l == 0, by = in && l == 128;
+      vlo[0] = rd ? fmin(vlo[0], mn) : vlo[0];
+      vhi[0] = rd ? fmax(vhi[0], mx) : vhi[0];
+      vlo[1] = by ? fmin(vlo[1], mn) : vlo[1];
+      vhi[1] = by ? fmax(vhi[1], mx) : vhi[1];
     }
     unsigned long long ered[4];  // max(~enc) <=> min(enc)
     if constexpr (sizeof(T) == 4) {
@@ -401,10 +406,17 @@ __global__ void __launch_bounds__(kThreads, GF_PREP_MIN_BLOCKS) k_prep(const __g
     }
   }
   __syncthreads();
+  // ... and vertical: bit c of s_vrow[y] <=> an Inpaint pixel within
+  // Chebyshev distance R of tile pixel (c, y)
+  if (threadIdx.x < kTile) {
+    unsigned int v = 0;
+    for (int dy = 0; dy <= 2 * R; ++dy) v |= s_hrow[threadIdx.x + dy];
+    s_vrow[threadIdx.x] = v;
+  }
+  __syncthreads();
 
   // 3. four consecutive pixels per thread: row ry, columns c0 .. c0+3
-  unsigned int vmask = 0;
-  for (int dy = 0; dy <= 2 * R; ++dy) vmask |= s_hrow[ry + dy];
+  const unsigned int vmask = s_vrow[ry];
   int n_inp = 0;
   bool anyg = false;
   uint32_t ent[4];
