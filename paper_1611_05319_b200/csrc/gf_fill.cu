@@ -802,8 +802,9 @@ __device__ __forceinline__ void write_out(const FillArgs& A, int f, uint32_t p, 
 // recorded each tile's Bystander value range: a tile whose range lies in
 // the frame's hull is already final (the clip is the identity), so only
 // tiles holding out-of-hull Bystanders are touched.  Tiles are handed out by
-// an atomic counter to warps with no fill work in a shell, the rest after
-// the last shell.
+// an atomic counter to every warp after the last shell (doing them in a
+// shell's idle warps could stretch that shell: a tile is several memory
+// round trips).
 __device__ __forceinline__ bool range_inside(const FillArgs& A, int f, const unsigned long long* r) {
   const unsigned long long hl = A.hull[2 * f], hh = A.hull[2 * f + 1];
   if (hh == 0ULL || r[1] == 0ULL) return true;  // no hull (no clip) or no Bystander
@@ -813,25 +814,42 @@ __device__ __forceinline__ bool range_inside(const FillArgs& A, int f, const uns
 template <typename T>
 __device__ __forceinline__ void clip_tile_rows(const FillArgs& A, int f, int tx0, int ty0, double lo,
                                                double hi) {
+  // lane = column; the tile's 32 label bytes of this column are loaded at
+  // once, then the Bystanders' values in two batches of 16 rows, so a tile
+  // costs a few memory round trips, not one per row
   const int lane = threadIdx.x & 31;
   const int x = tx0 + lane;
   if (x >= A.W) return;
   const uint8_t* lab = A.labels + (size_t)f * A.HW;
   const T* in = reinterpret_cast<const T*>(A.image) + (size_t)f * A.HW * A.C;
   T* out = reinterpret_cast<T*>(A.out) + (size_t)f * A.HW * A.C;
-  for (int y0 = ty0; y0 < min(A.H, ty0 + kTile); y0 += 8) {
-    uint8_t l[8];
+  const int rows = min(kTile, A.H - ty0);
+  unsigned bys = 0;  // bit y: row ty0 + y of this column is a Bystander
 #pragma unroll
-    for (int i = 0; i < 8; ++i) l[i] = (y0 + i < A.H) ? lab[(size_t)(y0 + i) * A.W + x] : 0;
+  for (int y = 0; y < kTile; ++y)
+    if (y < rows && lab[(size_t)(ty0 + y) * A.W + x] == 128) bys |= 1u << y;
 #pragma unroll
-    for (int i = 0; i < 8; ++i)
-      if (l[i] == 128) {
-        const size_t g = ((size_t)(y0 + i) * A.W + x) * A.C;
-        for (int c = 0; c < A.C; ++c) {
-          double v = (double)in[g + c];
-          v = (v < lo) ? lo : ((v > hi) ? hi : v);
-          out[g + c] = (T)v;
-        }
+  for (int h = 0; h < 2; ++h) {
+    T v[16][4];
+#pragma unroll
+    for (int y = 0; y < 16; ++y)
+      if ((bys >> (16 * h + y)) & 1u) {
+        const size_t g = ((size_t)(ty0 + 16 * h + y) * A.W + x) * A.C;
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          if (c < A.C) v[y][c] = in[g + c];
+      }
+#pragma unroll
+    for (int y = 0; y < 16; ++y)
+      if ((bys >> (16 * h + y)) & 1u) {
+        const size_t g = ((size_t)(ty0 + 16 * h + y) * A.W + x) * A.C;
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          if (c < A.C) {
+            double val = (double)v[y][c];
+            val = (val < lo) ? lo : ((val > hi) ? hi : val);
+            out[g + c] = (T)val;
+          }
       }
   }
 }
@@ -1267,8 +1285,6 @@ __global__ void __launch_bounds__(kShellThreads, GF_SHELL_MIN_BLOCKS)
       if (lane == 0 && wf >= 0 && wfills > 0) atomicAdd(&A.fills[cur * A.nF + wf], wfills);
       GF_FINE(const unsigned long long ff1 = fine_after((unsigned)wn);
               if (lane == 0 && wf >= 0) fine_put(A, k, 5, ff1 - ff0);)
-      // a warp without fill work this shell clips one chunk of Bystanders
-      if (clip_work && u0 >= U) clip_claim(A);
       if (A.trace && lane == 0 && k < A.trace_cap)
         atomicMax(&A.trace[k * kTraceSlots + 1], gtimer());
     }
@@ -1482,7 +1498,7 @@ __global__ void __launch_bounds__(kShellThreads, GF_SHELL_MIN_BLOCKS)
       load_p0(A, S, nxt);
     }
   }
-  // the Bystander chunks no idle warp took
+  // Bystander clip of the tiles that need it
   while (clip_work && clip_claim(A)) {
   }
   timeline_mark(A, 1, false);
