@@ -1,3 +1,3 @@
 mkdir -p gpurun_out
-./tools/micro/evalb > gpurun_out/micro.log 2>&1
+./tools/micro/shellsim > gpurun_out/micro.log 2>&1
 cat gpurun_out/micro.log

@@ -18,7 +18,7 @@ __device__ void my_sync(unsigned* count, unsigned* gen, unsigned nb, int sleep_n
   __syncthreads();
 }
 __global__ void __launch_bounds__(256, 2) sim(float4* buf, unsigned n, int rounds, int active, unsigned long long* acc,
-                                              int sleep_ns, unsigned* bar, int delay) {
+                                              int sleep_ns, unsigned* bar, int delay, int pattern) {
   cg::grid_group grid = cg::this_grid();
   const int lane = threadIdx.x & 31;
   const int gw = blockIdx.x * 8 + (threadIdx.x >> 5);
@@ -28,7 +28,11 @@ __global__ void __launch_bounds__(256, 2) sim(float4* buf, unsigned n, int round
       if (delay) { long long t = clock64(); while (clock64() - t < delay) {} }
       unsigned base = hash32(gw * 7919u + r * 104729u);
       unsigned q[4];
-      for (int t = 0; t < 4; ++t) q[t] = hash32(base + t * 31 + lane) % n;
+      for (int t = 0; t < 4; ++t) {
+        if (pattern == 0) q[t] = hash32(base + t * 31 + lane) % n;            // 32 random lines / instr
+        else if (pattern == 1) q[t] = (hash32(base + t) % (n - 64)) + lane;   // 4 contiguous lines / instr
+        else q[t] = (hash32(base) % (n - 4096)) + (lane & 7) + 1920 * ((lane >> 3) + 4 * t);  // 7x7-ball-like: 4 rows x 8 px
+      }
       long long t0 = clock64();
       float4 v[4];
       for (int t = 0; t < 4; ++t) v[t] = buf[q[t]];
@@ -48,11 +52,11 @@ int main() {
   cudaMalloc(&buf, (size_t)n * 16); cudaMemset(buf, 0, (size_t)n * 16);
   cudaMalloc(&acc, 16); cudaMalloc(&bar, 8);
   int dev = 0, sms = 0; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  for (int per : {2}) for (int sleep_ns : {-1, 0, 200, 1000}) for (int delay : {0, 20000}) for (int active : {30, 2368}) {
+  for (int per : {2}) for (int sleep_ns : {-1}) for (int delay : {0}) for (int pattern : {0, 1, 2}) for (int active : {30, 296, 2368}) {
     int grid = sms * per;
     cudaMemset(acc, 0, 16); cudaMemset(bar, 0, 8);
     int rounds = 50;
-    void* args[] = {&buf, (void*)&n, &rounds, &active, &acc, &sleep_ns, &bar, &delay};
+    void* args[] = {&buf, (void*)&n, &rounds, &active, &acc, &sleep_ns, &bar, &delay, &pattern};
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
     cudaEventRecord(e0);
     cudaLaunchCooperativeKernel((void*)sim, grid, 256, args, 0, 0);
@@ -60,8 +64,8 @@ int main() {
     float ms; cudaEventElapsedTime(&ms, e0, e1);
     unsigned long long h[2];
     cudaMemcpy(h, acc, 16, cudaMemcpyDeviceToHost);
-    printf("grid %4d sleep %5d delay %5d active %5d: load %5.0f cycles, %.2f us/round\n", grid, sleep_ns, delay, active,
-           (double)h[0] / h[1], ms * 1e3 / rounds);
+    printf("pattern %d grid %4d active %5d: load %5.0f cycles, %.2f us/round\n", pattern, grid, active,
+           (double)h[0] / h[1], ms * 1e3 / rounds); (void)sleep_ns; (void)delay;
   }
   printf("err: %s\n", cudaGetErrorString(cudaGetLastError()));
 }
