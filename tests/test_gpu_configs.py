@@ -165,3 +165,30 @@ def test_fill_graph_replay_matches_eager():
         assert torch.equal(out["out"], eager["out"])
         assert torch.equal(out["fillshell"], eager["fillshell"])
         assert torch.equal(out["stats"], eager["stats"])
+
+
+@pytest.mark.parametrize("r,order,nb", [(7, "smart", "rotated_ball"), (8, "onion", "axis_ball"),
+                                        (9, "smart_with_data_term", "rotated_ball")])
+def test_large_ball_generic_evaluator(r, order, nb):
+    """r >= 7 (K > 128: several pairwise leaves) runs the runtime-K evaluator."""
+    sc = scenes.small_scene(120, 200, band=10, gx=3, gy=2, n_spl=3, seed=31 + r)
+    field = build_guide_field(_splines(sc), sc.labels)
+    p = FillParams(r=r, mu=50.0, order=order, neighborhood=nb)
+    ref = orc.fill(sc.image, sc.labels, field, orc.Params.of(p), tracked=True)
+    for tracked in (True, False):
+        u, rep, maps = engine._run_fill(sc.image, sc.labels, field, p, tracked=tracked,
+                                        order_log=True)
+        assert np.array_equal(maps["fillshell"], ref["fillshell"])
+        assert np.array_equal(maps["enter"], ref["enter"])
+        assert float(np.abs(u - ref["u"]).max()) <= 1e-4
+
+
+@pytest.mark.parametrize("r", [2, 3, 5])
+def test_fixed_guide_source(r):
+    sc = scenes.small_scene(100, 160, band=8, gx=3, gy=2, n_spl=2, seed=5 + r)
+    p = FillParams(r=r, mu=50.0, order="smart", neighborhood="rotated_ball", g_source="fixed",
+                   g_fixed=(0.6, -0.8))
+    ref = orc.fill(sc.image, sc.labels, None, orc.Params.of(p), tracked=True)
+    u, rep, maps = engine._run_fill(sc.image, sc.labels, None, p, tracked=True, order_log=True)
+    assert np.array_equal(maps["fillshell"], ref["fillshell"])
+    assert float(np.abs(u - ref["u"]).max()) <= 1e-4
