@@ -20,7 +20,6 @@ struct FillArgs {
   int dtype;
   const void* image;
   const uint8_t* labels;
-  const double* guide;
   const double* gsrc;  // caller's per-pixel guide (g_mode 2 without splines)
   double4* gbuf;       // per Inpaint pixel (gx, gy, ux, uy), written by k_prep, or nullptr
   void* out;

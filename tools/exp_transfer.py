@@ -16,3 +16,23 @@ _staging._CHUNK = 8 << 20
 tm("labels .to(dev) pageable", lambda: torch.from_numpy(sc.labels).to(dev))
 tm("labels staged", lambda: _staging.upload(sc.labels, dev, "lab"))
 tm("image .to(dev) pageable", lambda: torch.from_numpy(sc.image).to(dev))
+
+# page-lock the caller's own buffer in place, DMA from it, unlock
+cudart = torch.cuda.cudart()
+def reg_upload():
+    a = sc.image
+    ptr, nb = a.ctypes.data, a.nbytes
+    err = cudart.cudaHostRegister(ptr, nb, 0)
+    assert int(err) == 0, err
+    src = torch.from_numpy(a)
+    dst = torch.empty(a.shape, dtype=torch.float64, device=dev)
+    dst.copy_(src, non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    cudart.cudaHostUnregister(ptr)
+    return dst
+tm("upload via cudaHostRegister (in place)", reg_upload)
+def reg_only():
+    a = sc.image
+    cudart.cudaHostRegister(a.ctypes.data, a.nbytes, 0)
+    cudart.cudaHostUnregister(a.ctypes.data)
+tm("register+unregister only", reg_only)
