@@ -28,6 +28,9 @@ int set_error(int code, const char* msg) {
 
 // Disk offsets (n, m), n^2 + m^2 <= r^2, meshgrid order (m outer, n inner),
 // centre moved to the front and then dropped (engine.py:172).
+static const int kNbDi[8] = {-1, 0, 1, -1, 1, -1, 0, 1};
+static const int kNbDj[8] = {-1, -1, -1, 0, 0, 1, 1, 1};
+
 static int build_ball(const gf_fill_params* p, BallParams& P, BallTables& T) {
   if (p->r < 1) return set_error(GF_E_INVALID, "r must be >= 1");
   if (p->r > GF_MAX_RADIUS) return set_error(GF_E_UNSUPPORTED, "r exceeds GF_MAX_RADIUS");
@@ -48,10 +51,16 @@ static int build_ball(const gf_fill_params* p, BallParams& P, BallTables& T) {
       T.w0[K] = 1.0 / hypot_np((double)n, (double)m);
       T.ni[K] = n;
       T.mi[K] = m;
+      T.kn[K] = -1;
+      for (int o = 0; o < 8; ++o)  // NEIGHBOR_OFFSETS (grid.py:29-33)
+        if (n == kNbDi[o] && m == kNbDj[o]) T.kn[K] = (signed char)o;
       ++K;
     }
   P.r = r;
   P.K = K;
+  P.nb_unknown = 0;
+  for (int o = 0; o < 8; ++o)
+    if (kNbDi[o] * kNbDi[o] + kNbDj[o] * kNbDj[o] > r * r) P.nb_unknown |= 1u << o;
   P.rotated = p->neighborhood == GF_BALL_ROTATED;
   P.periodic = p->periodic_x != 0;
   P.mu_inf = isinf(p->mu) ? 1 : 0;

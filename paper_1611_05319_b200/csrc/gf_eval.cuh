@@ -71,6 +71,20 @@ __device__ __forceinline__ void eval_lattice(const BallParams& P, const BallTabl
 #pragma unroll
   for (int t = 0; t < KPL; ++t)
     if (q[t] >= 0 && __float_as_int(v[t].w) <= src.shell) okm |= 1u << t;
+  // the 8-neighbours this lane sampled that are Inpaint and not yet in a
+  // frontier: only those can be activated by a fill (tracker.py:42-79)
+  unsigned inact = 0;
+#pragma unroll
+  for (int t = 0; t < KPL; ++t) {
+    const int k = glane + LG * t;
+    if (k < B::K && q[t] >= 0) {
+      const int o = T.kn[k];
+      if (o >= 0 && (__float_as_int(v[t].w) & ~kRotBit) == kStampInactive) inact |= 1u << o;
+    }
+  }
+#pragma unroll
+  for (int o = 1; o < LG; o <<= 1) inact |= __shfl_xor_sync(0xffffffffu, inact, o, LG);
+  out.nb = inact | P.nb_unknown;
   double acc0 = 0.0, acc1 = 0.0;  // accumulators glane (and glane + 4 when LG == 4)
 #pragma unroll
   for (int t = 0; t < B::N8 / LG; ++t)

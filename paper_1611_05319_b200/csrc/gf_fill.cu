@@ -939,14 +939,16 @@ __device__ __forceinline__ uint32_t claim(float4* fw, int q) {
 template <int LG>
 __device__ __forceinline__ void activate(const FillArgs& A, uint32_t* reg, int& n, bool staged,
                                          uint32_t* nxt_list, int nxt, float4* fw, int f, int k,
-                                         int gl, bool filled, uint32_t e) {
+                                         int gl, bool filled, uint32_t e, unsigned cand = 0xffu) {
   constexpr int NPL = 8 / LG;  // neighbours per lane
   const bool survive = gl == 0 && !filled;
   uint32_t qe[NPL];
 #pragma unroll
   for (int r = 0; r < NPL; ++r) {
     qe[r] = 0xffffffffu;
-    if (gl >= 0 && filled) {
+    // cand: the neighbours that can still be claimed (the others are
+    // Readable, Bystander, filled or already in a frontier: no CAS needed)
+    if (gl >= 0 && filled && ((cand >> (gl + LG * r)) & 1u)) {
       bool in;
       const int q = neighbor_of(A, e & kEntryPix, gl + LG * r, in);
       if (in) {
@@ -1119,6 +1121,7 @@ __global__ void __launch_bounds__(kShellThreads, GF_SHELL_MIN_BLOCKS)
     S.tab.w0[i] = tables.w0[i];
     S.tab.ni[i] = tables.ni[i];
     S.tab.mi[i] = tables.mi[i];
+    S.tab.kn[i] = tables.kn[i];
   }
   pdl_wait();
   timeline_mark(A, 1, true);
@@ -1264,7 +1267,8 @@ __global__ void __launch_bounds__(kShellThreads, GF_SHELL_MIN_BLOCKS)
           filled = __shfl_sync(0xffffffffu, filled, 0, LG);
           GF_FINE(const unsigned long long fl3 = fine_after(filled ? 1u : 0u);)
           if (kTracked)
-            activate<LG>(A, reg, wn, uniform, nxt_list, nxt, fw, fs, k, valid ? lglane : -1, filled, e);
+            activate<LG>(A, reg, wn, uniform, nxt_list, nxt, fw, fs, k, valid ? lglane : -1, filled, e,
+                         R > 0 ? res.nb : 0xffu);
           GF_FINE(const unsigned long long fl4 = fine_after((unsigned)wn);
                   if (valid && lglane == 0) {
                     fine_put(A, k, 0, fl1 - fl0); fine_put(A, k, 1, fl2 - fl1);

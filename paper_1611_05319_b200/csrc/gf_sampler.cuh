@@ -39,6 +39,7 @@ __host__ __device__ __forceinline__ bool stamp_unfilled(int st) {
 
 struct BallParams {
   int r, K;
+  unsigned nb_unknown;  // 8-neighbours (NEIGHBOR_OFFSETS order) that are not ball samples
   double tw0;      // numpy pairwise sum of the g = 0 weights (the lattice-path tw)
   int rotated;   // rotated_ball (engine.py:150-164) vs axis_ball
   int periodic;  // periodic_x
@@ -56,11 +57,15 @@ struct BallTables {
   double w0[kMaxK];
   int ni[kMaxK];  // the same offsets as integers (lattice path)
   int mi[kMaxK];
+  signed char kn[kMaxK];  // sample k is 8-neighbour kn[k] of the centre, or -1
 };
 
 struct SampleResult {
   double rw, tw;  // readable / total weight mass (exact numpy bits)
   double v[4];    // weighted average colour, 0 where rw == 0
+  unsigned nb;    // 8-neighbours that may need activation (lattice path: the
+                  // ones Inpaint-inactive at the shell's start, plus those
+                  // the ball does not sample); 0xff when unknown
 #ifdef GF_FINE_TRACE
   unsigned long long t0, t1;  // fetch issued / first fetch arrived (phase trace)
 #endif
