@@ -452,9 +452,18 @@ __global__ void __launch_bounds__(kThreads, GF_PREP_MIN_BLOCKS) k_prep(const __g
           double dmin = INFINITY;
           int nearest = 0x7fffffff;
           const double fx = (double)gx, fy = (double)gy;
+          // a segment whose bounding box lies farther than 3 eta cannot give
+          // this pixel a non-zero g (d > cut for it), so its exact distance
+          // is skipped; the bound is padded well past rounding, keeping every
+          // segment with d <= cut -- the only ones that decide g
+          const double cut2 = A.cut * A.cut * (1.0 + 1e-9) + 1e-9;
           for (int cc = 0; cc < n_eval; ++cc) {
             const int sidx = exhaustive ? e0 + cc : s_cand[cc];
-            const double d = seg_dist(fx, fy, A.seg[sidx]);
+            const double4 sg = A.seg[sidx];
+            const double bx = fmax(fmax(fmin(sg.x, sg.z) - fx, fx - fmax(sg.x, sg.z)), 0.0);
+            const double by = fmax(fmax(fmin(sg.y, sg.w) - fy, fy - fmax(sg.y, sg.w)), 0.0);
+            if (bx * bx + by * by > cut2) continue;
+            const double d = seg_dist(fx, fy, sg);
             const int sp = A.seg_spline[sidx];
             if (d < dmin || (d == dmin && sp < nearest)) {
               dmin = d;
