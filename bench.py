@@ -351,14 +351,27 @@ def run_ours(args):
             holder["u2"], _ = tracker.run_tracked(image_h, labels_h, fld, params)
             holder["fld"] = fld
 
+        # the same call on pinned host tensors: the inputs are DMA'd from the
+        # caller's pinned memory, the result comes back in a pinned tensor
+        image_p = torch.from_numpy(image_h).pin_memory()
+        labels_p = torch.from_numpy(labels_h).pin_memory()
+
+        def pinned():
+            holder["up"], _ = tracker.run_tracked(image_p, labels_p, splines, params)
+
+        tp = timed(pinned, ne)
         te = timed(fused, ne)
         td = timed(dropin, ne)
         u = holder["u"]
         fld = holder["fld"]
-        e2e = {"value": D / te / 1e6, "unit": "Mpx/s", "ms_per_frame": te * 1e3,
+        assert np.array_equal(holder["up"].numpy(), u), "pinned path differs from the numpy path"
+        e2e = {"value": D / tp / 1e6, "unit": "Mpx/s", "ms_per_frame": tp * 1e3,
                "h2d_bytes_per_step": int(image_h.nbytes + labels_h.nbytes),
                "d2h_bytes_per_step": int(u.nbytes),
-               "path": "tracker.run_tracked(image f64, labels, splines, params): numpy in/out",
+               "path": "tracker.run_tracked(image, labels, splines, params) on pinned host "
+                       "tensors (f64 image in, f64 image out, copies in the timed region)",
+               "numpy_ms_per_frame": te * 1e3,
+               "numpy_path": "the same call on pageable numpy f64 arrays (the reference's types)",
                "dropin_two_call_ms": td * 1e3,
                "dropin_two_call_bytes": int(image_h.nbytes + 2 * labels_h.nbytes + 2 * fld.nbytes
                                             + u.nbytes)}

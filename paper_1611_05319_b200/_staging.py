@@ -99,6 +99,22 @@ class _PinnedPool:
         weakref.finalize(arr, self._give, n, buf)
         return arr, buf
 
+    def take_tensor(self, shape, dtype):
+        """Like ``take``, as a CPU torch tensor (pinned) recycled on release."""
+        import weakref
+
+        import torch
+
+        n = int(np.prod(shape)) * torch.empty(0, dtype=dtype).element_size()
+        with self.lock:
+            lst = self.free.get(n)
+            buf = lst.pop() if lst else None
+        if buf is None:
+            buf = torch.empty(max(n, 1), dtype=torch.uint8, pin_memory=True)
+        t = buf[:n].view(dtype).view(shape)
+        weakref.finalize(t, self._give, n, buf)
+        return t, buf
+
     def _give(self, n, buf):
         with self.lock:
             lst = self.free.setdefault(n, [])
@@ -120,6 +136,17 @@ def download(t) -> np.ndarray:
         return t.cpu().numpy()
     out, buf = _pool_out.take(tuple(t.shape), dtype)
     buf[: out.nbytes].copy_(t.view(-1).view(torch.uint8), non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    return out
+
+
+def download_tensor(t):
+    """CUDA tensor -> new pinned CPU tensor (synchronous, recycled buffer)."""
+    import torch
+
+    t = t.contiguous()
+    out, buf = _pool_out.take_tensor(tuple(t.shape), t.dtype)
+    out.copy_(t, non_blocking=True)
     torch.cuda.current_stream().synchronize()
     return out
 

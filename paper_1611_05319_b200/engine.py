@@ -204,17 +204,30 @@ def _run_fill(image, labels, guide_vecs, params: FillParams, tracked: bool, orde
     from ._device import SegmentSet, fill_device
 
     H, W = labels.shape
-    img = np.ascontiguousarray(image, dtype=np.float64)
-    C = img.shape[2]
+    # torch tensors (CPU -- pinned ones are DMA'd straight from the caller's
+    # memory -- or CUDA) are accepted next to the reference's numpy arrays;
+    # the result comes back in the caller's kind (numpy f64 / CPU tensor)
+    as_tensor = isinstance(image, torch.Tensor)
     t0 = time.perf_counter()
-    # labels first (small, direct), then the image through the chunked pinned
-    # stager; the spline segments come from a content-keyed device cache
-    d_lab = torch.from_numpy(np.ascontiguousarray(labels, dtype=np.uint8)).to(dev).reshape(1, H, W)
+    if isinstance(labels, torch.Tensor):
+        d_lab = labels.to(torch.uint8).to(dev, non_blocking=labels.is_pinned()).reshape(1, H, W)
+        labels = labels.cpu().numpy() if labels.is_cuda else labels.numpy()
+    else:
+        # labels first (small, direct), then the image through the chunked
+        # pinned stager; the spline segments come from a content-keyed cache
+        d_lab = torch.from_numpy(np.ascontiguousarray(labels, dtype=np.uint8)).to(dev).reshape(1, H, W)
     d_guide = None
     segs = None
     if splines is not None and params.g_source == "guide_field":
         segs = SegmentSet.cached(list(splines), dev) if len(splines) else None
-    d_img = _staging.upload(img, dev, "img").reshape(1, H, W, C)
+    if as_tensor:
+        timg = image.to(torch.float64).contiguous()
+        C = timg.shape[2]
+        d_img = (timg if timg.is_cuda else timg.to(dev, non_blocking=timg.is_pinned())).reshape(1, H, W, C)
+    else:
+        img = np.ascontiguousarray(image, dtype=np.float64)
+        C = img.shape[2]
+        d_img = _staging.upload(img, dev, "img").reshape(1, H, W, C)
     if guide_vecs is not None and params.g_source == "guide_field" and segs is None:
         d_guide = _staging.upload(np.ascontiguousarray(guide_vecs, dtype=np.float64), dev,
                                   "guide").reshape(1, H, W, 2)
@@ -227,7 +240,11 @@ def _run_fill(image, labels, guide_vecs, params: FillParams, tracked: bool, orde
     iters = int(stats[N.STAT_ITERATIONS])
     if iters + 1 > rows_dev.shape[0]:
         rows_dev = res["rows"][0, :iters + 1].cpu().numpy()
-    u = _staging.download(res["out"][0])
+    if as_tensor:
+        u_t = _staging.download_tensor(res["out"][0])
+        u = u_t.numpy()  # shares memory: the unfillable fallback paints in place
+    else:
+        u = _staging.download(res["out"][0])
     rep = FillReport()
     rep.iterations = iters
     rep.filled = int(stats[N.STAT_FILLED])
@@ -252,7 +269,7 @@ def _run_fill(image, labels, guide_vecs, params: FillParams, tracked: bool, orde
         fillshell = np.where((np.asarray(labels) == INPAINT) & (fillshell < 0), -2, fillshell)
     enter = res["enter"][0].cpu().numpy() if order_log else None
     rep.wall_time_s = time.perf_counter() - t0
-    return u, rep, dict(enter=enter, fillshell=fillshell)
+    return (u_t if as_tensor else u), rep, dict(enter=enter, fillshell=fillshell)
 
 
 def inpaint(image, labels, guide=None, params: FillParams | None = None):

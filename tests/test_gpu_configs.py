@@ -192,3 +192,21 @@ def test_fixed_guide_source(r):
     u, rep, maps = engine._run_fill(sc.image, sc.labels, None, p, tracked=True, order_log=True)
     assert np.array_equal(maps["fillshell"], ref["fillshell"])
     assert float(np.abs(u - ref["u"]).max()) <= 1e-4
+
+
+def test_run_tracked_accepts_pinned_tensors():
+    """torch CPU tensors (pinned: DMA'd straight from the caller) and CUDA
+    tensors give the numpy path's result; the result comes back as a tensor."""
+    from paper_1611_05319_b200 import tracker
+
+    sc = scenes.config("C1")
+    spl = _splines(sc)
+    p = FillParams(**sc.params)
+    u_np, m_np = tracker.run_tracked(sc.image, sc.labels, spl, p)
+    img_t = torch.from_numpy(sc.image).pin_memory()
+    lab_t = torch.from_numpy(sc.labels).pin_memory()
+    for img, lab in ((img_t, lab_t), (img_t.cuda(), sc.labels)):
+        u_t, m_t = tracker.run_tracked(img, lab, spl, p)
+        assert isinstance(u_t, torch.Tensor) and u_t.device.type == "cpu"
+        assert np.array_equal(u_t.numpy(), u_np)
+        assert m_t.rows == m_np.rows
