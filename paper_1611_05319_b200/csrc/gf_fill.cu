@@ -791,8 +791,9 @@ __device__ __forceinline__ void warp_flush(const FillArgs& A, uint32_t* reg, int
 // Output of a filled pixel: its fp32 fill value clipped to the frame's value
 // hull of the initially Readable values (engine.py:372-375), stored in the
 // caller's dtype.
-__device__ __forceinline__ void write_out(const FillArgs& A, int f, uint32_t p, const float* v) {
-  const unsigned long long elo = ~A.hull[2 * f], ehi = A.hull[2 * f + 1];
+__device__ __forceinline__ void write_out(const FillArgs& A, int f, uint32_t p, const float* v,
+                                          unsigned long long hl, unsigned long long hh) {
+  const unsigned long long elo = ~hl, ehi = hh;
   const bool has_hull = ehi != 0ULL;
   const double lo = has_hull ? dec_ordered(elo) : 0.0;
   const double hi = has_hull ? dec_ordered(ehi) : 0.0;
@@ -887,9 +888,13 @@ __device__ __forceinline__ bool clip_claim(const FillArgs& A) {
 // ready / fill decision of one item (engine.py:317-333) and the in-place
 // write of its colour with the shell stamp (snapshot-safe: stamp k+1 is
 // unreadable for every other item of shell k).
+// hl / hh: the frame's encoded hull, loaded by the caller when the unit
+// starts so the output store never waits on it (in-order issue would stall
+// the group's shuffle behind that load).
 __device__ __forceinline__ bool decide_and_write(const FillArgs& A, int f, int j, uint32_t p, int k,
                                                  bool dt_eff, double gx, double gy,
-                                                 const SampleResult& r) {
+                                                 const SampleResult& r, unsigned long long hl,
+                                                 unsigned long long hh) {
   const double conf = r.rw / r.tw;
   bool ready;
   if (A.order == 0) {
@@ -900,7 +905,8 @@ __device__ __forceinline__ bool decide_and_write(const FillArgs& A, int f, int j
     ready = (hypot_np(gx, gy) > A.c2) && (conf > A.c);
   }
   const bool fill = ready && (r.rw > 0.0);
-  A.conf[(size_t)f * A.cap + j] = conf;
+  // the guard only reads confidences of frames where no item filled
+  if (!fill) A.conf[(size_t)f * A.cap + j] = conf;
   if (fill) {
     float4 o;
     o.x = (float)r.v[0];
@@ -910,7 +916,7 @@ __device__ __forceinline__ bool decide_and_write(const FillArgs& A, int f, int j
     A.work[(size_t)f * A.HW + p] = o;
     const float v[4] = {o.x, o.y, o.z, (float)r.v[3]};
     if (A.c3) A.c3[(size_t)f * A.HW + p] = v[3];
-    write_out(A, f, p, v);
+    write_out(A, f, p, v, hl, hh);
     if (A.fillshell) A.fillshell[(size_t)f * A.HW + p] = k;
   }
   return fill;
@@ -1212,6 +1218,7 @@ __global__ void __launch_bounds__(kShellThreads, GF_SHELL_MIN_BLOCKS)
             wfills = 0;
             wf = f;
           }
+          const unsigned long long hl = A.hull[2 * f], hh = A.hull[2 * f + 1];
           const bool dt_eff = (A.order == 2) && !dt_dead_at(A, f, k, prv) && frontier_has_g(A, cur, f);
           const double4 g4 = A.gbuf[(size_t)f * A.HW + p];
           const double gx = g4.x, gy = g4.y;
@@ -1225,7 +1232,7 @@ __global__ void __launch_bounds__(kShellThreads, GF_SHELL_MIN_BLOCKS)
           GF_FINE(if (A.trace && lane == 0) trace_max_val(A, k, 7, gtimer() - tw0);)
           GF_FINE(const unsigned long long fr2 = fine_after((unsigned)(__double_as_longlong(res.rw) >> 32));)
           bool filled = false;
-          if (lane == 0) filled = decide_and_write(A, f, j, p, k, dt_eff, gx, gy, res);
+          if (lane == 0) filled = decide_and_write(A, f, j, p, k, dt_eff, gx, gy, res, hl, hh);
           filled = __shfl_sync(0xffffffffu, filled, 0);
           GF_FINE(const unsigned long long fr3 = fine_after(filled ? 1u : 0u);)
           if (lane == 0 && filled) ++wfills;
@@ -1251,6 +1258,7 @@ __global__ void __launch_bounds__(kShellThreads, GF_SHELL_MIN_BLOCKS)
             wf = uniform ? f0 : -1;
           }
           const int fs = valid ? f : 0;
+          const unsigned long long hl = A.hull[2 * fs], hh = A.hull[2 * fs + 1];
           const int j = valid ? t - pf[fs] : 0;
           const uint32_t e = valid ? cur_list[(size_t)fs * A.cap + j] : 0u;
           const uint32_t p = e & kEntryPix;
@@ -1272,7 +1280,7 @@ __global__ void __launch_bounds__(kShellThreads, GF_SHELL_MIN_BLOCKS)
           GF_FINE(if (A.trace && valid && lglane == 0) trace_max_val(A, k, 6, gtimer() - te0);)
           GF_FINE(const unsigned long long fl2 = fine_after((unsigned)(__double_as_longlong(res.rw) >> 32));)
           bool filled = false;
-          if (valid && lglane == 0) filled = decide_and_write(A, fs, j, p, k, dt_eff, gx, gy, res);
+          if (valid && lglane == 0) filled = decide_and_write(A, fs, j, p, k, dt_eff, gx, gy, res, hl, hh);
           filled = __shfl_sync(0xffffffffu, filled, 0, LG);
           GF_FINE(const unsigned long long fl3 = fine_after(filled ? 1u : 0u);)
           if (kTracked)
@@ -1442,7 +1450,7 @@ __global__ void __launch_bounds__(kShellThreads, GF_SHELL_MIN_BLOCKS)
             A.work[(size_t)f * A.HW + p] = o;
             const float fv[4] = {o.x, o.y, o.z, (float)v[3]};
             if (A.c3) A.c3[(size_t)f * A.HW + p] = fv[3];
-            write_out(A, f, (uint32_t)p, fv);
+            write_out(A, f, (uint32_t)p, fv, A.hull[2 * f], A.hull[2 * f + 1]);
             if (A.fillshell) A.fillshell[(size_t)f * A.HW + p] = k;
             A.fills[cur * A.nF + f] = 1;
             A.deadlocks[f] += 1;
