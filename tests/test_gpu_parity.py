@@ -178,3 +178,31 @@ def test_spline_guide_extension_equals_field():
     v1, r1 = engine.inpaint(sc.image, sc.labels, field, p)
     v2, r2 = engine.inpaint(sc.image, sc.labels, spl, p)
     assert np.array_equal(v1, v2) and r1.rows == r2.rows
+
+
+@pytest.mark.parametrize("bad_at", [(0, 0), (31, 46), (17, 5)])
+def test_bad_label_raises_reference_message(bad_at):
+    """k_prep flags labels outside {0, 128, 255} (GF_STAT_BAD_LABELS); the API
+    raises grid.py:36-46's ValueError with the first bad location."""
+    from paper_1611_05319_b200 import tracker
+
+    case = ALL_CASES[0]
+    lab = np.array(case["labels"], dtype=np.uint8, copy=True)
+    j, i = bad_at
+    j, i = min(j, lab.shape[0] - 1), min(i, lab.shape[1] - 1)
+    lab[j, i] = 7
+    with pytest.raises(ValueError, match="label mask holds value 7"):
+        tracker.run_tracked(case["image"], lab, case["guide"], FillParams(**case["params"]))
+    with pytest.raises(ValueError, match="label mask holds value 7"):
+        engine.inpaint(case["image"], lab, case["guide"], FillParams(**case["params"]))
+
+
+def test_frame_without_inpaint_pixels():
+    case = ALL_CASES[0]
+    lab = np.where(case["labels"] == 255, 0, case["labels"]).astype(np.uint8)
+    p = FillParams(**case["params"])
+    u, rep, maps = engine._run_fill(case["image"], lab, case["guide"], p, tracked=True,
+                                    order_log=True)
+    ref = orc.fill(case["image"], lab, case["guide"], orc.Params.of(p), tracked=True)
+    assert rep.iterations == ref["iterations"] == 0
+    assert np.array_equal(u, ref["u"])
