@@ -24,20 +24,23 @@ _pinned = {}
 
 def _executor():
     global _pool
-    if _pool is None:
-        _pool = ThreadPoolExecutor(max_workers=max(1, min(16, os.cpu_count() or 1)))
-    return _pool
+    with _lock:
+        if _pool is None:
+            _pool = ThreadPoolExecutor(max_workers=max(1, min(16, os.cpu_count() or 1)))
+        return _pool
 
 
 def _staging(nbytes: int, slot: str):
-    """Cached pinned uint8 buffer of at least nbytes (one per slot)."""
+    """Cached pinned uint8 buffer of at least nbytes, one per (slot, calling
+    thread): concurrent fills from several host threads never share one."""
     import torch
 
+    key = (slot, threading.get_ident())
     with _lock:
-        buf = _pinned.get(slot)
+        buf = _pinned.get(key)
         if buf is None or buf.numel() < nbytes:
             buf = torch.empty(max(nbytes, 1), dtype=torch.uint8, pin_memory=True)
-            _pinned[slot] = buf
+            _pinned[key] = buf
         return buf
 
 
@@ -160,7 +163,7 @@ def read_report(stats, rows, max_rows=4096):
     import torch
 
     n_rows = min(rows.shape[0], max_rows)
-    key = (stats.numel(), n_rows)
+    key = (stats.numel(), n_rows, threading.get_ident())
     with _lock:
         buf = _report_buf.get(key)
         if buf is None:

@@ -210,3 +210,26 @@ def test_run_tracked_accepts_pinned_tensors():
         assert isinstance(u_t, torch.Tensor) and u_t.device.type == "cpu"
         assert np.array_equal(u_t.numpy(), u_np)
         assert m_t.rows == m_np.rows
+
+
+def test_concurrent_host_threads():
+    """Fills issued from several host threads (re-entrancy: service.py:28-104
+    serialises per project, callers may still run projects in parallel)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from paper_1611_05319_b200 import tracker
+
+    cases = [scenes.small_scene(90, 140, band=6, gx=3, gy=2, n_spl=2, seed=s) for s in range(4)]
+    want = []
+    for sc in cases:
+        p = FillParams(**sc.params)
+        want.append(tracker.run_tracked(sc.image, sc.labels, _splines(sc), p)[0])
+
+    def job(i):
+        sc = cases[i]
+        return tracker.run_tracked(sc.image, sc.labels, _splines(sc), FillParams(**sc.params))[0]
+
+    with ThreadPoolExecutor(4) as ex:
+        got = list(ex.map(job, [0, 1, 2, 3, 0, 1, 2, 3]))
+    for i, u in enumerate(got):
+        assert np.array_equal(u, want[i % 4])
