@@ -46,11 +46,17 @@ __device__ __forceinline__ void eval_lattice(const BallParams& P, const BallTabl
   constexpr int KPL = (B::K + LG - 1) / LG;
   int q[KPL];
   float4 v[KPL];
+  // a ball that lies inside the lattice (the usual case) indexes its samples
+  // by flat offset; near the border each sample is bounds-checked / wrapped
+  const bool inner = pi >= R && pi + R < src.W && pj >= R && pj + R < src.H;
+  const int p = pj * src.W + pi;
 #pragma unroll
   for (int t = 0; t < KPL; ++t) {
     const int k = glane + LG * t;
-    q[t] = (valid && k < B::K) ? lattice_index(pi + T.ni[k], pj + T.mi[k], src.H, src.W, P.periodic)
-                               : -1;
+    q[t] = (valid && k < B::K)
+               ? (inner ? p + T.off[k]
+                        : lattice_index(pi + T.ni[k], pj + T.mi[k], src.H, src.W, P.periodic))
+               : -1;
   }
 #ifdef GF_FINE_TRACE
   {

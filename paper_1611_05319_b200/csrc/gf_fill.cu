@@ -922,14 +922,19 @@ __device__ __forceinline__ bool decide_and_write(const FillArgs& A, int f, int j
   return fill;
 }
 
-__device__ __forceinline__ int neighbor_of(const FillArgs& A, uint32_t p, int o, bool& in) {
+// 8-neighbour o (grid.py:29-33 order) of pixel (pi, pj)
+__device__ __forceinline__ int neighbor_at(const FillArgs& A, int pi, int pj, int o, bool& in) {
   const int di = (o < 3) ? o - 1 : (o == 3 ? -1 : (o == 4 ? 1 : o - 6));
   const int dj = (o < 3) ? -1 : (o < 5 ? 0 : 1);
-  int ii = (int)p % A.W + di;
-  const int jj = (int)p / A.W + dj;
-  if (A.periodic) ii = pos_mod(ii, A.W);
+  int ii = pi + di;
+  const int jj = pj + dj;
+  if (A.periodic) ii = ii < 0 ? ii + A.W : (ii >= A.W ? ii - A.W : ii);
   in = ii >= 0 && ii < A.W && jj >= 0 && jj < A.H;
   return in ? jj * A.W + ii : 0;
+}
+
+__device__ __forceinline__ int neighbor_of(const FillArgs& A, uint32_t p, int o, bool& in) {
+  return neighbor_at(A, (int)p % A.W, (int)p / A.W, o, in);
 }
 
 // Claim Inpaint neighbour q for the next frontier: INACTIVE -> ACTIVE (the
@@ -954,7 +959,8 @@ __device__ __forceinline__ uint32_t claim(float4* fw, int q) {
 template <int LG>
 __device__ __forceinline__ void activate(const FillArgs& A, uint32_t* reg, int& n, bool staged,
                                          uint32_t* nxt_list, int nxt, float4* fw, int f, int k,
-                                         int gl, bool filled, uint32_t e, unsigned cand = 0xffu) {
+                                         int gl, bool filled, uint32_t e, unsigned cand, int pi,
+                                         int pj) {
   constexpr int NPL = 8 / LG;  // neighbours per lane
   const bool survive = gl == 0 && !filled;
   uint32_t qe[NPL];
@@ -965,7 +971,7 @@ __device__ __forceinline__ void activate(const FillArgs& A, uint32_t* reg, int& 
     // Readable, Bystander, filled or already in a frontier: no CAS needed)
     if (gl >= 0 && filled && ((cand >> (gl + LG * r)) & 1u)) {
       bool in;
-      const int q = neighbor_of(A, e & kEntryPix, gl + LG * r, in);
+      const int q = neighbor_at(A, pi, pj, gl + LG * r, in);
       if (in) {
         qe[r] = claim(fw, q);
         if (qe[r] != 0xffffffffu && A.enter) A.enter[(size_t)f * A.HW + q] = k + 1;
@@ -1137,6 +1143,7 @@ __global__ void __launch_bounds__(kShellThreads, GF_SHELL_MIN_BLOCKS)
     S.tab.ni[i] = tables.ni[i];
     S.tab.mi[i] = tables.mi[i];
     S.tab.kn[i] = tables.kn[i];
+    S.tab.off[i] = tables.ni[i] + tables.mi[i] * A.W;
   }
   pdl_wait();
   timeline_mark(A, 1, true);
@@ -1237,7 +1244,8 @@ __global__ void __launch_bounds__(kShellThreads, GF_SHELL_MIN_BLOCKS)
           GF_FINE(const unsigned long long fr3 = fine_after(filled ? 1u : 0u);)
           if (lane == 0 && filled) ++wfills;
           if (kTracked)
-            activate<8>(A, reg, wn, true, nxt_list, nxt, fw, f, k, lane < 8 ? lane : -1, filled, e);
+            activate<8>(A, reg, wn, true, nxt_list, nxt, fw, f, k, lane < 8 ? lane : -1, filled, e,
+                        0xffu, (int)p % A.W, (int)p / A.W);
           GF_FINE(if (lane == 0) fine_put(A, k, 7, fr2 - fr1); (void)fr0; (void)fr3;)
         } else {
           // ---- lattice round: items IPU q .. IPU q + IPU-1 of the concatenated
@@ -1262,6 +1270,7 @@ __global__ void __launch_bounds__(kShellThreads, GF_SHELL_MIN_BLOCKS)
           const int j = valid ? t - pf[fs] : 0;
           const uint32_t e = valid ? cur_list[(size_t)fs * A.cap + j] : 0u;
           const uint32_t p = e & kEntryPix;
+          const int pi = (int)p % A.W, pj = (int)p / A.W;
           GF_FINE(const unsigned long long fl1 = fine_after(e);)
           float4* fw = A.work + (size_t)fs * A.HW;
           WorkSource src{fw, A.c3 ? A.c3 + (size_t)fs * A.HW : nullptr, A.H, A.W, A.C, k};
@@ -1271,7 +1280,7 @@ __global__ void __launch_bounds__(kShellThreads, GF_SHELL_MIN_BLOCKS)
           SampleResult res;
           GF_FINE(const unsigned long long te0 = A.trace ? gtimer() : 0ULL;)
           if constexpr (R > 0) {
-            eval_lattice<R, LG>(P, S.tab, src, lglane, lsub, valid, (int)p % A.W, (int)p / A.W, res);
+            eval_lattice<R, LG>(P, S.tab, src, lglane, lsub, valid, pi, pj, res);
           } else {
             if (valid && (e & kEntryRot)) frame_guide(A, fs, (int)p, gx, gy);
             eval_item<NL, 0>(P, S.tab, src, glane, valid, (double)((int)p % A.W),
@@ -1285,7 +1294,7 @@ __global__ void __launch_bounds__(kShellThreads, GF_SHELL_MIN_BLOCKS)
           GF_FINE(const unsigned long long fl3 = fine_after(filled ? 1u : 0u);)
           if (kTracked)
             activate<LG>(A, reg, wn, uniform, nxt_list, nxt, fw, fs, k, valid ? lglane : -1, filled, e,
-                         R > 0 ? res.nb : 0xffu);
+                         R > 0 ? res.nb : 0xffu, pi, pj);
           GF_FINE(const unsigned long long fl4 = fine_after((unsigned)wn);
                   if (valid && lglane == 0) {
                     fine_put(A, k, 0, fl1 - fl0); fine_put(A, k, 1, fl2 - fl1);

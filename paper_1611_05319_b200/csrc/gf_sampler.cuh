@@ -58,6 +58,7 @@ struct BallTables {
   int ni[kMaxK];  // the same offsets as integers (lattice path)
   int mi[kMaxK];
   signed char kn[kMaxK];  // sample k is 8-neighbour kn[k] of the centre, or -1
+  int off[kMaxK];         // n + m * W (shell kernel's shared copy only): flat offsets
 };
 
 struct SampleResult {
