@@ -122,30 +122,33 @@ __device__ __forceinline__ void eval_lattice(const BallParams& P, const BallTabl
       if ((tb >> (k % LG)) & 1u) acc = acc + T.w0[k];
     }
   }
-  double num[4] = {0.0, 0.0, 0.0, 0.0};
+  // colour numerators: off the decision path (values only need 1e-4 and are
+  // stored fp32), so they accumulate in fp32 with explicit FMAs -- the fp64
+  // masses above keep numpy's exact bits
+  float num[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
   for (int t = 0; t < KPL; ++t)
     if ((okm >> t) & 1u) {
-      const double w = T.w0[glane + LG * t];
-      num[0] += w * (double)v[t].x;
-      num[1] += w * (double)v[t].y;
-      num[2] += w * (double)v[t].z;
+      const float w = (float)T.w0[glane + LG * t];
+      num[0] = __fmaf_rn(w, v[t].x, num[0]);
+      num[1] = __fmaf_rn(w, v[t].y, num[1]);
+      num[2] = __fmaf_rn(w, v[t].z, num[2]);
     }
   if (src.c3) {
 #pragma unroll
     for (int t = 0; t < KPL; ++t)
-      if ((okm >> t) & 1u) num[3] += T.w0[glane + LG * t] * (double)src.c3[q[t]];
+      if ((okm >> t) & 1u) num[3] = __fmaf_rn((float)T.w0[glane + LG * t], src.c3[q[t]], num[3]);
   }
   const double inv = (acc != 0.0) ? 1.0 / acc : 0.0;
 #pragma unroll
   for (int c = 0; c < 4; ++c) {
-    double s = 0.0;
+    float s = 0.f;
     if (c < 3 || src.c3) {
       s = num[c];
 #pragma unroll
       for (int o = 1; o < LG; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o, LG);
     }
-    out.v[c] = s * inv;
+    out.v[c] = (double)s * inv;
   }
   out.rw = acc;
   out.tw = P.tw0;
