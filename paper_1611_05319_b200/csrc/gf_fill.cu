@@ -78,7 +78,7 @@ __device__ __forceinline__ int* stamp_ptr(float4* work, int q) {
 // ---------------------------------------------------------------- prep
 //
 // One pass over every pixel in 32x32 tiles, frame-major grid
-// (blockIdx.y = frame).  Labels of the tile plus an (r+1)-pixel halo are
+// (blockIdx.z = frame).  Labels of the tile plus an (r+1)-pixel halo are
 // staged in shared memory; from them the block derives
 //   * which pixels can ever be read by the shell loop -- those within
 //     Chebyshev distance r+1 of an Inpaint pixel (a ball sample lies within
@@ -103,7 +103,7 @@ __device__ __forceinline__ unsigned long long gtimer0() {
 // pipeline timeline in the last trace row: slots 2i = ~start (max of ~t =
 // earliest start), 2i+1 = latest end; i = 0 prep, 1 shell loop, 2 finalize
 __device__ __forceinline__ void timeline_mark(const FillArgs& A, int stage, bool start) {
-  if (!A.trace || A.trace_cap < 2 || threadIdx.x != 0) return;
+  if (threadIdx.x != 0 || !A.trace || A.trace_cap < 2) return;
   unsigned long long* row = A.trace + (size_t)(A.trace_cap - 1) * 8;
   const unsigned long long t = gtimer0();
   atomicMax(&row[2 * stage + (start ? 0 : 1)], start ? ~t : t);
@@ -132,7 +132,7 @@ __device__ __forceinline__ double seg_dist(double px, double py, const double4 s
   return hypot_np(px - (ax + t * abx), py - (ay + t * aby));
 }
 
-// One pass over every pixel in 32x32 tiles, frame-major grid (blockIdx.y =
+// One pass over every pixel in 32x32 tiles, frame-major grid (blockIdx.z =
 // frame).  Every tile copies its pixels to the output (Readable pixels are
 // final: the closing hull clip, engine.py:372-375, is the identity on them;
 // fills and the Bystander clip overwrite the others later) and reduces the
@@ -143,9 +143,11 @@ template <typename T, int C>
 #define GF_PREP_MIN_BLOCKS 4
 #endif
 __global__ void __launch_bounds__(kThreads, GF_PREP_MIN_BLOCKS) k_prep(const __grid_constant__ FillArgs A) {
-  const int f = blockIdx.y;
-  const int tiles_x = (A.W + kTile - 1) / kTile;
-  const int tix = (int)(blockIdx.x % tiles_x), tiy = (int)(blockIdx.x / tiles_x);
+  // grid (tile column, tile row, frame): no division for the tile index
+  const int f = blockIdx.z;
+  const int tiles_x = gridDim.x;
+  const int tix = blockIdx.x, tiy = blockIdx.y;
+  const int tile = tiy * tiles_x + tix;
   const int tx0 = tix * kTile;
   const int ty0 = tiy * kTile;
   timeline_mark(A, 0, true);
@@ -321,13 +323,19 @@ __global__ void __launch_bounds__(kThreads, GF_PREP_MIN_BLOCKS) k_prep(const __g
     unsigned long long ered[4];  // max(~enc) <=> min(enc)
     if constexpr (sizeof(T) == 4) {
       // fp32 values: order-preserving 32-bit codes, one redux per quantity
+      unsigned m[4];
 #pragma unroll
       for (int b = 0; b < 2; ++b) {
         const bool any = vlo[b] <= vhi[b];
-        const unsigned mlo = __reduce_max_sync(0xffffffffu, any ? ~enc32((float)vlo[b]) : 0u);
-        const unsigned mhi = __reduce_max_sync(0xffffffffu, any ? enc32((float)vhi[b]) : 0u);
-        ered[2 * b] = mlo ? ~enc_ordered((double)dec32(~mlo)) : 0ULL;
-        ered[2 * b + 1] = mhi ? enc_ordered((double)dec32(mhi)) : 0ULL;
+        m[2 * b] = __reduce_max_sync(0xffffffffu, any ? ~enc32((float)vlo[b]) : 0u);
+        m[2 * b + 1] = __reduce_max_sync(0xffffffffu, any ? enc32((float)vhi[b]) : 0u);
+      }
+      if (lane == 0) {  // the fp64 codes, once per warp
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+          ered[2 * b] = m[2 * b] ? ~enc_ordered((double)dec32(~m[2 * b])) : 0ULL;
+          ered[2 * b + 1] = m[2 * b + 1] ? enc_ordered((double)dec32(m[2 * b + 1])) : 0ULL;
+        }
       }
     } else {
 #pragma unroll
@@ -361,7 +369,7 @@ __global__ void __launch_bounds__(kThreads, GF_PREP_MIN_BLOCKS) k_prep(const __g
       // shell loop's clip, and the frame's
       unsigned long long* fr = i < 2 ? &A.hull[2 * f + i] : &A.bys_frame[2 * f + i - 2];
       if (e != 0ULL && e > *(volatile unsigned long long*)fr) atomicMax(fr, e);
-      if (i >= 2) A.bys[((size_t)f * A.ntiles + blockIdx.x) * 2 + i - 2] = e;
+      if (i >= 2) A.bys[((size_t)f * A.ntiles + tile) * 2 + i - 2] = e;
     }
   }
   if (!tile_d) {
@@ -1740,7 +1748,8 @@ int fill_launch(const gf_frames* fr, const gf_fill_params* prm, const gf_fill_ou
   if (cudaMemsetAsync(base + L.ints, 0, L.u64 + (size_t)nF * 6 * sizeof(unsigned long long) - L.ints,
                       stream) != cudaSuccess)
     return set_error(GF_E_CUDA, "memset failed");
-  launch_prep(fr->dtype == GF_F64, C, dim3(tiles_of(H, W), nF), stream, A);
+  launch_prep(fr->dtype == GF_F64, C, dim3((W + kTile - 1) / kTile, (H + kTile - 1) / kTile, nF), stream,
+              A);
   if (cudaPeekAtLastError() != cudaSuccess)
     return set_error(GF_E_CUDA, cudaGetErrorString(cudaGetLastError()));
 
