@@ -197,10 +197,13 @@ __global__ void __launch_bounds__(kThreads, GF_PREP_MIN_BLOCKS) k_prep(const __g
         unsigned w[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) w[i] = i < nw ? __ldg(row + i) : 0x80808080u;
+        // for the label values 0 / 128 / 255: Inpaint <=> bit 0 set, Readable
+        // <=> bit 7 clear (any other value flags the frame as invalid above
+        // and its result is discarded)
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-          im |= (unsigned long long)nib4(__vcmpeq4(w[i], 0xffffffffu)) << (4 * i);
-          rm |= (unsigned long long)nib4(__vcmpeq4(w[i], 0u)) << (4 * i);
+          im |= (unsigned long long)nib4(w[i]) << (4 * i);
+          rm |= (unsigned long long)nib4(~w[i] >> 7) << (4 * i);
         }
         im = (im >> sh) & ext_mask;
         rm = (rm >> sh) & ext_mask;
