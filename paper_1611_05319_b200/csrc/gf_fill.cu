@@ -187,27 +187,35 @@ __global__ void __launch_bounds__(kThreads, GF_PREP_MIN_BLOCKS) k_prep(const __g
   const int nw = (ext + sh + 3) >> 2;  // words per row (<= 16)
   const unsigned long long ext_mask = ext >= 64 ? ~0ULL : ((1ULL << ext) - 1);
   if ((A.W & 3) == 0 && ws >= 0 && ws + 4 * nw <= A.W) {
-    // one thread per ext row: up to 16 aligned words, all loads in flight
-    const int y = threadIdx.x;
+    // four threads per ext row (all warps busy), four aligned words each,
+    // combined with two xor shuffles
+    const int y = threadIdx.x >> 2, part = threadIdx.x & 3;
     const int gyy = ty0 - R + y;
-    if (y < ext) {
-      unsigned long long im = 0ULL, rm = 0ULL;
-      if (gyy >= 0 && gyy < A.H) {
-        const unsigned* row = reinterpret_cast<const unsigned*>(lab + (size_t)gyy * A.W + ws);
-        unsigned w[16];
+    unsigned long long im = 0ULL, rm = 0ULL;
+    if (y < ext && gyy >= 0 && gyy < A.H) {
+      const unsigned* row = reinterpret_cast<const unsigned*>(lab + (size_t)gyy * A.W + ws);
+      unsigned w[4];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) w[i] = i < nw ? __ldg(row + i) : 0x80808080u;
-        // for the label values 0 / 128 / 255: Inpaint <=> bit 0 set, Readable
-        // <=> bit 7 clear (any other value flags the frame as invalid above
-        // and its result is discarded)
+      for (int i = 0; i < 4; ++i) w[i] = 4 * part + i < nw ? __ldg(row + 4 * part + i) : 0x80808080u;
+      // for the label values 0 / 128 / 255: Inpaint <=> bit 0 set, Readable
+      // <=> bit 7 clear (any other value flags the frame as invalid above and
+      // its result is discarded)
+      unsigned ib = 0, rb = 0;
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          im |= (unsigned long long)nib4(w[i]) << (4 * i);
-          rm |= (unsigned long long)nib4(~w[i] >> 7) << (4 * i);
-        }
-        im = (im >> sh) & ext_mask;
-        rm = (rm >> sh) & ext_mask;
+      for (int i = 0; i < 4; ++i) {
+        ib |= nib4(w[i]) << (4 * i);
+        rb |= nib4(~w[i] >> 7) << (4 * i);
       }
+      im = (unsigned long long)ib << (16 * part);
+      rm = (unsigned long long)rb << (16 * part);
+    }
+    im |= __shfl_xor_sync(0xffffffffu, im, 1);
+    rm |= __shfl_xor_sync(0xffffffffu, rm, 1);
+    im |= __shfl_xor_sync(0xffffffffu, im, 2);
+    rm |= __shfl_xor_sync(0xffffffffu, rm, 2);
+    if (part == 0 && y < ext) {
+      im = (im >> sh) & ext_mask;
+      rm = (rm >> sh) & ext_mask;
       s_hrow64[y] = im;
       s_rrow64[y] = rm;
       any_inp = im != 0ULL;
