@@ -65,6 +65,19 @@ __device__ __forceinline__ unsigned enc32(float x) {
 __device__ __forceinline__ float dec32(unsigned e) {
   return __uint_as_float((e >> 31) ? (e & 0x7fffffffu) : ~e);
 }
+// horizontal dilation of a halo row's Inpaint mask: bit c <=> an Inpaint
+// pixel in ext columns [c, c + 2R]
+__device__ __forceinline__ unsigned int hdilate(unsigned long long m, int R) {
+  unsigned long long h = m;
+  int w = 1;  // h covers a window of w columns
+  while (2 * w <= 2 * R + 1) {
+    h |= h >> w;
+    w *= 2;
+  }
+  if (w < 2 * R + 1) h |= h >> (2 * R + 1 - w);
+  return (unsigned int)h;
+}
+
 // 4 byte-wise test results (0xff / 0x00 per byte) -> 4 bits, byte i -> bit i
 __device__ __forceinline__ unsigned nib4(unsigned m) { return ((m & 0x01010101u) * 0x01020408u) >> 24; }
 
@@ -218,6 +231,7 @@ __global__ void __launch_bounds__(kThreads, GF_PREP_MIN_BLOCKS) k_prep(const __g
       rm = (rm >> sh) & ext_mask;
       s_hrow64[y] = im;
       s_rrow64[y] = rm;
+      s_hrow[y] = hdilate(im, R);
       any_inp = im != 0ULL;
     }
   } else {
@@ -248,6 +262,7 @@ __global__ void __launch_bounds__(kThreads, GF_PREP_MIN_BLOCKS) k_prep(const __g
       if (lane == 0 && y < ext) {
         s_hrow64[y] = ((unsigned long long)hi << 32) | lo;
         s_rrow64[y] = ((unsigned long long)rhi << 32) | rlo;
+        s_hrow[y] = hdilate(((unsigned long long)hi << 32) | lo, R);
       }
     }
   }
@@ -409,22 +424,8 @@ __global__ void __launch_bounds__(kThreads, GF_PREP_MIN_BLOCKS) k_prep(const __g
       }
     }
   }
-  // 2. horizontal dilation of the Inpaint indicator: bit c of s_hrow[y] <=>
-  //    an Inpaint pixel in ext columns [c, c + 2R]
-  {
-    for (int y = threadIdx.x; y < ext; y += kThreads) {
-      const unsigned long long m = s_hrow64[y];
-      unsigned long long h = m;
-      int w = 1;  // h covers a window of w columns
-      while (2 * w <= 2 * R + 1) {
-        h |= h >> w;
-        w *= 2;
-      }
-      if (w < 2 * R + 1) h |= h >> (2 * R + 1 - w);
-      s_hrow[y] = (unsigned int)h;
-    }
-  }
-  __syncthreads();
+  // 2. dilation of the Inpaint indicator (the rows were dilated horizontally
+  //    when they were built; visible since the label barrier)
   // ... and vertical: bit c of s_vrow[y] <=> an Inpaint pixel within
   // Chebyshev distance R of tile pixel (c, y)
   if (threadIdx.x < kTile) {
