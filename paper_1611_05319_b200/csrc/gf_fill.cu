@@ -526,9 +526,10 @@ __global__ void __launch_bounds__(kThreads, GF_PREP_MIN_BLOCKS) k_prep(const __g
     // initial frontier entry of this pixel (published per block below)
     ent[u] = active ? ((uint32_t)p | (rot ? kEntryRot : 0u)) : 0xffffffffu;
   }
-  // block-aggregated append of the initial frontier: lattice entries to the
-  // front of the list, rotated-ball entries to the back (when split); one
-  // atomic per part per block
+  // block-aggregated append of the initial frontier (lattice entries to the
+  // front of the list, rotated-ball entries to the back when split), |D| and
+  // the data-term flag: one barrier gathers the warps' counts, one atomic per
+  // quantity per block, one barrier hands out the list bases
   {
     const unsigned lt = (1u << lane) - 1;
     int wL = 0, wR = 0;
@@ -539,22 +540,33 @@ __global__ void __launch_bounds__(kThreads, GF_PREP_MIN_BLOCKS) k_prep(const __g
       wL += __popc(__ballot_sync(0xffffffffu, act && !back));
       wR += __popc(__ballot_sync(0xffffffffu, back));
     }
+    const int w_inp = __reduce_add_sync(0xffffffffu, (unsigned)n_inp);
+    const bool w_ag = __any_sync(0xffffffffu, anyg);
     if (lane == 0) {
       s_wl[warp] = wL;
       s_wr[warp] = wR;
+      s_cnt[warp] = w_inp | (w_ag ? (1 << 30) : 0);
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-      int tL = 0, tR = 0;
+      int tL = 0, tR = 0, tot = 0;
+      bool ag = false;
       for (int w = 0; w < kThreads / 32; ++w) {
         const int a = s_wl[w], b = s_wr[w];
         s_wl[w] = tL;
         s_wr[w] = tR;
         tL += a;
         tR += b;
+        tot += s_cnt[w] & ((1 << 30) - 1);
+        ag |= (s_cnt[w] >> 30) != 0;
       }
       s_bL = tL > 0 ? atomicAdd(&A.cnt[f], tL) : 0;
       s_bR = tR > 0 ? atomicAdd(&A.cntR[f], tR) : 0;
+      if (tot) {
+        atomicAdd(&A.remaining[f], tot);
+        atomicAdd(&A.inpaint[f], tot);
+      }
+      if (ag) A.anyg[f] = 1;
     }
     __syncthreads();
     int bL = s_bL + s_wl[warp], bR = s_bR + s_wr[warp];
@@ -569,20 +581,6 @@ __global__ void __launch_bounds__(kThreads, GF_PREP_MIN_BLOCKS) k_prep(const __g
       bL += __popc(mL);
       bR += __popc(mR);
     }
-  }
-  // block reductions: |D| and the data-term flag -> one atomic each per block
-  for (int o = 16; o > 0; o >>= 1) n_inp += __shfl_xor_sync(0xffffffffu, n_inp, o);
-  const bool blk_anyg = __syncthreads_or(anyg);
-  if (lane == 0) s_cnt[warp] = n_inp;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int tot = 0;
-    for (int w = 0; w < kThreads / 32; ++w) tot += s_cnt[w];
-    if (tot) {
-      atomicAdd(&A.remaining[f], tot);
-      atomicAdd(&A.inpaint[f], tot);
-    }
-    if (blk_anyg) A.anyg[f] = 1;
   }
   timeline_mark(A, 0, false);
 }
