@@ -233,3 +233,50 @@ def test_concurrent_host_threads():
         got = list(ex.map(job, [0, 1, 2, 3, 0, 1, 2, 3]))
     for i, u in enumerate(got):
         assert np.array_equal(u, want[i % 4])
+
+
+def test_c_abi_argument_errors():
+    """The C ABI's status codes and messages (include/guidefill_b200.h:29-33)."""
+    import ctypes
+
+    lib = N.load()
+    dev = torch.device("cuda")
+    H, W = 40, 64
+    img = torch.rand(1, H, W, 3, device=dev)
+    lab = torch.zeros(1, H, W, dtype=torch.uint8, device=dev)
+    lab[0, 10:20, 10:30] = 255
+    out = torch.empty_like(img)
+    stats = torch.zeros(1, N.GF_STATS, dtype=torch.int32, device=dev)
+    rows = torch.zeros(1, 64, 2, dtype=torch.int32, device=dev)
+    fr = N.FramesC(1, H, W, 3, N.GF_F32, img.data_ptr(), lab.data_ptr(), 0, out.data_ptr())
+    from paper_1611_05319_b200._device import params_to_c
+
+    pc = params_to_c(FillParams(r=3), True, N.GF_G_ZERO)
+    oc = N.FillOutputsC(stats.data_ptr(), rows.data_ptr(), 64, 0, 0, 0, 0)
+    need = lib.gf_fill_workspace_bytes(ctypes.byref(fr), ctypes.byref(pc))
+    ws = torch.empty(need, dtype=torch.uint8, device=dev)
+    stream = N.stream_ptr()
+    # too small a workspace
+    rc = lib.gf_fill(ctypes.byref(fr), ctypes.byref(pc), ctypes.byref(oc),
+                     ctypes.c_void_p(ws.data_ptr()), need - 1, stream)
+    assert rc == -3 and b"workspace" in lib.gf_last_error()
+    # NULL outputs
+    rc = lib.gf_fill(ctypes.byref(fr), ctypes.byref(pc), None, ctypes.c_void_p(ws.data_ptr()),
+                     need, stream)
+    assert rc == -1 and b"NULL" in lib.gf_last_error()
+    # a ball beyond GF_MAX_RADIUS
+    big = params_to_c(FillParams(r=3), True, N.GF_G_ZERO)
+    big.r = 13
+    rc = lib.gf_fill(ctypes.byref(fr), ctypes.byref(big), ctypes.byref(oc),
+                     ctypes.c_void_p(ws.data_ptr()), need, stream)
+    assert rc == -4
+    # zero frames: nothing to do
+    fr0 = N.FramesC(0, H, W, 3, N.GF_F32, img.data_ptr(), lab.data_ptr(), 0, out.data_ptr())
+    assert lib.gf_fill(ctypes.byref(fr0), ctypes.byref(pc), ctypes.byref(oc),
+                       ctypes.c_void_p(ws.data_ptr()), need, stream) == 0
+    # and the valid call
+    rc = lib.gf_fill(ctypes.byref(fr), ctypes.byref(pc), ctypes.byref(oc),
+                     ctypes.c_void_p(ws.data_ptr()), need, stream)
+    assert rc == 0
+    torch.cuda.synchronize()
+    assert int(stats[0, N.STAT_FILLED]) == 200 and int(stats[0, N.STAT_REMAINING]) == 0
