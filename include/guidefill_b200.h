@@ -208,6 +208,34 @@ int gf_boundary_masks(int32_t height, int32_t width, const uint8_t* labels,
                       int32_t periodic_x, uint8_t* active, uint8_t* inner,
                       uint8_t* outer, void* stream);
 
+/*
+ * Output delta for host-side results.  A fill returns every Readable pixel
+ * bit for bit as it came in (engine.py:364-376 only writes u[filled] and
+ * clips to the Readable hull), so a host caller can DMA the INPUT into its
+ * pinned result buffer while the frame uploads and then call this after the
+ * fill: every pixel whose output differs bitwise from the input is written
+ * into host_out (pinned, mapped: cudaHostAlloc / cudaHostRegister memory).
+ * input/output: device [n_px][channels] of dtype GF_F32/GF_F64.
+ * n_changed (device, nullable) is incremented by the pixels written.
+ * Stream-ordered: host_out must already hold the input copy on `stream`.
+ * No reference counterpart (the reference returns a fresh numpy array,
+ * engine.py:289,376); it is the transfer half of the drop-in fill.
+ */
+int gf_output_delta(int64_t n_px, int32_t channels, int32_t dtype, const void* input,
+                    const void* output, void* host_out, unsigned long long* n_changed,
+                    void* stream);
+
+/*
+ * The upload half of the same path: copies nbytes host_src -> dev_dst on
+ * `stream` in `chunk`-byte pieces and, as each piece lands, copies it back
+ * dev_dst -> host_mirror on `side_stream` (the link's two directions run
+ * concurrently).  host_src and host_mirror must be pinned for the copies to
+ * be asynchronous.  The caller joins side_stream into its stream before
+ * gf_output_delta.
+ */
+int gf_upload_mirrored(const void* host_src, void* dev_dst, void* host_mirror, int64_t nbytes,
+                       int64_t chunk, void* stream, void* side_stream);
+
 /* Thread-local message for the last failing call on this thread. */
 const char* gf_last_error(void);
 int gf_abi_version(void);

@@ -14,6 +14,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("GF_B200_LIB", os.path.join(_HERE, "libgf_b200.so"))
 
 GF_OK = 0
+GF_E_INVALID, GF_E_CUDA, GF_E_WORKSPACE, GF_E_UNSUPPORTED = -1, -2, -3, -4
 GF_F32, GF_F64 = 0, 1
 GF_ORDER = {"onion": 0, "smart": 1, "smart_with_data_term": 2}
 GF_BALL = {"rotated_ball": 0, "axis_ball": 1}
@@ -27,8 +28,8 @@ STAT_BAD_LABELS = 8
 EXPORTS = (
     "gf_fill_workspace_bytes", "gf_fill_splines_workspace_bytes", "gf_fill", "gf_fill_splines",
     "gf_guide_field", "gf_sample_points",
-    "gf_bilinear_gather", "gf_boundary_masks", "gf_last_error", "gf_abi_version",
-    "gf_host_exp", "gf_host_hypot", "gf_host_pairwise_sum",
+    "gf_bilinear_gather", "gf_boundary_masks", "gf_output_delta", "gf_upload_mirrored", "gf_last_error",
+    "gf_abi_version", "gf_host_exp", "gf_host_hypot", "gf_host_pairwise_sum",
 )
 
 
@@ -129,6 +130,10 @@ def load(required: bool = True):
                                        ctypes.c_int32, P, P, ctypes.c_int32, P, P, P]
     lib.gf_boundary_masks.restype = ctypes.c_int
     lib.gf_boundary_masks.argtypes = [ctypes.c_int32, ctypes.c_int32, P, ctypes.c_int32, P, P, P, P]
+    lib.gf_output_delta.restype = ctypes.c_int
+    lib.gf_output_delta.argtypes = [ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, P, P, P, P, P]
+    lib.gf_upload_mirrored.restype = ctypes.c_int
+    lib.gf_upload_mirrored.argtypes = [P, P, P, ctypes.c_int64, ctypes.c_int64, P, P]
     lib.gf_last_error.restype = ctypes.c_char_p
     lib.gf_abi_version.restype = ctypes.c_int
     lib.gf_host_exp.argtypes = [P, P, ctypes.c_int64]

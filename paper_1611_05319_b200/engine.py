@@ -220,19 +220,33 @@ def _run_fill(image, labels, guide_vecs, params: FillParams, tracked: bool, orde
     segs = None
     if splines is not None and params.g_source == "guide_field":
         segs = SegmentSet.cached(list(splines), dev) if len(splines) else None
+    mirror = None
     if as_tensor:
         timg = image.to(torch.float64).contiguous()
         C = timg.shape[2]
-        d_img = (timg if timg.is_cuda else timg.to(dev, non_blocking=timg.is_pinned())).reshape(1, H, W, C)
+        if (not timg.is_cuda and timg.is_pinned() and timg.numel() * 8 >= (1 << 20)
+                and _staging.mirror_supported(dev)):
+            d_img, mirror = _staging.upload_mirrored(timg, dev, True)
+            d_img = d_img.reshape(1, H, W, C)
+        else:
+            d_img = (timg if timg.is_cuda else timg.to(dev, non_blocking=timg.is_pinned())).reshape(1, H, W, C)
     else:
         img = np.ascontiguousarray(image, dtype=np.float64)
         C = img.shape[2]
-        d_img = _staging.upload(img, dev, "img").reshape(1, H, W, C)
+        if img.nbytes >= (1 << 20) and _staging.mirror_supported(dev):
+            d_img, mirror = _staging.upload_mirrored(img, dev, False)
+            d_img = d_img.reshape(1, H, W, C)
+        else:
+            d_img = _staging.upload(img, dev, "img").reshape(1, H, W, C)
     if guide_vecs is not None and params.g_source == "guide_field" and segs is None:
         d_guide = _staging.upload(np.ascontiguousarray(guide_vecs, dtype=np.float64), dev,
                                   "guide").reshape(1, H, W, 2)
     res = fill_device(d_img, d_lab, d_guide, params, tracked=tracked, order_log=order_log,
                       rows_cap=H * W + 1, splines=segs, eta=eta, want_fillshell=True)
+    if mirror is not None:
+        # result = the mirrored input + the changed pixels (the read-back of
+        # the report below synchronises the stream)
+        mirror.finish(d_img, res["out"])
     stats, rows_dev = _staging.read_report(res["stats"][0], res["rows"][0])
     if validate and stats[N.STAT_BAD_LABELS]:
         grid.validate_labels(labels)  # k_prep saw a bad label: the reference's message
@@ -240,7 +254,13 @@ def _run_fill(image, labels, guide_vecs, params: FillParams, tracked: bool, orde
     iters = int(stats[N.STAT_ITERATIONS])
     if iters + 1 > rows_dev.shape[0]:
         rows_dev = res["rows"][0, :iters + 1].cpu().numpy()
-    if as_tensor:
+    if mirror is not None:
+        if as_tensor:
+            u_t = mirror.result
+            u = u_t.numpy()
+        else:
+            u = mirror.result
+    elif as_tensor:
         u_t = _staging.download_tensor(res["out"][0])
         u = u_t.numpy()  # shares memory: the unfillable fallback paints in place
     else:

@@ -280,3 +280,113 @@ def test_c_abi_argument_errors():
     assert rc == 0
     torch.cuda.synchronize()
     assert int(stats[0, N.STAT_FILLED]) == 200 and int(stats[0, N.STAT_REMAINING]) == 0
+
+
+def _force_mirror(on: bool):
+    from paper_1611_05319_b200 import _staging
+
+    key = str(torch.device("cuda", torch.cuda.current_device()))
+    prev = _staging._mirror_ok.get(key)
+    if on:
+        _staging._mirror_ok.pop(key, None)
+        assert _staging.mirror_supported(torch.device("cuda", torch.cuda.current_device()))
+    else:
+        _staging._mirror_ok[key] = False
+    return key, prev
+
+
+@pytest.mark.parametrize("dtype,C", [(torch.float64, 3), (torch.float32, 1), (torch.float32, 4),
+                                     (torch.float64, 2)])
+def test_output_delta_kernel(dtype, C):
+    """gf_output_delta writes exactly the bitwise-changed pixels (incl. -0.0
+    vs 0.0 and NaN payloads) into a mapped pinned buffer holding the input."""
+    import ctypes
+
+    gen = torch.Generator().manual_seed(C)
+    n_px = 300_001
+    a = torch.rand((n_px, C), generator=gen, dtype=torch.float64).to(dtype)
+    b = a.clone()
+    idx = torch.randperm(n_px, generator=gen)[:5000]
+    b[idx, 0] = torch.rand(5000, generator=gen, dtype=torch.float64).to(dtype)
+    b[7, C - 1] = float("nan")
+    a[11, 0] = 0.0
+    b[11, 0] = -0.0
+    host = a.clone().pin_memory()
+    cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+    da, db = a.cuda(), b.cuda()
+    lib = N.load()
+    rc = lib.gf_output_delta(n_px, C, N.GF_F64 if dtype == torch.float64 else N.GF_F32,
+                             ctypes.c_void_p(da.data_ptr()), ctypes.c_void_p(db.data_ptr()),
+                             ctypes.c_void_p(host.data_ptr()), ctypes.c_void_p(cnt.data_ptr()),
+                             N.stream_ptr())
+    assert rc == N.GF_OK
+    torch.cuda.synchronize()
+    iv = torch.int64 if dtype == torch.float64 else torch.int32
+    assert torch.equal(host.view(iv), b.view(iv))
+    changed = int((a.view(iv) != b.view(iv)).any(dim=1).sum())
+    assert int(cnt.item()) == changed
+    # pageable memory is refused (not device-mapped), nothing is launched
+    page = a.clone()
+    rc = lib.gf_output_delta(n_px, C, N.GF_F64 if dtype == torch.float64 else N.GF_F32,
+                             ctypes.c_void_p(da.data_ptr()), ctypes.c_void_p(db.data_ptr()),
+                             ctypes.c_void_p(page.data_ptr()), None, N.stream_ptr())
+    assert rc == N.GF_E_INVALID
+
+
+@pytest.mark.parametrize("scene", ["C2", "clip"])
+def test_mirrored_result_path_equals_full_download(scene):
+    """The mirrored host result (input DMA'd back during the upload + changed
+    pixels after the fill) equals the full-download result and the oracle,
+    for numpy and pinned-tensor callers, including the Bystander clip."""
+    from paper_1611_05319_b200 import _staging, tracker
+
+    if scene == "C2":
+        sc = scenes.config("C2")
+        img, lab, guide = sc.image, sc.labels, _splines(sc)
+        p = FillParams(**sc.params)
+        field = build_guide_field(guide, lab)
+    else:
+        img, lab = _clip_scene(7, H=400, W=520)
+        guide, field = None, None
+        p = FillParams(r=3, mu=50.0, order="smart", neighborhood="rotated_ball")
+    assert img.nbytes >= (1 << 20)
+    ref = orc.fill(img, lab, field, orc.Params.of(p), tracked=True)
+    key, prev = _force_mirror(False)
+    try:
+        u_full, m_full = tracker.run_tracked(img, lab, guide, p)
+    finally:
+        _staging._mirror_ok.pop(key, None)
+    _force_mirror(True)
+    u_np, m_np = tracker.run_tracked(img, lab, guide, p)
+    u_t, m_t = tracker.run_tracked(torch.from_numpy(img).pin_memory(),
+                                   torch.from_numpy(lab).pin_memory(), guide, p)
+    assert np.array_equal(u_np, u_full)
+    assert np.array_equal(u_t.numpy(), u_full)
+    assert m_np.rows == m_full.rows == m_t.rows
+    assert float(np.abs(u_np - ref["u"]).max()) <= 1e-4
+    assert np.array_equal(u_np[lab == 0], img[lab == 0])
+    if scene == "clip":
+        assert np.array_equal(u_np[lab == 128], ref["u"][lab == 128])
+
+
+def test_mirrored_path_concurrent_threads():
+    """Several host threads on the mirrored path (per-thread side streams and
+    result buffers) give the serial results."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from paper_1611_05319_b200 import tracker
+
+    cases = [scenes.small_scene(270, 480, band=8, gx=5, gy=3, n_spl=4, seed=40 + s)
+             for s in range(3)]
+    assert cases[0].image.nbytes >= (1 << 20)
+    want = [tracker.run_tracked(sc.image, sc.labels, _splines(sc), FillParams(**sc.params))[0]
+            for sc in cases]
+
+    def job(i):
+        sc = cases[i]
+        return tracker.run_tracked(sc.image, sc.labels, _splines(sc), FillParams(**sc.params))[0]
+
+    with ThreadPoolExecutor(3) as ex:
+        got = list(ex.map(job, [0, 1, 2, 0, 1, 2]))
+    for i, u in enumerate(got):
+        assert np.array_equal(u, want[i % 3])
