@@ -59,6 +59,13 @@ def upload(arr: np.ndarray, device, slot: str = "up"):
         return dst
     if n < (1 << 20):
         return torch.from_numpy(a).to(device)
+    ta = torch.from_numpy(a.reshape(-1).view(np.uint8))
+    if ta.is_pinned():
+        # already in page-locked memory (e.g. an array this package returned):
+        # one DMA, no staging copy
+        # (stream-ordered; every public entry synchronises before it returns)
+        dst.view(-1).view(torch.uint8).copy_(ta, non_blocking=True)
+        return dst
     stage = _staging(n, slot)
     src = a.reshape(-1).view(np.uint8)
     host = stage.numpy()
@@ -296,6 +303,10 @@ def upload_mirrored(src, device, as_tensor: bool):
     n = a.nbytes
     dst = torch.empty(a.shape, dtype=torch.from_numpy(a[:0].reshape(-1)).dtype, device=device)
     mir = Mirror(device, a.shape, dst.dtype, False)
+    if torch.from_numpy(a.reshape(-1).view(np.uint8)).is_pinned():
+        # page-locked numpy memory (e.g. a result of this package): DMA directly
+        mir.upload(a.ctypes.data, dst.data_ptr(), 0, n)
+        return dst, mir
     stage = _staging(n, "img")
     srcb = a.reshape(-1).view(np.uint8)
     host = stage.numpy()

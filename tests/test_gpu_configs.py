@@ -390,3 +390,22 @@ def test_mirrored_path_concurrent_threads():
         got = list(ex.map(job, [0, 1, 2, 0, 1, 2]))
     for i, u in enumerate(got):
         assert np.array_equal(u, want[i % 3])
+
+
+def test_page_locked_numpy_inputs_take_the_direct_dma():
+    """numpy arrays living in page-locked memory (a field returned by
+    build_guide_field, a view of a pinned tensor) are DMA'd without the
+    staging copy and give the same result as pageable arrays."""
+    from paper_1611_05319_b200 import tracker
+
+    sc = scenes.config("C2")
+    spl = _splines(sc)
+    p = FillParams(**sc.params)
+    field = build_guide_field(spl, sc.labels)
+    assert torch.from_numpy(field.reshape(-1).view(np.uint8)).is_pinned()
+    img_locked = torch.from_numpy(sc.image).pin_memory().numpy()
+    u_ref, m_ref = tracker.run_tracked(sc.image, sc.labels, field.copy(), p)
+    u, m = tracker.run_tracked(img_locked, sc.labels, field, p)
+    assert np.array_equal(u, u_ref) and m.rows == m_ref.rows
+    u2, _ = tracker.run_tracked(sc.image, sc.labels, spl, p)
+    assert np.array_equal(u2, u_ref)

@@ -13,7 +13,7 @@ def tm(name, fn, n=20):
     torch.cuda.synchronize(); t0 = time.perf_counter()
     for _ in range(n): fn()
     torch.cuda.synchronize(); print(f"{name:40s} {(time.perf_counter()-t0)/n*1e3:8.3f} ms", flush=True)
-for chunk in (8 << 20, 12 << 20, 16 << 20, 26 << 20):
+for chunk in (8 << 20,):
     _staging._MIRROR_CHUNK = chunk
     _staging._mirror_ok.pop(key, None)
     print("mirror supported:", _staging.mirror_supported(torch.device("cuda", 0)), "chunk MB", chunk >> 20)
@@ -35,3 +35,15 @@ def both():
 tm("raw H2D 50MB", lambda: dA.copy_(hA, non_blocking=True))
 tm("raw D2H 50MB", lambda: hB.copy_(dB, non_blocking=True))
 tm("raw H2D + D2H 50MB concurrently", both)
+
+from paper_1611_05319_b200 import build_guide_field
+_staging._mirror_ok.pop(key, None)
+def two_call():
+    f = build_guide_field(spl, sc.labels)
+    return tracker.run_tracked(sc.image, sc.labels, f, p)
+tm("two-call drop-in (numpy)", two_call)
+tm("build_guide_field alone", lambda: build_guide_field(spl, sc.labels))
+f0 = build_guide_field(spl, sc.labels)
+tm("run_tracked(numpy img, returned field)", lambda: tracker.run_tracked(sc.image, sc.labels, f0, p))
+f1 = f0.copy()
+tm("run_tracked(numpy img, pageable field)", lambda: tracker.run_tracked(sc.image, sc.labels, f1, p))
