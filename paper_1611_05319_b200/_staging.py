@@ -17,6 +17,9 @@ from concurrent.futures import ThreadPoolExecutor
 import numpy as np
 
 _CHUNK = 8 << 20
+# below this a plain pageable .to() is faster than the threaded stager
+# (B200 box, 2 MB labels: 0.13 ms direct vs 0.37 ms staged)
+_STAGE_MIN = 4 << 20
 _lock = threading.Lock()
 _pool = None
 _pinned = {}
@@ -57,7 +60,7 @@ def upload(arr: np.ndarray, device, slot: str = "up"):
     dst = torch.empty(a.shape, dtype=torch.from_numpy(a[:0].reshape(-1)).dtype, device=device)
     if n == 0:
         return dst
-    if n < (1 << 20):
+    if n < _STAGE_MIN:
         return torch.from_numpy(a).to(device)
     ta = torch.from_numpy(a.reshape(-1).view(np.uint8))
     if ta.is_pinned():

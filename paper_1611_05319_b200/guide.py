@@ -37,7 +37,7 @@ def build_guide_field(splines, labels, eta: float = DEFAULT_ETA) -> np.ndarray:
     from . import _staging
 
     dev = N.require_cuda()
-    segs = SegmentSet(splines, dev)
+    segs = SegmentSet.cached(splines, dev)
     d_lab = _staging.upload(np.ascontiguousarray(labels, dtype=np.uint8), dev, "lab")
     return _staging.download(guide_field_device(d_lab, segs, eta))
 

@@ -13,10 +13,10 @@ def tm(name, fn, n=20):
     torch.cuda.synchronize(); t0 = time.perf_counter()
     for _ in range(n): fn()
     torch.cuda.synchronize(); print(f"{name:40s} {(time.perf_counter()-t0)/n*1e3:8.3f} ms", flush=True)
-for chunk in (8 << 20,):
-    _staging._MIRROR_CHUNK = chunk
+for chunk in (1 << 20, 2 << 20, 4 << 20, 8 << 20):
+    _staging._CHUNK = chunk
     _staging._mirror_ok.pop(key, None)
-    print("mirror supported:", _staging.mirror_supported(torch.device("cuda", 0)), "chunk MB", chunk >> 20)
+    print("mirror supported:", _staging.mirror_supported(torch.device("cuda", 0)), "stage chunk MB", chunk >> 20, "threads", _staging._executor()._max_workers)
     tm("pinned tensors, mirrored", lambda: tracker.run_tracked(img_p, lab_p, spl, p))
     tm("numpy, mirrored", lambda: tracker.run_tracked(sc.image, sc.labels, spl, p))
 _staging._mirror_ok[key] = False
