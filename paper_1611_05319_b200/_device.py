@@ -204,7 +204,7 @@ class SegmentSet:
     _cache_order = []
 
     @classmethod
-    def cached(cls, splines, device, max_entries=8):
+    def cached(cls, splines, device, max_entries=64):
         """A SegmentSet for ``splines`` reused across calls: keyed on the
         splines' content (control points, kind, direction), so repeated
         fills with the same guide curves skip the host flattening and upload."""

@@ -188,6 +188,27 @@ def _is_spline_list(guide) -> bool:
     return isinstance(guide, (list, tuple)) and all(hasattr(s, "polyline") for s in guide)
 
 
+def _report_from(stats, rows_dev, tracked: bool, H: int, W: int) -> FillReport:
+    """FillReport of one frame from its device stats and (F, filled) rows."""
+    iters = int(stats[N.STAT_ITERATIONS])
+    rep = FillReport()
+    rep.iterations = iters
+    rep.filled = int(stats[N.STAT_FILLED])
+    rep.deadlock_fills = int(stats[N.STAT_DEADLOCK])
+    rows = []
+    for k in range(iters):
+        F, filled = int(rows_dev[k, 0]), int(rows_dev[k, 1])
+        if tracked:
+            # candidates == next frontier size (the active filter never
+            # removes a candidate, SURVEY.md section 0.7)
+            cand = int(rows_dev[k + 1, 0]) if k + 1 < iters else int(stats[N.STAT_LAST_FRONTIER])
+            rows.append((k, F, cand, F, filled))
+        else:
+            rows.append((k, F, W * H, W * H, filled))
+    rep.rows = rows
+    return rep
+
+
 def _run_fill(image, labels, guide_vecs, params: FillParams, tracked: bool, order_log=False,
               splines=None, eta=3.0, validate=False):
     """Fill one frame on the GPU.  Returns (u float64 (H,W,C), FillReport, maps).
@@ -265,21 +286,7 @@ def _run_fill(image, labels, guide_vecs, params: FillParams, tracked: bool, orde
         u = u_t.numpy()  # shares memory: the unfillable fallback paints in place
     else:
         u = _staging.download(res["out"][0])
-    rep = FillReport()
-    rep.iterations = iters
-    rep.filled = int(stats[N.STAT_FILLED])
-    rep.deadlock_fills = int(stats[N.STAT_DEADLOCK])
-    rows = []
-    for k in range(iters):
-        F, filled = int(rows_dev[k, 0]), int(rows_dev[k, 1])
-        if tracked:
-            # candidates == next frontier size (the active filter never
-            # removes a candidate)
-            cand = int(rows_dev[k + 1, 0]) if k + 1 < iters else int(stats[N.STAT_LAST_FRONTIER])
-            rows.append((k, F, cand, F, filled))
-        else:
-            rows.append((k, F, W * H, W * H, filled))
-    rep.rows = rows
+    rep = _report_from(stats, rows_dev, tracked, H, W)
     fillshell = None
     if order_log or stats[N.STAT_UNFILLABLE]:
         fillshell = res["fillshell"][0].cpu().numpy()

@@ -37,3 +37,150 @@ def fill_video(images, labels, splines, params, tracked=True, device=None, works
 
     return fill_device(images, labels, None, params, tracked=tracked, splines=splines,
                        workspace=workspace)
+
+
+def fill_video_host(images, labels, splines, params, tracked=True, depth=3, on_frame=None):
+    """Fill a sequence of HOST frames with transfers and fills pipelined.
+
+    images: sequence of (H, W, C) frames, float64 numpy arrays or pinned CPU
+    tensors (what a decoder writing into page-locked buffers hands over);
+    labels: one (H, W) uint8 mask shared by all frames, or a sequence of
+    them; splines: a Spline list shared by all frames (rastered inside each
+    fill), a sequence of per-frame Spline lists, or None for g = 0.  Returns [(u, FillReport)] in frame order,
+    u of the input's kind (numpy float64 / pinned CPU tensor).
+
+    Three streams: uploads, fills (one stream, so the cooperative shell
+    kernels never run side by side) and downloads.  While frame n fills,
+    frame n+1 uploads and frame n-1 downloads: the PCIe link carries both
+    directions at once and the fill hides under the transfers.  ``depth``
+    frames are in flight.  Per-frame results equal ``tracker.run_tracked``
+    (tests/test_gpu_configs.py).
+
+    With ``on_frame(f, u, report)`` each result is handed over in frame order
+    as soon as it lands and is not retained (returns None): a streaming
+    consumer keeps the pinned result buffers recycling instead of pinning
+    new host memory for every frame.
+    """
+    import torch
+
+    from . import _native as N
+    from . import _staging
+    from ._device import SegmentSet, fill_device
+    from .engine import _report_from, _run_fill
+
+    dev = N.require_cuda()
+    n = len(images)
+    if n == 0:
+        return []
+    depth = max(1, int(depth))
+    shared_lab = not isinstance(labels, (list, tuple))
+    per_frame_spl = bool(splines) and isinstance(splines[0], (list, tuple))
+    segs = SegmentSet.cached(list(splines), dev) if splines and not per_frame_spl else None
+    s_up, s_fill, s_down = (torch.cuda.Stream(device=dev) for _ in range(3))
+    caller = torch.cuda.current_stream()
+    for s in (s_up, s_fill, s_down):
+        s.wait_stream(caller)  # labels / segments the caller's stream produced
+    stage = [None] * depth
+    lab_stage = [None] * depth
+    rep_bufs = [None] * depth
+    ws = None
+    d_lab_shared = None
+    if shared_lab:
+        lab0 = np.asarray(labels)
+        d_lab_shared = torch.from_numpy(np.ascontiguousarray(lab0, dtype=np.uint8)).to(dev)
+        d_lab_shared = d_lab_shared.reshape(1, *lab0.shape)
+        for s in (s_up, s_fill, s_down):
+            s.wait_stream(caller)
+    pending = [None] * depth
+    results = [None] * n
+
+    def finish(slot):
+        f, ev, u_host, u_ret, st_h, rw_h, _keep = pending[slot]
+        ev.synchronize()
+        H, W = u_host.shape[:2]
+        stats = st_h.numpy()
+        rows = rw_h.numpy()
+        if stats[N.STAT_UNFILLABLE] or int(stats[N.STAT_ITERATIONS]) + 1 > rows.shape[0]:
+            # rare: stranded pixels (host EDT fallback) or a long report -- the
+            # single-frame path handles both
+            lab_f = labels if shared_lab else labels[f]
+            spl_f = splines[f] if per_frame_spl else splines
+            u, rep, _ = _run_fill(images[f], lab_f, None, params, tracked, splines=spl_f)
+        else:
+            u, rep = u_ret, _report_from(stats, rows, tracked, H, W)
+        pending[slot] = None
+        if on_frame is not None:
+            on_frame(f, u, rep)
+        else:
+            results[f] = (u, rep)
+
+    for f in range(n):
+        slot = f % depth
+        if pending[slot] is not None:
+            finish(slot)
+        src = images[f]
+        as_tensor = isinstance(src, torch.Tensor)
+        if as_tensor and src.is_pinned() and src.dtype == torch.float64 and src.is_contiguous():
+            h_img = src
+        else:
+            a = np.ascontiguousarray(src.numpy() if as_tensor else src, dtype=np.float64)
+            if stage[slot] is None or stage[slot].numel() < a.size:
+                stage[slot] = torch.empty(a.size, dtype=torch.float64, pin_memory=True)
+            h_img = stage[slot][:a.size].view(a.shape)
+            np.copyto(h_img.numpy(), a)  # this slot's previous upload has finished
+        H, W, C = h_img.shape
+        with torch.cuda.stream(s_fill):
+            d_img = torch.empty((1, H, W, C), dtype=torch.float64, device=dev)
+            d_lab = d_lab_shared if shared_lab else torch.empty((1, H, W), dtype=torch.uint8,
+                                                                device=dev)
+        with torch.cuda.stream(s_up):
+            d_img.view(H, W, C).copy_(h_img, non_blocking=True)
+            h_lab = None
+            if not shared_lab:
+                lf = labels[f]
+                if isinstance(lf, torch.Tensor) and lf.is_pinned() and lf.dtype == torch.uint8:
+                    h_lab = lf.contiguous()
+                else:
+                    la = np.ascontiguousarray(lf.numpy() if isinstance(lf, torch.Tensor) else lf,
+                                              dtype=np.uint8)
+                    if lab_stage[slot] is None or lab_stage[slot].numel() < la.size:
+                        lab_stage[slot] = torch.empty(la.size, dtype=torch.uint8, pin_memory=True)
+                    h_lab = lab_stage[slot][:la.size].view(la.shape)
+                    np.copyto(h_lab.numpy(), la)  # this slot's previous upload has finished
+                d_lab.view(H, W).copy_(h_lab, non_blocking=True)
+            up = torch.cuda.Event()
+            up.record()
+        s_fill.wait_event(up)
+        with torch.cuda.stream(s_fill):
+            seg_f = segs
+            if per_frame_spl:
+                seg_f = SegmentSet.cached(list(splines[f]), dev) if len(splines[f]) else None
+            res = fill_device(d_img, d_lab, None, params, tracked=tracked, rows_cap=4096,
+                              workspace=ws, splines=seg_f)
+            ws = res["workspace"]
+            done = torch.cuda.Event()
+            done.record()
+        s_down.wait_event(done)
+        with torch.cuda.stream(s_down):
+            if as_tensor:
+                u_host, _ = _staging._pool_out.take_tensor((H, W, C), torch.float64)
+                u_ret = u_host
+            else:
+                u_ret, buf = _staging._pool_out.take((H, W, C), np.float64)
+                u_host = buf[:u_ret.nbytes].view(torch.float64).view(H, W, C)
+            u_host.copy_(res["out"][0], non_blocking=True)
+            if rep_bufs[slot] is None:
+                rep_bufs[slot] = (torch.empty(N.GF_STATS, dtype=torch.int32, pin_memory=True),
+                                  torch.empty((4096, 2), dtype=torch.int32, pin_memory=True))
+            st_h, rw_h = rep_bufs[slot]
+            st_h.copy_(res["stats"][0], non_blocking=True)
+            rw_h.copy_(res["rows"][0], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record()
+        # device buffers stay referenced until the download event has passed
+        pending[slot] = (f, ev, u_host, u_ret, st_h, rw_h, (d_img, d_lab, res, h_img, h_lab))
+    for k in range(n, n + depth):
+        if pending[k % depth] is not None:
+            finish(k % depth)
+    caller.wait_stream(s_down)
+    return None if on_frame is not None else results

@@ -409,3 +409,38 @@ def test_page_locked_numpy_inputs_take_the_direct_dma():
     assert np.array_equal(u, u_ref) and m.rows == m_ref.rows
     u2, _ = tracker.run_tracked(sc.image, sc.labels, spl, p)
     assert np.array_equal(u2, u_ref)
+
+
+@pytest.mark.parametrize("kind,depth", [("numpy", 2), ("pinned", 2), ("pinned", 1),
+                                        ("numpy", 3)])
+def test_fill_video_host_pipelined_equals_single_calls(kind, depth):
+    """video.fill_video_host (uploads / fills / downloads on three streams)
+    gives every frame's run_tracked result, with shared and per-frame masks
+    and splines."""
+    from paper_1611_05319_b200 import tracker, video
+
+    frames = [scenes.small_scene(270, 480, band=8, gx=5, gy=3, n_spl=4, seed=1611, frame=f)
+              for f in range(5)]
+    p = FillParams(**frames[0].params)
+    spl = [_splines(sc) for sc in frames]
+    want = [tracker.run_tracked(sc.image, sc.labels, spl[i], p) for i, sc in enumerate(frames)]
+    if kind == "pinned":
+        imgs = [torch.from_numpy(sc.image).pin_memory() for sc in frames]
+    else:
+        imgs = [sc.image for sc in frames]
+    got = video.fill_video_host(imgs, [sc.labels for sc in frames], spl, p, depth=depth)
+    for (u, rep), (u_w, m_w) in zip(got, want):
+        u = u.numpy() if isinstance(u, torch.Tensor) else u
+        assert np.array_equal(u, u_w)
+        assert rep.rows == m_w.rows and rep.iterations == m_w.iterations
+    seen = []
+    assert video.fill_video_host(imgs, [sc.labels for sc in frames], spl, p, depth=depth,
+                                 on_frame=lambda f, u, rep: seen.append((f, rep.rows))) is None
+    assert [f for f, _ in seen] == list(range(5))
+    assert all(rows == want[f][1].rows for f, rows in seen)
+    # one mask and one spline set for all frames
+    got = video.fill_video_host(imgs[:3], frames[0].labels, spl[0], p, depth=depth)
+    for i, (u, rep) in enumerate(got):
+        u_w, m_w = tracker.run_tracked(frames[i].image, frames[0].labels, spl[0], p)
+        u = u.numpy() if isinstance(u, torch.Tensor) else u
+        assert np.array_equal(u, u_w) and rep.rows == m_w.rows
