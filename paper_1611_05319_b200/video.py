@@ -39,6 +39,22 @@ def fill_video(images, labels, splines, params, tracked=True, device=None, works
                        workspace=workspace)
 
 
+_streams = {}
+
+
+def _pipeline_streams(dev):
+    import threading
+
+    import torch
+
+    key = (str(dev), threading.get_ident())
+    got = _streams.get(key)
+    if got is None:
+        got = tuple(torch.cuda.Stream(device=dev) for _ in range(3))
+        _streams[key] = got
+    return got
+
+
 def fill_video_host(images, labels, splines, params, tracked=True, depth=3, on_frame=None):
     """Fill a sequence of HOST frames with transfers and fills pipelined.
 
@@ -76,7 +92,10 @@ def fill_video_host(images, labels, splines, params, tracked=True, depth=3, on_f
     shared_lab = not isinstance(labels, (list, tuple))
     per_frame_spl = bool(splines) and isinstance(splines[0], (list, tuple))
     segs = SegmentSet.cached(list(splines), dev) if splines and not per_frame_spl else None
-    s_up, s_fill, s_down = (torch.cuda.Stream(device=dev) for _ in range(3))
+    # the same three streams on every call: torch's caching allocator keeps
+    # freed blocks per stream, so fresh streams would cudaMalloc every frame
+    # buffer anew (and stall on cudaFree when the cache is trimmed)
+    s_up, s_fill, s_down = _pipeline_streams(dev)
     caller = torch.cuda.current_stream()
     for s in (s_up, s_fill, s_down):
         s.wait_stream(caller)  # labels / segments the caller's stream produced
