@@ -198,12 +198,19 @@ __device__ __forceinline__ void eval_rot_warp(const BallParams& P, const BallTab
     thr = mloc + P.tol_inf;
   }
   double w[KPW], wr[KPW];
-  double num[4] = {0.0, 0.0, 0.0, 0.0};
+  // colour path in fp32 (off the decision path, tolerance 1e-4): the sample
+  // colour sv and, after the warp knows its largest readable weight, the
+  // numerators with weights scaled by a power of two so the largest is in
+  // [1, 2) -- tiny Eq. 3.2 weights (1e-61 in test_engine.py:77-139) never
+  // underflow the dominant terms
+  float sv[KPW][4];
 #pragma unroll
   for (int s = 0; s < KPW; ++s) {
     const int k = lane + 32 * s;
     w[s] = 0.0;
     wr[s] = 0.0;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) sv[s][c] = 0.f;
     if (k < B::K) {
       double px = T.n[k], py = T.m[k];
       if (P.rotated) {
@@ -250,25 +257,36 @@ __device__ __forceinline__ void eval_rot_warp(const BallParams& P, const BallTab
       }
       w[s] = ws;
       bool ok = !outside;
-      double sv[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
       for (int c = 0; c < 4; ++c)
         if ((live >> c) & 1u) {
           const int a = c >> 1, b = c & 1;
-          const double wc = (a ? tx : 1.0 - tx) * (b ? ty : 1.0 - ty);
+          const float wc = (float)((a ? tx : 1.0 - tx) * (b ? ty : 1.0 - ty));
           ok = ok && __float_as_int(v[c].w) <= src.shell;
-          sv[0] += wc * (double)v[c].x;
-          sv[1] += wc * (double)v[c].y;
-          sv[2] += wc * (double)v[c].z;
-          sv[3] += wc * (double)c3v[c];
+          sv[s][0] = __fmaf_rn(wc, v[c].x, sv[s][0]);
+          sv[s][1] = __fmaf_rn(wc, v[c].y, sv[s][1]);
+          sv[s][2] = __fmaf_rn(wc, v[c].z, sv[s][2]);
+          sv[s][3] = __fmaf_rn(wc, c3v[c], sv[s][3]);
         }
       wr[s] = ok ? ws : 0.0;
-      if (ok) {
-#pragma unroll
-        for (int c = 0; c < 4; ++c) num[c] += ws * sv[c];
-      }
     }
   }
+  // binary exponent of the warp's largest readable weight (0 when none)
+  int e_loc = -2000;
+#pragma unroll
+  for (int s = 0; s < KPW; ++s)
+    if (wr[s] > 0.0) e_loc = max(e_loc, ilogb(wr[s]));
+  const int e_max = __reduce_max_sync(0xffffffffu, e_loc);
+  const int e_use = e_max < -1100 ? 0 : e_max;
+  const double down = scalbn(1.0, -e_use);  // exact power of two
+  float num[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+  for (int s = 0; s < KPW; ++s)
+    if (wr[s] != 0.0) {
+      const float wsf = (float)(wr[s] * down);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) num[c] = __fmaf_rn(wsf, sv[s][c], num[c]);
+    }
   double acc_rw = 0.0, acc_tw = 0.0;
 #pragma unroll
   for (int t = 0; t < B::N8 / 8; ++t) {
@@ -285,15 +303,16 @@ __device__ __forceinline__ void eval_rot_warp(const BallParams& P, const BallTab
     tw = tw + __shfl_sync(0xffffffffu, w[i >> 5], i & 31);
   }
   const double inv = (rw != 0.0) ? 1.0 / rw : 0.0;
+  const double up = scalbn(1.0, e_use);
 #pragma unroll
   for (int c = 0; c < 4; ++c) {
-    double sacc = 0.0;
+    float sacc = 0.f;
     if (c < 3 || src.c3) {
       sacc = num[c];
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, o);
     }
-    out.v[c] = sacc * inv;
+    out.v[c] = ((double)sacc * up) * inv;
   }
   out.rw = rw;
   out.tw = tw;
