@@ -262,13 +262,20 @@ def _run_fill(image, labels, guide_vecs, params: FillParams, tracked: bool, orde
     if guide_vecs is not None and params.g_source == "guide_field" and segs is None:
         d_guide = _staging.upload(np.ascontiguousarray(guide_vecs, dtype=np.float64), dev,
                                   "guide").reshape(1, H, W, 2)
-    res = fill_device(d_img, d_lab, d_guide, params, tracked=tracked, order_log=order_log,
-                      rows_cap=H * W + 1, splines=segs, eta=eta, want_fillshell=True)
-    if mirror is not None:
-        # result = the mirrored input + the changed pixels (the read-back of
-        # the report below synchronises the stream)
-        mirror.finish(d_img, res["out"])
-    stats, rows_dev = _staging.read_report(res["stats"][0], res["rows"][0])
+    try:
+        res = fill_device(d_img, d_lab, d_guide, params, tracked=tracked, order_log=order_log,
+                          rows_cap=H * W + 1, splines=segs, eta=eta, want_fillshell=True)
+        if mirror is not None:
+            # result = the mirrored input + the changed pixels (the read-back of
+            # the report below synchronises the stream)
+            mirror.finish(d_img, res["out"])
+        stats, rows_dev = _staging.read_report(res["stats"][0], res["rows"][0])
+    except BaseException:
+        if mirror is not None:
+            # the mirror DMA still targets the pooled result buffer: let it land
+            # before the buffer can be handed to another caller
+            mirror.side.synchronize()
+        raise
     if validate and stats[N.STAT_BAD_LABELS]:
         grid.validate_labels(labels)  # k_prep saw a bad label: the reference's message
         raise ValueError("label mask holds values outside {0, 128, 255}")

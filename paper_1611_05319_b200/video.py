@@ -62,8 +62,9 @@ def fill_video_host(images, labels, splines, params, tracked=True, depth=3, on_f
     tensors (what a decoder writing into page-locked buffers hands over);
     labels: one (H, W) uint8 mask shared by all frames, or a sequence of
     them; splines: a Spline list shared by all frames (rastered inside each
-    fill), a sequence of per-frame Spline lists, or None for g = 0.  Returns [(u, FillReport)] in frame order,
-    u of the input's kind (numpy float64 / pinned CPU tensor).
+    fill), a sequence of per-frame Spline lists, or None for g = 0.
+    Returns [(u, FillReport)] in frame order, u of the input's kind (numpy
+    float64 / pinned CPU tensor).
 
     Three streams: uploads, fills (one stream, so the cooperative shell
     kernels never run side by side) and downloads.  While frame n fills,
@@ -80,8 +81,7 @@ def fill_video_host(images, labels, splines, params, tracked=True, depth=3, on_f
     import torch
 
     from . import _native as N
-    from . import _staging
-    from ._device import SegmentSet, fill_device
+    from ._device import SegmentSet
     from .engine import _report_from, _run_fill
 
     dev = N.require_cuda()
@@ -102,7 +102,6 @@ def fill_video_host(images, labels, splines, params, tracked=True, depth=3, on_f
     stage = [None] * depth
     lab_stage = [None] * depth
     rep_bufs = [None] * depth
-    ws = None
     d_lab_shared = None
     if shared_lab:
         lab0 = np.asarray(labels)
@@ -119,6 +118,14 @@ def fill_video_host(images, labels, splines, params, tracked=True, depth=3, on_f
         H, W = u_host.shape[:2]
         stats = st_h.numpy()
         rows = rw_h.numpy()
+        if stats[N.STAT_BAD_LABELS]:
+            # k_prep saw a label outside {0, 128, 255}: the reference's ValueError
+            from . import grid
+
+            lab_f = labels if shared_lab else labels[f]
+            grid.validate_labels(np.asarray(lab_f.numpy() if isinstance(lab_f, torch.Tensor)
+                                            else lab_f))
+            raise ValueError("label mask holds values outside {0, 128, 255}")
         if stats[N.STAT_UNFILLABLE] or int(stats[N.STAT_ITERATIONS]) + 1 > rows.shape[0]:
             # rare: stranded pixels (host EDT fallback) or a long report -- the
             # single-frame path handles both
@@ -133,6 +140,30 @@ def fill_video_host(images, labels, splines, params, tracked=True, depth=3, on_f
         else:
             results[f] = (u, rep)
 
+    try:
+        _pipeline(n, depth, pending, finish, images, labels, splines, params, tracked, dev,
+                  shared_lab, d_lab_shared, per_frame_spl, segs, stage, lab_stage, rep_bufs,
+                  s_up, s_fill, s_down)
+    except BaseException:
+        # in-flight copies still target pooled host buffers: drain before unwinding
+        for s_ in (s_up, s_fill, s_down):
+            s_.synchronize()
+        raise
+    caller.wait_stream(s_down)
+    return None if on_frame is not None else results
+
+
+def _pipeline(n, depth, pending, finish, images, labels, splines, params, tracked, dev,
+              shared_lab, d_lab_shared, per_frame_spl, segs, stage, lab_stage, rep_bufs,
+              s_up, s_fill, s_down):
+    """The frame loop of fill_video_host (enqueue frame f, retire frame f - depth)."""
+    import torch
+
+    from . import _native as N
+    from . import _staging
+    from ._device import SegmentSet, fill_device
+
+    ws = None
     for f in range(n):
         slot = f % depth
         if pending[slot] is not None:
@@ -201,5 +232,3 @@ def fill_video_host(images, labels, splines, params, tracked=True, depth=3, on_f
     for k in range(n, n + depth):
         if pending[k % depth] is not None:
             finish(k % depth)
-    caller.wait_stream(s_down)
-    return None if on_frame is not None else results

@@ -444,3 +444,22 @@ def test_fill_video_host_pipelined_equals_single_calls(kind, depth):
         u_w, m_w = tracker.run_tracked(frames[i].image, frames[0].labels, spl[0], p)
         u = u.numpy() if isinstance(u, torch.Tensor) else u
         assert np.array_equal(u, u_w) and rep.rows == m_w.rows
+
+
+def test_fill_video_host_bad_labels_raise_and_drain():
+    """A bad mask mid-stream raises the reference's ValueError (grid.py:36-46);
+    the pipeline drains its in-flight copies, and the next call is clean."""
+    from paper_1611_05319_b200 import tracker, video
+
+    frames = [scenes.small_scene(270, 480, band=8, gx=5, gy=3, n_spl=4, seed=7, frame=f)
+              for f in range(4)]
+    p = FillParams(**frames[0].params)
+    labs = [sc.labels.copy() for sc in frames]
+    labs[2][5, 5] = 7
+    with pytest.raises(ValueError):
+        video.fill_video_host([sc.image for sc in frames], labs, [_splines(sc) for sc in frames], p)
+    got = video.fill_video_host([sc.image for sc in frames[:2]], [sc.labels for sc in frames[:2]],
+                                [_splines(sc) for sc in frames[:2]], p)
+    for (u, rep), sc in zip(got, frames[:2]):
+        u_w, m_w = tracker.run_tracked(sc.image, sc.labels, _splines(sc), p)
+        assert np.array_equal(u, u_w) and rep.rows == m_w.rows
