@@ -236,6 +236,23 @@ int gf_output_delta(int64_t n_px, int32_t channels, int32_t dtype, const void* i
 int gf_upload_mirrored(const void* host_src, void* dev_dst, void* host_mirror, int64_t nbytes,
                        int64_t chunk, void* stream, void* side_stream);
 
+/*
+ * Unfillable fallback on the device (engine.py:270-283): every stranded
+ * pixel (Inpaint with fillshell < 0) takes the colour, in `out`, of its
+ * nearest readable pixel (Readable, or Inpaint with fillshell >= 0) as
+ * scipy.ndimage.distance_transform_edt(~readable, return_indices=True)
+ * picks it, ties included; 0.5 in every channel when nothing is readable.
+ * One frame: labels [H][W] u8, fillshell [H][W] int32 (gf_fill_outputs),
+ * out [H][W][C] of dtype GF_F32/GF_F64, updated in place.  n_painted
+ * (device, nullable) is incremented by the stranded pixel count.
+ * workspace: gf_paint_unfillable_workspace_bytes(H, W) device bytes.
+ */
+size_t gf_paint_unfillable_workspace_bytes(int32_t height, int32_t width);
+int gf_paint_unfillable(int32_t height, int32_t width, int32_t channels, int32_t dtype,
+                        const uint8_t* labels, const int32_t* fillshell, void* out,
+                        void* workspace, size_t workspace_bytes, int32_t* n_painted,
+                        void* stream);
+
 /* Thread-local message for the last failing call on this thread. */
 const char* gf_last_error(void);
 int gf_abi_version(void);

@@ -165,23 +165,22 @@ def ready(conf: float, g, params: FillParams, data_term_live: bool = True) -> bo
     return gnorm > params.c2 and conf > params.c
 
 
-def _paint_unfillable(u, labels, fillshell):
-    """Nearest-readable colour for stranded Inpaint pixels (engine.py:270-283)."""
-    from scipy import ndimage
+def _paint_unfillable_device(out, labels_dev, fillshell_dev):
+    """Stranded Inpaint pixels take their nearest readable colour on the
+    device (engine.py:270-283 via gf_paint_unfillable: scipy's EDT feature
+    transform restated, ties included).  out (H, W, C) CUDA tensor, in place.
+    Returns the painted pixel count (synchronises)."""
+    import torch
 
-    lab = np.asarray(labels)
-    stranded = (lab == INPAINT) & (fillshell < 0)
-    count = int(stranded.sum())
-    if count == 0:
-        return 0
-    readable = (lab == READABLE) | ((lab == INPAINT) & (fillshell >= 0))
-    if readable.any():
-        _, (jn, inn) = ndimage.distance_transform_edt(~readable, return_indices=True)
-        jr, ir = np.nonzero(stranded)
-        u[jr, ir] = u[jn[jr, ir], inn[jr, ir]]
-    else:
-        u[stranded] = 0.5
-    return count
+    lib = N.load()
+    H, W, C = out.shape
+    need = lib.gf_paint_unfillable_workspace_bytes(H, W)
+    ws = torch.empty(need, dtype=torch.uint8, device=out.device)
+    cnt = torch.zeros(1, dtype=torch.int32, device=out.device)
+    N.check(lib.gf_paint_unfillable(H, W, C, N.GF_F64 if out.dtype == torch.float64 else N.GF_F32,
+                                    N.ptr(labels_dev), N.ptr(fillshell_dev), N.ptr(out), N.ptr(ws),
+                                    need, N.ptr(cnt), N.stream_ptr()))
+    return int(cnt.item())
 
 
 def _is_spline_list(guide) -> bool:
@@ -280,17 +279,22 @@ def _run_fill(image, labels, guide_vecs, params: FillParams, tracked: bool, orde
         grid.validate_labels(labels)  # k_prep saw a bad label: the reference's message
         raise ValueError("label mask holds values outside {0, 128, 255}")
     iters = int(stats[N.STAT_ITERATIONS])
+    n_painted = 0
+    if stats[N.STAT_UNFILLABLE]:
+        # stranded pixels: painted on the device before the result leaves it
+        n_painted = _paint_unfillable_device(res["out"][0], d_lab[0], res["fillshell"][0])
+        if mirror is not None:
+            mirror.finish(d_img, res["out"])  # the painted pixels join the delta
     if iters + 1 > rows_dev.shape[0]:
         rows_dev = res["rows"][0, :iters + 1].cpu().numpy()
     if mirror is not None:
+        torch.cuda.current_stream().synchronize()  # the delta has landed
         if as_tensor:
             u_t = mirror.result
-            u = u_t.numpy()
         else:
             u = mirror.result
     elif as_tensor:
         u_t = _staging.download_tensor(res["out"][0])
-        u = u_t.numpy()  # shares memory: the unfillable fallback paints in place
     else:
         u = _staging.download(res["out"][0])
     rep = _report_from(stats, rows_dev, tracked, H, W)
@@ -299,7 +303,7 @@ def _run_fill(image, labels, guide_vecs, params: FillParams, tracked: bool, orde
         fillshell = res["fillshell"][0].cpu().numpy()
     if stats[N.STAT_UNFILLABLE]:
         rep.unfillable = True
-        rep.unfillable_count = _paint_unfillable(u, labels, fillshell)
+        rep.unfillable_count = n_painted
         fillshell = np.where((np.asarray(labels) == INPAINT) & (fillshell < 0), -2, fillshell)
     enter = res["enter"][0].cpu().numpy() if order_log else None
     rep.wall_time_s = time.perf_counter() - t0

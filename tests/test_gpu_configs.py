@@ -463,3 +463,63 @@ def test_fill_video_host_bad_labels_raise_and_drain():
     for (u, rep), sc in zip(got, frames[:2]):
         u_w, m_w = tracker.run_tracked(sc.image, sc.labels, _splines(sc), p)
         assert np.array_equal(u, u_w) and rep.rows == m_w.rows
+
+
+def _paint_reference(u, labels, fillshell):
+    """engine.py:270-283 with scipy's EDT (test-side checker)."""
+    from scipy import ndimage
+
+    stranded = (labels == 255) & (fillshell < 0)
+    readable = (labels == 0) | ((labels == 255) & (fillshell >= 0))
+    u = u.copy()
+    if readable.any():
+        _, (jn, inn) = ndimage.distance_transform_edt(~readable, return_indices=True)
+        jr, ir = np.nonzero(stranded)
+        u[jr, ir] = u[jn[jr, ir], inn[jr, ir]]
+    else:
+        u[stranded] = 0.5
+    return u, int(stranded.sum())
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_unfillable_paint_matches_scipy_edt(seed):
+    """gf_paint_unfillable == scipy distance_transform_edt indices, ties
+    included: sparse readable sets on lattices of many shapes (every pixel a
+    distinct colour, so any wrong nearest pixel shows)."""
+    from paper_1611_05319_b200.engine import _paint_unfillable_device
+
+    rng = np.random.default_rng(seed)
+    H, W = int(rng.integers(1, 90)), int(rng.integers(1, 130))
+    C = int(rng.integers(1, 5))
+    dtype = np.float64 if seed % 2 == 0 else np.float32
+    labels = rng.choice(np.array([0, 128, 255], np.uint8), size=(H, W),
+                        p=[0.02, 0.05, 0.93] if seed % 3 else [0.2, 0.3, 0.5])
+    fillshell = np.where(rng.random((H, W)) < 0.03, 1, -1).astype(np.int32)
+    fillshell[labels != 255] = -1
+    if seed == 5:
+        labels[labels == 0] = 128  # nothing Readable
+        fillshell[:] = -1
+    u = rng.random((H, W, C)).astype(dtype)
+    want, n_want = _paint_reference(u, labels, fillshell)
+    d_u = torch.from_numpy(u).cuda()
+    n = _paint_unfillable_device(d_u, torch.from_numpy(labels).cuda(),
+                                 torch.from_numpy(fillshell).cuda())
+    assert n == n_want
+    assert np.array_equal(d_u.cpu().numpy(), want)
+
+
+def test_unfillable_paint_large_ties():
+    """A 1080p lattice with three readable pixels: long equidistant ridges."""
+    from paper_1611_05319_b200.engine import _paint_unfillable_device
+
+    H, W = 1080, 1920
+    labels = np.full((H, W), 255, np.uint8)
+    for (r, c) in ((100, 100), (100, 1700), (900, 960)):
+        labels[r, c] = 0
+    fillshell = np.full((H, W), -1, np.int32)
+    u = np.random.default_rng(3).random((H, W, 3))
+    want, n_want = _paint_reference(u, labels, fillshell)
+    d_u = torch.from_numpy(u).cuda()
+    assert _paint_unfillable_device(d_u, torch.from_numpy(labels).cuda(),
+                                    torch.from_numpy(fillshell).cuda()) == n_want
+    assert np.array_equal(d_u.cpu().numpy(), want)
