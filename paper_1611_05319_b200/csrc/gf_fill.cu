@@ -1188,7 +1188,10 @@ __global__ void __launch_bounds__(kShellThreads, GF_SHELL_MIN_BLOCKS)
 #ifndef GF_LATTICE_LANES
 #define GF_LATTICE_LANES 4
 #endif
-  constexpr int LG = (R > 0 && R <= 3) ? GF_LATTICE_LANES : 8;
+#ifndef GF_LG4_MAX_R
+#define GF_LG4_MAX_R 3
+#endif
+  constexpr int LG = (R > 0 && R <= GF_LG4_MAX_R) ? GF_LATTICE_LANES : 8;
   constexpr int IPU = 32 / LG;
   const int lglane = lane & (LG - 1);
   const int lsub = lane / LG;
