@@ -253,6 +253,24 @@ int gf_paint_unfillable(int32_t height, int32_t width, int32_t channels, int32_t
                         void* workspace, size_t workspace_bytes, int32_t* n_painted,
                         void* stream);
 
+/*
+ * Coherence-transport guide directions (g_source "modified_structure_tensor"):
+ * replaces guide.coherence_directions (guide.py:330-355) as called per shell
+ * by engine._resolve_g (engine.py:243-249).  The masked structure tensor of
+ * guide._tensor_field (guide.py:91-120) over image [H][W][C] float64 with
+ * readable = (labels == 0), evaluated at the n flat pixel indices idx
+ * (device int64), eigen split as guide.eigen_2x2 (guide.py:123-136):
+ * g[n][2] = tanh((hi - lo) / lam) * minor eigenvector, 0 where the rho
+ * window holds no readable mass.  sigma / rho: Gaussian scales (truncate 2,
+ * radius int(2 s + 0.5) <= 63).  H, W >= 2 (np.gradient needs 2 samples).
+ * workspace: gf_coherence_workspace_bytes(H, W, C) device bytes.
+ */
+size_t gf_coherence_workspace_bytes(int32_t height, int32_t width, int32_t channels);
+int gf_coherence_directions(int32_t height, int32_t width, int32_t channels,
+                            const double* image, const uint8_t* labels, int32_t n,
+                            const int64_t* idx, double sigma, double rho, double lam,
+                            double* g, void* workspace, size_t workspace_bytes, void* stream);
+
 /* Thread-local message for the last failing call on this thread. */
 const char* gf_last_error(void);
 int gf_abi_version(void);

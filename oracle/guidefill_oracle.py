@@ -199,8 +199,61 @@ def point_sample(u, labels, point, g, params):
 
 # --------------------------------------------------------------- fill loop
 
-def _frontier_g(params, guide_vecs, frontier):
-    """engine.py:234-242 (guide_field / fixed sources)."""
+def _smooth(arr, s):
+    """guide.py:46-48."""
+    return ndimage.gaussian_filter(arr, sigma=s, truncate=2.0, mode="constant", cval=0.0)
+
+
+def tensor_field(image, indicator, sigma, rho):
+    """guide.py:91-120: indicator-weighted structure tensor (J11, J12, J22, mass_r)."""
+    ind = indicator.astype(np.float64)
+    mass_s = _smooth(ind, sigma)
+    safe_s = np.where(mass_s > 0.0, mass_s, 1.0)
+    J11 = np.zeros(ind.shape)
+    J12 = np.zeros(ind.shape)
+    J22 = np.zeros(ind.shape)
+    for ch in range(image.shape[2]):
+        v = _smooth(ind * image[:, :, ch], sigma) / safe_s
+        gy, gx = np.gradient(v)
+        J11 += gx * gx
+        J12 += gx * gy
+        J22 += gy * gy
+    J11 *= ind
+    J12 *= ind
+    J22 *= ind
+    mass_r = _smooth(ind, rho)
+    safe_r = np.where(mass_r > 0.0, mass_r, 1.0)
+    return (_smooth(J11, rho) / safe_r, _smooth(J12, rho) / safe_r,
+            _smooth(J22, rho) / safe_r, mass_r)
+
+
+def coherence_directions(image, readable, ix, iy, sigma=2.0, rho=4.0, lam=1e-5):
+    """guide.py:330-355 (crop to the queries' box + cascade_radius + 2, guide.py:60-62),
+    eigen split guide.py:123-136."""
+    ix = np.asarray(ix)
+    iy = np.asarray(iy)
+    H, W = readable.shape
+    pad = int(math.ceil(2.0 * sigma + 2.0 * rho)) + 2
+    j0 = max(0, int(iy.min()) - pad)
+    j1 = min(H, int(iy.max()) + pad + 1)
+    i0 = max(0, int(ix.min()) - pad)
+    i1 = min(W, int(ix.max()) + pad + 1)
+    J11, J12, J22, mass_r = tensor_field(image[j0:j1, i0:i1], readable[j0:j1, i0:i1], sigma, rho)
+    qj = iy - j0
+    qi = ix - i0
+    a, b, c = J11[qj, qi], J12[qj, qi], J22[qj, qi]
+    mean = (a + c) / 2.0
+    disc = np.sqrt(((a - c) / 2.0) ** 2 + b * b)
+    phi = 0.5 * np.arctan2(2.0 * b, a - c)
+    lo, hi, vx, vy = mean - disc, mean + disc, -np.sin(phi), np.cos(phi)
+    coh = np.tanh((hi - lo) / lam)
+    g = np.stack([coh * vx, coh * vy], axis=-1)
+    g[mass_r[qj, qi] <= 0.0] = 0.0
+    return g
+
+
+def _frontier_g(params, guide_vecs, frontier, u=None, lab=None):
+    """engine.py:234-249."""
     if params.g_source == "fixed":
         gf = params.g_fixed or (0.0, 0.0)
         return np.array([float(gf[0]), float(gf[1])])
@@ -208,7 +261,9 @@ def _frontier_g(params, guide_vecs, frontier):
         if guide_vecs is None:
             return np.zeros(2)
         return guide_vecs.reshape(-1, 2)[frontier]
-    raise NotImplementedError("coherence g source is outside the oracle's scope")
+    iy, ix = np.divmod(frontier, lab.shape[1])
+    return coherence_directions(u, lab == READABLE, ix, iy, sigma=params.sigma,
+                                rho=params.rho, lam=params.coherence_lambda)
 
 
 def _neighbor_mean(u, readable, idx, W, periodic_x):
@@ -323,7 +378,7 @@ def fill(image, labels, guide=None, params=None, tracked: bool = True):
             out["unfillable_count"] = cnt
             fillshell[stranded.reshape(-1)] = -2
             break
-        g = _frontier_g(params, guide_vecs, frontier)
+        g = _frontier_g(params, guide_vecs, frontier, u, lab)
         fy, fx = np.divmod(frontier, W)
         vals, rw, tw = sample_frontier(u, readable, fx.astype(np.float64),
                                        fy.astype(np.float64), g, params, offs)
@@ -473,7 +528,10 @@ class Params:
 
     def __init__(self, r=3, mu=50.0, c=0.05, c2=0.0, order="smart",
                  neighborhood="rotated_ball", g_source="guide_field", g_fixed=None,
-                 periodic_x=False):
+                 periodic_x=False, sigma=2.0, rho=4.0, coherence_lambda=1e-5):
+        self.sigma = sigma
+        self.rho = rho
+        self.coherence_lambda = coherence_lambda
         self.r = r
         self.mu = mu
         self.c = c
@@ -488,7 +546,9 @@ class Params:
     def of(cls, p):
         return cls(r=p.r, mu=p.mu, c=p.c, c2=p.c2, order=p.order,
                    neighborhood=p.neighborhood, g_source=p.g_source,
-                   g_fixed=p.g_fixed, periodic_x=p.periodic_x)
+                   g_fixed=p.g_fixed, periodic_x=p.periodic_x,
+                   sigma=getattr(p, "sigma", 2.0), rho=getattr(p, "rho", 4.0),
+                   coherence_lambda=getattr(p, "coherence_lambda", 1e-5))
 
 
 def numpy_exp_flavour() -> str:

@@ -39,8 +39,9 @@ def resolve_g_mode(params, guide_present: bool) -> int:
     if params.g_source == "guide_field":
         return N.GF_G_FIELD if guide_present else N.GF_G_ZERO
     raise NotImplementedError(
-        "g_source='modified_structure_tensor' (coherence transport) is not part of the "
-        "B200 fill path yet (SURVEY.md section 8f-2)")
+        "g_source='modified_structure_tensor' (coherence transport) recomputes g from the "
+        "image every shell: it runs through engine.inpaint / tracker.run_tracked (the "
+        "shell-by-shell loop of coherence.py), not the batched persistent kernel")
 
 
 def _fill_setup(image, labels, guide, params, tracked=True, order_log=False, rows_cap=None,

@@ -29,7 +29,8 @@ EXPORTS = (
     "gf_fill_workspace_bytes", "gf_fill_splines_workspace_bytes", "gf_fill", "gf_fill_splines",
     "gf_guide_field", "gf_sample_points",
     "gf_bilinear_gather", "gf_boundary_masks", "gf_output_delta", "gf_upload_mirrored",
-    "gf_paint_unfillable_workspace_bytes", "gf_paint_unfillable", "gf_last_error",
+    "gf_paint_unfillable_workspace_bytes", "gf_paint_unfillable",
+    "gf_coherence_workspace_bytes", "gf_coherence_directions", "gf_last_error",
     "gf_abi_version", "gf_host_exp", "gf_host_hypot", "gf_host_pairwise_sum",
 )
 
@@ -137,6 +138,12 @@ def load(required: bool = True):
     lib.gf_upload_mirrored.argtypes = [P, P, P, ctypes.c_int64, ctypes.c_int64, P, P]
     lib.gf_paint_unfillable_workspace_bytes.restype = ctypes.c_size_t
     lib.gf_paint_unfillable_workspace_bytes.argtypes = [ctypes.c_int32, ctypes.c_int32]
+    lib.gf_coherence_workspace_bytes.restype = ctypes.c_size_t
+    lib.gf_coherence_workspace_bytes.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32]
+    lib.gf_coherence_directions.restype = ctypes.c_int
+    lib.gf_coherence_directions.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, P, P,
+                                            ctypes.c_int32, P, ctypes.c_double, ctypes.c_double,
+                                            ctypes.c_double, P, P, ctypes.c_size_t, P]
     lib.gf_paint_unfillable.restype = ctypes.c_int
     lib.gf_paint_unfillable.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
                                         ctypes.c_int32, P, P, P, P, ctypes.c_size_t, P, P]

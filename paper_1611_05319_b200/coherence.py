@@ -1,0 +1,202 @@
+"""Coherence-transport fill (g_source = "modified_structure_tensor") on the GPU.
+
+The reference resolves g per shell from the current image (engine._resolve_g,
+engine.py:243-249 -> guide.coherence_directions, guide.py:330-355): every
+shell's guidance reads the pixels the previous shell filled, so g cannot be
+precomputed the way the guide field is.  This loop therefore runs shell by
+shell from the host, with every per-pixel step on the device:
+
+* g at the frontier: gf_coherence_directions (csrc/gf_coherence.cu, the masked
+  structure tensor of guide._tensor_field as separable passes over the frame);
+* weights, ghost gathers, masses and colours: gf_sample_points (the same ball
+  evaluator the persistent shell kernel uses, engine.py:131-199);
+* ready predicate, deadlock guard, scatter/relabel and the tracked frontier
+  update (tracker.py:42-79): torch device ops on the index lists;
+* unfillable fallback: gf_paint_unfillable.
+
+The host only reads the frontier size and "anything filled?" per shell (the
+loop's own control flow, engine.py:304-348).  Structure follows
+engine._fill_loop (engine.py:286-376) step for step.
+"""
+
+from __future__ import annotations
+
+import time
+
+import numpy as np
+
+from . import _native as N
+from ._device import boundary_device, sample_points_device
+from .grid import INPAINT, NEIGHBOR_OFFSETS, READABLE
+
+
+def coherence_directions_device(u, lab, idx, sigma=2.0, rho=4.0, lam=1e-5, workspace=None):
+    """guide.coherence_directions (guide.py:330-355) at flat pixel indices ``idx``
+    (int64 CUDA tensor): (n, 2) float64 CUDA tensor."""
+    import torch
+
+    lib = N.load()
+    H, W, C = u.shape
+    n = int(idx.numel())
+    g = torch.empty((n, 2), dtype=torch.float64, device=u.device)
+    need = lib.gf_coherence_workspace_bytes(H, W, C)
+    if workspace is None or workspace.numel() < need:
+        workspace = torch.empty(need, dtype=torch.uint8, device=u.device)
+    N.check(lib.gf_coherence_directions(H, W, C, N.ptr(u), N.ptr(lab), n, N.ptr(idx),
+                                        float(sigma), float(rho), float(lam), N.ptr(g),
+                                        N.ptr(workspace), need, N.stream_ptr()))
+    return g
+
+
+def _active(lab, periodic_x):
+    """grid.active_boundary_mask (grid.py:59-76) on the device, flattened."""
+    return boundary_device(lab, periodic_x)[0].reshape(-1)
+
+
+def _neighbours(idx, H, W, periodic_x):
+    """tracker._neighbor_indices (tracker.py:42-56): [(valid, flat)] in NEIGHBOR_OFFSETS order."""
+    import torch
+
+    jy = torch.div(idx, W, rounding_mode="floor")
+    ix = idx - jy * W
+    out = []
+    for di, dj in NEIGHBOR_OFFSETS:
+        ii = ix + di
+        jj = jy + dj
+        if periodic_x:
+            ii = torch.remainder(ii, W)
+            valid = (jj >= 0) & (jj < H)
+        else:
+            valid = (ii >= 0) & (ii < W) & (jj >= 0) & (jj < H)
+        out.append((valid, jj * W + torch.where(valid, ii, torch.zeros_like(ii))))
+    return out
+
+
+def _neighbor_mean(u, lab, p, H, W, periodic_x):
+    """engine._neighbor_mean (engine.py:252-267): readable 8-neighbours, fixed order."""
+    import torch
+
+    C = u.shape[2]
+    flat_u = u.reshape(-1, C)
+    flat_l = lab.reshape(-1)
+    acc = torch.zeros(C, dtype=torch.float64, device=u.device)
+    n = 0
+    j, i = divmod(p, W)
+    for di, dj in NEIGHBOR_OFFSETS:
+        ii, jj = i + di, j + dj
+        if periodic_x:
+            ii %= W
+        if 0 <= ii < W and 0 <= jj < H and int(flat_l[jj * W + ii]) == READABLE:
+            acc += flat_u[jj * W + ii]
+            n += 1
+    if n == 0:
+        return None
+    return acc / n
+
+
+def run_coherence_fill(u, lab0, params, tracked=True, order_log=False):
+    """engine._fill_loop (engine.py:286-376) with g from the masked structure tensor.
+
+    ``u``: (H, W, C) float64 CUDA tensor (consumed: filled in place); ``lab0``:
+    (H, W) uint8 CUDA tensor (not modified).  Returns (u, report fields dict,
+    enter, fillshell) with the order maps as int32 CUDA tensors (enter None
+    unless order_log).
+    """
+    import torch
+
+    H, W, C = u.shape
+    dev = u.device
+    lab = lab0.clone()
+    flat_u = u.reshape(-1, C)
+    flat_l = lab.reshape(-1)
+    readable = lab == READABLE
+    hull = None
+    if bool(readable.any()):
+        seed = u[readable]
+        hull = (seed.min(), seed.max())
+    remaining = int((lab == INPAINT).sum())
+    data_term_live = params.order == "smart_with_data_term"
+    px = bool(params.periodic_x)
+    frontier = torch.nonzero(_active(lab, px)).reshape(-1)
+    fillshell = torch.full((H * W,), -1, dtype=torch.int32, device=dev)
+    enter = torch.full((H * W,), -1, dtype=torch.int32, device=dev) if order_log else None
+    ws = torch.empty(N.load().gf_coherence_workspace_bytes(H, W, C), dtype=torch.uint8,
+                     device=dev)
+    rep = dict(rows=[], iterations=0, filled=0, deadlock_fills=0, unfillable=False,
+               unfillable_count=0)
+    t0 = time.perf_counter()
+    it = 0
+    while remaining > 0:
+        F = int(frontier.numel())
+        if F == 0:
+            rep["unfillable"] = True
+            break
+        if enter is not None:
+            cur = enter[frontier]
+            enter[frontier] = torch.where(cur < 0, torch.full_like(cur, it), cur)
+        g = coherence_directions_device(u, lab, frontier, params.sigma, params.rho,
+                                        params.coherence_lambda, ws)
+        fy = torch.div(frontier, W, rounding_mode="floor")
+        pts = torch.stack([(frontier - fy * W).to(torch.float64), fy.to(torch.float64)], 1)
+        rw, tw, vals = sample_points_device(u, lab, pts.contiguous(), g, params)
+        conf = rw / tw
+        if params.order == "onion":
+            ready = torch.ones(F, dtype=torch.bool, device=dev)
+        elif params.order == "smart" or not data_term_live:
+            ready = conf > params.c
+        else:
+            gnorm = torch.hypot(g[:, 0], g[:, 1])
+            if not bool((gnorm > 0.0).any()):
+                data_term_live = False
+                ready = conf > params.c
+            else:
+                ready = (gnorm > params.c2) & (conf > params.c)
+        fill = ready & (rw > 0.0)
+        if not bool(fill.any()):
+            # deadlock guard (engine.py:334-348): first maximal confidence, NaN first
+            c_h = conf.cpu().numpy()
+            k = int(np.argmax(c_h))
+            if float(rw[k]) > 0.0:
+                fill[k] = True
+            else:
+                fb = _neighbor_mean(u, lab, int(frontier[k]), H, W, px)
+                if fb is None:
+                    rep["unfillable"] = True
+                    break
+                vals[k] = fb
+                fill[k] = True
+            rep["deadlock_fills"] += 1
+        filled_idx = frontier[fill]
+        n = int(filled_idx.numel())
+        flat_u[filled_idx] = vals[fill]
+        flat_l[filled_idx] = READABLE
+        fillshell[filled_idx] = it
+        remaining -= n
+        rep["filled"] += n
+        act = _active(lab, px)
+        if tracked:
+            # tracker._update_arrays (tracker.py:59-79): survivors + INPAINT
+            # neighbours of the filled pixels, sorted dedup, active filter
+            pool = [frontier[~fill]]
+            for valid, nbr in _neighbours(filled_idx, H, W, px):
+                live = valid & (flat_l[torch.where(valid, nbr, torch.zeros_like(nbr))] == INPAINT)
+                pool.append(nbr[live])
+            cand = torch.unique(torch.cat(pool))
+            candidates = int(cand.numel())
+            new_frontier = cand[act[cand] != 0]
+            threads = F
+        else:
+            new_frontier = torch.nonzero(act).reshape(-1)
+            candidates = threads = W * H
+        rep["rows"].append((it, F, candidates, threads, n))
+        frontier = new_frontier
+        it += 1
+    rep["iterations"] = it
+    if rep["unfillable"]:
+        from .engine import _paint_unfillable_device
+
+        rep["unfillable_count"] = _paint_unfillable_device(u, lab0, fillshell.reshape(H, W))
+    if hull is not None:
+        u.clamp_(hull[0], hull[1])
+    rep["wall_time_s"] = time.perf_counter() - t0
+    return u, rep, enter, fillshell

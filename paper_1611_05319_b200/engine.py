@@ -220,6 +220,8 @@ def _run_fill(image, labels, guide_vecs, params: FillParams, tracked: bool, orde
     if validate and not torch.cuda.is_available():
         grid.validate_labels(labels)  # same ValueError without a device
     dev = N.require_cuda()
+    if params.g_source == "modified_structure_tensor":
+        return _run_coherence(image, labels, params, tracked, order_log, dev)
     from . import _staging
     from ._device import SegmentSet, fill_device
 
@@ -310,6 +312,47 @@ def _run_fill(image, labels, guide_vecs, params: FillParams, tracked: bool, orde
     return (u_t if as_tensor else u), rep, dict(enter=enter, fillshell=fillshell)
 
 
+def _run_coherence(image, labels, params, tracked, order_log, dev):
+    """Coherence-transport g source (engine.py:243-249): the shell-by-shell device
+    loop of coherence.run_coherence_fill.  Same return layout as _run_fill."""
+    import torch
+
+    from .coherence import run_coherence_fill
+
+    t0 = time.perf_counter()
+    as_tensor = isinstance(image, torch.Tensor)
+    if isinstance(labels, torch.Tensor):
+        labels = labels.cpu().numpy()
+    lab_np = np.ascontiguousarray(labels, dtype=np.uint8)
+    H, W = lab_np.shape
+    d_lab = torch.from_numpy(lab_np).to(dev)
+    bad = (d_lab != READABLE) & (d_lab != grid.BYSTANDER) & (d_lab != INPAINT)
+    if bool(bad.any()):
+        grid.validate_labels(labels)
+        raise ValueError("label mask holds values outside {0, 128, 255}")
+    if as_tensor:
+        d_img = image.to(dev, torch.float64).contiguous().clone()
+    else:
+        d_img = torch.from_numpy(np.ascontiguousarray(image, dtype=np.float64)).to(dev)
+    u, r, enter, fillshell = run_coherence_fill(d_img, d_lab, params, tracked, order_log)
+    rep = FillReport()
+    rep.iterations = r["iterations"]
+    rep.filled = r["filled"]
+    rep.deadlock_fills = r["deadlock_fills"]
+    rep.unfillable = r["unfillable"]
+    rep.unfillable_count = r["unfillable_count"]
+    rep.rows = r["rows"]
+    out = u.cpu() if as_tensor else u.cpu().numpy()
+    fs = None
+    if order_log or rep.unfillable:
+        fs = fillshell.reshape(H, W).cpu().numpy()
+        if rep.unfillable:
+            fs = np.where((lab_np == INPAINT) & (fs < 0), -2, fs)
+    en = enter.reshape(H, W).cpu().numpy() if enter is not None else None
+    rep.wall_time_s = time.perf_counter() - t0
+    return out, rep, dict(enter=en, fillshell=fs)
+
+
 def inpaint(image, labels, guide=None, params: FillParams | None = None):
     """Fill all Inpaint pixels of ``labels`` in ``image`` (engine.py:379-408).
 
@@ -344,6 +387,6 @@ def inpaint(image, labels, guide=None, params: FillParams | None = None):
 
 
 def coherence_transport_mode(image, labels, **param_overrides):
-    """engine.py:411-414 -- the coherence g source is not on the B200 path yet."""
+    """engine.py:411-414: coherence transport (masked structure-tensor g, axis ball, onion)."""
     params = FillParams.coherence_transport(**param_overrides)
     return inpaint(image, labels, None, params)

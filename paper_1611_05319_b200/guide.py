@@ -5,10 +5,10 @@
 flattened polyline, the first nearest spline, and the Gaussian falloff
 g = dir * exp(-d^2 / (2 eta^2)), zero beyond 3 eta and outside D.
 
-Automatic spline detection (guide.py:55-283: measurement ring, Canny edge
-seeds, structure tensor, ray tracing) and the coherence-transport g source
-(guide.py:330-355) are outside the accelerated path (SURVEY.md section
-8f-1/8f-2) and raise NotImplementedError here.
+``coherence_directions`` (guide.py:330-355) runs the masked structure tensor
+on the device (gf_coherence_directions).  Automatic spline detection
+(guide.py:55-283: measurement ring, Canny edge seeds, ray tracing) is outside
+the accelerated path and raises NotImplementedError.
 """
 
 from __future__ import annotations
@@ -49,5 +49,25 @@ def detect_splines(image, labels, *args, **kwargs):
         "pass user splines to build_guide_field")
 
 
-def coherence_directions(*args, **kwargs):
-    raise NotImplementedError("coherence-transport directions are outside the accelerated path")
+def coherence_directions(image, readable, ix, iy, sigma: float = DEFAULT_SIGMA,
+                         rho: float = DEFAULT_RHO, lam: float = DEFAULT_LAMBDA) -> np.ndarray:
+    """Masked-tensor transport directions at the queried pixels: (F, 2) float64
+    (guide.py:330-355); 0 where the rho window holds no readable mass."""
+    import torch
+    from . import _native as N
+    from .coherence import coherence_directions_device
+
+    dev = N.require_cuda()
+    readable = np.asarray(readable, dtype=bool)
+    H, W = readable.shape
+    img = np.asarray(image, dtype=np.float64)
+    if img.ndim == 2:
+        img = img[:, :, None]
+    idx = np.asarray(iy, dtype=np.int64) * W + np.asarray(ix, dtype=np.int64)
+    if idx.size == 0:
+        return np.zeros((0, 2))
+    lab = np.where(readable, 0, INPAINT).astype(np.uint8)
+    g = coherence_directions_device(torch.from_numpy(np.ascontiguousarray(img)).to(dev),
+                                    torch.from_numpy(lab).to(dev),
+                                    torch.from_numpy(idx.reshape(-1)).to(dev), sigma, rho, lam)
+    return g.cpu().numpy()

@@ -214,3 +214,43 @@ def guide_cases(n=12, seed=303):
         eta = float(rng.choice([3.0, 1.5, 4.0]))
         out.append(dict(name=f"gf{k}", labels=lab, splines=raw, eta=eta))
     return out
+
+
+def edge_block():
+    """test_guide.py _vertical_edge_block analogue: a vertical colour edge with an
+    Inpaint block across it (coherence-direction fixtures)."""
+    H, W = 64, 64
+    img = np.zeros((H, W, 3))
+    img[:, 30:, :] = 1.0
+    img[:, :, 1] *= 0.5
+    lab = _block(H, W, 20, 40, 22, 42)
+    img[lab == INPAINT] = 0.0
+    return img, lab
+
+
+def coherence_scenes(n=10, seed=4242):
+    """g_source = modified_structure_tensor (engine.py:243-249): the coherence-transport
+    preset (engine.py:66-76: r=5, axis ball, onion) on an edge scene and random
+    islands, plus smart-order / rotated-ball variants (order then reads g)."""
+    rng = np.random.default_rng(seed)
+    out = []
+    img, lab = edge_block()
+    ct = dict(r=5, neighborhood="axis_ball", order="onion", g_source="modified_structure_tensor")
+    out.append(_case("ct_edge preset", img, lab, tracked=True, **ct))
+    out.append(_case("ct_edge preset untracked", img, lab, tracked=False, **ct))
+    out.append(_case("ct_edge smart rotated", img, lab, tracked=True, r=3, mu=50.0, order="smart",
+                     neighborhood="rotated_ball", g_source="modified_structure_tensor"))
+    for k in range(n):
+        lab = islands_labels(rng, 20, 56)
+        H, W = lab.shape
+        C = int(rng.integers(1, 5))
+        img = rng.uniform(size=(H, W, C))
+        img[lab == INPAINT] = 0.0
+        if k < n - 2:
+            p = dict(ct, r=int(rng.choice([3, 4, 5])), mu=float(rng.choice([10.0, 50.0, 100.0, math.inf])),
+                     sigma=float(rng.choice([1.0, 2.0])), rho=float(rng.choice([2.0, 4.0])))
+        else:
+            p = dict(r=3, mu=50.0, order="smart", neighborhood="rotated_ball",
+                     g_source="modified_structure_tensor")
+        out.append(_case(f"ct_rand{k}", img, lab, tracked=bool(k % 2 == 0), **p))
+    return out

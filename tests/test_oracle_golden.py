@@ -79,3 +79,29 @@ def test_known_answers():
 def test_disk_sizes():
     # test_grid.py:185-190 disk cardinalities 5/13/29
     assert [len(orc.disk_offsets(r)) for r in (1, 2, 3)] == [5, 13, 29]
+
+
+CT_CASES = cases.coherence_scenes()
+
+
+@pytest.mark.parametrize("idx", range(len(CT_CASES)))
+def test_coherence_fill_matches_reference(idx):
+    """g_source = modified_structure_tensor (engine.py:243-249, guide.py:330-355)."""
+    gold = np.load(os.path.join(GOLD, "coherence_golden.npz"))
+    case = CT_CASES[idx]
+    key = f"c{idx:03d}"
+    assert str(gold[f"{key}_name"]) == case["name"]
+    res = orc.fill(case["image"], case["labels"], case["guide"], orc.Params(**case["params"]),
+                   tracked=case["tracked"])
+    assert res["u"].tobytes() == gold[f"{key}_u"].tobytes()
+    assert np.array_equal(np.array(res["rows"], dtype=np.int64).reshape(-1, 5), gold[f"{key}_rows"])
+    assert np.array_equal(res["enter"], gold[f"{key}_enter"])
+    assert np.array_equal(res["fillshell"], gold[f"{key}_fillshell"])
+
+
+def test_coherence_directions_match_reference():
+    gold = np.load(os.path.join(GOLD, "coherence_golden.npz"))
+    img, lab = cases.edge_block()
+    for s, r in ((2.0, 4.0), (1.0, 2.0)):
+        g = orc.coherence_directions(img, lab == 0, gold["dirs_ii"], gold["dirs_jj"], sigma=s, rho=r)
+        assert g.tobytes() == gold[f"dirs_s{s:g}_r{r:g}"].tobytes()
