@@ -271,6 +271,19 @@ int gf_coherence_directions(int32_t height, int32_t width, int32_t channels,
                             const int64_t* idx, double sigma, double rho, double lam,
                             double* g, void* workspace, size_t workspace_bytes, void* stream);
 
+/*
+ * Tracked frontier update of one shell (tracker._update_arrays,
+ * tracker.py:59-79), for a frontier of n sorted flat indices with fill[n]
+ * (u8) after the filled pixels were relabelled Readable in labels.  Writes
+ * mark[p] = 1 for every candidate (a surviving frontier pixel, or an
+ * in-lattice / x-periodic Inpaint 8-neighbour of a filled one) and 2 for a
+ * candidate that passes _active_filter.  mark: device [H][W] u8, zeroed by
+ * the caller; the sorted nonzero positions are np.unique(pool).
+ */
+int gf_frontier_candidates(int32_t height, int32_t width, const uint8_t* labels,
+                           int32_t periodic_x, int32_t n, const int64_t* frontier,
+                           const uint8_t* fill, uint8_t* mark, void* stream);
+
 /* Thread-local message for the last failing call on this thread. */
 const char* gf_last_error(void);
 int gf_abi_version(void);

@@ -10,8 +10,9 @@ shell from the host, with every per-pixel step on the device:
   structure tensor of guide._tensor_field as separable passes over the frame);
 * weights, ghost gathers, masses and colours: gf_sample_points (the same ball
   evaluator the persistent shell kernel uses, engine.py:131-199);
-* ready predicate, deadlock guard, scatter/relabel and the tracked frontier
-  update (tracker.py:42-79): torch device ops on the index lists;
+* tracked frontier update (tracker.py:59-79): gf_frontier_candidates marks the
+  candidates and their active flag in one pass; ready predicate, deadlock
+  guard and scatter/relabel: torch device ops on the index lists;
 * unfillable fallback: gf_paint_unfillable.
 
 The host only reads the frontier size and "anything filled?" per shell (the
@@ -51,25 +52,6 @@ def coherence_directions_device(u, lab, idx, sigma=2.0, rho=4.0, lam=1e-5, works
 def _active(lab, periodic_x):
     """grid.active_boundary_mask (grid.py:59-76) on the device, flattened."""
     return boundary_device(lab, periodic_x)[0].reshape(-1)
-
-
-def _neighbours(idx, H, W, periodic_x):
-    """tracker._neighbor_indices (tracker.py:42-56): [(valid, flat)] in NEIGHBOR_OFFSETS order."""
-    import torch
-
-    jy = torch.div(idx, W, rounding_mode="floor")
-    ix = idx - jy * W
-    out = []
-    for di, dj in NEIGHBOR_OFFSETS:
-        ii = ix + di
-        jj = jy + dj
-        if periodic_x:
-            ii = torch.remainder(ii, W)
-            valid = (jj >= 0) & (jj < H)
-        else:
-            valid = (ii >= 0) & (ii < W) & (jj >= 0) & (jj < H)
-        out.append((valid, jj * W + torch.where(valid, ii, torch.zeros_like(ii))))
-    return out
 
 
 def _neighbor_mean(u, lab, p, H, W, periodic_x):
@@ -120,8 +102,9 @@ def run_coherence_fill(u, lab0, params, tracked=True, order_log=False):
     frontier = torch.nonzero(_active(lab, px)).reshape(-1)
     fillshell = torch.full((H * W,), -1, dtype=torch.int32, device=dev)
     enter = torch.full((H * W,), -1, dtype=torch.int32, device=dev) if order_log else None
-    ws = torch.empty(N.load().gf_coherence_workspace_bytes(H, W, C), dtype=torch.uint8,
-                     device=dev)
+    lib = N.load()
+    ws = torch.empty(lib.gf_coherence_workspace_bytes(H, W, C), dtype=torch.uint8, device=dev)
+    mark = torch.zeros(H * W, dtype=torch.uint8, device=dev)
     rep = dict(rows=[], iterations=0, filled=0, deadlock_fills=0, unfillable=False,
                unfillable_count=0)
     t0 = time.perf_counter()
@@ -173,20 +156,19 @@ def run_coherence_fill(u, lab0, params, tracked=True, order_log=False):
         fillshell[filled_idx] = it
         remaining -= n
         rep["filled"] += n
-        act = _active(lab, px)
         if tracked:
-            # tracker._update_arrays (tracker.py:59-79): survivors + INPAINT
+            # tracker._update_arrays (tracker.py:59-79): survivors + Inpaint
             # neighbours of the filled pixels, sorted dedup, active filter
-            pool = [frontier[~fill]]
-            for valid, nbr in _neighbours(filled_idx, H, W, px):
-                live = valid & (flat_l[torch.where(valid, nbr, torch.zeros_like(nbr))] == INPAINT)
-                pool.append(nbr[live])
-            cand = torch.unique(torch.cat(pool))
+            mark.zero_()
+            N.check(lib.gf_frontier_candidates(H, W, N.ptr(lab), 1 if px else 0, F,
+                                               N.ptr(frontier), N.ptr(fill.to(torch.uint8)),
+                                               N.ptr(mark), N.stream_ptr()))
+            cand = torch.nonzero(mark).reshape(-1)
             candidates = int(cand.numel())
-            new_frontier = cand[act[cand] != 0]
+            new_frontier = cand[mark[cand] == 2]
             threads = F
         else:
-            new_frontier = torch.nonzero(act).reshape(-1)
+            new_frontier = torch.nonzero(_active(lab, px)).reshape(-1)
             candidates = threads = W * H
         rep["rows"].append((it, F, candidates, threads, n))
         frontier = new_frontier

@@ -16,7 +16,8 @@
 //   tensor   v_c = S_c / (S_ind > 0 ? S_ind : 1); (gy, gx) = np.gradient(v_c)
 //            (central /2.0 inside, one-sided at the frame edges);
 //            J11 += gx*gx, J12 += gx*gy, J22 += gy*gy over channels; J *= ind
-//   smooth   the four planes [J11, J12, J22, ind] with rho
+//   smooth   the four planes [J11, J12, J22, ind] with rho -- only at the
+//            queried pixels (k_ct_query: column sums, then the row sum)
 //   query    a = J11s / safe_r ...; eigen split; coh = tanh((hi - lo) / lam);
 //            g = coh * (-sin phi, cos phi), g = 0 where mass_r <= 0.
 // The weights follow scipy's _gaussian_kernel1d: exp(-0.5 / s^2 * x^2) / sum,
@@ -58,16 +59,6 @@ int make_taps(double s, Taps& t) {
   return GF_OK;
 }
 
-__global__ void k_ct_seed(int64_t HW, int C, const double* __restrict__ u,
-                          const uint8_t* __restrict__ labels, double* __restrict__ P) {
-  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < HW;
-       p += (int64_t)gridDim.x * blockDim.x) {
-    const double ind = labels[p] == 0 ? 1.0 : 0.0;
-    P[p] = ind;
-    for (int c = 0; c < C; ++c) P[(int64_t)(c + 1) * HW + p] = ind * u[p * C + c];
-  }
-}
-
 // one separable pass along axis 0 (rows, stride W) or axis 1 (columns, stride 1)
 template <int AXIS>
 __global__ void k_ct_smooth(int H, int W, int nplanes, const Taps t, const double* __restrict__ in,
@@ -92,6 +83,30 @@ __global__ void k_ct_smooth(int H, int W, int nplanes, const Taps t, const doubl
   }
 }
 
+// seed fused into the sigma stage's axis-0 pass: plane 0 = ind, plane c+1 = ind*u_c
+__global__ void k_ct_seed_smooth0(int H, int W, int C, const Taps t, const double* __restrict__ u,
+                                  const uint8_t* __restrict__ labels, double* __restrict__ out) {
+  const int64_t HW = (int64_t)H * W;
+  const int64_t total = HW * (C + 1);
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < total;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const int f = (int)(q / HW);
+    const int64_t p = q - (int64_t)f * HW;
+    const int j = (int)(p / W);
+    auto seed = [&](int64_t pp) -> double {
+      const double ind = labels[pp] == 0 ? 1.0 : 0.0;
+      return f == 0 ? ind : ind * u[pp * C + (f - 1)];
+    };
+    double acc = seed(p) * t.w[0];
+    for (int k = t.R; k >= 1; --k) {
+      const double a = j - k >= 0 ? seed(p - (int64_t)k * W) : 0.0;
+      const double b = j + k < H ? seed(p + (int64_t)k * W) : 0.0;
+      acc += (a + b) * t.w[k];
+    }
+    out[q] = acc;
+  }
+}
+
 __device__ __forceinline__ double ct_v(const double* S, int64_t HW, int c, int64_t p) {
   const double m = S[p];
   return S[(int64_t)(c + 1) * HW + p] / (m > 0.0 ? m : 1.0);
@@ -106,7 +121,7 @@ __device__ __forceinline__ double ct_grad(const double* S, int64_t HW, int c, in
 }
 
 __global__ void k_ct_tensor(int H, int W, int C, const double* __restrict__ S,
-                            double* __restrict__ Q) {
+                            const uint8_t* __restrict__ labels, double* __restrict__ Q) {
   const int64_t HW = (int64_t)H * W;
   for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < HW;
        p += (int64_t)gridDim.x * blockDim.x) {
@@ -119,27 +134,55 @@ __global__ void k_ct_tensor(int H, int W, int C, const double* __restrict__ S,
       J12 += gx * gy;
       J22 += gy * gy;
     }
-    const double ind = Q[3 * HW + p];
+    const double ind = labels[p] == 0 ? 1.0 : 0.0;
+    Q[3 * HW + p] = ind;
     Q[p] = J11 * ind;
     Q[HW + p] = J12 * ind;
     Q[2 * HW + p] = J22 * ind;
   }
 }
 
-__global__ void k_ct_ind(int64_t HW, const uint8_t* __restrict__ labels, double* __restrict__ ind) {
-  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < HW;
-       p += (int64_t)gridDim.x * blockDim.x)
-    ind[p] = labels[p] == 0 ? 1.0 : 0.0;
+// The rho stage evaluated only at the queried pixels, in scipy's order: the
+// axis-0 pass T(j, i') for the 2R+1 columns i' of the window (0 outside the
+// frame: cval of the axis-1 pass), then the axis-1 pass over them.
+__device__ __forceinline__ double ct_col(const double* P, int H, int W, int j, int i,
+                                         const Taps& t) {
+  if (i < 0 || i >= W) return 0.0;
+  const double* x = P + (int64_t)j * W + i;
+  double acc = x[0] * t.w[0];
+  for (int k = t.R; k >= 1; --k) {
+    const double a = j - k >= 0 ? x[-(int64_t)k * W] : 0.0;
+    const double b = j + k < H ? x[(int64_t)k * W] : 0.0;
+    acc += (a + b) * t.w[k];
+  }
+  return acc;
 }
 
-__global__ void k_ct_query(int64_t HW, int n, const int64_t* __restrict__ idx,
-                           const double* __restrict__ Q, double lam, double* __restrict__ g) {
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= n) return;
-  const int64_t p = idx[k];
-  const double mass = Q[3 * HW + p];
+__device__ double ct_rho_at(const double* P, int H, int W, int j, int i, const Taps& t) {
+  double acc = ct_col(P, H, W, j, i, t) * t.w[0];
+  for (int k = t.R; k >= 1; --k)
+    acc += (ct_col(P, H, W, j, i - k, t) + ct_col(P, H, W, j, i + k, t)) * t.w[k];
+  return acc;
+}
+
+// one warp-quarter (8 lanes) per query: lane l < 4 evaluates plane l
+__global__ void k_ct_query(int H, int W, int n, const int64_t* __restrict__ idx,
+                           const double* __restrict__ Q, const Taps t, double lam,
+                           double* __restrict__ g) {
+  const int64_t HW = (int64_t)H * W;
+  const int gt = blockIdx.x * blockDim.x + threadIdx.x;
+  const int k = gt >> 2, lane = gt & 3;
+  const bool live = k < n;
+  const int64_t p = live ? idx[k] : 0;
+  const int j = (int)(p / W), i = (int)(p % W);
+  const double v = live ? ct_rho_at(Q + lane * HW, H, W, j, i, t) : 0.0;
+  const unsigned m = __activemask();
+  const int base = threadIdx.x & ~3;
+  const double J11 = __shfl_sync(m, v, base & 31), J12 = __shfl_sync(m, v, (base + 1) & 31);
+  const double J22 = __shfl_sync(m, v, (base + 2) & 31), mass = __shfl_sync(m, v, (base + 3) & 31);
+  if (!live || lane) return;
   const double safe = mass > 0.0 ? mass : 1.0;
-  const double a = Q[p] / safe, b = Q[HW + p] / safe, c = Q[2 * HW + p] / safe;
+  const double a = J11 / safe, b = J12 / safe, c = J22 / safe;
   const double mean = (a + c) / 2.0;
   const double h = (a - c) / 2.0;
   const double disc = sqrt(h * h + b * b);
@@ -150,6 +193,47 @@ __global__ void k_ct_query(int64_t HW, int n, const int64_t* __restrict__ idx,
   if (mass <= 0.0) gx = gy = 0.0;
   g[2 * k] = gx;
   g[2 * k + 1] = gy;
+}
+
+__device__ __forceinline__ bool ct_active(const uint8_t* lab, int H, int W, int periodic, int j,
+                                          int i) {
+  if (lab[(int64_t)j * W + i] != 255) return false;
+  for (int dj = -1; dj <= 1; ++dj)
+    for (int di = -1; di <= 1; ++di) {
+      if (!di && !dj) continue;
+      int ii = i + di;
+      const int jj = j + dj;
+      if (periodic) ii = (ii % W + W) % W;
+      if (ii >= 0 && ii < W && jj >= 0 && jj < H && lab[(int64_t)jj * W + ii] == 0) return true;
+    }
+  return false;
+}
+
+// tracker._update_arrays (tracker.py:59-79) as a byte map: survivors and the
+// Inpaint 8-neighbours of filled pixels are candidates (mark >= 1); mark = 2
+// when the candidate passes _active_filter (Inpaint with a Readable neighbour).
+// Every writer of a pixel stores the same value.
+__global__ void k_ct_mark(int H, int W, int periodic, const uint8_t* __restrict__ lab, int n,
+                          const int64_t* __restrict__ frontier, const uint8_t* __restrict__ fill,
+                          uint8_t* __restrict__ mark) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const int64_t p = frontier[k];
+  const int j = (int)(p / W), i = (int)(p % W);
+  if (!fill[k]) {
+    mark[p] = 1 + ct_active(lab, H, W, periodic, j, i);
+    return;
+  }
+  for (int dj = -1; dj <= 1; ++dj)
+    for (int di = -1; di <= 1; ++di) {
+      if (!di && !dj) continue;
+      int ii = i + di;
+      const int jj = j + dj;
+      if (periodic) ii = (ii % W + W) % W;
+      if (ii < 0 || ii >= W || jj < 0 || jj >= H) continue;
+      const int64_t q = (int64_t)jj * W + ii;
+      if (lab[q] == 255) mark[q] = 1 + ct_active(lab, H, W, periodic, jj, ii);
+    }
 }
 
 int grid_for(int64_t n, int block) {
@@ -191,19 +275,28 @@ extern "C" int gf_coherence_directions(int32_t height, int32_t width, int32_t ch
   double* A = static_cast<double*>(workspace);
   double* B = A + (size_t)planes * HW;
   const int bs = 256;
-  // sigma stage: A = seed, B = axis 0, A = axis 1 (S)
-  k_ct_seed<<<grid_for(HW, bs), bs, 0, s>>>(HW, channels, image, labels, A);
-  k_ct_smooth<0><<<grid_for(HW * (channels + 1), bs), bs, 0, s>>>(height, width, channels + 1, ts,
-                                                                   A, B);
+  // sigma stage (seed fused into axis 0): B = axis 0, A = axis 1 (S)
+  k_ct_seed_smooth0<<<grid_for(HW * (channels + 1), bs), bs, 0, s>>>(height, width, channels, ts,
+                                                                     image, labels, B);
   k_ct_smooth<1><<<grid_for(HW * (channels + 1), bs), bs, 0, s>>>(height, width, channels + 1, ts,
                                                                    B, A);
-  // tensor: B[3] = ind, B[0..2] = J * ind
-  k_ct_ind<<<grid_for(HW, bs), bs, 0, s>>>(HW, labels, B + 3 * HW);
-  k_ct_tensor<<<grid_for(HW, bs), bs, 0, s>>>(height, width, channels, A, B);
-  // rho stage over [J11, J12, J22, ind]: B -> A -> B
-  k_ct_smooth<0><<<grid_for(HW * 4, bs), bs, 0, s>>>(height, width, 4, tr, B, A);
-  k_ct_smooth<1><<<grid_for(HW * 4, bs), bs, 0, s>>>(height, width, 4, tr, A, B);
-  k_ct_query<<<(n + 127) / 128, 128, 0, s>>>(HW, n, idx, B, lam, g);
+  // tensor: B = [J11, J12, J22, ind] (J * ind)
+  k_ct_tensor<<<grid_for(HW, bs), bs, 0, s>>>(height, width, channels, A, labels, B);
+  // rho stage at the queries only
+  k_ct_query<<<(4 * n + 127) / 128, 128, 0, s>>>(height, width, n, idx, B, tr, lam, g);
+  cudaError_t e = cudaPeekAtLastError();
+  if (e != cudaSuccess) return set_error(GF_E_CUDA, cudaGetErrorString(e));
+  return GF_OK;
+}
+
+extern "C" int gf_frontier_candidates(int32_t height, int32_t width, const uint8_t* labels,
+                                      int32_t periodic_x, int32_t n, const int64_t* frontier,
+                                      const uint8_t* fill, uint8_t* mark, void* stream) {
+  if (height <= 0 || width <= 0 || n < 0) return set_error(GF_E_INVALID, "bad geometry");
+  if (n == 0) return GF_OK;
+  if (!labels || !frontier || !fill || !mark) return set_error(GF_E_INVALID, "NULL buffer");
+  k_ct_mark<<<(n + 127) / 128, 128, 0, static_cast<cudaStream_t>(stream)>>>(
+      height, width, periodic_x, labels, n, frontier, fill, mark);
   cudaError_t e = cudaPeekAtLastError();
   if (e != cudaSuccess) return set_error(GF_E_CUDA, cudaGetErrorString(e));
   return GF_OK;
