@@ -262,7 +262,8 @@ int gf_paint_unfillable(int32_t height, int32_t width, int32_t channels, int32_t
  * (device int64), eigen split as guide.eigen_2x2 (guide.py:123-136):
  * g[n][2] = tanh((hi - lo) / lam) * minor eigenvector, 0 where the rho
  * window holds no readable mass.  sigma / rho: Gaussian scales (truncate 2,
- * radius int(2 s + 0.5) <= 63).  H, W >= 2 (np.gradient needs 2 samples).
+ * radius int(2 s + 0.5) <= 63).  2 <= H <= 65535, W >= 2 (np.gradient needs
+ * 2 samples).
  * workspace: gf_coherence_workspace_bytes(H, W, C) device bytes.
  */
 size_t gf_coherence_workspace_bytes(int32_t height, int32_t width, int32_t channels);

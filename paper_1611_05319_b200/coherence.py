@@ -135,7 +135,8 @@ def run_coherence_fill(u, lab0, params, tracked=True, order_log=False):
             else:
                 ready = (gnorm > params.c2) & (conf > params.c)
         fill = ready & (rw > 0.0)
-        if not bool(fill.any()):
+        filled_idx = frontier[fill]  # the shell's one synchronisation before the scatter
+        if filled_idx.numel() == 0:
             # deadlock guard (engine.py:334-348): first maximal confidence, NaN first
             c_h = conf.cpu().numpy()
             k = int(np.argmax(c_h))
@@ -149,7 +150,7 @@ def run_coherence_fill(u, lab0, params, tracked=True, order_log=False):
                 vals[k] = fb
                 fill[k] = True
             rep["deadlock_fills"] += 1
-        filled_idx = frontier[fill]
+            filled_idx = frontier[fill]
         n = int(filled_idx.numel())
         flat_u[filled_idx] = vals[fill]
         flat_l[filled_idx] = READABLE
@@ -163,9 +164,8 @@ def run_coherence_fill(u, lab0, params, tracked=True, order_log=False):
             N.check(lib.gf_frontier_candidates(H, W, N.ptr(lab), 1 if px else 0, F,
                                                N.ptr(frontier), N.ptr(fill.to(torch.uint8)),
                                                N.ptr(mark), N.stream_ptr()))
-            cand = torch.nonzero(mark).reshape(-1)
-            candidates = int(cand.numel())
-            new_frontier = cand[mark[cand] == 2]
+            candidates = (mark != 0).sum()  # device scalar, read after the loop
+            new_frontier = torch.nonzero(mark == 2).reshape(-1)
             threads = F
         else:
             new_frontier = torch.nonzero(_active(lab, px)).reshape(-1)
@@ -174,6 +174,7 @@ def run_coherence_fill(u, lab0, params, tracked=True, order_log=False):
         frontier = new_frontier
         it += 1
     rep["iterations"] = it
+    rep["rows"] = [(k, F, int(c), t, n) for (k, F, c, t, n) in rep["rows"]]
     if rep["unfillable"]:
         from .engine import _paint_unfillable_device
 

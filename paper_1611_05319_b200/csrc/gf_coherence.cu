@@ -59,81 +59,107 @@ int make_taps(double s, Taps& t) {
   return GF_OK;
 }
 
-// one separable pass along axis 0 (rows, stride W) or axis 1 (columns, stride 1)
-template <int AXIS>
-__global__ void k_ct_smooth(int H, int W, int nplanes, const Taps t, const double* __restrict__ in,
-                            double* __restrict__ out) {
-  const int64_t HW = (int64_t)H * W;
-  const int64_t total = HW * nplanes;
-  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < total;
-       q += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t p = q % HW;
-    const int j = (int)(p / W), i = (int)(p % W);
-    const int pos = AXIS == 0 ? j : i;
-    const int len = AXIS == 0 ? H : W;
-    const int64_t stride = AXIS == 0 ? W : 1;
-    const double* x = in + q;
-    double acc = x[0] * t.w[0];
-    for (int k = t.R; k >= 1; --k) {
-      const double a = pos - k >= 0 ? x[-k * stride] : 0.0;
-      const double b = pos + k < len ? x[k * stride] : 0.0;
-      acc += (a + b) * t.w[k];
-    }
-    out[q] = acc;
+// Grids are 2-D: x over columns (128 per block), y over rows -- no 64-bit
+// division per pixel.
+
+// axis-1 pass of one plane row (blockIdx.z = plane)
+__global__ void k_ct_smooth1(int H, int W, const Taps t, const double* __restrict__ in,
+                             double* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= W) return;
+  const int64_t row = ((int64_t)blockIdx.z * H + blockIdx.y) * W;
+  const double* x = in + row + i;
+  double acc = x[0] * t.w[0];
+  for (int k = t.R; k >= 1; --k) {
+    const double a = i - k >= 0 ? x[-k] : 0.0;
+    const double b = i + k < W ? x[k] : 0.0;
+    acc += (a + b) * t.w[k];
   }
+  out[row + i] = acc;
 }
 
-// seed fused into the sigma stage's axis-0 pass: plane 0 = ind, plane c+1 = ind*u_c
-__global__ void k_ct_seed_smooth0(int H, int W, int C, const Taps t, const double* __restrict__ u,
+// seed fused into the sigma stage's axis-0 pass, all C + 1 planes per thread:
+// plane 0 = ind, plane c+1 = ind*u_c
+template <int C>
+__global__ void k_ct_seed_smooth0(int H, int W, const Taps t, const double* __restrict__ u,
                                   const uint8_t* __restrict__ labels, double* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= W) return;
+  const int j = blockIdx.y;
   const int64_t HW = (int64_t)H * W;
-  const int64_t total = HW * (C + 1);
-  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < total;
-       q += (int64_t)gridDim.x * blockDim.x) {
-    const int f = (int)(q / HW);
-    const int64_t p = q - (int64_t)f * HW;
-    const int j = (int)(p / W);
-    auto seed = [&](int64_t pp) -> double {
-      const double ind = labels[pp] == 0 ? 1.0 : 0.0;
-      return f == 0 ? ind : ind * u[pp * C + (f - 1)];
-    };
-    double acc = seed(p) * t.w[0];
-    for (int k = t.R; k >= 1; --k) {
-      const double a = j - k >= 0 ? seed(p - (int64_t)k * W) : 0.0;
-      const double b = j + k < H ? seed(p + (int64_t)k * W) : 0.0;
-      acc += (a + b) * t.w[k];
-    }
-    out[q] = acc;
+  double acc[C + 1];
+  auto tap = [&](int jj, double (&v)[C + 1]) {
+    const int64_t pp = (int64_t)jj * W + i;
+    const double ind = labels[pp] == 0 ? 1.0 : 0.0;
+    v[0] = ind;
+#pragma unroll
+    for (int c = 0; c < C; ++c) v[c + 1] = ind * u[pp * C + c];
+  };
+  double v0[C + 1];
+  tap(j, v0);
+#pragma unroll
+  for (int f = 0; f <= C; ++f) acc[f] = v0[f] * t.w[0];
+  for (int k = t.R; k >= 1; --k) {
+    double a[C + 1], b[C + 1];
+    if (j - k >= 0) tap(j - k, a);
+    else
+#pragma unroll
+      for (int f = 0; f <= C; ++f) a[f] = 0.0;
+    if (j + k < H) tap(j + k, b);
+    else
+#pragma unroll
+      for (int f = 0; f <= C; ++f) b[f] = 0.0;
+#pragma unroll
+    for (int f = 0; f <= C; ++f) acc[f] += (a[f] + b[f]) * t.w[k];
   }
+  const int64_t p = (int64_t)j * W + i;
+#pragma unroll
+  for (int f = 0; f <= C; ++f) out[f * HW + p] = acc[f];
 }
 
-__device__ __forceinline__ double ct_v(const double* S, int64_t HW, int c, int64_t p) {
-  const double m = S[p];
-  return S[(int64_t)(c + 1) * HW + p] / (m > 0.0 ? m : 1.0);
-}
+constexpr int kTensorRows = 8;
 
-// np.gradient along one axis at position pos of len (len >= 2)
-__device__ __forceinline__ double ct_grad(const double* S, int64_t HW, int c, int64_t p, int pos,
-                                          int len, int64_t stride) {
-  if (pos == 0) return (ct_v(S, HW, c, p + stride) - ct_v(S, HW, c, p)) / 1.0;
-  if (pos == len - 1) return (ct_v(S, HW, c, p) - ct_v(S, HW, c, p - stride)) / 1.0;
-  return (ct_v(S, HW, c, p + stride) - ct_v(S, HW, c, p - stride)) / 2.0;
-}
-
-__global__ void k_ct_tensor(int H, int W, int C, const double* __restrict__ S,
+// v_c = S_c / (S_ind > 0 ? S_ind : 1) once per pixel into a shared tile of
+// (kTensorRows + 2) x (128 + 2) pixels, then np.gradient (central /2.0 inside,
+// one-sided /1.0 at the frame edges) and J = sum_c (gx gx, gx gy, gy gy) * ind.
+template <int C>
+__global__ void k_ct_tensor(int H, int W, const double* __restrict__ S,
                             const uint8_t* __restrict__ labels, double* __restrict__ Q) {
+  __shared__ double v[kTensorRows + 2][130][C];
   const int64_t HW = (int64_t)H * W;
-  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < HW;
-       p += (int64_t)gridDim.x * blockDim.x) {
-    const int j = (int)(p / W), i = (int)(p % W);
+  const int i0 = blockIdx.x * 128, j0 = blockIdx.y * kTensorRows;
+  for (int e = threadIdx.x; e < (kTensorRows + 2) * 130; e += blockDim.x) {
+    const int r = e / 130, cc = e - r * 130;
+    const int j = j0 + r - 1, i = i0 + cc - 1;
+    if (j < 0 || j >= H || i < 0 || i >= W) continue;
+    const int64_t p = (int64_t)j * W + i;
+    const double m = S[p];
+    const double safe = m > 0.0 ? m : 1.0;
+#pragma unroll
+    for (int c = 0; c < C; ++c) v[r][cc][c] = S[(int64_t)(c + 1) * HW + p] / safe;
+  }
+  __syncthreads();
+  const int i = i0 + threadIdx.x;
+  if (i >= W) return;
+  const int cc = threadIdx.x + 1;
+  for (int r = 1; r <= kTensorRows; ++r) {
+    const int j = j0 + r - 1;
+    if (j >= H) break;
     double J11 = 0.0, J12 = 0.0, J22 = 0.0;
+#pragma unroll
     for (int c = 0; c < C; ++c) {
-      const double gy = ct_grad(S, HW, c, p, j, H, W);
-      const double gx = ct_grad(S, HW, c, p, i, W, 1);
+      double gy, gx;
+      if (j == 0) gy = (v[r + 1][cc][c] - v[r][cc][c]) / 1.0;
+      else if (j == H - 1) gy = (v[r][cc][c] - v[r - 1][cc][c]) / 1.0;
+      else gy = (v[r + 1][cc][c] - v[r - 1][cc][c]) / 2.0;
+      if (i == 0) gx = (v[r][cc + 1][c] - v[r][cc][c]) / 1.0;
+      else if (i == W - 1) gx = (v[r][cc][c] - v[r][cc - 1][c]) / 1.0;
+      else gx = (v[r][cc + 1][c] - v[r][cc - 1][c]) / 2.0;
       J11 += gx * gx;
       J12 += gx * gy;
       J22 += gy * gy;
     }
+    const int64_t p = (int64_t)j * W + i;
     const double ind = labels[p] == 0 ? 1.0 : 0.0;
     Q[3 * HW + p] = ind;
     Q[p] = J11 * ind;
@@ -158,29 +184,36 @@ __device__ __forceinline__ double ct_col(const double* P, int H, int W, int j, i
   return acc;
 }
 
-__device__ double ct_rho_at(const double* P, int H, int W, int j, int i, const Taps& t) {
-  double acc = ct_col(P, H, W, j, i, t) * t.w[0];
-  for (int k = t.R; k >= 1; --k)
-    acc += (ct_col(P, H, W, j, i - k, t) + ct_col(P, H, W, j, i + k, t)) * t.w[k];
-  return acc;
-}
+constexpr int kQueryWarps = 4;
 
-// one warp-quarter (8 lanes) per query: lane l < 4 evaluates plane l
+// one warp per query: the 4 x (2R+1) column sums are spread over the lanes
+// and parked in shared memory, lanes 0..3 then run the ordered row sums
 __global__ void k_ct_query(int H, int W, int n, const int64_t* __restrict__ idx,
                            const double* __restrict__ Q, const Taps t, double lam,
                            double* __restrict__ g) {
+  __shared__ double cols[kQueryWarps][4][2 * kMaxTaps + 1];
+  __shared__ double red[kQueryWarps][4];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int k = blockIdx.x * kQueryWarps + warp;
+  if (k >= n) return;  // whole warp
   const int64_t HW = (int64_t)H * W;
-  const int gt = blockIdx.x * blockDim.x + threadIdx.x;
-  const int k = gt >> 2, lane = gt & 3;
-  const bool live = k < n;
-  const int64_t p = live ? idx[k] : 0;
+  const int64_t p = idx[k];
   const int j = (int)(p / W), i = (int)(p % W);
-  const double v = live ? ct_rho_at(Q + lane * HW, H, W, j, i, t) : 0.0;
-  const unsigned m = __activemask();
-  const int base = threadIdx.x & ~3;
-  const double J11 = __shfl_sync(m, v, base & 31), J12 = __shfl_sync(m, v, (base + 1) & 31);
-  const double J22 = __shfl_sync(m, v, (base + 2) & 31), mass = __shfl_sync(m, v, (base + 3) & 31);
-  if (!live || lane) return;
+  const int ncol = 2 * t.R + 1;
+  for (int e = lane; e < 4 * ncol; e += 32) {
+    const int plane = e / ncol, c = e - plane * ncol;
+    cols[warp][plane][c] = ct_col(Q + plane * HW, H, W, j, i + c - t.R, t);
+  }
+  __syncwarp();
+  if (lane < 4) {
+    const double* T = cols[warp][lane] + t.R;
+    double acc = T[0] * t.w[0];
+    for (int d = t.R; d >= 1; --d) acc += (T[-d] + T[d]) * t.w[d];
+    red[warp][lane] = acc;
+  }
+  __syncwarp();
+  if (lane) return;
+  const double J11 = red[warp][0], J12 = red[warp][1], J22 = red[warp][2], mass = red[warp][3];
   const double safe = mass > 0.0 ? mass : 1.0;
   const double a = J11 / safe, b = J12 / safe, c = J22 / safe;
   const double mean = (a + c) / 2.0;
@@ -236,11 +269,6 @@ __global__ void k_ct_mark(int H, int W, int periodic, const uint8_t* __restrict_
     }
 }
 
-int grid_for(int64_t n, int block) {
-  int64_t b = (n + block - 1) / block;
-  const int64_t cap = 148LL * 16;
-  return (int)(b < 1 ? 1 : (b > cap ? cap : b));
-}
 
 }  // namespace
 
@@ -259,7 +287,7 @@ extern "C" int gf_coherence_directions(int32_t height, int32_t width, int32_t ch
                                        const int64_t* idx, double sigma, double rho, double lam,
                                        double* g, void* workspace, size_t workspace_bytes,
                                        void* stream) {
-  if (height < 2 || width < 2 || channels < 1 || channels > 4 || n < 0)
+  if (height < 2 || width < 2 || height > 65535 || channels < 1 || channels > 4 || n < 0)
     return set_error(GF_E_INVALID, "bad geometry");
   if (!image || !labels || (n > 0 && (!idx || !g)) || !workspace)
     return set_error(GF_E_INVALID, "NULL buffer");
@@ -274,16 +302,27 @@ extern "C" int gf_coherence_directions(int32_t height, int32_t width, int32_t ch
   const int planes = channels + 1 > 4 ? channels + 1 : 4;
   double* A = static_cast<double*>(workspace);
   double* B = A + (size_t)planes * HW;
-  const int bs = 256;
   // sigma stage (seed fused into axis 0): B = axis 0, A = axis 1 (S)
-  k_ct_seed_smooth0<<<grid_for(HW * (channels + 1), bs), bs, 0, s>>>(height, width, channels, ts,
-                                                                     image, labels, B);
-  k_ct_smooth<1><<<grid_for(HW * (channels + 1), bs), bs, 0, s>>>(height, width, channels + 1, ts,
-                                                                   B, A);
+  const dim3 blk(128);
+  const dim3 rows((width + 127) / 128, height, 1);
+  switch (channels) {
+    case 1: k_ct_seed_smooth0<1><<<rows, blk, 0, s>>>(height, width, ts, image, labels, B); break;
+    case 2: k_ct_seed_smooth0<2><<<rows, blk, 0, s>>>(height, width, ts, image, labels, B); break;
+    case 3: k_ct_seed_smooth0<3><<<rows, blk, 0, s>>>(height, width, ts, image, labels, B); break;
+    default: k_ct_seed_smooth0<4><<<rows, blk, 0, s>>>(height, width, ts, image, labels, B); break;
+  }
+  k_ct_smooth1<<<dim3(rows.x, height, channels + 1), blk, 0, s>>>(height, width, ts, B, A);
   // tensor: B = [J11, J12, J22, ind] (J * ind)
-  k_ct_tensor<<<grid_for(HW, bs), bs, 0, s>>>(height, width, channels, A, labels, B);
+  const dim3 tiles((width + 127) / 128, (height + kTensorRows - 1) / kTensorRows, 1);
+  switch (channels) {
+    case 1: k_ct_tensor<1><<<tiles, blk, 0, s>>>(height, width, A, labels, B); break;
+    case 2: k_ct_tensor<2><<<tiles, blk, 0, s>>>(height, width, A, labels, B); break;
+    case 3: k_ct_tensor<3><<<tiles, blk, 0, s>>>(height, width, A, labels, B); break;
+    default: k_ct_tensor<4><<<tiles, blk, 0, s>>>(height, width, A, labels, B); break;
+  }
   // rho stage at the queries only
-  k_ct_query<<<(4 * n + 127) / 128, 128, 0, s>>>(height, width, n, idx, B, tr, lam, g);
+  k_ct_query<<<(n + kQueryWarps - 1) / kQueryWarps, 32 * kQueryWarps, 0, s>>>(height, width, n,
+                                                                            idx, B, tr, lam, g);
   cudaError_t e = cudaPeekAtLastError();
   if (e != cudaSuccess) return set_error(GF_E_CUDA, cudaGetErrorString(e));
   return GF_OK;
