@@ -83,3 +83,30 @@ def test_cli_inpaint_matches_oracle(tmp_path):
     assert np.abs(out - fileio.to_uint8(ref["u"]) / 255.0).max() <= 1.0 / 255 + 1e-12
     rep = json.loads((tmp_path / "rep.json").read_text())
     assert rep["iterations"] == ref["iterations"] and rep["tracked"] is True
+
+
+@pytest.mark.gpu
+def test_cli_coherence_preset_matches_oracle(tmp_path):
+    """`guidefill inpaint --preset coherence_transport` needs no splines (cli.py:97-106):
+    g comes from the masked structure tensor on the device."""
+    from oracle import guidefill_oracle as orc
+    from paper_1611_05319_b200 import scenes
+
+    sc = scenes.small_scene(64, 96, band=6, gx=3, gy=2, n_spl=2, seed=5)
+    img = fileio.to_uint8(sc.image).astype(np.float64) / 255.0
+    fileio.save_image(tmp_path / "in.png", img)
+    fileio.save_labels(tmp_path / "m.pgm", sc.labels)
+    r = CliRunner().invoke(main, ["inpaint", "--image", str(tmp_path / "in.png"),
+                                  "--mask", str(tmp_path / "m.pgm"),
+                                  "--preset", "coherence_transport",
+                                  "--out", str(tmp_path / "out.png"),
+                                  "--report", str(tmp_path / "rep.json")])
+    assert r.exit_code == 0, r.output
+    ref = orc.fill(img, sc.labels, None, orc.Params.of(FillParams.coherence_transport()),
+                   tracked=True)
+    out = fileio.load_image(tmp_path / "out.png")
+    assert np.abs(out - fileio.to_uint8(ref["u"]) / 255.0).max() <= 1.0 / 255 + 1e-12
+    rep = json.loads((tmp_path / "rep.json").read_text())
+    assert rep["iterations"] == ref["iterations"]
+    assert rep["frontier_sizes"] == [x[1] for x in ref["rows"]]
+    assert rep["filled_per_iteration"] == [x[4] for x in ref["rows"]]
