@@ -285,6 +285,21 @@ int gf_frontier_candidates(int32_t height, int32_t width, const uint8_t* labels,
                            int32_t periodic_x, int32_t n, const int64_t* frontier,
                            const uint8_t* fill, uint8_t* mark, void* stream);
 
+/*
+ * Decision and scatter of one shell (engine.py:317-356), after
+ * gf_sample_points at the n frontier pixels: conf = rw / tw; ready_mode 0 =
+ * onion (all ready), 1 = conf > c, 2 = (hypot(g) > c2) & (conf > c) (the
+ * data-term order while its latch is live; g: device [n][2]);
+ * fill[k] = ready & (rw > 0).  Filled pixels get image[p] = vals[k] (float64
+ * [H][W][C]), labels[p] = 0 (Readable) and fillshell[p] = shell; *count
+ * (device int32, zeroed by the caller) += the number filled.  A shell with
+ * no fill is the caller's deadlock guard (engine.py:334-348).
+ */
+int gf_commit_shell(int32_t channels, int32_t n, const int64_t* frontier, const double* rw,
+                    const double* tw, const double* vals, const double* g, int32_t ready_mode,
+                    double c, double c2, int32_t shell, double* image, uint8_t* labels,
+                    int32_t* fillshell, uint8_t* fill, int32_t* count, void* stream);
+
 /* Thread-local message for the last failing call on this thread. */
 const char* gf_last_error(void);
 int gf_abi_version(void);

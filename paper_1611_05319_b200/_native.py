@@ -31,7 +31,7 @@ EXPORTS = (
     "gf_bilinear_gather", "gf_boundary_masks", "gf_output_delta", "gf_upload_mirrored",
     "gf_paint_unfillable_workspace_bytes", "gf_paint_unfillable",
     "gf_coherence_workspace_bytes", "gf_coherence_directions", "gf_frontier_candidates",
-    "gf_last_error",
+    "gf_commit_shell", "gf_last_error",
     "gf_abi_version", "gf_host_exp", "gf_host_hypot", "gf_host_pairwise_sum",
 )
 
@@ -148,6 +148,10 @@ def load(required: bool = True):
     lib.gf_frontier_candidates.restype = ctypes.c_int
     lib.gf_frontier_candidates.argtypes = [ctypes.c_int32, ctypes.c_int32, P, ctypes.c_int32,
                                            ctypes.c_int32, P, P, P, P]
+    lib.gf_commit_shell.restype = ctypes.c_int
+    lib.gf_commit_shell.argtypes = [ctypes.c_int32, ctypes.c_int32, P, P, P, P, P, ctypes.c_int32,
+                                    ctypes.c_double, ctypes.c_double, ctypes.c_int32, P, P, P, P,
+                                    P, P]
     lib.gf_paint_unfillable.restype = ctypes.c_int
     lib.gf_paint_unfillable.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
                                         ctypes.c_int32, P, P, P, P, ctypes.c_size_t, P, P]

@@ -10,9 +10,10 @@ shell from the host, with every per-pixel step on the device:
   structure tensor of guide._tensor_field as separable passes over the frame);
 * weights, ghost gathers, masses and colours: gf_sample_points (the same ball
   evaluator the persistent shell kernel uses, engine.py:131-199);
+* ready predicate, fill mask, scatter and relabel (engine.py:317-356):
+  gf_commit_shell; the deadlock guard (one pixel) with torch device ops;
 * tracked frontier update (tracker.py:59-79): gf_frontier_candidates marks the
-  candidates and their active flag in one pass; ready predicate, deadlock
-  guard and scatter/relabel: torch device ops on the index lists;
+  candidates and their active flag in one pass;
 * unfillable fallback: gf_paint_unfillable.
 
 The host only reads the frontier size and "anything filled?" per shell (the
@@ -105,6 +106,7 @@ def run_coherence_fill(u, lab0, params, tracked=True, order_log=False):
     lib = N.load()
     ws = torch.empty(lib.gf_coherence_workspace_bytes(H, W, C), dtype=torch.uint8, device=dev)
     mark = torch.zeros(H * W, dtype=torch.uint8, device=dev)
+    count = torch.zeros(1, dtype=torch.int32, device=dev)
     rep = dict(rows=[], iterations=0, filled=0, deadlock_fills=0, unfillable=False,
                unfillable_count=0)
     t0 = time.perf_counter()
@@ -122,39 +124,40 @@ def run_coherence_fill(u, lab0, params, tracked=True, order_log=False):
         fy = torch.div(frontier, W, rounding_mode="floor")
         pts = torch.stack([(frontier - fy * W).to(torch.float64), fy.to(torch.float64)], 1)
         rw, tw, vals = sample_points_device(u, lab, pts.contiguous(), g, params)
-        conf = rw / tw
         if params.order == "onion":
-            ready = torch.ones(F, dtype=torch.bool, device=dev)
+            mode = 0
         elif params.order == "smart" or not data_term_live:
-            ready = conf > params.c
+            mode = 1
         else:
-            gnorm = torch.hypot(g[:, 0], g[:, 1])
-            if not bool((gnorm > 0.0).any()):
+            mode = 2
+            if not bool((torch.hypot(g[:, 0], g[:, 1]) > 0.0).any()):
                 data_term_live = False
-                ready = conf > params.c
-            else:
-                ready = (gnorm > params.c2) & (conf > params.c)
-        fill = ready & (rw > 0.0)
-        filled_idx = frontier[fill]  # the shell's one synchronisation before the scatter
-        if filled_idx.numel() == 0:
+                mode = 1
+        count.zero_()
+        fill = torch.empty(F, dtype=torch.uint8, device=dev)
+        N.check(lib.gf_commit_shell(C, F, N.ptr(frontier), N.ptr(rw), N.ptr(tw), N.ptr(vals),
+                                    N.ptr(g), mode, float(params.c), float(params.c2), it,
+                                    N.ptr(u), N.ptr(lab), N.ptr(fillshell), N.ptr(fill),
+                                    N.ptr(count), N.stream_ptr()))
+        n = int(count.item())  # the shell's one synchronisation before the update
+        if n == 0:
             # deadlock guard (engine.py:334-348): first maximal confidence, NaN first
-            c_h = conf.cpu().numpy()
+            c_h = (rw / tw).cpu().numpy()
             k = int(np.argmax(c_h))
             if float(rw[k]) > 0.0:
-                fill[k] = True
+                val = vals[k]
             else:
-                fb = _neighbor_mean(u, lab, int(frontier[k]), H, W, px)
-                if fb is None:
+                val = _neighbor_mean(u, lab, int(frontier[k]), H, W, px)
+                if val is None:
                     rep["unfillable"] = True
                     break
-                vals[k] = fb
-                fill[k] = True
+            p_k = frontier[k]
+            flat_u[p_k] = val
+            flat_l[p_k] = READABLE
+            fillshell[p_k] = it
+            fill[k] = 1
+            n = 1
             rep["deadlock_fills"] += 1
-            filled_idx = frontier[fill]
-        n = int(filled_idx.numel())
-        flat_u[filled_idx] = vals[fill]
-        flat_l[filled_idx] = READABLE
-        fillshell[filled_idx] = it
         remaining -= n
         rep["filled"] += n
         if tracked:
@@ -162,7 +165,7 @@ def run_coherence_fill(u, lab0, params, tracked=True, order_log=False):
             # neighbours of the filled pixels, sorted dedup, active filter
             mark.zero_()
             N.check(lib.gf_frontier_candidates(H, W, N.ptr(lab), 1 if px else 0, F,
-                                               N.ptr(frontier), N.ptr(fill.to(torch.uint8)),
+                                               N.ptr(frontier), N.ptr(fill),
                                                N.ptr(mark), N.stream_ptr()))
             candidates = (mark != 0).sum()  # device scalar, read after the loop
             new_frontier = torch.nonzero(mark == 2).reshape(-1)

@@ -270,6 +270,35 @@ __global__ void k_ct_mark(int H, int W, int periodic, const uint8_t* __restrict_
 }
 
 
+// engine.py:317-356 for one shell: ready predicate (onion / conf > c /
+// (|g| > c2) & (conf > c)), fill = ready & (rw > 0), then the scatter and
+// relabel of the filled pixels.
+__global__ void k_ct_commit(int C, int n, const int64_t* __restrict__ frontier,
+                            const double* __restrict__ rw, const double* __restrict__ tw,
+                            const double* __restrict__ vals, const double* __restrict__ g,
+                            int ready_mode, double c, double c2, int shell, double* __restrict__ u,
+                            uint8_t* __restrict__ lab, int32_t* __restrict__ fillshell,
+                            uint8_t* __restrict__ fill, int32_t* __restrict__ count) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  bool f = false;
+  if (k < n) {
+    const double conf = rw[k] / tw[k];
+    bool ready = true;
+    if (ready_mode == 1) ready = conf > c;
+    else if (ready_mode == 2) ready = hypot_np(g[2 * k], g[2 * k + 1]) > c2 && conf > c;
+    f = ready && rw[k] > 0.0;
+    fill[k] = f ? 1 : 0;
+    if (f) {
+      const int64_t p = frontier[k];
+      for (int ch = 0; ch < C; ++ch) u[p * C + ch] = vals[(int64_t)k * C + ch];
+      lab[p] = 0;
+      fillshell[p] = shell;
+    }
+  }
+  const unsigned b = __ballot_sync(0xffffffffu, f);
+  if ((threadIdx.x & 31) == 0 && b) atomicAdd(count, __popc(b));
+}
+
 }  // namespace
 
 }  // namespace gf
@@ -336,6 +365,25 @@ extern "C" int gf_frontier_candidates(int32_t height, int32_t width, const uint8
   if (!labels || !frontier || !fill || !mark) return set_error(GF_E_INVALID, "NULL buffer");
   k_ct_mark<<<(n + 127) / 128, 128, 0, static_cast<cudaStream_t>(stream)>>>(
       height, width, periodic_x, labels, n, frontier, fill, mark);
+  cudaError_t e = cudaPeekAtLastError();
+  if (e != cudaSuccess) return set_error(GF_E_CUDA, cudaGetErrorString(e));
+  return GF_OK;
+}
+
+extern "C" int gf_commit_shell(int32_t channels, int32_t n, const int64_t* frontier,
+                               const double* rw, const double* tw, const double* vals,
+                               const double* g, int32_t ready_mode, double c, double c2,
+                               int32_t shell, double* image, uint8_t* labels, int32_t* fillshell,
+                               uint8_t* fill, int32_t* count, void* stream) {
+  if (channels < 1 || channels > 4 || n < 0 || ready_mode < 0 || ready_mode > 2)
+    return set_error(GF_E_INVALID, "bad arguments");
+  if (n == 0) return GF_OK;
+  if (!frontier || !rw || !tw || !vals || !image || !labels || !fillshell || !fill || !count ||
+      (ready_mode == 2 && !g))
+    return set_error(GF_E_INVALID, "NULL buffer");
+  k_ct_commit<<<(n + 127) / 128, 128, 0, static_cast<cudaStream_t>(stream)>>>(
+      channels, n, frontier, rw, tw, vals, g, ready_mode, c, c2, shell, image, labels, fillshell,
+      fill, count);
   cudaError_t e = cudaPeekAtLastError();
   if (e != cudaSuccess) return set_error(GF_E_CUDA, cudaGetErrorString(e));
   return GF_OK;
