@@ -60,11 +60,29 @@ int make_taps(double s, Taps& t) {
 }
 
 // Grids are 2-D: x over columns (128 per block), y over rows -- no 64-bit
-// division per pixel.
+// division per pixel.  Work is limited to the 128 x kTileRows tiles that a
+// query can reach (k_ct_tiles): a query reads J within R_rho, J reads S
+// within 1, S reads the axis-0 output within R_sigma columns -- every value
+// outside the reach box R_rho + R_sigma + 1 is never read.
+constexpr int kTileRows = 8;
+
+__global__ void k_ct_tiles(int H, int W, int n, const int64_t* __restrict__ idx, int D,
+                           int tiles_x, uint8_t* __restrict__ tiles) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const int64_t p = idx[k];
+  const int j = (int)(p / W), i = (int)(p % W);
+  const int ty0 = max(0, j - D) / kTileRows, ty1 = min(H - 1, j + D) / kTileRows;
+  const int tx0 = max(0, i - D) / 128, tx1 = min(W - 1, i + D) / 128;
+  for (int ty = ty0; ty <= ty1; ++ty)
+    for (int tx = tx0; tx <= tx1; ++tx) tiles[ty * tiles_x + tx] = 1;
+}
 
 // axis-1 pass of one plane row (blockIdx.z = plane)
 __global__ void k_ct_smooth1(int H, int W, const Taps t, const double* __restrict__ in,
-                             double* __restrict__ out) {
+                             double* __restrict__ out, const uint8_t* __restrict__ tiles,
+                             int tiles_x) {
+  if (!tiles[(blockIdx.y / kTileRows) * tiles_x + blockIdx.x]) return;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= W) return;
   const int64_t row = ((int64_t)blockIdx.z * H + blockIdx.y) * W;
@@ -82,7 +100,9 @@ __global__ void k_ct_smooth1(int H, int W, const Taps t, const double* __restric
 // plane 0 = ind, plane c+1 = ind*u_c
 template <int C>
 __global__ void k_ct_seed_smooth0(int H, int W, const Taps t, const double* __restrict__ u,
-                                  const uint8_t* __restrict__ labels, double* __restrict__ out) {
+                                  const uint8_t* __restrict__ labels, double* __restrict__ out,
+                                  const uint8_t* __restrict__ tiles, int tiles_x) {
+  if (!tiles[(blockIdx.y / kTileRows) * tiles_x + blockIdx.x]) return;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= W) return;
   const int j = blockIdx.y;
@@ -117,15 +137,17 @@ __global__ void k_ct_seed_smooth0(int H, int W, const Taps t, const double* __re
   for (int f = 0; f <= C; ++f) out[f * HW + p] = acc[f];
 }
 
-constexpr int kTensorRows = 8;
+constexpr int kTensorRows = kTileRows;
 
 // v_c = S_c / (S_ind > 0 ? S_ind : 1) once per pixel into a shared tile of
 // (kTensorRows + 2) x (128 + 2) pixels, then np.gradient (central /2.0 inside,
 // one-sided /1.0 at the frame edges) and J = sum_c (gx gx, gx gy, gy gy) * ind.
 template <int C>
 __global__ void k_ct_tensor(int H, int W, const double* __restrict__ S,
-                            const uint8_t* __restrict__ labels, double* __restrict__ Q) {
+                            const uint8_t* __restrict__ labels, double* __restrict__ Q,
+                            const uint8_t* __restrict__ tiles) {
   __shared__ double v[kTensorRows + 2][130][C];
+  if (!tiles[blockIdx.y * gridDim.x + blockIdx.x]) return;
   const int64_t HW = (int64_t)H * W;
   const int i0 = blockIdx.x * 128, j0 = blockIdx.y * kTensorRows;
   for (int e = threadIdx.x; e < (kTensorRows + 2) * 130; e += blockDim.x) {
@@ -308,7 +330,8 @@ using namespace gf;
 extern "C" size_t gf_coherence_workspace_bytes(int32_t height, int32_t width, int32_t channels) {
   if (height <= 0 || width <= 0 || channels < 1) return 0;
   const size_t planes = (size_t)(channels + 1 > 4 ? channels + 1 : 4);
-  return 2 * planes * (size_t)height * width * sizeof(double);
+  const size_t tiles = (size_t)((width + 127) / 128) * ((height + kTileRows - 1) / kTileRows);
+  return 2 * planes * (size_t)height * width * sizeof(double) + tiles;
 }
 
 extern "C" int gf_coherence_directions(int32_t height, int32_t width, int32_t channels,
@@ -331,23 +354,29 @@ extern "C" int gf_coherence_directions(int32_t height, int32_t width, int32_t ch
   const int planes = channels + 1 > 4 ? channels + 1 : 4;
   double* A = static_cast<double*>(workspace);
   double* B = A + (size_t)planes * HW;
+  const int tiles_x = (width + 127) / 128, tiles_y = (height + kTileRows - 1) / kTileRows;
+  uint8_t* tmask = reinterpret_cast<uint8_t*>(B + (size_t)planes * HW);
+  cudaMemsetAsync(tmask, 0, (size_t)tiles_x * tiles_y, s);
+  k_ct_tiles<<<(n + 127) / 128, 128, 0, s>>>(height, width, n, idx, tr.R + ts.R + 1, tiles_x,
+                                            tmask);
   // sigma stage (seed fused into axis 0): B = axis 0, A = axis 1 (S)
   const dim3 blk(128);
   const dim3 rows((width + 127) / 128, height, 1);
   switch (channels) {
-    case 1: k_ct_seed_smooth0<1><<<rows, blk, 0, s>>>(height, width, ts, image, labels, B); break;
-    case 2: k_ct_seed_smooth0<2><<<rows, blk, 0, s>>>(height, width, ts, image, labels, B); break;
-    case 3: k_ct_seed_smooth0<3><<<rows, blk, 0, s>>>(height, width, ts, image, labels, B); break;
-    default: k_ct_seed_smooth0<4><<<rows, blk, 0, s>>>(height, width, ts, image, labels, B); break;
+    case 1: k_ct_seed_smooth0<1><<<rows, blk, 0, s>>>(height, width, ts, image, labels, B, tmask, tiles_x); break;
+    case 2: k_ct_seed_smooth0<2><<<rows, blk, 0, s>>>(height, width, ts, image, labels, B, tmask, tiles_x); break;
+    case 3: k_ct_seed_smooth0<3><<<rows, blk, 0, s>>>(height, width, ts, image, labels, B, tmask, tiles_x); break;
+    default: k_ct_seed_smooth0<4><<<rows, blk, 0, s>>>(height, width, ts, image, labels, B, tmask, tiles_x); break;
   }
-  k_ct_smooth1<<<dim3(rows.x, height, channels + 1), blk, 0, s>>>(height, width, ts, B, A);
+  k_ct_smooth1<<<dim3(rows.x, height, channels + 1), blk, 0, s>>>(height, width, ts, B, A, tmask,
+                                                                 tiles_x);
   // tensor: B = [J11, J12, J22, ind] (J * ind)
-  const dim3 tiles((width + 127) / 128, (height + kTensorRows - 1) / kTensorRows, 1);
+  const dim3 tiles(tiles_x, tiles_y, 1);
   switch (channels) {
-    case 1: k_ct_tensor<1><<<tiles, blk, 0, s>>>(height, width, A, labels, B); break;
-    case 2: k_ct_tensor<2><<<tiles, blk, 0, s>>>(height, width, A, labels, B); break;
-    case 3: k_ct_tensor<3><<<tiles, blk, 0, s>>>(height, width, A, labels, B); break;
-    default: k_ct_tensor<4><<<tiles, blk, 0, s>>>(height, width, A, labels, B); break;
+    case 1: k_ct_tensor<1><<<tiles, blk, 0, s>>>(height, width, A, labels, B, tmask); break;
+    case 2: k_ct_tensor<2><<<tiles, blk, 0, s>>>(height, width, A, labels, B, tmask); break;
+    case 3: k_ct_tensor<3><<<tiles, blk, 0, s>>>(height, width, A, labels, B, tmask); break;
+    default: k_ct_tensor<4><<<tiles, blk, 0, s>>>(height, width, A, labels, B, tmask); break;
   }
   // rho stage at the queries only
   k_ct_query<<<(n + kQueryWarps - 1) / kQueryWarps, 32 * kQueryWarps, 0, s>>>(height, width, n,
