@@ -264,13 +264,16 @@ int gf_paint_unfillable(int32_t height, int32_t width, int32_t channels, int32_t
  * window holds no readable mass.  sigma / rho: Gaussian scales (truncate 2,
  * radius int(2 s + 0.5) <= 63).  2 <= H <= 65535, W >= 2 (np.gradient needs
  * 2 samples).
+ * points (nullable): device [n][2] float64, receives (x, y) = (i, j) of each
+ * query, ready for gf_sample_points.
  * workspace: gf_coherence_workspace_bytes(H, W, C) device bytes.
  */
 size_t gf_coherence_workspace_bytes(int32_t height, int32_t width, int32_t channels);
 int gf_coherence_directions(int32_t height, int32_t width, int32_t channels,
                             const double* image, const uint8_t* labels, int32_t n,
                             const int64_t* idx, double sigma, double rho, double lam,
-                            double* g, void* workspace, size_t workspace_bytes, void* stream);
+                            double* g, double* points, void* workspace, size_t workspace_bytes,
+                            void* stream);
 
 /*
  * Tracked frontier update of one shell (tracker._update_arrays,

@@ -144,7 +144,7 @@ def load(required: bool = True):
     lib.gf_coherence_directions.restype = ctypes.c_int
     lib.gf_coherence_directions.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, P, P,
                                             ctypes.c_int32, P, ctypes.c_double, ctypes.c_double,
-                                            ctypes.c_double, P, P, ctypes.c_size_t, P]
+                                            ctypes.c_double, P, P, P, ctypes.c_size_t, P]
     lib.gf_frontier_candidates.restype = ctypes.c_int
     lib.gf_frontier_candidates.argtypes = [ctypes.c_int32, ctypes.c_int32, P, ctypes.c_int32,
                                            ctypes.c_int32, P, P, P, P]

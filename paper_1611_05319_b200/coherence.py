@@ -32,9 +32,11 @@ from ._device import boundary_device, sample_points_device
 from .grid import INPAINT, NEIGHBOR_OFFSETS, READABLE
 
 
-def coherence_directions_device(u, lab, idx, sigma=2.0, rho=4.0, lam=1e-5, workspace=None):
+def coherence_directions_device(u, lab, idx, sigma=2.0, rho=4.0, lam=1e-5, workspace=None,
+                                points=None):
     """guide.coherence_directions (guide.py:330-355) at flat pixel indices ``idx``
-    (int64 CUDA tensor): (n, 2) float64 CUDA tensor."""
+    (int64 CUDA tensor): (n, 2) float64 CUDA tensor.  ``points`` (optional (n, 2)
+    float64 CUDA tensor) receives the queries' (x, y)."""
     import torch
 
     lib = N.load()
@@ -46,7 +48,7 @@ def coherence_directions_device(u, lab, idx, sigma=2.0, rho=4.0, lam=1e-5, works
         workspace = torch.empty(need, dtype=torch.uint8, device=u.device)
     N.check(lib.gf_coherence_directions(H, W, C, N.ptr(u), N.ptr(lab), n, N.ptr(idx),
                                         float(sigma), float(rho), float(lam), N.ptr(g),
-                                        N.ptr(workspace), need, N.stream_ptr()))
+                                        N.ptr(points), N.ptr(workspace), need, N.stream_ptr()))
     return g
 
 
@@ -119,11 +121,10 @@ def run_coherence_fill(u, lab0, params, tracked=True, order_log=False):
         if enter is not None:
             cur = enter[frontier]
             enter[frontier] = torch.where(cur < 0, torch.full_like(cur, it), cur)
+        pts = torch.empty((F, 2), dtype=torch.float64, device=dev)
         g = coherence_directions_device(u, lab, frontier, params.sigma, params.rho,
-                                        params.coherence_lambda, ws)
-        fy = torch.div(frontier, W, rounding_mode="floor")
-        pts = torch.stack([(frontier - fy * W).to(torch.float64), fy.to(torch.float64)], 1)
-        rw, tw, vals = sample_points_device(u, lab, pts.contiguous(), g, params)
+                                        params.coherence_lambda, ws, pts)
+        rw, tw, vals = sample_points_device(u, lab, pts, g, params)
         if params.order == "onion":
             mode = 0
         elif params.order == "smart" or not data_term_live:

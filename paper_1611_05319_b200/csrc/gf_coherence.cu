@@ -67,11 +67,15 @@ int make_taps(double s, Taps& t) {
 constexpr int kTileRows = 8;
 
 __global__ void k_ct_tiles(int H, int W, int n, const int64_t* __restrict__ idx, int D,
-                           int tiles_x, uint8_t* __restrict__ tiles) {
+                           int tiles_x, uint8_t* __restrict__ tiles, double* __restrict__ points) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= n) return;
   const int64_t p = idx[k];
   const int j = (int)(p / W), i = (int)(p % W);
+  if (points) {  // (x, y) of the query for gf_sample_points
+    points[2 * k] = (double)i;
+    points[2 * k + 1] = (double)j;
+  }
   const int ty0 = max(0, j - D) / kTileRows, ty1 = min(H - 1, j + D) / kTileRows;
   const int tx0 = max(0, i - D) / 128, tx1 = min(W - 1, i + D) / 128;
   for (int ty = ty0; ty <= ty1; ++ty)
@@ -337,8 +341,8 @@ extern "C" size_t gf_coherence_workspace_bytes(int32_t height, int32_t width, in
 extern "C" int gf_coherence_directions(int32_t height, int32_t width, int32_t channels,
                                        const double* image, const uint8_t* labels, int32_t n,
                                        const int64_t* idx, double sigma, double rho, double lam,
-                                       double* g, void* workspace, size_t workspace_bytes,
-                                       void* stream) {
+                                       double* g, double* points, void* workspace,
+                                       size_t workspace_bytes, void* stream) {
   if (height < 2 || width < 2 || height > 65535 || channels < 1 || channels > 4 || n < 0)
     return set_error(GF_E_INVALID, "bad geometry");
   if (!image || !labels || (n > 0 && (!idx || !g)) || !workspace)
@@ -358,7 +362,7 @@ extern "C" int gf_coherence_directions(int32_t height, int32_t width, int32_t ch
   uint8_t* tmask = reinterpret_cast<uint8_t*>(B + (size_t)planes * HW);
   cudaMemsetAsync(tmask, 0, (size_t)tiles_x * tiles_y, s);
   k_ct_tiles<<<(n + 127) / 128, 128, 0, s>>>(height, width, n, idx, tr.R + ts.R + 1, tiles_x,
-                                            tmask);
+                                            tmask, points);
   // sigma stage (seed fused into axis 0): B = axis 0, A = axis 1 (S)
   const dim3 blk(128);
   const dim3 rows((width + 127) / 128, height, 1);
