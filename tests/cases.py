@@ -253,4 +253,21 @@ def coherence_scenes(n=10, seed=4242):
             p = dict(r=3, mu=50.0, order="smart", neighborhood="rotated_ball",
                      g_source="modified_structure_tensor")
         out.append(_case(f"ct_rand{k}", img, lab, tracked=bool(k % 2 == 0), **p))
+    # periodic x, data-term order, and a Bystander moat (unfillable fallback)
+    lab = islands_labels(rng, 24, 48)
+    H, W = lab.shape
+    img = rng.uniform(size=(H, W, 3))
+    img[lab == INPAINT] = 0.0
+    out.append(_case("ct_periodic", img, lab, tracked=True, periodic_x=True, **ct))
+    out.append(_case("ct_periodic untracked", img, lab, tracked=False, periodic_x=True, **ct))
+    out.append(_case("ct_data_term", img, lab, tracked=True, r=3, mu=50.0,
+                     order="smart_with_data_term", c2=0.5, neighborhood="rotated_ball",
+                     g_source="modified_structure_tensor"))
+    lab = np.zeros((40, 44), dtype=np.uint8)
+    lab[6:30, 8:36] = INPAINT
+    lab[14:22, 16:28] = BYSTANDER
+    lab[17:19, 21:23] = INPAINT  # pocket cut off by the Bystander moat
+    img = rng.uniform(size=(40, 44, 2))
+    img[lab == INPAINT] = 0.0
+    out.append(_case("ct_moat", img, lab, tracked=True, **ct))
     return out

@@ -20,8 +20,8 @@ orig_sp = coherence.sample_points_device
 log = []
 
 
-def wrapped(u, lab, idx, sigma=2.0, rho=4.0, lam=1e-5, workspace=None):
-    g = orig(u, lab, idx, sigma, rho, lam, workspace)
+def wrapped(u, lab, idx, sigma=2.0, rho=4.0, lam=1e-5, workspace=None, points=None):
+    g = orig(u, lab, idx, sigma, rho, lam, workspace, points)
     W = lab.shape[1]
     f = idx.cpu().numpy()
     iy, ix = np.divmod(f, W)
@@ -41,7 +41,7 @@ def wrapped_sp(u, lab, pts, g, params):
 
 coherence.coherence_directions_device = wrapped
 coherence.sample_points_device = wrapped_sp
-for idx in (11, 12):
+for idx in [int(a) for a in sys.argv[1:]] or (11, 12):
     log.clear()
     case = CT[idx]
     p = FillParams(**case["params"])
