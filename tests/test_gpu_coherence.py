@@ -89,3 +89,19 @@ def test_public_entry_points():
         bad = lab.copy()
         bad[0, 0] = 7
         engine.coherence_transport_mode(img, bad)
+
+
+def test_tensor_inputs_and_no_mutation():
+    import torch
+
+    img, lab = cases.edge_block()
+    img0 = img.copy()
+    u_np, rep = engine.coherence_transport_mode(img, lab)
+    assert np.array_equal(img, img0)  # the reference never mutates its inputs
+    for t in (torch.from_numpy(img), torch.from_numpy(img).cuda(), torch.from_numpy(img).float()):
+        t0 = t.clone()
+        u_t, rep_t = engine.coherence_transport_mode(t, torch.from_numpy(lab))
+        assert torch.equal(t, t0)
+        assert [r[4] for r in rep_t.rows] == [r[4] for r in rep.rows]
+        tol = 0.0 if t.dtype == torch.float64 else 1e-6
+        assert float(np.abs(u_t.numpy() - u_np).max()) <= tol
