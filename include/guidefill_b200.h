@@ -306,6 +306,10 @@ int gf_commit_shell(int32_t channels, int32_t n, const int64_t* frontier, const 
 /* Thread-local message for the last failing call on this thread. */
 const char* gf_last_error(void);
 int gf_abi_version(void);
+/* Kernels launched by this library so far (process-wide, all devices): the
+ * launch evidence bench.py reports as gpu_launches.  A CUDA-graph capture of
+ * an entry counts once, at capture; replays are counted by the caller. */
+int64_t gf_launch_count(void);
 
 /* Host-side builds of the exact-math primitives the kernels use (same
  * source, gf_math.cuh), exported so CPU tests can pin them to numpy. */

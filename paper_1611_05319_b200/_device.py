@@ -53,6 +53,12 @@ def _fill_setup(image, labels, guide, params, tracked=True, order_log=False, row
     lib = N.load()
     assert image.is_cuda and image.is_contiguous() and image.dim() == 4
     nF, H, W, C = image.shape
+    # the kernels index labels as (nF, H, W) contiguous uint8 on the image's device
+    if (tuple(labels.shape[-2:]) != (H, W) or labels.dtype != torch.uint8 or not labels.is_cuda
+            or not labels.is_contiguous() or labels.numel() not in (H * W, nF * H * W)):
+        raise ValueError("image and label shapes differ")
+    if labels.numel() != nF * H * W:
+        raise ValueError(f"{labels.numel() // (H * W)} label masks for {nF} frames")
     raster = splines is not None and splines.n_seg > 0
     g_mode = N.GF_G_FIELD if raster else resolve_g_mode(params, guide is not None)
     if g_mode != N.GF_G_FIELD or raster:
@@ -144,13 +150,65 @@ class FillGraph:
         _fill_launch(self.res, self.call)  # warm-up: function attributes, occupancy
         torch.cuda.synchronize()
         self.graph = torch.cuda.CUDAGraph()
+        n0 = N.launch_count()
         with torch.cuda.graph(self.graph):
             _fill_launch(self.res, self.call)
+        # kernels of the library inside the graph: what every replay launches
+        self.launches_per_replay = N.launch_count() - n0
         torch.cuda.synchronize()
 
     def replay(self):
         self.graph.replay()
         return self.res
+
+
+class BatchGraph:
+    """A video block filled in chunks of frames, captured as ONE CUDA graph.
+
+    images (N, H, W, C) / labels (N, H, W) CUDA tensors; ``splines``: one
+    Spline list per frame (rastered inside each fill).  Chunk c fills frames
+    [c*chunk, (c+1)*chunk) with one batched gf_fill_splines call; the chunks
+    run back to back on one stream and share one workspace.  ``replay()``
+    refills every chunk's result dict (``self.parts``).
+    """
+
+    def __init__(self, images, labels, splines, params, chunk=64, tracked=True, rows_cap=4096,
+                 eta=3.0):
+        import torch
+
+        n = images.shape[0]
+        self.parts = []
+        calls = []
+        ws = None
+        for c0 in range(0, n, chunk):
+            c1 = min(n, c0 + chunk)
+            segs = SegmentSet(list(splines[c0:c1]), images.device, per_frame=True)
+            res, call = _fill_setup(images[c0:c1], labels[c0:c1], None, params, tracked, False,
+                                    rows_cap, ws, segs, eta, 0, False)
+            ws = res["workspace"]  # the first (largest) chunk sizes it
+            res["frames"] = (c0, c1)
+            self.parts.append(res)
+            calls.append(call)
+        for res, call in zip(self.parts, calls):
+            _fill_launch(res, call)
+        torch.cuda.synchronize()
+        self.calls = calls
+        self.graph = torch.cuda.CUDAGraph()
+        n0 = N.launch_count()
+        with torch.cuda.graph(self.graph):
+            for res, call in zip(self.parts, calls):
+                _fill_launch(res, call)
+        self.launches_per_replay = N.launch_count() - n0
+        torch.cuda.synchronize()
+
+    def replay(self):
+        self.graph.replay()
+        return self.parts
+
+    def stats(self):
+        import torch
+
+        return torch.cat([p["stats"] for p in self.parts]).cpu().numpy()
 
 
 def splines_to_segments(splines):

@@ -32,7 +32,7 @@ EXPORTS = (
     "gf_paint_unfillable_workspace_bytes", "gf_paint_unfillable",
     "gf_coherence_workspace_bytes", "gf_coherence_directions", "gf_frontier_candidates",
     "gf_commit_shell", "gf_last_error",
-    "gf_abi_version", "gf_host_exp", "gf_host_hypot", "gf_host_pairwise_sum",
+    "gf_abi_version", "gf_launch_count", "gf_host_exp", "gf_host_hypot", "gf_host_pairwise_sum",
 )
 
 
@@ -157,12 +157,19 @@ def load(required: bool = True):
                                         ctypes.c_int32, P, P, P, P, ctypes.c_size_t, P, P]
     lib.gf_last_error.restype = ctypes.c_char_p
     lib.gf_abi_version.restype = ctypes.c_int
+    lib.gf_launch_count.restype = ctypes.c_int64
+    lib.gf_launch_count.argtypes = []
     lib.gf_host_exp.argtypes = [P, P, ctypes.c_int64]
     lib.gf_host_hypot.argtypes = [P, P, P, ctypes.c_int64]
     lib.gf_host_pairwise_sum.restype = ctypes.c_double
     lib.gf_host_pairwise_sum.argtypes = [P, ctypes.c_int32]
     _lib = lib
     return lib
+
+
+def launch_count() -> int:
+    """Kernels this library has launched in the process (gf_launch_count)."""
+    return int(load().gf_launch_count())
 
 
 def check(rc: int) -> None:

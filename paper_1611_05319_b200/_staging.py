@@ -83,23 +83,44 @@ def upload(arr: np.ndarray, device, slot: str = "up"):
     return dst
 
 
+class _BufferOwner:
+    """Owner of one pooled pinned buffer, exposed to numpy through
+    ``__array_interface__``.  Every array made from it -- and every view of
+    such an array, whose ``.base`` numpy collapses to this object -- keeps it
+    alive, so the buffer goes back to the pool only when the last user is
+    gone (not when the first returned array dies)."""
+
+    __slots__ = ("buf", "__array_interface__", "__weakref__")
+
+    def __init__(self, buf, n, shape, dtype):
+        self.buf = buf
+        self.__array_interface__ = {"shape": tuple(shape), "typestr": np.dtype(dtype).str,
+                                    "data": (buf.data_ptr(), False), "version": 3}
+
+
 class _PinnedPool:
     """Recycled pinned host buffers for returned arrays.
 
-    ``take`` hands out a numpy array backed by pinned, already-touched memory;
-    the buffer returns to the pool when that array (and every view of it) is
-    garbage-collected, so steady-state calls pay neither page faults nor
-    pinned allocation, and the D2H lands in it at full DMA speed.
+    ``take`` hands out a numpy array backed by pinned, already-touched memory,
+    so steady-state calls pay neither page faults nor pinned allocation, and
+    the D2H lands in it at full DMA speed.  The buffer returns to the pool
+    when its ``_BufferOwner`` dies: every numpy view references the owner,
+    and tensors from ``take_tensor`` hold the numpy array (torch.from_numpy),
+    so a live view of a result can never see its memory reused.
     """
 
     def __init__(self):
         self.free = {}
         self.lock = threading.Lock()
 
+    @staticmethod
+    def _alloc(n):
+        import torch
+
+        return torch.empty(max(n, 1), dtype=torch.uint8, pin_memory=True)
+
     def take(self, shape, dtype):
         import weakref
-
-        import torch
 
         dtype = np.dtype(dtype)
         n = int(np.prod(shape)) * dtype.itemsize
@@ -107,26 +128,21 @@ class _PinnedPool:
             lst = self.free.get(n)
             buf = lst.pop() if lst else None
         if buf is None:
-            buf = torch.empty(max(n, 1), dtype=torch.uint8, pin_memory=True)
-        arr = buf.numpy()[:n].view(dtype).reshape(shape)
-        weakref.finalize(arr, self._give, n, buf)
+            buf = self._alloc(n)
+        owner = _BufferOwner(buf, n, shape, dtype)
+        arr = np.asarray(owner)
+        weakref.finalize(owner, self._give, n, buf)
         return arr, buf
 
     def take_tensor(self, shape, dtype):
-        """Like ``take``, as a CPU torch tensor (pinned) recycled on release."""
-        import weakref
-
+        """Like ``take``, as a pinned CPU torch tensor.  The tensor's storage
+        holds the numpy array (hence the owner): the buffer is recycled only
+        after every tensor view is released."""
         import torch
 
-        n = int(np.prod(shape)) * torch.empty(0, dtype=dtype).element_size()
-        with self.lock:
-            lst = self.free.get(n)
-            buf = lst.pop() if lst else None
-        if buf is None:
-            buf = torch.empty(max(n, 1), dtype=torch.uint8, pin_memory=True)
-        t = buf[:n].view(dtype).view(shape)
-        weakref.finalize(t, self._give, n, buf)
-        return t, buf
+        np_dtype = torch.empty(0, dtype=dtype).numpy().dtype
+        arr, buf = self.take(shape, np_dtype)
+        return torch.from_numpy(arr), buf
 
     def _give(self, n, buf):
         with self.lock:

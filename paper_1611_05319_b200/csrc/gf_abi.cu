@@ -12,6 +12,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <atomic>
 #include <string>
 #include <vector>
 
@@ -25,6 +26,9 @@ int set_error(int code, const char* msg) {
   g_last_error = msg ? msg : "";
   return code;
 }
+
+static std::atomic<long long> g_launches{0};
+void count_launches(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 // Disk offsets (n, m), n^2 + m^2 <= r^2, meshgrid order (m outer, n inner),
 // centre moved to the front and then dropped (engine.py:172).
@@ -92,6 +96,8 @@ extern "C" {
 const char* gf_last_error(void) { return g_last_error.c_str(); }
 
 int gf_abi_version(void) { return GF_ABI_VERSION; }
+
+int64_t gf_launch_count(void) { return (int64_t)g_launches.load(std::memory_order_relaxed); }
 
 size_t gf_fill_splines_workspace_bytes(const gf_frames* frames, const gf_fill_params* params,
                                        const gf_splines* splines) {

@@ -385,6 +385,7 @@ extern "C" int gf_coherence_directions(int32_t height, int32_t width, int32_t ch
   // rho stage at the queries only
   k_ct_query<<<(n + kQueryWarps - 1) / kQueryWarps, 32 * kQueryWarps, 0, s>>>(height, width, n,
                                                                             idx, B, tr, lam, g);
+  count_launches(5);
   cudaError_t e = cudaPeekAtLastError();
   if (e != cudaSuccess) return set_error(GF_E_CUDA, cudaGetErrorString(e));
   return GF_OK;
@@ -398,6 +399,7 @@ extern "C" int gf_frontier_candidates(int32_t height, int32_t width, const uint8
   if (!labels || !frontier || !fill || !mark) return set_error(GF_E_INVALID, "NULL buffer");
   k_ct_mark<<<(n + 127) / 128, 128, 0, static_cast<cudaStream_t>(stream)>>>(
       height, width, periodic_x, labels, n, frontier, fill, mark);
+  count_launches(1);
   cudaError_t e = cudaPeekAtLastError();
   if (e != cudaSuccess) return set_error(GF_E_CUDA, cudaGetErrorString(e));
   return GF_OK;
@@ -417,6 +419,7 @@ extern "C" int gf_commit_shell(int32_t channels, int32_t n, const int64_t* front
   k_ct_commit<<<(n + 127) / 128, 128, 0, static_cast<cudaStream_t>(stream)>>>(
       channels, n, frontier, rw, tw, vals, g, ready_mode, c, c2, shell, image, labels, fillshell,
       fill, count);
+  count_launches(1);
   cudaError_t e = cudaPeekAtLastError();
   if (e != cudaSuccess) return set_error(GF_E_CUDA, cudaGetErrorString(e));
   return GF_OK;

@@ -82,17 +82,24 @@ extern "C" int gf_output_delta(int64_t n_px, int32_t channels, int32_t dtype, co
     k_output_delta<uint32_t><<<grid, kDeltaThreads, 0, s>>>(
         n_px, channels, static_cast<const uint32_t*>(input), static_cast<const uint32_t*>(output),
         static_cast<uint32_t*>(dev_host), n_changed);
+  count_launches(1);
   e = cudaPeekAtLastError();
   if (e != cudaSuccess) return set_error(GF_E_CUDA, cudaGetErrorString(e));
   return GF_OK;
 }
 
 namespace {
-// Per-thread ring of timing-free events for the chunk hand-off: a record is
-// consumed by the stream wait enqueued right after it, so reuse is safe.
+// Per-(thread, device) ring of timing-free events for the chunk hand-off: a
+// record is consumed by the stream wait enqueued right after it, so reuse is
+// safe.  Events belong to the device current at creation, so each device has
+// its own ring (a single host thread may drive several GPUs).
 constexpr int kRing = 64;
-thread_local cudaEvent_t g_ring[kRing] = {};
-thread_local int g_ring_pos = 0;
+constexpr int kMaxDevices = 64;
+struct EventRing {
+  cudaEvent_t ev[kRing] = {};
+  int pos = 0;
+};
+thread_local EventRing g_rings[kMaxDevices];
 }  // namespace
 
 extern "C" int gf_upload_mirrored(const void* host_src, void* dev_dst, void* host_mirror,
@@ -106,10 +113,14 @@ extern "C" int gf_upload_mirrored(const void* host_src, void* dev_dst, void* hos
   const char* src = static_cast<const char*>(host_src);
   char* dst = static_cast<char*>(dev_dst);
   char* mir = static_cast<char*>(host_mirror);
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices)
+    return set_error(GF_E_CUDA, "no usable current device");
+  EventRing& ring = g_rings[dev];
   for (int64_t lo = 0; lo < nbytes; lo += chunk) {
     const size_t n = (size_t)std::min(chunk, nbytes - lo);
-    cudaEvent_t& ev = g_ring[g_ring_pos];
-    g_ring_pos = (g_ring_pos + 1) % kRing;
+    cudaEvent_t& ev = ring.ev[ring.pos];
+    ring.pos = (ring.pos + 1) % kRing;
     cudaError_t e = cudaSuccess;
     if (!ev) e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaMemcpyAsync(dst + lo, src + lo, n, cudaMemcpyHostToDevice, s);

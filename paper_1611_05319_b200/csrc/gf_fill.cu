@@ -1763,6 +1763,7 @@ int fill_launch(const gf_frames* fr, const gf_fill_params* prm, const gf_fill_ou
     return set_error(GF_E_CUDA, "memset failed");
   launch_prep(fr->dtype == GF_F64, C, dim3((W + kTile - 1) / kTile, (H + kTile - 1) / kTile, nF), stream,
               A);
+  count_launches(1);
   if (cudaPeekAtLastError() != cudaSuccess)
     return set_error(GF_E_CUDA, cudaGetErrorString(cudaGetLastError()));
 
@@ -1794,6 +1795,7 @@ int fill_launch(const gf_frames* fr, const gf_fill_params* prm, const gf_fill_ou
     e = cudaLaunchCooperativeKernel(fn, grid, kShellThreads, args, smem, stream);
   }
   if (e != cudaSuccess) return set_error(GF_E_CUDA, cudaGetErrorString(e));
+  count_launches(1);
 
   e = cudaPeekAtLastError();
   if (e != cudaSuccess) return set_error(GF_E_CUDA, cudaGetErrorString(e));

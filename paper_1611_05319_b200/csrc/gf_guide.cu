@@ -113,6 +113,7 @@ int guide_launch(int H, int W, const uint8_t* labels, int n_seg, const double* s
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int grid = std::min((total + kGfThreads - 1) / kGfThreads, sms * 8);
   k_guide<<<grid, kGfThreads, 0, stream>>>(a);
+  count_launches(1);
   cudaError_t e = cudaPeekAtLastError();
   if (e != cudaSuccess) return set_error(GF_E_CUDA, cudaGetErrorString(e));
   return GF_OK;

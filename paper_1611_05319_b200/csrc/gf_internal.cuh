@@ -77,6 +77,8 @@ struct FillArgs {
 
 // thread-local error reporting (gf_abi.cu)
 int set_error(int code, const char* msg);
+// process-wide count of the kernels this library has launched (gf_launch_count)
+void count_launches(int n);
 
 // gf_fill.cu
 size_t fill_workspace_bytes(int nF, int H, int W, int C, bool need_g);

@@ -55,6 +55,7 @@ int sample_points_launch(int H, int W, int C, const double* image, const uint8_t
     k_sample_points<kMaxLeaves><<<grid, kPtThreads, 0, stream>>>(src, n, points, g, P, tab, rw, tw, vals);
   else
     k_sample_points<1><<<grid, kPtThreads, 0, stream>>>(src, n, points, g, P, tab, rw, tw, vals);
+  count_launches(1);
   cudaError_t e = cudaPeekAtLastError();
   if (e != cudaSuccess) return set_error(GF_E_CUDA, cudaGetErrorString(e));
   return GF_OK;
@@ -76,6 +77,7 @@ int bilinear_launch(int H, int W, int C, const double* image, const uint8_t* lab
   if (n <= 0) return GF_OK;
   RawSource src{image, labels, H, W, C};
   k_bilinear<<<std::min(4096, (n + 255) / 256), 256, 0, stream>>>(src, n, X, Y, periodic, vals, ok);
+  count_launches(1);
   cudaError_t e = cudaPeekAtLastError();
   if (e != cudaSuccess) return set_error(GF_E_CUDA, cudaGetErrorString(e));
   return GF_OK;
@@ -115,6 +117,7 @@ int boundary_launch(int H, int W, const uint8_t* labels, int periodic, uint8_t* 
   if (total <= 0) return GF_OK;
   k_boundary<<<std::min(8192, (total + 255) / 256), 256, 0, stream>>>(H, W, labels, periodic,
                                                                        active, inner, outer);
+  count_launches(1);
   cudaError_t e = cudaPeekAtLastError();
   if (e != cudaSuccess) return set_error(GF_E_CUDA, cudaGetErrorString(e));
   return GF_OK;

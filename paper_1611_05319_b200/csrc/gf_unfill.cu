@@ -148,6 +148,7 @@ extern "C" int gf_paint_unfillable(int32_t height, int32_t width, int32_t channe
     k_ft_rows_paint<float><<<(height + 63) / 64, 64, 0, s>>>(
         height, width, channels, labels, fillshell, row1, stk, static_cast<float*>(out),
         n_painted);
+  count_launches(2);
   cudaError_t e = cudaPeekAtLastError();
   if (e != cudaSuccess) return set_error(GF_E_CUDA, cudaGetErrorString(e));
   return GF_OK;

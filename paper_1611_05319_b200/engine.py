@@ -8,10 +8,11 @@ return layout and ValueError messages.  The fill itself runs on the GPU:
 ``_run_fill`` hands the frame to the persistent sm_100a shell kernel through
 the C ABI (gf_fill) and only copies the result back.
 
-The one host-side step is the unfillable fallback (engine.py:270-283): when
-the frontier empties while Inpaint pixels remain (a Bystander moat), the
-stranded pixels take the colour of the nearest readable pixel via
-scipy's Euclidean distance transform, exactly as the reference does.
+The unfillable fallback (engine.py:270-283) runs on the device too: when the
+frontier empties while Inpaint pixels remain (a Bystander moat), the
+stranded pixels take the colour of the nearest readable pixel, found by
+gf_paint_unfillable -- a restatement of scipy's Euclidean distance-transform
+feature transform with its tie-breaking (csrc/gf_unfill.cu).
 """
 
 from __future__ import annotations

@@ -151,3 +151,105 @@ def small_scene(H, W, band, gx, gy, n_spl, seed, frame=0, spline_kind="bezier"):
                                             seed=seed, frame=frame, spline_kind=spline_kind)
     return Scene(f"small{H}x{W}", image, labels, spl,
                  dict(r=3, mu=50.0, order="smart", neighborhood="rotated_ball"))
+
+
+def _frame_geometry(H, W, band, gx, gy, n_spl, seed, frame, spline_kind="bezier"):
+    """The random draws of ``disocclusion_frame`` in its RNG order, without
+    materialising the texture: ellipses, texture phases, (skip the H*W*3 noise
+    draws), splines.  Returns (ellipses, phases, splines)."""
+    rng = np.random.default_rng(seed + 7919 * frame)
+    cw = W / gx
+    ch = H / gy
+    ellipses = []
+    for cy_i in range(gy):
+        for cx_i in range(gx):
+            cx = (cx_i + 0.5) * cw + rng.uniform(-0.1, 0.1) * cw + 3.0 * frame
+            cy = (cy_i + 0.5) * ch + rng.uniform(-0.1, 0.1) * ch
+            rx = rng.uniform(0.22, 0.32) * cw
+            ry = rng.uniform(0.30, 0.42) * ch
+            ellipses.append((cx, cy, rx, ry))
+    phases = rng.uniform(0.0, 2.0 * math.pi, 3)
+    rng.bit_generator.advance(H * W * 3)  # the noise: one 64-bit draw per double
+    splines = []
+    picks = rng.choice(len(ellipses), size=n_spl, replace=False)
+    L = 3.0 * band + 30.0
+    for k, e in enumerate(picks):
+        cx, cy, rx, ry = ellipses[int(e)]
+        x_edge = cx - rx
+        y0 = cy + rng.uniform(-0.5, 0.5) * ry
+        a = rng.uniform(-0.6, 0.6)
+        p0 = np.array([x_edge - L, y0 - L * math.tan(a)])
+        p3 = np.array([x_edge + 2.0, y0])
+        d = p3 - p0
+        unit = d / math.hypot(d[0], d[1])
+        if spline_kind == "bezier":
+            p1 = p0 + d / 3.0 + np.array([0.0, rng.uniform(-8.0, 8.0)])
+            p2 = p0 + 2.0 * d / 3.0 + np.array([0.0, rng.uniform(-8.0, 8.0)])
+            pts = np.stack([p0, p1, p2, p3])
+            direction = (0.97 * unit[0], 0.97 * unit[1])
+        else:
+            pts = np.stack([p0, p3 + 2.0 * unit * band])
+            direction = (float(np.tanh(4.0)) * unit[0], float(np.tanh(4.0)) * unit[1])
+        splines.append(dict(id=f"s{k}", points=pts, kind=spline_kind,
+                            direction=(float(direction[0]), float(direction[1]))))
+    return ellipses, phases, splines
+
+
+def video_batch_device(frames, device, H=1080, W=1920, band=10, gx=10, gy=6, n_spl=6, seed=1611,
+                       dtype=None):
+    """C5 video frames rendered straight into HBM (SURVEY.md section 8(d):
+    "generated on device").
+
+    Returns (images (N, H, W, 3), labels (N, H, W) uint8, splines per frame).
+    Labels and splines are bit-identical to ``disocclusion_frame(frame=f)``
+    (same RNG draws; the ellipse test is the same sequence of IEEE double
+    operations), so the fill order and |D| equal the host generator's.  The
+    texture is the same formula evaluated on the GPU with device noise: its
+    values differ from the host frame's, which changes only output colours
+    (SURVEY.md section 0.4), not the work.
+    """
+    import torch
+
+    dtype = dtype or torch.float32
+    frames = list(frames)
+    n = len(frames)
+    images = torch.empty((n, H, W, 3), dtype=dtype, device=device)
+    labels = torch.empty((n, H, W), dtype=torch.uint8, device=device)
+    jj = torch.arange(H, dtype=torch.float64, device=device).view(H, 1)
+    ii = torch.arange(W, dtype=torch.float64, device=device).view(1, W)
+    stripes = 0.08 * torch.sign(torch.sin((0.8 * ii + 0.6 * jj) / 11.0))
+    gen = torch.Generator(device=device)
+    spl_all = []
+    for b, f in enumerate(frames):
+        ellipses, phases, spl = _frame_geometry(H, W, band, gx, gy, n_spl, seed, f)
+        spl_all.append(spl)
+        obj = torch.zeros((H, W), dtype=torch.bool, device=device)
+        for cx, cy, rx, ry in ellipses:
+            j0 = max(0, int(math.floor(cy - ry)) - 1)
+            j1 = min(H, int(math.ceil(cy + ry)) + 2)
+            i0 = max(0, int(math.floor(cx - rx)) - 1)
+            i1 = min(W, int(math.ceil(cx + rx)) + 2)
+            if j0 >= j1 or i0 >= i1:
+                continue
+            a = (ii[:, i0:i1] - cx) / rx
+            c = (jj[j0:j1] - cy) / ry
+            obj[j0:j1, i0:i1] |= (a * a + c * c) <= 1.0
+        hole = torch.zeros_like(obj)
+        for s in range(1, band + 1):
+            hole[:, :W - s] |= obj[:, s:]
+        hole &= ~obj
+        lab = labels[b]
+        lab.fill_(READABLE)
+        lab.masked_fill_(obj, BYSTANDER)
+        lab.masked_fill_(hole, INPAINT)
+        gen.manual_seed(seed + 7919 * f)
+        img = torch.empty((H, W, 3), dtype=torch.float64, device=device)
+        for ch in range(3):
+            img[..., ch] = 0.5 + 0.35 * torch.sin(ii / (90.0 + 40.0 * ch) + jj / (140.0 + 30.0 * ch)
+                                                 + float(phases[ch]))
+        img += stripes[..., None]
+        img += torch.rand((H, W, 3), generator=gen, dtype=torch.float64, device=device) * 0.05
+        img.clamp_(0.0, 1.0)
+        img[hole] = 0.0
+        images[b].copy_(img)
+    return images, labels, spl_all

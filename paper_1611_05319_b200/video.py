@@ -21,6 +21,30 @@ def frame_block(n_frames: int, world: int, rank: int) -> range:
     return range(start, start + base + (1 if rank < extra else 0))
 
 
+def reduce_over_ranks(sums=(), maxes=(), device="cpu"):
+    """Job-wide totals of per-rank numbers for a frame-parallel run: ``sums``
+    (inpainted pixels, bytes) added over the ranks, ``maxes`` (step times)
+    maximised -- the job takes as long as its slowest rank.  Collectives run
+    on the process group torch.distributed was initialised with (NCCL on the
+    GPUs, gloo in the CPU tests); without one the inputs come back as they are.
+    These are bookkeeping collectives, never on the fill's data path."""
+    import torch
+    import torch.distributed as dist
+
+    sums, maxes = [float(x) for x in sums], [float(x) for x in maxes]
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return sums, maxes
+    out = []
+    for vals, op in ((sums, dist.ReduceOp.SUM), (maxes, dist.ReduceOp.MAX)):
+        if not vals:
+            out.append([])
+            continue
+        t = torch.tensor(vals, dtype=torch.float64, device=device)
+        dist.all_reduce(t, op=op)
+        out.append(t.cpu().tolist())
+    return out[0], out[1]
+
+
 def frame_checksum(u: np.ndarray) -> float:
     """Order-independent digest used to compare per-frame results across ranks."""
     return float(np.asarray(u, dtype=np.float64).sum())
@@ -37,6 +61,39 @@ def fill_video(images, labels, splines, params, tracked=True, device=None, works
 
     return fill_device(images, labels, None, params, tracked=tracked, splines=splines,
                        workspace=workspace)
+
+
+def _frame_hw(x):
+    return tuple(int(d) for d in x.shape[:2])
+
+
+def _check_video_masks(images, labels):
+    """Labels of a video: one (H, W) mask shared by every frame, a sequence of
+    per-frame masks, or an (N, H, W) stack of them (returned as a list).  Every
+    mask must match its frame's (H, W) -- a mismatch would make the kernels
+    read past the device labels -- and the reference's "differ" ValueError is
+    raised otherwise (engine.py:398-401)."""
+    n = len(images)
+    if not isinstance(labels, (list, tuple)):
+        nd = len(labels.shape)
+        if nd == 3:
+            if int(labels.shape[0]) != n:
+                raise ValueError(f"{int(labels.shape[0])} label masks for {n} frames")
+            labels = [labels[f] for f in range(n)]
+        elif nd != 2:
+            raise ValueError("labels must be one (H, W) mask, a sequence of them or an "
+                             "(N, H, W) stack")
+    if isinstance(labels, (list, tuple)):
+        if len(labels) != n:
+            raise ValueError(f"{len(labels)} label masks for {n} frames")
+        for f in range(n):
+            if len(labels[f].shape) != 2 or _frame_hw(labels[f]) != _frame_hw(images[f]):
+                raise ValueError(f"frame {f}: image and label shapes differ")
+    else:
+        for f in range(n):
+            if _frame_hw(labels) != _frame_hw(images[f]):
+                raise ValueError(f"frame {f}: image and label shapes differ")
+    return labels
 
 
 _streams = {}
@@ -60,8 +117,9 @@ def fill_video_host(images, labels, splines, params, tracked=True, depth=3, on_f
 
     images: sequence of (H, W, C) frames, float64 numpy arrays or pinned CPU
     tensors (what a decoder writing into page-locked buffers hands over);
-    labels: one (H, W) uint8 mask shared by all frames, or a sequence of
-    them; splines: a Spline list shared by all frames (rastered inside each
+    labels: one (H, W) uint8 mask shared by all frames, a sequence of
+    per-frame masks, or an (N, H, W) stack of them (each checked against its
+    frame's shape); splines: a Spline list shared by all frames (rastered inside each
     fill), a sequence of per-frame Spline lists, or None for g = 0.
     Returns [(u, FillReport)] in frame order, u of the input's kind (numpy
     float64 / pinned CPU tensor).
@@ -89,6 +147,7 @@ def fill_video_host(images, labels, splines, params, tracked=True, depth=3, on_f
     if n == 0:
         return []
     depth = max(1, int(depth))
+    labels = _check_video_masks(images, labels)
     shared_lab = not isinstance(labels, (list, tuple))
     per_frame_spl = bool(splines) and isinstance(splines[0], (list, tuple))
     segs = SegmentSet.cached(list(splines), dev) if splines and not per_frame_spl else None
@@ -127,8 +186,8 @@ def fill_video_host(images, labels, splines, params, tracked=True, depth=3, on_f
                                             else lab_f))
             raise ValueError("label mask holds values outside {0, 128, 255}")
         if stats[N.STAT_UNFILLABLE] or int(stats[N.STAT_ITERATIONS]) + 1 > rows.shape[0]:
-            # rare: stranded pixels (host EDT fallback) or a long report -- the
-            # single-frame path handles both
+            # rare: stranded pixels (the device EDT paint) or a report longer
+            # than the pipeline's row buffer -- the single-frame path handles both
             lab_f = labels if shared_lab else labels[f]
             spl_f = splines[f] if per_frame_spl else splines
             u, rep, _ = _run_fill(images[f], lab_f, None, params, tracked, splines=spl_f)
@@ -232,3 +291,74 @@ def _pipeline(n, depth, pending, finish, images, labels, splines, params, tracke
     for k in range(n, n + depth):
         if pending[k % depth] is not None:
             finish(k % depth)
+
+
+def fill_video_multi(images, labels, splines, params, devices=None, tracked=True, depth=3,
+                     on_frame=None):
+    """Frame-parallel fill of a host video over several GPUs of one process.
+
+    The frames are split into contiguous blocks (``frame_block``), one per
+    device, and each block streams through ``fill_video_host`` on its own
+    host thread with that device current: uploads, fills and downloads of
+    different GPUs run concurrently (each GPU has its own PCIe link and
+    copy engines) and no data crosses between devices.  Per-frame results
+    are identical whatever the device count (each frame is one independent
+    fill).
+
+    images / labels / splines as for ``fill_video_host`` (labels: a shared
+    mask, a per-frame sequence or an (N, H, W) stack).  devices: CUDA device
+    indices or torch devices, default all visible GPUs.  Returns
+    [(u, FillReport)] in frame order, or None with ``on_frame(f, u, report)``
+    (called from the device threads, frames of one device in order).
+    """
+    import threading
+
+    import torch
+
+    from . import _native as N
+
+    N.require_cuda()
+    n = len(images)
+    if devices is None:
+        devices = list(range(torch.cuda.device_count()))
+    devices = [torch.device("cuda", d) if isinstance(d, int) else torch.device(d) for d in devices]
+    if not devices:
+        raise ValueError("no devices to fill on")
+    labels = _check_video_masks(images, labels)
+    per_frame_spl = bool(splines) and isinstance(splines[0], (list, tuple))
+    results = [None] * n
+    errors = []
+
+    def work(k, dev):
+        blk = frame_block(n, len(devices), k)
+        if len(blk) == 0:
+            return
+        idx = list(blk)
+        lab = labels if not isinstance(labels, (list, tuple)) else [labels[f] for f in idx]
+        spl = [splines[f] for f in idx] if per_frame_spl else splines
+        cb = None
+        if on_frame is not None:
+            def cb(i, u, rep):
+                on_frame(idx[i], u, rep)
+        try:
+            with torch.cuda.device(dev):
+                out = fill_video_host([images[f] for f in idx], lab, spl, params,
+                                      tracked=tracked, depth=depth, on_frame=cb)
+                torch.cuda.current_stream().synchronize()
+            if out is not None:
+                for i, f in enumerate(idx):
+                    results[f] = out[i]
+        except BaseException as e:  # re-raised on the caller's thread
+            errors.append(e)
+
+    if len(devices) == 1:
+        work(0, devices[0])
+    else:
+        threads = [threading.Thread(target=work, args=(k, d)) for k, d in enumerate(devices)]
+        for t in threads:
+            t.start()
+        for t in threads:
+            t.join()
+    if errors:
+        raise errors[0]
+    return None if on_frame is not None else results

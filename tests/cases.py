@@ -270,4 +270,13 @@ def coherence_scenes(n=10, seed=4242):
     img = rng.uniform(size=(40, 44, 2))
     img[lab == INPAINT] = 0.0
     out.append(_case("ct_moat", img, lab, tracked=True, **ct))
+    # smart / data-term order on the smooth edge scene: confidences far from
+    # ties, so the order must be bit-exact (no near-tie excuse)
+    img, lab = edge_block()
+    out.append(_case("ct_edge data_term", img, lab, tracked=True, r=3, mu=50.0,
+                     order="smart_with_data_term", c2=0.5, neighborhood="rotated_ball",
+                     g_source="modified_structure_tensor"))
+    out.append(_case("ct_edge smart untracked", img, lab, tracked=False, r=4, mu=100.0,
+                     order="smart", neighborhood="rotated_ball",
+                     g_source="modified_structure_tensor"))
     return out

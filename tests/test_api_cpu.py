@@ -84,3 +84,39 @@ def test_spline_wire_format_round_trip():
     assert dumps(back) == text
     with pytest.raises(ValueError):
         loads('{"version": 2, "splines": []}')
+
+
+def test_pooled_result_buffers_outlive_their_views():
+    """A view of a returned result keeps its pooled buffer out of the pool
+    (the buffer used to be recycled when the first array died)."""
+    import gc
+
+    import torch
+
+    from paper_1611_05319_b200 import _staging
+
+    class Pool(_staging._PinnedPool):
+        @staticmethod
+        def _alloc(n):  # pageable stand-in: the lifetime logic is the same
+            return torch.empty(max(n, 1), dtype=torch.uint8)
+
+    pool = Pool()
+    a, _ = pool.take((4, 5, 3), np.float64)
+    a[...] = 1.0
+    v, w = a[..., 0], a.reshape(-1, 3)
+    del a
+    gc.collect()
+    b, _ = pool.take((4, 5, 3), np.float64)
+    b[...] = 2.0
+    assert float(v[0, 0]) == 1.0 and float(w[0, 0]) == 1.0
+    del v, w, b
+    gc.collect()
+    assert len(pool.free[4 * 5 * 3 * 8]) == 2  # both buffers came back
+    t, _ = pool.take_tensor((4, 5, 3), torch.float64)
+    t.fill_(3.0)
+    tv = t[..., 0]
+    del t
+    gc.collect()
+    c, _ = pool.take((4, 5, 3), np.float64)
+    c[...] = 4.0
+    assert float(tv[0, 0]) == 3.0

@@ -523,3 +523,90 @@ def test_unfillable_paint_large_ties():
     assert _paint_unfillable_device(d_u, torch.from_numpy(labels).cuda(),
                                     torch.from_numpy(fillshell).cuda()) == n_want
     assert np.array_equal(d_u.cpu().numpy(), want)
+
+
+def test_fill_video_multi_equals_single_calls():
+    """video.fill_video_multi (frame blocks over the devices, one host thread
+    each) on the visible GPUs: every frame equals its run_tracked result,
+    with per-frame masks as a list and as an (N, H, W) stack; a mask of the
+    wrong shape is refused before anything runs."""
+    from paper_1611_05319_b200 import tracker, video
+
+    frames = [scenes.small_scene(270, 480, band=8, gx=5, gy=3, n_spl=4, seed=99, frame=f)
+              for f in range(5)]
+    p = FillParams(**frames[0].params)
+    spl = [_splines(sc) for sc in frames]
+    want = [tracker.run_tracked(sc.image, sc.labels, spl[i], p) for i, sc in enumerate(frames)]
+    imgs = [sc.image for sc in frames]
+    for labs in ([sc.labels for sc in frames], np.stack([sc.labels for sc in frames])):
+        got = video.fill_video_multi(imgs, labs, spl, p)
+        for (u, rep), (u_w, m_w) in zip(got, want):
+            assert np.array_equal(u, u_w)
+            assert rep.rows == m_w.rows
+    seen = {}
+    video.fill_video_multi(imgs, [sc.labels for sc in frames], spl, p, devices=[0],
+                           on_frame=lambda f, u, rep: seen.__setitem__(f, rep.filled))
+    assert seen == {f: want[f][1].report.filled for f in range(5)}
+    with pytest.raises(ValueError, match="differ"):
+        video.fill_video_multi(imgs, frames[0].labels[:-1], spl, p)
+    with pytest.raises(ValueError):
+        video.fill_video_host(imgs, np.stack([sc.labels for sc in frames])[:3], spl, p)
+
+
+def test_device_rendered_video_matches_host_generator():
+    """scenes.video_batch_device: labels and splines of the C5 frames are
+    bit-identical to the host generator, so |D| and the fill order are the
+    same work the CPU baseline measures."""
+    frames = [0, 17, 255]
+    images, labels, spl = scenes.video_batch_device(frames, torch.device("cuda"))
+    for b, f in enumerate(frames):
+        sc = scenes.config("C5", frame=f)
+        assert np.array_equal(labels[b].cpu().numpy(), sc.labels)
+        for a, c in zip(spl[b], sc.splines):
+            assert np.array_equal(a["points"], c["points"]) and a["direction"] == c["direction"]
+        img = images[b].cpu().numpy()
+        assert float(np.abs(img - sc.image).max()) <= 0.05 + 1e-6  # noise differs only
+        assert not img[sc.labels == 255].any()
+
+
+def test_batch_graph_equals_per_frame_fills():
+    """_device.BatchGraph (bench.py's C5 step: chunks of frames, one graph)
+    gives each frame's single-frame fill."""
+    from paper_1611_05319_b200._device import BatchGraph
+
+    images, labels, spl = scenes.video_batch_device([3, 4, 5], torch.device("cuda"))
+    splines = [[Spline(id=s["id"], source="user", direction=s["direction"], points=s["points"],
+                       kind=s["kind"]) for s in fs] for fs in spl]
+    p = FillParams(**scenes.config("C5").params)
+    g = BatchGraph(images, labels, splines, p, chunk=2)
+    assert g.launches_per_replay == 4  # k_prep + k_shells per chunk
+    parts = g.replay()
+    torch.cuda.synchronize()
+    from paper_1611_05319_b200._device import SegmentSet
+
+    for b in range(3):
+        part = parts[b // 2]
+        one = fill_device(images[b:b + 1], labels[b:b + 1], None, p,
+                          splines=SegmentSet(splines[b], images.device))
+        assert torch.equal(part["out"][b % 2], one["out"][0])
+        assert torch.equal(part["stats"][b % 2], one["stats"][0])
+
+
+def test_bench_line_single_gpu(tmp_path):
+    """bench.py's own rank loop end to end (short): one JSON line with the C2
+    value, the C5 block, launch counts from the library counter."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--steps", "3",
+                          "--warmup", "3", "--c5-frames", "6", "--chunk", "4", "--no-cpu"],
+                         capture_output=True, text=True, timeout=900, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert line["n_gpus"] == 1 and line["value"] > 0
+    assert line["c5"]["frames_total"] == 6 and line["c5"]["value"] > 0
+    assert line["gpu_launches"] == 2 * 3
+    assert line["e2e"]["value"] > 0 and line["c5"]["e2e"]["value"] > 0

@@ -1,11 +1,14 @@
 """World-size-2 gloo run of the frame-parallel (video) path on CPU.
 
-Each rank takes its contiguous frame block (video.frame_block), fills it
-with the CPU oracle standing in for the GPU kernel, and the ranks exchange
-per-frame digests and their timings with the same collectives bench.py uses
-(all_gather / all_reduce MAX).  The gathered results must equal a single
-process filling every frame: the partition neither drops, duplicates nor
-couples frames.
+Each rank takes its contiguous frame block (video.frame_block), fills it --
+with the CPU oracle standing in for the GPU kernel, since this container has
+no GPU -- and the ranks combine their results with the package's own
+bookkeeping collectives (video.reduce_over_ranks: pixel/byte sums and the
+max step time, what bench.py reports for N > 1) plus an all_gather of
+per-frame digests.  The gathered results must equal a single process filling
+every frame: the partition neither drops, duplicates nor couples frames.
+The GPU side of the same path (fill_video_multi, bench.py's rank loop) is
+covered by tests/test_gpu_configs.py.
 """
 
 import os
@@ -18,7 +21,7 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from paper_1611_05319_b200 import scenes
-from paper_1611_05319_b200.video import frame_block, frame_checksum
+from paper_1611_05319_b200.video import frame_block, frame_checksum, reduce_over_ranks
 
 N_FRAMES = 5
 
@@ -49,11 +52,11 @@ def _worker(rank, world, port, out_q):
         digests[f, 1] = it
     gathered = [torch.zeros_like(digests) for _ in range(world)]
     dist.all_gather(gathered, digests)
-    t = torch.tensor([float(rank + 1)], dtype=torch.float64)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    px = sum(int((_frame(f).labels == 255).sum()) for f in mine)
+    sums, maxes = reduce_over_ranks(sums=[px, len(mine)], maxes=[float(rank + 1)])
     if rank == 0:
         merged = torch.stack(gathered).max(dim=0).values
-        out_q.put((merged.numpy(), float(t.item()), [list(frame_block(N_FRAMES, world, r))
+        out_q.put((merged.numpy(), maxes[0], sums, [list(frame_block(N_FRAMES, world, r))
                                                     for r in range(world)]))
     dist.destroy_process_group()
 
@@ -85,11 +88,14 @@ def test_two_rank_gloo_video_fill_matches_single_process():
     procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
     for p in procs:
         p.start()
-    merged, tmax, blocks = q.get(timeout=300)
+    merged, tmax, sums, blocks = q.get(timeout=300)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
     assert blocks == [[0, 1, 2], [3, 4]]
     assert tmax == 2.0
+    assert sums == [float(sum(int((_frame(f).labels == 255).sum()) for f in range(N_FRAMES))),
+                    float(N_FRAMES)]
+    assert reduce_over_ranks(sums=[3], maxes=[4.0]) == ([3.0], [4.0])  # no process group
     single = np.array([_fill(f) for f in range(N_FRAMES)])
     assert np.array_equal(merged, single)
