@@ -280,3 +280,28 @@ def coherence_scenes(n=10, seed=4242):
                      order="smart", neighborhood="rotated_ball",
                      g_source="modified_structure_tensor"))
     return out
+
+
+def deadlock_scenes(size=256, thetas=(10.0, 25.0, 40.0, 73.0), mus=(50.0, 100.0), seed=2019):
+    """SURVEY.md Appendix B / section 7 hard part 2: half-planes with a rotated
+    guide, smart order -- the reference's deadlock-chain scene
+    (test_engine.py:277-291) at 256x256.  Low angles fill one pixel per
+    shell through the deadlock guard for 16-22K shells."""
+    out = []
+    H = W = size
+    jj, ii = np.mgrid[0:H, 0:W].astype(np.float64)
+    base = np.stack([0.5 + 0.3 * np.sin(ii / (9.0 + 4.0 * c) + jj / (13.0 + 3.0 * c) + seed % 7 + c)
+                     for c in range(3)], axis=-1)  # smooth: the fixtures compress
+    for th_deg in thetas:
+        for mu in mus:
+            lab = np.zeros((H, W), dtype=np.uint8)
+            lab[H // 2:, :] = INPAINT
+            img = base.copy()
+            img[lab == INPAINT] = 0.0
+            th = math.radians(th_deg)
+            g = np.zeros((H, W, 2))
+            g[..., 0] = math.cos(th)
+            g[..., 1] = math.sin(th)
+            out.append(_case(f"halfplane_{th_deg:g}deg_mu{mu:g}", img, lab, g, tracked=True,
+                             r=3, mu=mu, order="smart", neighborhood="rotated_ball"))
+    return out

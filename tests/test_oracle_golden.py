@@ -105,3 +105,24 @@ def test_coherence_directions_match_reference():
     for s, r in ((2.0, 4.0), (1.0, 2.0)):
         g = orc.coherence_directions(img, lab == 0, gold["dirs_ii"], gold["dirs_jj"], sigma=s, rho=r)
         assert g.tobytes() == gold[f"dirs_s{s:g}_r{r:g}"].tobytes()
+
+
+DL_CASES = cases.deadlock_scenes(thetas=(73.0,), mus=(50.0,))
+
+
+def test_oracle_deadlock_chain_matches_reference():
+    """The oracle in the deadlock regime: the 73 degree
+    half-plane, 4,288 shells, bit-exact against the reference's fixture (the
+    other angles take minutes on the CPU and are checked on the GPU only)."""
+    gold = np.load(os.path.join(GOLD, "deadlock_golden.npz"))
+    case = DL_CASES[0]
+    key = "d006"
+    assert str(gold[f"{key}_name"]) == case["name"]
+    res = orc.fill(case["image"], case["labels"], case["guide"],
+                   orc.Params(**case["params"]), tracked=True)
+    assert np.array_equal(res["fillshell"], gold[f"{key}_fillshell"])
+    assert np.array_equal(res["enter"], gold[f"{key}_enter"])
+    rows = np.array([(r[1], r[4]) for r in res["rows"]], dtype=np.int32).reshape(-1, 2)
+    assert np.array_equal(rows, gold[f"{key}_rows"])
+    inp = case["labels"] == 255
+    assert float(np.abs(res["u"][inp] - gold[f"{key}_uq"] / 65535.0).max()) <= 1e-5
