@@ -1,0 +1,4 @@
+timeout -s KILL 900 python -m pytest tests/test_gpu_deadlock.py tests/test_gpu_parity.py -q -x > gpurun_out/pytest_dl.log 2>&1; echo "pytest rc=$?"; tail -5 gpurun_out/pytest_dl.log
+timeout -s KILL 600 python tools/exp_deadlock.py --reps 2 2>&1 | tee gpurun_out/exp_dl.json
+timeout -s KILL 900 python bench.py --no-cpu --no-e2e --steps 30 > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"; python -c "
+import json; d=json.loads(open('gpurun_out/bench.json').read().strip().splitlines()[-1]); print('C2 ms', d['ms_per_step'], 'C5 ms/frame', d['c5']['ms_per_frame_per_gpu'], d['c5']['roofline']['frac'])"; tail -5 gpurun_out/bench.err
