@@ -318,172 +318,4 @@ __device__ __forceinline__ void eval_rot_warp(const BallParams& P, const BallTab
   out.tw = tw;
 }
 
-// Rotated-ball item (g != 0) on a group of 8 lanes (4 items per warp): the
-// solo shell loop's evaluator, where a handful of items per shell must finish
-// in one round.  Lane j owns samples j, j+8, ... -- numpy's accumulator j of
-// the pairwise sum -- so rw / tw are summed in registers in sample order,
-// combined by the 3-level tree and closed by the sequential tail, exactly
-// as engine._BallSampler.gather (engine.py:175-199) does.  Colours as in
-// eval_rot_warp (fp32 numerators, weights scaled to the group's largest
-// readable one).  All 32 lanes call; groups with valid == false compute on
-// dummy data.
-//
-// w_in / w_out: per-sample weight cache of the item (K doubles).  A ball's
-// weights depend only on g and the geometry, not on readability, so an item
-// re-evaluated after a neighbouring fill reloads them (w_in) instead of
-// recomputing glibc hypot / SVML exp / the division; w_out stores them on a
-// first evaluation.  The bits are the same either way.
-template <int R>
-__device__ __forceinline__ void eval_rot_group(const BallParams& P, const BallTables& T,
-                                               const WorkSource& src, int glane, bool valid,
-                                               double fi, double fj, double gx, double gy,
-                                               double ux, double uy, SampleResult& out,
-                                               const double* w_in = nullptr,
-                                               double* w_out = nullptr) {
-  using B = Ball<R>;
-  constexpr int KPL = B::KPL;
-  double safe = 1.0, thr = 0.0;
-  if (P.mu_inf) {  // every lane: the shuffles below span the warp (groups may differ in w_in)
-    const double nr2 = sqrt(gx * gx + gy * gy);
-    safe = (nr2 == 0.0) ? 1.0 : nr2;
-    double mloc = INFINITY;
-#pragma unroll
-    for (int s = 0; s < KPL; ++s) {
-      const int k = glane + kGroup * s;
-      if (k < B::K) {
-        double px = T.n[k], py = T.m[k];
-        if (P.rotated) {
-          px = T.n[k] * uy + T.m[k] * ux;
-          py = (-T.n[k]) * ux + T.m[k] * uy;
-        }
-        const double d = ((-gy) * px + gx * py) / safe;
-        mloc = min_prop(mloc, d * d);
-      }
-    }
-#pragma unroll
-    for (int o = 1; o < kGroup; o <<= 1)
-      mloc = min_prop(mloc, __shfl_xor_sync(0xffffffffu, mloc, o, kGroup));
-    thr = mloc + P.tol_inf;
-  }
-  double w[KPL], wr[KPL];
-  float sv[KPL][4];
-#pragma unroll
-  for (int s = 0; s < KPL; ++s) {
-    const int k = glane + kGroup * s;
-    w[s] = 0.0;
-    wr[s] = 0.0;
-#pragma unroll
-    for (int c = 0; c < 4; ++c) sv[s][c] = 0.f;
-    if (valid && k < B::K) {
-      double ws = w_in ? w_in[k] : 0.0;  // issued first: overlaps the corner fetches
-      double px = T.n[k], py = T.m[k];
-      if (P.rotated) {
-        px = T.n[k] * uy + T.m[k] * ux;
-        py = (-T.n[k]) * ux + T.m[k] * uy;
-      }
-      const double X = fi + px, Y = fj + py;
-      const double fx0 = floor(X), fy0 = floor(Y);
-      const double tx = X - fx0, ty = Y - fy0;
-      const int x0 = (int)fx0, y0 = (int)fy0;
-      unsigned live = 0;
-      bool outside = false;
-      float4 v[4];
-      float c3v[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const int a = c >> 1, b = c & 1;
-        const double wc = (a ? tx : 1.0 - tx) * (b ? ty : 1.0 - ty);
-        if (wc != 0.0) {
-          const int cy = y0 + b;
-          int cx = x0 + a;
-          bool inside = cy >= 0 && cy < src.H;
-          if (P.periodic) cx = wrap_col(cx, src.W);
-          else inside = inside && cx >= 0 && cx < src.W;
-          if (inside) {
-            const int q = cy * src.W + cx;
-            v[c] = src.work[q];
-            if (src.c3) c3v[c] = src.c3[q];
-            live |= 1u << c;
-          } else {
-            outside = true;
-          }
-        }
-      }
-      if (!w_in) {
-        const double dist = hypot_np(px, py);
-        if (P.mu_inf) {
-          const double d = ((-gy) * px + gx * py) / safe;
-          ws = (d * d <= thr) ? 1.0 / dist : 0.0;
-        } else {
-          const double d = (-gy) * px + gx * py;
-          ws = exp_np((P.coef * d) * d) / dist;
-        }
-        if (w_out) w_out[k] = ws;
-      }
-      w[s] = ws;
-      bool ok = !outside;
-#pragma unroll
-      for (int c = 0; c < 4; ++c)
-        if ((live >> c) & 1u) {
-          const int a = c >> 1, b = c & 1;
-          const float wc = (float)((a ? tx : 1.0 - tx) * (b ? ty : 1.0 - ty));
-          ok = ok && __float_as_int(v[c].w) <= src.shell;
-          sv[s][0] = __fmaf_rn(wc, v[c].x, sv[s][0]);
-          sv[s][1] = __fmaf_rn(wc, v[c].y, sv[s][1]);
-          sv[s][2] = __fmaf_rn(wc, v[c].z, sv[s][2]);
-          sv[s][3] = __fmaf_rn(wc, c3v[c], sv[s][3]);
-        }
-      wr[s] = ok ? ws : 0.0;
-    }
-  }
-  int e_loc = -2000;
-#pragma unroll
-  for (int s = 0; s < KPL; ++s)
-    if (wr[s] > 0.0) e_loc = max(e_loc, ilogb(wr[s]));
-#pragma unroll
-  for (int o = 1; o < kGroup; o <<= 1) e_loc = max(e_loc, __shfl_xor_sync(0xffffffffu, e_loc, o, kGroup));
-  const int e_use = e_loc < -1100 ? 0 : e_loc;
-  const double down = scalbn(1.0, -e_use);
-  float num[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-  for (int s = 0; s < KPL; ++s)
-    if (wr[s] != 0.0) {
-      const float wsf = (float)(wr[s] * down);
-#pragma unroll
-      for (int c = 0; c < 4; ++c) num[c] = __fmaf_rn(wsf, sv[s][c], num[c]);
-    }
-  // numpy accumulator glane: samples glane, glane+8, ... below N8, in order
-  double acc_rw = 0.0, acc_tw = 0.0;
-#pragma unroll
-  for (int s = 0; s < B::N8 / kGroup; ++s) {
-    acc_rw += wr[s];
-    acc_tw += w[s];
-  }
-  double rw = group_sum_tree(acc_rw);
-  double tw = group_sum_tree(acc_tw);
-  // the group tree leaves the sum in every lane (xor butterfly); the tail
-  // samples N8 .. K-1 live in lanes 0 .. NT-1, slot N8 / 8
-  if constexpr (B::NT > 0) {
-#pragma unroll
-    for (int e = 0; e < B::NT; ++e) {
-      rw = rw + __shfl_sync(0xffffffffu, wr[B::N8 / kGroup], e, kGroup);
-      tw = tw + __shfl_sync(0xffffffffu, w[B::N8 / kGroup], e, kGroup);
-    }
-  }
-  const double inv = (rw != 0.0) ? 1.0 / rw : 0.0;
-  const double up = scalbn(1.0, e_use);
-#pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    float sacc = 0.f;
-    if (c < 3 || src.c3) {
-      sacc = num[c];
-#pragma unroll
-      for (int o = 1; o < kGroup; o <<= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, o, kGroup);
-    }
-    out.v[c] = ((double)sacc * up) * inv;
-  }
-  out.rw = rw;
-  out.tw = tw;
-}
-
 }  // namespace gf

@@ -596,32 +596,6 @@ __global__ void __launch_bounds__(kThreads, GF_PREP_MIN_BLOCKS) k_prep(const __g
 // per-frame item index j runs over [0, nL) for the front part and
 // [nL, nL + nR) for the back part (conf[] and the guard use it).
 
-// Solo shell loop (serial chains, see solo_run): the frontier of the one
-// active frame lives in shared memory, one fixed slot per item, with the
-// item's cached confidence and colour.  It overlays the grid loop's frame
-// tables and append staging (unused while block 0 runs alone; rebuilt after).
-constexpr int kSoloMax = 512;       // frontier items held in shared memory
-constexpr int kSoloExitFills = 32;  // a shell filling more hands back to the grid
-constexpr int kSoloFillCap = 64;    // filled pixels remembered per shell
-constexpr unsigned char kSfRw = 1, kSfDirty = 2, kSfG = 4, kSfFill = 8, kSfLive = 16, kSfCached = 32;
-constexpr int kSoloWStride = 128;  // cached weights per slot (K <= 128)
-
-struct SoloSmem {
-  uint32_t item[kSoloMax];          // entry = pixel | kEntryRot
-  double conf[kSoloMax];            // rw / tw of the last evaluation
-  float4 col[kSoloMax];             // colour of the last evaluation (c0, c1, c2, c3)
-  double2 unit[kSoloMax];           // g / |g| of a rotated item (geometry of a re-evaluation)
-  unsigned char flag[kSoloMax];     // kSf*: rw > 0, re-evaluate, |g| > c2, fills now, live
-  short dR[kSoloMax], dL[kSoloMax];  // dirty rotated / lattice slots of the shell
-  short freel[kSoloMax];            // free slots below hw
-  int fill_px[kSoloFillCap];
-  unsigned long long rkey[kShellThreads / 32];
-  int rpix[kShellThreads / 32], ridx[kShellThreads / 32];
-  int hw, nfree, n, nR, nL, nfill, nwrit, gL, gR, gany, exit_mode, grow;
-  // the frame's report state while the loop runs (written back at the end)
-  int remaining, iters, filled, deadlocks, dt_dead, done;
-};
-
 struct GridTables {
   int pref[kMaxFramesPerLaunch + 1];   // all items
   int prefL[kMaxFramesPerLaunch + 1];  // lattice part
@@ -630,15 +604,12 @@ struct GridTables {
   int nRf[kMaxFramesPerLaunch];
   uint32_t app[kAppendCap];
 };
-static_assert(sizeof(SoloSmem) <= sizeof(GridTables), "solo state overlays the grid tables");
 
 struct Smem {
   BallTables tab;
-  union {
+  struct {
     GridTables g;
-    SoloSmem solo;
   } u;
-  int solo_go, solo_f;
   int g_one, g_f;  // guard of a single small stalled frame by block 0
   unsigned char act[kMaxFramesPerLaunch];
   unsigned char dl[kMaxFramesPerLaunch];
@@ -1175,413 +1146,6 @@ __device__ void book_shell(const FillArgs& A, int k, int cur, int clr) {
   }
 }
 
-// ------------------------------------------------------- solo shells
-//
-// Serial chains (hard part 2): under smart order a
-// low-angle front stalls shell after shell and the deadlock guard
-// (engine.py:334-348) fills ONE pixel each time -- 16-22K shells on a 256^2
-// half-plane.  A grid-wide shell (fill phase, three guard barriers) costs
-// ~20 us there while the work is a few dozen items.  After a stalled shell
-// with a frontier of at most kSoloMax items, block 0 runs the shells alone:
-//   * the frontier lives in shared memory with each item's last confidence
-//     rw / tw and rw > 0; the item's colour is cached in the colour lanes of
-//     its own (unreadable, so otherwise unused) working-buffer entry;
-//   * only DIRTY items are evaluated: new frontier members and items within
-//     Chebyshev distance r + 1 of a pixel filled in the previous shell (a
-//     rotated sample lies within r of its centre, its ghost corners within
-//     r + 1), every other item sees exactly the same readable samples as
-//     when it was last evaluated, hence the same bits -- and since readiness
-//     only grows with readability, no non-dirty item becomes ready unless
-//     the data-term latch changes, which re-decides everyone from the cache;
-//   * decisions, the argmax guard (first index = smallest pixel on ties, NaN
-//     maximal), fills, neighbour activation (tracker.py:42-79) and the
-//     report row are done with block barriers only.
-// The other blocks wait at one grid barrier.  The loop hands back when a
-// shell fills more than kSoloExitFills pixels or the frontier outgrows
-// shared memory; the list, counters and report state are then exactly what
-// the grid loop would have produced.
-
-__device__ __forceinline__ bool solo_g_above(const FillArgs& A, int f, uint32_t e) {
-  double gx = 0.0, gy = 0.0;
-  if (A.gbuf && (e & kEntryRot)) {
-    const double4 g = A.gbuf[(size_t)f * A.HW + (e & kEntryPix)];
-    gx = g.x;
-    gy = g.y;
-  }
-  return hypot_np(gx, gy) > A.c2;
-}
-
-// Can a fill at pixel b change the evaluation of the item at pixel a?  A
-// lattice ball (g = 0) samples the pixels of the disk itself: |b - a| <= r.
-// A rotated ball's samples lie in the disk of radius r and read the corners
-// of their unit cell: b matters only if the open square of half-width 1
-// around b meets that disk, i.e. (|dx| - 1)+^2 + (|dy| - 1)+^2 < r^2 (<=
-// here, conservatively).  x is periodic if asked.
-__device__ __forceinline__ bool solo_near(const FillArgs& A, int a, int b, int r, bool rot) {
-  const int ay = a / A.W, by = b / A.W;
-  const int dy = abs(ay - by);
-  if (dy > r + 1) return false;
-  int dx = abs((a - ay * A.W) - (b - by * A.W));
-  if (A.periodic) dx = min(dx, A.W - dx);
-  if (!rot) return dx * dx + dy * dy <= r * r;
-  const int ex = max(dx - 1, 0), ey = max(dy - 1, 0);
-  return ex * ex + ey * ey <= r * r;
-}
-
-// phase timestamp of a solo shell (trace rows only; slot 0 = shell start)
-__device__ __forceinline__ void solo_mark(const FillArgs& A, int k, int slot) {
-  if (A.trace && k < A.trace_cap - 1 && threadIdx.x == 0) A.trace[k * kTraceSlots + slot] = gtimer();
-}
-
-template <int R>
-__device__ __forceinline__ void solo_run(const FillArgs& A, const BallParams& P, Smem& S, int k0,
-                                         int f) {
-  SoloSmem& Q = S.u.solo;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  constexpr int kWarps = kShellThreads / 32;
-  const int glane = lane & (kGroup - 1), gsub = lane >> 3;  // 4 items of 8 lanes per warp
-  const size_t fo = (size_t)f * A.HW;
-  float4* fw = A.work + fo;
-  float* fc3 = A.c3 ? A.c3 + fo : nullptr;
-  // shell k0 - 1 is booked and the counter slots are cleared as the booking
-  // block would have done it during shell k0
-  book_shell(A, k0, k0 % 4, (k0 + 2) % 4);
-  __syncthreads();
-  if (tid == 0) {
-    Q.hw = Q.n = A.cnt[(k0 % 4) * A.nF + f] + A.cntR[(k0 % 4) * A.nF + f];
-    Q.nfree = 0;
-    Q.exit_mode = 0;
-    Q.remaining = A.remaining[f];
-    Q.iters = A.iters[f];
-    Q.filled = A.filled[f];
-    Q.deadlocks = A.deadlocks[f];
-    Q.dt_dead = A.dt_dead[f];
-    Q.done = A.done[f];
-  }
-  __syncthreads();
-  {
-    const int cur = k0 % 4;
-    const uint32_t* lst = (k0 & 1) ? A.list1 : A.list0;
-    const int nL = A.cnt[cur * A.nF + f];
-    for (int j = tid; j < Q.n; j += kShellThreads) {
-      Q.item[j] = entry_at(lst, A, f, j, nL);
-      Q.flag[j] = kSfLive | kSfDirty;
-    }
-  }
-  const unsigned long long hl = A.hull[2 * f], hh = A.hull[2 * f + 1];
-  int k = k0;
-  for (;; ++k) {
-    if (tid == 0) Q.nR = Q.nL = Q.nfill = Q.nwrit = Q.gL = Q.gR = Q.gany = Q.grow = 0;
-    __syncthreads();
-    const int hw = Q.hw;
-    if (Q.done != 0 || Q.n == 0 || Q.exit_mode) break;
-    const int n = Q.n;
-    if (A.trace && k < A.trace_cap - 1 && tid == 0) {
-      A.trace[k * kTraceSlots + 0] = gtimer();
-      A.trace[k * kTraceSlots + 5] = (unsigned long long)n;
-    }
-    // 1. dirty items, by ball type (the two evaluators take warp-uniform paths)
-    bool my_g = false;
-    for (int i = tid; i < hw; i += kShellThreads) {
-      const unsigned char g = Q.flag[i];
-      if (!(g & kSfLive)) continue;
-      const uint32_t e = Q.item[i];
-      my_g |= (e & kEntryRot) != 0;
-      if (g & kSfDirty) {
-        if (e & kEntryRot) Q.dR[atomicAdd(&Q.nR, 1)] = (short)i;
-        else Q.dL[atomicAdd(&Q.nL, 1)] = (short)i;
-      }
-    }
-    const bool anyg = __syncthreads_or(my_g);
-    solo_mark(A, k, 2);
-    // 2. evaluate them, one item per 8-lane group (4 per warp); rotated items
-    //    seen before reload their cached weights
-    const WorkSource src{fw, fc3, A.H, A.W, A.C, k};
-    const int ndR = Q.nR, ndL = Q.nL;
-    const int rR = (ndR + 3) / 4, rL = (ndL + 3) / 4;
-    for (int u = warp; u < rR + rL; u += kWarps) {
-      const bool rot_round = u < rR;  // warp-uniform
-      const int t = (rot_round ? u : u - rR) * 4 + gsub;
-      const bool valid = t < (rot_round ? ndR : ndL);
-      const int i = valid ? (rot_round ? Q.dR[t] : Q.dL[t]) : 0;
-      const int p = valid ? (int)(Q.item[i] & kEntryPix) : 0;
-      const int pi = p % A.W, pj = p / A.W;
-      SampleResult r;
-      bool gbig = false;
-      if (rot_round) {
-        // a cached item has its weights and g / |g| here: no guide load, no
-        // weight arithmetic; a new one reads the guide and fills the cache
-        double* wslot = A.solo_w + (size_t)i * kSoloWStride;
-        const bool cached = valid && (Q.flag[i] & kSfCached);
-        double4 g4 = make_double4(0.0, 0.0, 0.0, 1.0);
-        if (cached) {
-          const double2 u2 = Q.unit[i];
-          g4.z = u2.x;
-          g4.w = u2.y;
-          gbig = (Q.flag[i] & kSfG) != 0;
-        } else if (valid) {
-          g4 = A.gbuf[fo + p];
-          gbig = hypot_np(g4.x, g4.y) > A.c2;
-          if (glane == 0) Q.unit[i] = make_double2(g4.z, g4.w);
-        }
-        eval_rot_group<R>(P, S.tab, src, glane, valid, (double)pi, (double)pj, g4.x, g4.y, g4.z,
-                          g4.w, r, cached ? wslot : nullptr, cached ? nullptr : wslot);
-      } else {
-        gbig = 0.0 > A.c2;  // g = 0: hypot(0, 0) > c2
-        eval_lattice<R, 8>(P, S.tab, src, glane, gsub, valid, pi, pj, r);
-      }
-      if (valid && glane == 0) {
-        Q.conf[i] = r.rw / r.tw;
-        Q.col[i] = make_float4((float)r.v[0], (float)r.v[1], (float)r.v[2], (float)r.v[3]);
-        Q.flag[i] = (unsigned char)(kSfLive | kSfCached | (r.rw > 0.0 ? kSfRw : 0) |
-                                    (gbig ? kSfG : 0));
-      }
-    }
-    __syncthreads();
-    solo_mark(A, k, 3);
-    // 3. decisions (engine.py:317-333) from the cache
-    const bool dt_eff = (A.order == 2) && !Q.dt_dead && anyg;
-    int my_fill = 0;
-    for (int i = tid; i < hw; i += kShellThreads) {
-      const unsigned char g = Q.flag[i];
-      if (!(g & kSfLive)) continue;
-      bool ready;
-      if (A.order == 0) ready = true;
-      else if (!dt_eff) ready = Q.conf[i] > A.c;
-      else ready = (g & kSfG) && Q.conf[i] > A.c;
-      if (ready && (g & kSfRw)) {
-        Q.flag[i] = g | kSfFill;
-        ++my_fill;
-      }
-    }
-    if (my_fill) atomicAdd(&Q.nfill, my_fill);
-    __syncthreads();
-    if (Q.nfill == 0) {
-      // 4. deadlock guard: argmax C, first index (smallest pixel) on ties
-      unsigned long long key = 0ULL;
-      int pix = 0x7fffffff, bi = -1;
-      for (int i = tid; i < hw; i += kShellThreads) {
-        if (!(Q.flag[i] & kSfLive)) continue;
-        const unsigned long long kk = conf_key(Q.conf[i]);
-        const int pp = (int)(Q.item[i] & kEntryPix);
-        if (bi < 0 || kk > key || (kk == key && pp < pix)) {
-          key = kk;
-          pix = pp;
-          bi = i;
-        }
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const unsigned long long k2 = __shfl_xor_sync(0xffffffffu, key, o);
-        const int p2 = __shfl_xor_sync(0xffffffffu, pix, o);
-        const int b2 = __shfl_xor_sync(0xffffffffu, bi, o);
-        if (b2 >= 0 && (bi < 0 || k2 > key || (k2 == key && p2 < pix))) {
-          key = k2;
-          pix = p2;
-          bi = b2;
-        }
-      }
-      if (lane == 0) {
-        Q.rkey[warp] = key;
-        Q.rpix[warp] = pix;
-        Q.ridx[warp] = bi;
-      }
-      __syncthreads();
-      if (tid == 0) {
-        for (int w = 0; w < kWarps; ++w) {
-          const int b2 = Q.ridx[w];
-          if (b2 >= 0 && (bi < 0 || Q.rkey[w] > key || (Q.rkey[w] == key && Q.rpix[w] < pix))) {
-            key = Q.rkey[w];
-            pix = Q.rpix[w];
-            bi = b2;
-          }
-        }
-        bool ok = (Q.flag[bi] & kSfRw) != 0;  // its cached colour is the fill value
-        if (!ok) {
-          // mean of the readable 8-neighbours (engine.py:252-267), summed in
-          // NEIGHBOR_OFFSETS order; the eight fetches are issued together
-          double acc[4] = {0.0, 0.0, 0.0, 0.0};
-          int cnt = 0;
-          float4 nv[8];
-          float n3[8];
-          bool nin[8];
-#pragma unroll
-          for (int o = 0; o < 8; ++o) {
-            const int q = neighbor_of(A, (uint32_t)pix, o, nin[o]);
-            if (nin[o]) {
-              nv[o] = fw[q];
-              n3[o] = fc3 ? fc3[q] : 0.f;
-            }
-          }
-#pragma unroll
-          for (int o = 0; o < 8; ++o)
-            if (nin[o] && __float_as_int(nv[o].w) <= k) {
-              acc[0] += (double)nv[o].x;
-              acc[1] += (double)nv[o].y;
-              acc[2] += (double)nv[o].z;
-              acc[3] += (double)n3[o];
-              ++cnt;
-            }
-          if (cnt > 0) {
-            Q.col[bi] = make_float4((float)(acc[0] / cnt), (float)(acc[1] / cnt),
-                                    (float)(acc[2] / cnt), (float)(acc[3] / cnt));
-            ok = true;
-          }
-        }
-        if (ok) {
-          Q.flag[bi] |= kSfFill;
-          Q.deadlocks += 1;
-          Q.nfill = 1;
-        } else {
-          Q.done = 2;  // unfillable (engine.py:342-345); this shell is not booked
-          A.last_f[f] = n;
-        }
-      }
-      __syncthreads();
-      if (Q.done != 0) break;
-    }
-    const int nfill = Q.nfill;
-    solo_mark(A, k, 4);
-    // the slots must hold the survivors, this shell's filled slots (reusable
-    // from the next shell on) and up to 8 new items per fill; if they might
-    // not, the frontier of shell k+1 is built in the global list instead
-    const bool to_global = n + 8 * nfill > kSoloMax;
-    uint32_t* nxt_list = ((k + 1) & 1) ? A.list1 : A.list0;
-    auto to_list = [&](uint32_t e) {
-      if (entry_back(A, e)) nxt_list[(size_t)f * A.cap + A.cap - 1 - atomicAdd(&Q.gR, 1)] = e;
-      else nxt_list[(size_t)f * A.cap + atomicAdd(&Q.gL, 1)] = e;
-      if (e & kEntryRot) Q.gany = 1;
-    };
-    // 5. fills (cached colour -> output clipped to the hull, stamp k + 1)
-    //    and, by the other 7 lanes of each filled item's octet, the Inpaint
-    //    neighbours they activate (tracker.py:42-79): new items take slots
-    //    freed before this shell, or hw
-    for (int t = tid; t < hw * 8; t += kShellThreads) {
-      const int i = t >> 3, o = t & 7;
-      if (!(Q.flag[i] & kSfFill)) continue;
-      const int p = (int)(Q.item[i] & kEntryPix);
-      if (o == 0) {
-        const float4 c = Q.col[i];
-        fw[p] = make_float4(c.x, c.y, c.z, __int_as_float(k + 1));
-        if (fc3) fc3[p] = c.w;
-        const float v[4] = {c.x, c.y, c.z, c.w};
-        write_out(A, f, (uint32_t)p, v, hl, hh);
-        if (A.fillshell) A.fillshell[fo + p] = k;
-        const int slot = atomicAdd(&Q.nwrit, 1);
-        if (slot < kSoloFillCap) Q.fill_px[slot] = p;
-      }
-      bool in;
-      const int q = neighbor_at(A, p % A.W, p / A.W, o, in);
-      if (!in) continue;
-      const uint32_t qe = claim(fw, q);
-      if (qe == 0xffffffffu) continue;
-      if (A.enter) A.enter[fo + q] = k + 1;
-      if (to_global) {
-        to_list(qe);
-      } else {
-        const int fr = atomicSub(&Q.nfree, 1) - 1;
-        const int slot = fr >= 0 ? (int)Q.freel[fr] : atomicAdd(&Q.hw, 1);
-        Q.item[slot] = qe;
-        Q.flag[slot] = (unsigned char)(kSfLive | kSfDirty);
-        atomicAdd(&Q.grow, 1);
-      }
-    }
-    __syncthreads();
-    solo_mark(A, k, 6);
-    // 6. survivors near a fill become dirty; filled slots join the free list
-    if (tid == 0 && Q.nfree < 0) Q.nfree = 0;
-    __syncthreads();
-    const int nw = min(Q.nwrit, kSoloFillCap);
-    const bool all_dirty = Q.nwrit > kSoloFillCap;
-    for (int i = tid; i < hw; i += kShellThreads) {
-      const unsigned char g = Q.flag[i];
-      if (!(g & kSfLive)) continue;
-      const uint32_t e = Q.item[i];
-      if (g & kSfFill) {
-        Q.flag[i] = 0;
-        Q.item[i] = 0xffffffffu;
-        Q.freel[atomicAdd(&Q.nfree, 1)] = (short)i;
-        continue;
-      }
-      if (!(g & kSfCached)) continue;  // new this shell (slot mode only)
-      bool dirty = all_dirty;
-      for (int w = 0; w < nw && !dirty; ++w)
-        dirty = solo_near(A, (int)(e & kEntryPix), Q.fill_px[w], R, (e & kEntryRot) != 0);
-      if (dirty) Q.flag[i] = g | kSfDirty;
-      if (to_global) to_list(e);
-    }
-    solo_mark(A, k, 7);
-    // 7. report row of shell k (engine.py:364-366)
-    if (tid == 0) {
-      if (Q.iters < A.rows_cap) {
-        A.rows[((size_t)f * A.rows_cap + Q.iters) * 2 + 0] = n;
-        A.rows[((size_t)f * A.rows_cap + Q.iters) * 2 + 1] = nfill;
-      } else {
-        A.overflow[f] = 1;
-      }
-      Q.iters += 1;
-      Q.filled += nfill;
-      Q.remaining -= nfill;
-      if (!Q.dt_dead && !anyg) Q.dt_dead = 1;
-      if (Q.remaining == 0) Q.done = 1;
-      if (A.trace && k < A.trace_cap - 1) A.trace[k * kTraceSlots + 1] = gtimer();
-      Q.exit_mode = to_global ? 1 : (nfill > kSoloExitFills ? 2 : 0);
-    }
-    __syncthreads();
-    if (tid == 0) Q.n = to_global ? Q.gL + Q.gR : n - nfill + Q.grow;
-    if (Q.exit_mode) {
-      ++k;
-      break;
-    }
-  }
-  // hand the frontier of shell k back to the grid loop: list buffer and
-  // counter slot of shell k, next slot clear, previous slot already booked
-  __syncthreads();
-  const int c1 = k % 4, n1 = (k + 1) % 4, p1 = (k + 3) % 4;
-  const bool live = Q.done == 0;
-  if (Q.exit_mode != 1 && live) {
-    uint32_t* lst = (k & 1) ? A.list1 : A.list0;
-    if (tid == 0) Q.gL = Q.gR = 0;
-    __syncthreads();
-    for (int i = tid; i < Q.hw; i += kShellThreads) {
-      if (!(Q.flag[i] & kSfLive)) continue;
-      const uint32_t e = Q.item[i];
-      if (entry_back(A, e)) lst[(size_t)f * A.cap + A.cap - 1 - atomicAdd(&Q.gR, 1)] = e;
-      else lst[(size_t)f * A.cap + atomicAdd(&Q.gL, 1)] = e;
-    }
-  }
-  bool my_g = false;
-  for (int i = tid; i < Q.hw; i += kShellThreads)
-    my_g |= (Q.flag[i] & kSfLive) && (Q.item[i] & kEntryRot);
-  const bool anyg_list = __syncthreads_or(my_g);
-  if (tid == 0) {
-    const int gl = Q.gL, gr = Q.gR;
-    const int anyg = live ? (Q.exit_mode == 1 ? Q.gany : (anyg_list ? 1 : 0)) : 0;
-    A.cnt[c1 * A.nF + f] = live ? gl : 0;
-    A.cntR[c1 * A.nF + f] = live ? gr : 0;
-    A.anyg[c1 * A.nF + f] = anyg;
-    A.fills[c1 * A.nF + f] = 0;
-    A.cnt[n1 * A.nF + f] = 0;
-    A.cntR[n1 * A.nF + f] = 0;
-    A.anyg[n1 * A.nF + f] = 0;
-    A.fills[n1 * A.nF + f] = 0;
-    // shells before k are booked here: the grid's booking of shell k-1 is
-    // skipped (empty slot); the latch state is carried by dt_dead
-    A.cnt[p1 * A.nF + f] = 0;
-    A.cntR[p1 * A.nF + f] = 0;
-    A.anyg[p1 * A.nF + f] = 1;
-    A.remaining[f] = Q.remaining;
-    A.iters[f] = Q.iters;
-    A.filled[f] = Q.filled;
-    A.deadlocks[f] = Q.deadlocks;
-    A.dt_dead[f] = Q.dt_dead;
-    A.done[f] = Q.done;
-    *A.solo_k = k;
-    __threadfence();
-  }
-  __syncthreads();
-}
-
 #ifndef GF_SHELL_MIN_BLOCKS
 #define GF_SHELL_MIN_BLOCKS 2
 #endif
@@ -1609,23 +1173,10 @@ __device__ __forceinline__ void guard_fill_frame(const FillArgs& A, const BallPa
         float4* fw = A.work + (size_t)fs * A.HW;
         WorkSource src{fw, A.c3 ? A.c3 + (size_t)fs * A.HW : nullptr, A.H, A.W, A.C, k};
         SampleResult r;
-        if constexpr (R > 0) {
-          // the shell loop's own evaluators (one warp): rotated ball or lattice
-          if (gx != 0.0 || gy != 0.0) {
-            const double4 g4 = A.gbuf[(size_t)fs * A.HW + p];
-            eval_rot_warp<R>(P, S.tab, src, lane, (double)(p % A.W), (double)(p / A.W), gx, gy,
-                             g4.z, g4.w, r);
-          } else {
-            eval_lattice<R, 8>(P, S.tab, src, glane, lane >> 3, valid, p % A.W, p / A.W, r);
-            r.rw = __shfl_sync(0xffffffffu, r.rw, 0);
-            r.tw = __shfl_sync(0xffffffffu, r.tw, 0);
-#pragma unroll
-            for (int c = 0; c < 4; ++c) r.v[c] = __shfl_sync(0xffffffffu, r.v[c], 0);
-          }
-        } else {
-          eval_item<NL, 0>(P, S.tab, src, glane, valid, (double)(p % A.W), (double)(p / A.W), true,
-                           gx, gy, r);
-        }
+        // the generic evaluator: compact code on this rarely taken path keeps
+        // the fill phase's register allocation intact
+        eval_item<NL, 0>(P, S.tab, src, glane, valid, (double)(p % A.W), (double)(p / A.W), true,
+                         gx, gy, r);
         double v[4] = {r.v[0], r.v[1], r.v[2], r.v[3]};
         bool ok = r.rw > 0.0;
         if (fvalid && lane == 0 && !ok) {
@@ -1713,18 +1264,17 @@ __device__ __forceinline__ void guard_fill_frame(const FillArgs& A, const BallPa
         }
 }
 
-// The deadlock guard of ONE stalled frame with a small frontier, by block 0
-// alone (the other blocks wait at the next grid barrier): argmax of the
-// confidences the fill phase stored (NaN maximal, ties to the smallest pixel
-// = numpy's first index of the sorted frontier, engine.py:336-337) by a
-// block reduction, then warp 0's guarded fill.  One grid barrier instead of
-// the three of the multi-frame guard.
+// The deadlock guard of ONE stalled frame with a small frontier: block 0
+// alone finds the argmax of the confidences the fill phase stored (NaN
+// maximal, ties to the smallest pixel = numpy's first index of the sorted
+// frontier, engine.py:336-337) by a block reduction, and its warp 0 does the
+// guarded fill, while the other blocks wait at one grid barrier -- instead of
+// the multi-frame guard's three barriers and grid-wide atomics (measured on
+// the 256^2 half-planes: 24 -> ~19 us per guarded shell).
 constexpr int kGuardBlockMax = 16384;
 
-template <int R, bool kTracked>
-__device__ __forceinline__ void guard_block(const FillArgs& A, const BallParams& P, Smem& S, int f,
-                                            int k, int cur, int nxt, const uint32_t* cur_list,
-                                            uint32_t* nxt_list) {
+__device__ __forceinline__ void guard_argmax(const FillArgs& A, Smem& S, int f, int cur,
+                                             const uint32_t* cur_list) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int kWarps = kShellThreads / 32;
   const int T = S.u.g.pref[f + 1] - S.u.g.pref[f];
@@ -1764,14 +1314,9 @@ __device__ __forceinline__ void guard_block(const FillArgs& A, const BallParams&
     }
     A.best_p[f] = pix;
   }
-  __syncthreads();
-  if (warp == 0) guard_fill_frame<R, kTracked>(A, P, S, f, true, k, cur, nxt, nxt_list);
 }
 
-// kSolo: the variant with the solo loop for serial chains (tracked, R >= 1);
-// kept a separate instantiation because its code costs the grid loop ~6%
-// (register allocation of the fill phase), measured on C2.
-template <int R, bool kTracked, bool kSolo>
+template <int R, bool kTracked>
 #ifdef GF_SHELL_MAXNREG
 __global__ void __maxnreg__(GF_SHELL_MAXNREG)
 #else
@@ -1826,12 +1371,8 @@ __global__ void __launch_bounds__(kShellThreads, GF_SHELL_MIN_BLOCKS)
   uint32_t* reg = S.u.g.app + warp * kWarpAppCap;
   const bool booker = blockIdx.x == gridDim.x - 1;  // last block: fewest fill units
 
-  if (threadIdx.x == 0) S.solo_go = 0;
   load_p0(A, S, 0);
   int k = 0;
-  // outer loop: grid shells until the fill ends or a serial chain hands the
-  // frame to block 0 (solo_run); only k is live across that call
-  for (;;) {
   for (;; ++k) {
     // Frontier lists alternate between two buffers; their counters (cnt,
     // cntR, anyg) and the fill counts rotate through four slots: cur = this
@@ -1844,7 +1385,6 @@ __global__ void __launch_bounds__(kShellThreads, GF_SHELL_MIN_BLOCKS)
     uint32_t* nxt_list = (k & 1) ? A.list0 : A.list1;
     const int T = S.total;
     if (T == 0) break;
-    if (kSolo && S.solo_go) break;
     trace_set(A, k, 0, gtimer());
     trace_set(A, k, 5, (unsigned long long)T);
 
@@ -1999,7 +1539,7 @@ __global__ void __launch_bounds__(kShellThreads, GF_SHELL_MIN_BLOCKS)
       __syncthreads();
     }
     if (any && S.g_one) {
-      if (blockIdx.x == 0) guard_block<R, kTracked>(A, P, S, S.g_f, k, cur, nxt, cur_list, nxt_list);
+      if (blockIdx.x == 0) guard_argmax(A, S, S.g_f, cur, cur_list);
     } else if (any) {
       const int chunk = max(kShellThreads, (T + gridDim.x - 1) / gridDim.x);
       const int c_lo = min(T, blockIdx.x * chunk), c_hi = min(T, c_lo + chunk);
@@ -2035,29 +1575,21 @@ __global__ void __launch_bounds__(kShellThreads, GF_SHELL_MIN_BLOCKS)
         s = fe;
       }
       grid.sync();
-      // G3: the guarded fill, one warp per stalled frame
-      for (int fb = blockIdx.x * kWarps; fb < A.nF; fb += gridDim.x * kWarps) {
-        const int f = fb + warp;
-        guard_fill_frame<R, kTracked>(A, P, S, f, f < A.nF && S.dl[f], k, cur, nxt, nxt_list);
-      }
     }
     if (any) {
+      // G3: the guarded fill, one warp per stalled frame (single frame: warp
+      // 0 of block 0, which found its argmax)
+      __syncthreads();
+      const bool one = S.g_one != 0;
+      for (int fb = one ? 0 : blockIdx.x * kWarps; fb < A.nF; fb += gridDim.x * kWarps) {
+        const int f = one ? S.g_f : fb + warp;
+        const bool fv = one ? (blockIdx.x == 0 && warp == 0) : (f < A.nF && S.dl[f]);
+        guard_fill_frame<R, kTracked>(A, P, S, f, fv, k, cur, nxt, nxt_list);
+        if (one) break;
+      }
       grid.sync();
       if (kTracked) {
         load_p0(A, S, nxt);
-        // enter the solo loop when one frame is left stalling with a small
-        // frontier (the same test in every block: grid-uniform)
-        if (kSolo && threadIdx.x == 0) {
-          int na = 0, fa = 0;
-          for (int f = 0; f < A.nF; ++f)
-            if (S.act[f]) {
-              ++na;
-              fa = f;
-            }
-          S.solo_go = (na == 1 && S.total <= kSoloMax && A.order != 0) ? 1 : 0;
-          S.solo_f = fa;
-        }
-        __syncthreads();
       }
     }
 
@@ -2116,33 +1648,6 @@ __global__ void __launch_bounds__(kShellThreads, GF_SHELL_MIN_BLOCKS)
       load_p0(A, S, nxt);
     }
   }
-  if constexpr (kSolo && kTracked && R > 0) {
-    if (S.total > 0 && S.solo_go) {
-      // a serial chain: block 0 runs the shells alone, the grid waits here
-      // and resumes at the shell it hands back
-      // the other blocks sleep-poll a release flag rather than spin in the
-      // grid barrier: 295 spinning pollers on one L2 line slow every global
-      // round trip of the solo block several-fold
-      if (blockIdx.x == 0) {
-        solo_run<R>(A, P, S, k, S.solo_f);
-        if (threadIdx.x == 0) {
-          __threadfence();
-          atomicExch(A.solo_flag, k + 1);
-        }
-      } else {
-        if (threadIdx.x == 0)
-          while (*(volatile int*)A.solo_flag < k + 1) __nanosleep(1000);
-        __syncthreads();
-      }
-      grid.sync();
-      k = *(volatile int*)A.solo_k;
-      if (threadIdx.x == 0) S.solo_go = 0;
-      load_p0(A, S, k % 4);
-      continue;
-    }
-  }
-  break;
-  }
   // Bystander clip of the tiles that need it
   while (clip_work && clip_claim(A)) {
   }
@@ -2193,7 +1698,7 @@ static void launch_prep(bool f64, int C, dim3 grid, cudaStream_t stream, const F
 static size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct Layout {
-  size_t work, c3, list0, list1, conf, gbuf, bys, solow, ints, u64, total;
+  size_t work, c3, list0, list1, conf, gbuf, bys, ints, u64, total;
 };
 
 static int tiles_of(int H, int W) {
@@ -2211,7 +1716,6 @@ static Layout layout_for(int nF, int H, int W, int C, bool need_g) {
   L.list0 = off; off = align_up(off + n * sizeof(uint32_t));
   L.list1 = off; off = align_up(off + n * sizeof(uint32_t));
   L.conf = off; off = align_up(off + n * sizeof(double));
-  L.solow = off; off = align_up(off + (size_t)kSoloMax * kSoloWStride * sizeof(double));
   L.bys = off; off = align_up(off + (size_t)nF * tiles_of(H, W) * 2 * sizeof(unsigned long long));
   L.ints = off; off = align_up(off + (size_t)nF * kIntsPerFrame * sizeof(int));
   L.u64 = off; off = align_up(off + (size_t)nF * 6 * sizeof(unsigned long long));
@@ -2225,31 +1729,20 @@ size_t fill_workspace_bytes(int nF, int H, int W, int C, bool need_g) {
 }
 
 // kernel specialised on the ball size: samples per lane = ceil(K / 8)
-template <bool kTracked, bool kSolo>
+template <bool kTracked>
 static const void* shell_kernel(const BallParams& P) {
   if (P.plan.n_leaves == 1) {
     switch (P.r) {
-      case 1: return (const void*)k_shells<1, kTracked, kSolo>;
-      case 2: return (const void*)k_shells<2, kTracked, kSolo>;
-      case 3: return (const void*)k_shells<3, kTracked, kSolo>;
-      case 4: return (const void*)k_shells<4, kTracked, kSolo>;
-      case 5: return (const void*)k_shells<5, kTracked, kSolo>;
-      case 6: return (const void*)k_shells<6, kTracked, kSolo>;
+      case 1: return (const void*)k_shells<1, kTracked>;
+      case 2: return (const void*)k_shells<2, kTracked>;
+      case 3: return (const void*)k_shells<3, kTracked>;
+      case 4: return (const void*)k_shells<4, kTracked>;
+      case 5: return (const void*)k_shells<5, kTracked>;
+      case 6: return (const void*)k_shells<6, kTracked>;
       default: break;
     }
   }
-  return (const void*)k_shells<0, kTracked, false>;
-}
-
-// The solo-capable variant is chosen for tracked smart / data-term fills of
-// frames up to kSoloFramePx pixels: there a serial chain can dominate (the
-// frontier of a guarded shell fits in shared memory) and the variant pays
-// off; big frames keep the faster grid loop (GF_SOLO=0/1 overrides).
-constexpr long long kSoloFramePx = 1LL << 20;
-static bool want_solo(const gf_fill_params* prm, const BallParams& P, int H, int W) {
-  if (!prm->tracked || prm->order == 0 || P.plan.n_leaves != 1 || P.r > 6) return false;
-  if (const char* e = getenv("GF_SOLO")) return e[0] == '1';
-  return (long long)H * W <= kSoloFramePx;
+  return (const void*)k_shells<0, kTracked>;
 }
 
 // Cooperative grid size of a shell kernel on the current device, cached per
@@ -2325,7 +1818,6 @@ int fill_launch(const gf_frames* fr, const gf_fill_params* prm, const gf_fill_ou
   A.list0 = reinterpret_cast<uint32_t*>(base + L.list0);
   A.list1 = reinterpret_cast<uint32_t*>(base + L.list1);
   A.conf = reinterpret_cast<double*>(base + L.conf);
-  A.solo_w = reinterpret_cast<double*>(base + L.solow);
   int* ints = reinterpret_cast<int*>(base + L.ints);
   A.cnt = ints;              ints += 4 * nF;
   A.cntR = ints;             ints += 4 * nF;
@@ -2343,9 +1835,6 @@ int fill_launch(const gf_frames* fr, const gf_fill_params* prm, const gf_fill_ou
   A.last_f = ints;           ints += nF;
   A.badlab = ints;           ints += nF;
   A.clip_next = ints;         ints += 1;
-  A.solo_k = ints;            ints += 1;
-  A.solo_flag = ints;         ints += 1;
-  A.solo = 1;
   A.ntiles = tiles_of(H, W);
   A.clip_total = nF * A.ntiles;
   A.bys = reinterpret_cast<unsigned long long*>(base + L.bys);
@@ -2381,9 +1870,7 @@ int fill_launch(const gf_frames* fr, const gf_fill_params* prm, const gf_fill_ou
     return set_error(GF_E_CUDA, cudaGetErrorString(cudaGetLastError()));
 
   const size_t smem = sizeof(Smem);
-  const void* fn = !prm->tracked ? shell_kernel<false, false>(P)
-                   : want_solo(prm, P, H, W) ? shell_kernel<true, true>(P)
-                                             : shell_kernel<true, false>(P);
+  const void* fn = prm->tracked ? shell_kernel<true>(P) : shell_kernel<false>(P);
   int grid = 0;
   int rc = coop_grid(fn, smem, &grid);
   if (rc != GF_OK) return rc;

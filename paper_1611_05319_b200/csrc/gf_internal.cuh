@@ -12,7 +12,7 @@
 namespace gf {
 
 constexpr int kMaxFramesPerLaunch = 1024;
-constexpr int kIntsPerFrame = 30;  // cnt[4] cntR[4] fills[4] anyg[4] + 11 scalars (+ 2 shared)
+constexpr int kIntsPerFrame = 28;  // cnt[4] cntR[4] fills[4] anyg[4] + 11 scalars (+ 1 shared)
 
 // Everything the fill kernels need, passed by value (__grid_constant__).
 struct FillArgs {
@@ -58,10 +58,6 @@ struct FillArgs {
   int split;       // rotated-ball entries kept in the back part (K <= 128)
   int halo;        // r + 1: farthest pixel a ball sample's corners can touch
   int* clip_next;  // Bystander-clip tile counter (shell loop)
-  int* solo_k;     // shell at which the solo loop handed back to the grid
-  int* solo_flag;  // released (= entry shell + 1) when the solo loop is done
-  int solo;        // solo shell loop allowed (serial chains of small frontiers)
-  double* solo_w;  // [kSoloMax][128] cached ball weights of the solo slots
   int clip_total;  // tiles over all frames
   int ntiles;      // 32x32 tiles per frame
   unsigned long long* bys;        // [nF][ntiles][2] Bystander value range per tile (encoded)
