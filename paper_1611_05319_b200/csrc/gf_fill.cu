@@ -25,6 +25,8 @@
 //                atomic per tile; untracked -- full-lattice rescan;
 // separated by grid-wide barriers, so the host never sees a shell.
 #include <cooperative_groups.h>
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -132,6 +134,15 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 constexpr int kMaxCand = 512;
+constexpr int kLabBoxMax = 64;  // label box row: columns tx0 - 16 .. tx0 + 47 (a TMA box
+                                // must start on a 16-byte boundary)
+
+// TMA descriptors of one k_prep_tma launch: image / output (W*C, H, nF) in the
+// caller's dtype, labels (W, H, nF) u8
+struct PrepMaps {
+  CUtensorMap img, out, lab;
+  int lab_bw;  // label box width in bytes (kLabBoxMax)
+};
 constexpr int kTile = 32;
 constexpr int kMaxHalo = GF_MAX_RADIUS + 1;
 constexpr int kTileExt = kTile + 2 * kMaxHalo;  // 58 <= 64: one 64-bit row mask
@@ -586,6 +597,462 @@ __global__ void __launch_bounds__(kThreads, GF_PREP_MIN_BLOCKS) k_prep(const __g
   }
   timeline_mark(A, 0, false);
 }
+
+// ------------------------------------------------------------ TMA helpers
+// (raw PTX: mbarrier transaction counts, 3-D bulk tensor copies)
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra.uni WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y, int z,
+                                            unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<unsigned long long>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, int x, int y, int z, const void* src) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+                   reinterpret_cast<unsigned long long>(map)),
+               "r"(x), "r"(y), "r"(z), "r"(smem_u32(src))
+               : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+
+// Prep with TMA (frames whose rows are 16-byte multiples, not periodic): the
+// same pass as k_prep, but the pixel tile and the label halo arrive by two
+// bulk tensor loads into shared memory and the copy to the output is one
+// bulk tensor store -- no per-thread global traffic on the streaming part.
+template <typename T, int C>
+__global__ void __launch_bounds__(kThreads, GF_PREP_MIN_BLOCKS)
+    k_prep_tma(const __grid_constant__ PrepMaps M, const __grid_constant__ FillArgs A) {
+  // (the maps come first: a CUtensorMap operand must be 64-byte aligned in
+  // the parameter space)
+  // grid (tile column, tile row, frame): no division for the tile index
+  const int f = blockIdx.z;
+  const int tiles_x = gridDim.x;
+  const int tix = blockIdx.x, tiy = blockIdx.y;
+  const int tile = tiy * tiles_x + tix;
+  const int tx0 = tix * kTile;
+  const int ty0 = tiy * kTile;
+  timeline_mark(A, 0, true);
+  // every prep block is resident once all have passed here: the shell
+  // kernel may start launching (it waits for this grid's completion)
+  pdl_trigger();
+  const int R = A.halo;
+  const int ext = kTile + 2 * R;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // the tile's pixels and its labels with the (r+1) halo, staged by TMA; the
+  // pixel tile goes straight back out to the output by a TMA store (the copy
+  // of engine.py:289 -- Readable pixels are final)
+  __shared__ __align__(128) T s_img[kTile * kTile * C];
+  __shared__ __align__(128) uint8_t s_lab[kTileExt * kLabBoxMax];
+  __shared__ __align__(8) unsigned long long s_bar;
+  if (threadIdx.x == 0) {
+    mbar_init(&s_bar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    mbar_expect_tx(&s_bar, (unsigned)(sizeof(T) * kTile * kTile * C + M.lab_bw * ext));
+    tma_load_3d(s_img, &M.img, tx0 * C, ty0, f, &s_bar);
+    tma_load_3d(s_lab, &M.lab, tx0 - 16, ty0 - R, f, &s_bar);
+  }
+  __shared__ unsigned int s_hrow[kTileExt];
+  __shared__ unsigned int s_vrow[kTile];
+  __shared__ unsigned long long s_hrow64[kTileExt];
+  __shared__ unsigned long long s_rrow64[kTileExt];
+  __shared__ int s_cand[kMaxCand];
+  __shared__ int s_ncand;
+  __shared__ int s_cnt[kThreads / 32];
+  __shared__ int s_wl[kThreads / 32], s_wr[kThreads / 32];
+  __shared__ int s_bL, s_bR;
+  __shared__ unsigned long long s_red[4][kThreads / 32];
+  const uint8_t* lab = A.labels + (size_t)f * A.HW;
+  const T* img = reinterpret_cast<const T*>(A.image) + (size_t)f * A.HW * C;
+  float4* work = A.work + (size_t)f * A.HW;
+  const bool raster = A.n_seg > 0;
+  const int ry = threadIdx.x >> 3;
+  const int c0 = (threadIdx.x & 7) * 4;
+  const int gy = ty0 + ry;
+
+  // 1. Inpaint / Readable bitmasks of the tile + halo rows (bit x <=> ext
+  //    column x; out of lattice = neither -- TMA fills those cells with 0,
+  //    so the lattice bounds mask them), four threads per ext row, 16 label
+  //    bytes each, packed 4 at a time (one multiply per word)
+  if (threadIdx.x == 0) s_ncand = 0;
+  bool any_inp = false;
+  const unsigned long long ext_mask = ext >= 64 ? ~0ULL : ((1ULL << ext) - 1);
+  // ext columns inside the lattice
+  unsigned long long col_ok = ext_mask;
+  if (tx0 - R < 0) col_ok &= ~0ULL << (R - tx0);
+  if (tx0 - R + ext > A.W) col_ok &= (A.W - (tx0 - R)) >= 64 ? ~0ULL : ((1ULL << (A.W - (tx0 - R))) - 1);
+  mbar_wait(&s_bar, 0);
+  if (threadIdx.x == 0) {
+    fence_proxy_async();
+    tma_store_3d(&M.out, tx0 * C, ty0, f, s_img);
+    bulk_commit();
+  }
+  {
+    const int y = threadIdx.x >> 2, part = threadIdx.x & 3;
+    const int gyy = ty0 - R + y;
+    unsigned long long im = 0ULL, rm = 0ULL;
+    if (y < ext && gyy >= 0 && gyy < A.H) {
+      const uint4 q = *reinterpret_cast<const uint4*>(s_lab + y * M.lab_bw + 16 * part);
+      const unsigned w[4] = {q.x, q.y, q.z, q.w};
+      unsigned ib = 0, rb = 0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        ib |= nib4(w[i]) << (4 * i);
+        rb |= nib4(~w[i] >> 7) << (4 * i);
+      }
+      im = (unsigned long long)ib << (16 * part);
+      rm = (unsigned long long)rb << (16 * part);
+    }
+    im |= __shfl_xor_sync(0xffffffffu, im, 1);
+    rm |= __shfl_xor_sync(0xffffffffu, rm, 1);
+    im |= __shfl_xor_sync(0xffffffffu, im, 2);
+    rm |= __shfl_xor_sync(0xffffffffu, rm, 2);
+    if (part == 0 && y < ext) {
+      // box column 16 - R is ext column 0
+      im = (im >> (16 - R)) & col_ok;
+      rm = (rm >> (16 - R)) & col_ok;
+      s_hrow64[y] = im;
+      s_rrow64[y] = rm;
+      s_hrow[y] = hdilate(im, R);
+      any_inp = im != 0ULL;
+    }
+  }
+  // labels of the thread's own 4 pixels (byte u = column c0 + u)
+  uint32_t own4 = 0x80808080u;
+  if (gy < A.H) {
+    const uint8_t* lr = s_lab + (ry + R) * M.lab_bw + 16 + c0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (tx0 + c0 + u < A.W) own4 = (own4 & ~(0xffu << (8 * u))) | ((uint32_t)lr[u] << (8 * u));
+  }
+  // the thread's 4 pixels, from the staged tile
+  const int gx0 = tx0 + c0;
+  constexpr int nv = (4 * C * (int)sizeof(T)) / 16;
+  constexpr bool vec_ok = (4 * C * (int)sizeof(T)) % 16 == 0;
+  const bool row_in = gy < A.H;
+  union {
+    T t[4 * C];
+    uint4 q[nv > 0 ? nv : 1];
+  } px;
+  {
+    const T* src = s_img + (size_t)ry * kTile * C + c0 * C;
+    if constexpr (vec_ok) {
+#pragma unroll
+      for (int i = 0; i < nv; ++i) px.q[i] = reinterpret_cast<const uint4*>(src)[i];
+    } else {
+#pragma unroll
+      for (int i = 0; i < 4 * C; ++i) px.t[i] = src[i];
+    }
+  }
+  // label validation (grid.py:36-46) rides on the own-pixel load: any byte
+  // outside {0, 128, 255} flags the frame
+  {
+    const unsigned bad = ~(__vcmpeq4(own4, 0u) | __vcmpeq4(own4, 0x80808080u) |
+                           __vcmpeq4(own4, 0xffffffffu));
+    if (bad && gy < A.H) {
+      unsigned valid = 0;  // bytes of in-lattice columns
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (tx0 + c0 + u < A.W) valid |= 0xffu << (8 * u);
+      if (bad & valid) A.badlab[f] = 1;
+    }
+  }
+  const bool tile_d = __syncthreads_or(any_inp);
+  // value hull of the Readable pixels (the copy is the TMA store above)
+  {
+    // [0] value hull of the Readable pixels, [1] range of the Bystanders
+    // per pixel: channel min / max, then merged into its class (branch-free)
+    T vlo[2] = {T(INFINITY), T(INFINITY)}, vhi[2] = {T(-INFINITY), T(-INFINITY)};
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint8_t l = (uint8_t)(own4 >> (8 * u));
+      T mn = px.t[u * C], mx = px.t[u * C];
+#pragma unroll
+      for (int ch = 1; ch < C; ++ch) {
+        mn = fmin(mn, px.t[u * C + ch]);
+        mx = fmax(mx, px.t[u * C + ch]);
+      }
+      const bool in = row_in && gx0 + u < A.W;
+      const bool rd = in && l == 0, by = in && l == 128;
+      vlo[0] = rd ? fmin(vlo[0], mn) : vlo[0];
+      vhi[0] = rd ? fmax(vhi[0], mx) : vhi[0];
+      vlo[1] = by ? fmin(vlo[1], mn) : vlo[1];
+      vhi[1] = by ? fmax(vhi[1], mx) : vhi[1];
+    }
+    unsigned long long ered[4];  // max(~enc) <=> min(enc)
+    if constexpr (sizeof(T) == 4) {
+      // fp32 values: order-preserving 32-bit codes, one redux per quantity
+      unsigned m[4];
+#pragma unroll
+      for (int b = 0; b < 2; ++b) {
+        const bool any = vlo[b] <= vhi[b];
+        m[2 * b] = __reduce_max_sync(0xffffffffu, any ? ~enc32((float)vlo[b]) : 0u);
+        m[2 * b + 1] = __reduce_max_sync(0xffffffffu, any ? enc32((float)vhi[b]) : 0u);
+      }
+      if (lane == 0) {  // the fp64 codes, once per warp
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+          ered[2 * b] = m[2 * b] ? ~enc_ordered((double)dec32(~m[2 * b])) : 0ULL;
+          ered[2 * b + 1] = m[2 * b + 1] ? enc_ordered((double)dec32(m[2 * b + 1])) : 0ULL;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int b = 0; b < 2; ++b) {
+        ered[2 * b] = vlo[b] <= vhi[b] ? ~enc_ordered((double)vlo[b]) : 0ULL;
+        ered[2 * b + 1] = vlo[b] <= vhi[b] ? enc_ordered((double)vhi[b]) : 0ULL;
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        for (int o = 16; o > 0; o >>= 1) {
+          const unsigned long long a = __shfl_xor_sync(0xffffffffu, ered[i], o);
+          ered[i] = a > ered[i] ? a : ered[i];
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (lane == 0) s_red[i][warp] = ered[i];
+    if (A.fillshell && row_in) {
+      int* fsh = A.fillshell + (size_t)f * A.HW + (size_t)gy * A.W + gx0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (gx0 + u < A.W) fsh[u] = -1;
+    }
+    __syncthreads();
+    if (threadIdx.x < 4) {
+      const int i = threadIdx.x;
+      unsigned long long e = 0ULL;
+      for (int w = 0; w < kThreads / 32; ++w) e = s_red[i][w] > e ? s_red[i][w] : e;
+      // i < 2: the frame's hull (most tiles cannot move it any more: skip
+      // their atomics); i >= 2: the tile's Bystander range, read by the
+      // shell loop's clip, and the frame's
+      unsigned long long* fr = i < 2 ? &A.hull[2 * f + i] : &A.bys_frame[2 * f + i - 2];
+      if (e != 0ULL && e > *(volatile unsigned long long*)fr) atomicMax(fr, e);
+      if (i >= 2) A.bys[((size_t)f * A.ntiles + tile) * 2 + i - 2] = e;
+    }
+  }
+  if (!tile_d) {
+    // no Inpaint pixel within reach: nothing of this tile is ever sampled
+    if (A.enter && row_in) {
+      int* en = A.enter + (size_t)f * A.HW + (size_t)gy * A.W + gx0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (gx0 + u < A.W) en[u] = -1;
+    }
+    timeline_mark(A, 0, false);
+    if (threadIdx.x == 0) bulk_wait_read0();
+    return;
+  }
+  if (raster) {
+    const double x0 = (double)tx0, x1 = (double)min(A.W - 1, tx0 + kTile - 1);
+    const double y0 = (double)ty0, y1 = (double)min(A.H - 1, ty0 + kTile - 1);
+    const int s0 = A.frame_seg ? A.frame_seg[f] : 0;
+    const int s1 = A.frame_seg ? A.frame_seg[f + 1] : A.n_seg;
+    for (int i = s0 + threadIdx.x; i < s1; i += kThreads) {
+      const double4 sg = A.seg[i];
+      const double lo_x = fmin(sg.x, sg.z) - A.cut, hi_x = fmax(sg.x, sg.z) + A.cut;
+      const double lo_y = fmin(sg.y, sg.w) - A.cut, hi_y = fmax(sg.y, sg.w) + A.cut;
+      if (hi_x >= x0 && lo_x <= x1 && hi_y >= y0 && lo_y <= y1) {
+        const int slot = atomicAdd(&s_ncand, 1);
+        if (slot < kMaxCand) s_cand[slot] = i;
+      }
+    }
+  }
+  // 2. dilation of the Inpaint indicator (the rows were dilated horizontally
+  //    when they were built; visible since the label barrier)
+  // ... and vertical: bit c of s_vrow[y] <=> an Inpaint pixel within
+  // Chebyshev distance R of tile pixel (c, y)
+  if (threadIdx.x < kTile) {
+    unsigned int v = 0;
+    for (int dy = 0; dy <= 2 * R; ++dy) v |= s_hrow[threadIdx.x + dy];
+    s_vrow[threadIdx.x] = v;
+  }
+  __syncthreads();
+
+  // 3. four consecutive pixels per thread: row ry, columns c0 .. c0+3
+  const unsigned int vmask = s_vrow[ry];
+  int n_inp = 0;
+  bool anyg = false;
+  uint32_t ent[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int c = c0 + u;
+    const int gx = tx0 + c;
+    const bool in = gy < A.H && gx < A.W;
+    const int p = gy * A.W + gx;
+    const uint8_t l = (uint8_t)(own4 >> (8 * u));
+    const bool near = (vmask >> c) & 1u;
+    bool active = false, rot = false;
+    if (in) {
+      if (l == 0) {
+        if (near) {
+          float cv[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+          for (int ch = 0; ch < C; ++ch) cv[ch] = (float)px.t[u * C + ch];
+          work[p] = make_float4(cv[0], cv[1], cv[2], __int_as_float(kStampReadable));
+          if (C > 3) A.c3[(size_t)f * A.HW + p] = cv[3];
+        }
+      } else if (l == 255) {
+        ++n_inp;
+        // a Readable 8-neighbour (the pixel itself is not Readable): the
+        // three ext columns c+R-1 .. c+R+1 of the rows above, at and below
+        const unsigned long long nb = s_rrow64[ry + R - 1] | s_rrow64[ry + R] | s_rrow64[ry + R + 1];
+        active = ((nb >> (c + R - 1)) & 7ull) != 0;
+        double gxv = 0.0, gyv = 0.0;
+        if (raster) {
+          const bool exhaustive = s_ncand > kMaxCand;
+          const int e0 = (exhaustive && A.frame_seg) ? A.frame_seg[f] : 0;
+          const int n_eval = exhaustive ? (A.frame_seg ? A.frame_seg[f + 1] - e0 : A.n_seg) : s_ncand;
+          double dmin = INFINITY;
+          int nearest = 0x7fffffff;
+          const double fx = (double)gx, fy = (double)gy;
+          // a segment whose bounding box lies farther than 3 eta cannot give
+          // this pixel a non-zero g (d > cut for it), so its exact distance
+          // is skipped; the bound is padded well past rounding, keeping every
+          // segment with d <= cut -- the only ones that decide g
+          const double cut2 = A.cut * A.cut * (1.0 + 1e-9) + 1e-9;
+          for (int cc = 0; cc < n_eval; ++cc) {
+            const int sidx = exhaustive ? e0 + cc : s_cand[cc];
+            const double4 sg = A.seg[sidx];
+            const double bx = fmax(fmax(fmin(sg.x, sg.z) - fx, fx - fmax(sg.x, sg.z)), 0.0);
+            const double by = fmax(fmax(fmin(sg.y, sg.w) - fy, fy - fmax(sg.y, sg.w)), 0.0);
+            if (bx * bx + by * by > cut2) continue;
+            const double d = seg_dist(fx, fy, sg);
+            const int sp = A.seg_spline[sidx];
+            if (d < dmin || (d == dmin && sp < nearest)) {
+              dmin = d;
+              nearest = sp;
+            }
+          }
+          if (dmin <= A.cut) {
+            const double fall = exp_np((-(dmin * dmin)) / A.c2eta);
+            const double2 dir = A.dirs[nearest];
+            gxv = dir.x * fall;
+            gyv = dir.y * fall;
+          }
+        } else if (A.g_mode == 2) {
+          const double2 g = reinterpret_cast<const double2*>(A.gsrc)[(size_t)f * A.HW + p];
+          gxv = g.x;
+          gyv = g.y;
+        } else if (A.g_mode == 1) {
+          gxv = A.gfx;
+          gyv = A.gfy;
+        }
+        rot = (gxv != 0.0 || gyv != 0.0);
+        if (active && rot) anyg = true;
+        if (A.gbuf) {
+          // the unit guide of the rotated ball (engine.py:155-158), once per pixel
+          double ux = 0.0, uy = 1.0;
+          if (rot) {
+            const double nr = hypot_np(gxv, gyv);
+            ux = gxv / nr;
+            uy = gyv / nr;
+          }
+          A.gbuf[(size_t)f * A.HW + p] = make_double4(gxv, gyv, ux, uy);
+        }
+        const int st = (active ? kStampActive : kStampInactive) | (rot ? kRotBit : 0);
+        work[p] = make_float4(0.f, 0.f, 0.f, __int_as_float(st));
+      } else if (near) {
+        work[p] = make_float4(0.f, 0.f, 0.f, __int_as_float(kStampBystander));
+      }
+      if (A.enter) A.enter[(size_t)f * A.HW + p] = active ? 0 : -1;
+    }
+    // initial frontier entry of this pixel (published per block below)
+    ent[u] = active ? ((uint32_t)p | (rot ? kEntryRot : 0u)) : 0xffffffffu;
+  }
+  // block-aggregated append of the initial frontier (lattice entries to the
+  // front of the list, rotated-ball entries to the back when split), |D| and
+  // the data-term flag: one barrier gathers the warps' counts, one atomic per
+  // quantity per block, one barrier hands out the list bases
+  {
+    const unsigned lt = (1u << lane) - 1;
+    int wL = 0, wR = 0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const bool act = ent[u] != 0xffffffffu;
+      const bool back = act && (ent[u] & kEntryRot) && A.split;
+      wL += __popc(__ballot_sync(0xffffffffu, act && !back));
+      wR += __popc(__ballot_sync(0xffffffffu, back));
+    }
+    const int w_inp = __reduce_add_sync(0xffffffffu, (unsigned)n_inp);
+    const bool w_ag = __any_sync(0xffffffffu, anyg);
+    if (lane == 0) {
+      s_wl[warp] = wL;
+      s_wr[warp] = wR;
+      s_cnt[warp] = w_inp | (w_ag ? (1 << 30) : 0);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int tL = 0, tR = 0, tot = 0;
+      bool ag = false;
+      for (int w = 0; w < kThreads / 32; ++w) {
+        const int a = s_wl[w], b = s_wr[w];
+        s_wl[w] = tL;
+        s_wr[w] = tR;
+        tL += a;
+        tR += b;
+        tot += s_cnt[w] & ((1 << 30) - 1);
+        ag |= (s_cnt[w] >> 30) != 0;
+      }
+      s_bL = tL > 0 ? atomicAdd(&A.cnt[f], tL) : 0;
+      s_bR = tR > 0 ? atomicAdd(&A.cntR[f], tR) : 0;
+      if (tot) {
+        atomicAdd(&A.remaining[f], tot);
+        atomicAdd(&A.inpaint[f], tot);
+      }
+      if (ag) A.anyg[f] = 1;
+    }
+    __syncthreads();
+    int bL = s_bL + s_wl[warp], bR = s_bR + s_wr[warp];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const bool act = ent[u] != 0xffffffffu;
+      const bool back = act && (ent[u] & kEntryRot) && A.split;
+      const unsigned mL = __ballot_sync(0xffffffffu, act && !back);
+      const unsigned mR = __ballot_sync(0xffffffffu, back);
+      if (back) A.list0[(size_t)f * A.cap + A.cap - 1 - (bR + __popc(mR & lt))] = ent[u];
+      else if (act) A.list0[(size_t)f * A.cap + bL + __popc(mL & lt)] = ent[u];
+      bL += __popc(mL);
+      bR += __popc(mR);
+    }
+  }
+  timeline_mark(A, 0, false);
+  if (threadIdx.x == 0) bulk_wait_read0();
+}
+
 
 // ------------------------------------------------------- shell loop
 //
@@ -1695,6 +2162,77 @@ static void launch_prep(bool f64, int C, dim3 grid, cudaStream_t stream, const F
 #undef GF_PREP
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &ptr, 12000, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  });
+  return fn;
+}
+
+// 3-D map (cols, rows, frames) with a (box_c, box_r, 1) box
+static bool encode_map(CUtensorMap* m, CUtensorMapDataType dt, size_t elem, void* base, int cols,
+                       int rows, int frames, int box_c, int box_r) {
+  auto enc = tensor_map_encoder();
+  if (!enc) return false;
+  const cuuint64_t dims[3] = {(cuuint64_t)cols, (cuuint64_t)rows, (cuuint64_t)frames};
+  const cuuint64_t strides[2] = {(cuuint64_t)cols * elem, (cuuint64_t)cols * rows * elem};
+  const cuuint32_t box[3] = {(cuuint32_t)box_c, (cuuint32_t)box_r, 1};
+  const cuuint32_t es[3] = {1, 1, 1};
+  return enc(m, dt, 3, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// The TMA prep applies when every row is a multiple of 16 bytes (the maps'
+// stride rule) and x is not periodic (a box does not wrap); GF_NO_TMA=1
+// forces the plain kernel (A/B experiments).
+static bool launch_prep_tma(bool f64, int C, dim3 grid, cudaStream_t stream, const FillArgs& A,
+                            const void* image, void* out, const uint8_t* labels) {
+  if (A.periodic || getenv("GF_NO_TMA")) return false;
+  const size_t elem = f64 ? 8 : 4;
+  if ((size_t)A.W * C * elem % 16 || A.W % 16) return false;
+  const int ext = kTile + 2 * A.halo;
+  PrepMaps M;
+  memset(&M, 0, sizeof(M));
+  M.lab_bw = kLabBoxMax;
+  if (A.halo > 16) return false;
+  const CUtensorMapDataType dt = f64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+  if (!encode_map(&M.img, dt, elem, const_cast<void*>(image), A.W * C, A.H, A.nF, kTile * C, kTile) ||
+      !encode_map(&M.out, dt, elem, out, A.W * C, A.H, A.nF, kTile * C, kTile) ||
+      !encode_map(&M.lab, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, const_cast<uint8_t*>(labels), A.W, A.H,
+                  A.nF, M.lab_bw, ext))
+    return false;
+#define GF_PREP_TMA(T, CC)                                       \
+  do {                                                          \
+    k_prep_tma<T, CC><<<grid, kThreads, 0, stream>>>(M, A);     \
+  } while (0)
+  if (f64) {
+    switch (C) {
+      case 1: GF_PREP_TMA(double, 1); break;
+      case 2: GF_PREP_TMA(double, 2); break;
+      case 3: GF_PREP_TMA(double, 3); break;
+      default: GF_PREP_TMA(double, 4); break;
+    }
+  } else {
+    switch (C) {
+      case 1: GF_PREP_TMA(float, 1); break;
+      case 2: GF_PREP_TMA(float, 2); break;
+      case 3: GF_PREP_TMA(float, 3); break;
+      default: GF_PREP_TMA(float, 4); break;
+    }
+  }
+#undef GF_PREP_TMA
+  return true;
+}
+
 static size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct Layout {
@@ -1863,8 +2401,11 @@ int fill_launch(const gf_frames* fr, const gf_fill_params* prm, const gf_fill_ou
   if (cudaMemsetAsync(base + L.ints, 0, L.u64 + (size_t)nF * 6 * sizeof(unsigned long long) - L.ints,
                       stream) != cudaSuccess)
     return set_error(GF_E_CUDA, "memset failed");
-  launch_prep(fr->dtype == GF_F64, C, dim3((W + kTile - 1) / kTile, (H + kTile - 1) / kTile, nF), stream,
-              A);
+  {
+    const dim3 pg((W + kTile - 1) / kTile, (H + kTile - 1) / kTile, nF);
+    if (!launch_prep_tma(fr->dtype == GF_F64, C, pg, stream, A, fr->image, fr->out, fr->labels))
+      launch_prep(fr->dtype == GF_F64, C, pg, stream, A);
+  }
   count_launches(1);
   if (cudaPeekAtLastError() != cudaSuccess)
     return set_error(GF_E_CUDA, cudaGetErrorString(cudaGetLastError()));
