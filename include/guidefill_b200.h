@@ -317,6 +317,51 @@ void gf_host_exp(const double* x, double* y, int64_t n);
 void gf_host_hypot(const double* x, const double* y, double* out, int64_t n);
 double gf_host_pairwise_sum(const double* a, int32_t n);
 
+/*
+ * The plain / masked structure tensor's eigen split at the n queries, as
+ * gf_coherence_directions but returning eig[n][8] = (vx, vy, coh, a, b, c,
+ * mass, 0): the minor eigenvector (guide.eigen_2x2, guide.py:123-136),
+ * tanh((hi - lo) / lam), the normalised tensor [[a, b], [b, c]] and the rho
+ * window's mass (ZeroMassError when <= 0, guide.py:164-166).
+ * With labels all 0 (every pixel readable) this is guide.structure_tensor
+ * (guide.py:139-156) as make_spline uses it (guide.py:221-223).
+ */
+int gf_structure_eigen(int32_t height, int32_t width, int32_t channels, const double* image,
+                       const uint8_t* labels, int32_t n, const int64_t* idx, double sigma,
+                       double rho, double lam, double* eig, void* workspace,
+                       size_t workspace_bytes, void* stream);
+
+/*
+ * Edge seeds of automatic spline detection (guide.detect_edge_seeds,
+ * guide.py:177-197, before the clustering): the measurement ring
+ * (compute_ring, guide.py:65-88: Readable pixels at chessboard distance
+ * ceil(2 sigma + 2 rho) + 1 from D u B), Canny restricted to the annulus
+ * around it (scikit-image's canny restated: masked Gaussian with bleed-over,
+ * Sobel, bilinear non-maximum suppression, hysteresis with low / high), and
+ * the ring pixels on an edge with strength hypot(np.gradient(gauss(gray))).
+ * Replaces guide.py:183-196.  Synchronous on `stream` (hysteresis passes
+ * until a fixpoint).  Up to cap hits: hit_idx (device int64 flat indices,
+ * unordered), hit_strength (device float64); *n_hits (HOST int32) = total
+ * hits (may exceed cap).  ring_out / edges_out (nullable, device [H][W] u8):
+ * the ring mask and the edge flags (bit 2 = edge).
+ * workspace: gf_detect_workspace_bytes(H, W) device bytes.
+ */
+size_t gf_detect_workspace_bytes(int32_t height, int32_t width);
+int gf_detect_edges(int32_t height, int32_t width, int32_t channels, const double* image,
+                    const uint8_t* labels, double sigma, double rho, double low, double high,
+                    int32_t cap, int64_t* hit_idx, double* hit_strength, int32_t* n_hits,
+                    uint8_t* ring_out, uint8_t* edges_out, void* workspace,
+                    size_t workspace_bytes, void* stream);
+
+/*
+ * make_spline's ray search and extension (guide.py:231-259) for n seeds
+ * (device [n][2] (i, j) float64) along unit directions v (device [n][2]):
+ * out[n][3] = (sign, t_entry, t_end), sign +1 (along v), -1 (along -v) or 0
+ * (no entry within `budget`, the seed yields no spline).
+ */
+int gf_trace_rays(int32_t height, int32_t width, const uint8_t* labels, int32_t n,
+                  const double* seeds, const double* v, double budget, double* out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -31,7 +31,8 @@ EXPORTS = (
     "gf_bilinear_gather", "gf_boundary_masks", "gf_output_delta", "gf_upload_mirrored",
     "gf_paint_unfillable_workspace_bytes", "gf_paint_unfillable",
     "gf_coherence_workspace_bytes", "gf_coherence_directions", "gf_frontier_candidates",
-    "gf_commit_shell", "gf_last_error",
+    "gf_commit_shell", "gf_structure_eigen", "gf_detect_workspace_bytes", "gf_detect_edges",
+    "gf_trace_rays", "gf_last_error",
     "gf_abi_version", "gf_launch_count", "gf_host_exp", "gf_host_hypot", "gf_host_pairwise_sum",
 )
 
@@ -155,6 +156,20 @@ def load(required: bool = True):
     lib.gf_paint_unfillable.restype = ctypes.c_int
     lib.gf_paint_unfillable.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
                                         ctypes.c_int32, P, P, P, P, ctypes.c_size_t, P, P]
+    lib.gf_structure_eigen.restype = ctypes.c_int
+    lib.gf_structure_eigen.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, P, P,
+                                       ctypes.c_int32, P, ctypes.c_double, ctypes.c_double,
+                                       ctypes.c_double, P, P, ctypes.c_size_t, P]
+    lib.gf_detect_workspace_bytes.restype = ctypes.c_size_t
+    lib.gf_detect_workspace_bytes.argtypes = [ctypes.c_int32, ctypes.c_int32]
+    lib.gf_detect_edges.restype = ctypes.c_int
+    lib.gf_detect_edges.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, P, P,
+                                    ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                    ctypes.c_double, ctypes.c_int32, P, P, P, P, P, P,
+                                    ctypes.c_size_t, P]
+    lib.gf_trace_rays.restype = ctypes.c_int
+    lib.gf_trace_rays.argtypes = [ctypes.c_int32, ctypes.c_int32, P, ctypes.c_int32, P, P,
+                                  ctypes.c_double, P, P]
     lib.gf_last_error.restype = ctypes.c_char_p
     lib.gf_abi_version.restype = ctypes.c_int
     lib.gf_launch_count.restype = ctypes.c_int64

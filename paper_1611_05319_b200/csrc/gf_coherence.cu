@@ -216,7 +216,7 @@ constexpr int kQueryWarps = 4;
 // and parked in shared memory, lanes 0..3 then run the ordered row sums
 __global__ void k_ct_query(int H, int W, int n, const int64_t* __restrict__ idx,
                            const double* __restrict__ Q, const Taps t, double lam,
-                           double* __restrict__ g) {
+                           double* __restrict__ g, double* __restrict__ eig) {
   __shared__ double cols[kQueryWarps][4][2 * kMaxTaps + 1];
   __shared__ double red[kQueryWarps][4];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -248,7 +248,21 @@ __global__ void k_ct_query(int H, int W, int n, const int64_t* __restrict__ idx,
   const double phi = 0.5 * atan2(2.0 * b, a - c);
   const double lo = mean - disc, hi = mean + disc;
   const double coh = tanh((hi - lo) / lam);
-  double gx = coh * -sin(phi), gy = coh * cos(phi);
+  const double vx = -sin(phi), vy = cos(phi);
+  if (eig) {  // guide.eigen_2x2's minor eigenvector and the coherence (make_spline),
+              // the normalised tensor (structure_tensor) and the rho mass
+    double* e = eig + 8 * k;
+    e[0] = vx;
+    e[1] = vy;
+    e[2] = coh;
+    e[3] = a;
+    e[4] = b;
+    e[5] = c;
+    e[6] = mass;
+    e[7] = 0.0;
+  }
+  if (!g) return;
+  double gx = coh * vx, gy = coh * vy;
   if (mass <= 0.0) gx = gy = 0.0;
   g[2 * k] = gx;
   g[2 * k + 1] = gy;
@@ -338,14 +352,38 @@ extern "C" size_t gf_coherence_workspace_bytes(int32_t height, int32_t width, in
   return 2 * planes * (size_t)height * width * sizeof(double) + tiles;
 }
 
+static int coherence_run(int32_t height, int32_t width, int32_t channels, const double* image,
+                         const uint8_t* labels, int32_t n, const int64_t* idx, double sigma,
+                         double rho, double lam, double* g, double* eig, double* points,
+                         void* workspace, size_t workspace_bytes, void* stream);
+
 extern "C" int gf_coherence_directions(int32_t height, int32_t width, int32_t channels,
                                        const double* image, const uint8_t* labels, int32_t n,
                                        const int64_t* idx, double sigma, double rho, double lam,
                                        double* g, double* points, void* workspace,
                                        size_t workspace_bytes, void* stream) {
+  if (n > 0 && !g) return set_error(GF_E_INVALID, "NULL buffer");
+  return coherence_run(height, width, channels, image, labels, n, idx, sigma, rho, lam, g, nullptr,
+                       points, workspace, workspace_bytes, stream);
+}
+
+extern "C" int gf_structure_eigen(int32_t height, int32_t width, int32_t channels,
+                                  const double* image, const uint8_t* labels, int32_t n,
+                                  const int64_t* idx, double sigma, double rho, double lam,
+                                  double* eig, void* workspace, size_t workspace_bytes,
+                                  void* stream) {
+  if (n > 0 && !eig) return set_error(GF_E_INVALID, "NULL buffer");
+  return coherence_run(height, width, channels, image, labels, n, idx, sigma, rho, lam, nullptr,
+                       eig, nullptr, workspace, workspace_bytes, stream);
+}
+
+static int coherence_run(int32_t height, int32_t width, int32_t channels, const double* image,
+                         const uint8_t* labels, int32_t n, const int64_t* idx, double sigma,
+                         double rho, double lam, double* g, double* eig, double* points,
+                         void* workspace, size_t workspace_bytes, void* stream) {
   if (height < 2 || width < 2 || height > 65535 || channels < 1 || channels > 4 || n < 0)
     return set_error(GF_E_INVALID, "bad geometry");
-  if (!image || !labels || (n > 0 && (!idx || !g)) || !workspace)
+  if (!image || !labels || (n > 0 && !idx) || !workspace)
     return set_error(GF_E_INVALID, "NULL buffer");
   if (workspace_bytes < gf_coherence_workspace_bytes(height, width, channels))
     return set_error(GF_E_WORKSPACE, "workspace too small");
@@ -384,7 +422,7 @@ extern "C" int gf_coherence_directions(int32_t height, int32_t width, int32_t ch
   }
   // rho stage at the queries only
   k_ct_query<<<(n + kQueryWarps - 1) / kQueryWarps, 32 * kQueryWarps, 0, s>>>(height, width, n,
-                                                                            idx, B, tr, lam, g);
+                                                                            idx, B, tr, lam, g, eig);
   count_launches(5);
   cudaError_t e = cudaPeekAtLastError();
   if (e != cudaSuccess) return set_error(GF_E_CUDA, cudaGetErrorString(e));

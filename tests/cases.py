@@ -305,3 +305,44 @@ def deadlock_scenes(size=256, thetas=(10.0, 25.0, 40.0, 73.0), mus=(50.0, 100.0)
             out.append(_case(f"halfplane_{th_deg:g}deg_mu{mu:g}", img, lab, g, tracked=True,
                              r=3, mu=mu, order="smart", neighborhood="rotated_ball"))
     return out
+
+
+def detect_scenes(seed=77):
+    """Automatic-detection scenes: the reference test scenes (test_guide.py:16-36,
+    200-209) plus random edge images around rectangular holes."""
+    out = []
+    jj, ii = np.mgrid[0:100, 0:100]
+    img = np.where(jj >= ii, 1.0, 0.5)[..., None]
+    lab = np.zeros((100, 100), dtype=np.uint8)
+    lab[50:, :] = INPAINT
+    img[lab != 0] = 0.0
+    out.append(("half_plane_45", img, lab))
+    lab = np.zeros((60, 60), dtype=np.uint8)
+    lab[24:36, 24:36] = INPAINT
+    img = np.zeros((60, 60, 3))
+    img[:, 30:, :] = 1.0
+    img[lab == INPAINT] = 0.0
+    out.append(("vertical_edge_block", img, lab))
+    img = np.where(jj >= 37.5, 1.0, 0.5)[..., None]
+    lab = np.zeros((100, 100), dtype=np.uint8)
+    lab[50:, :] = INPAINT
+    img[lab != 0] = 0.0
+    out.append(("parallel_edge", img, lab))
+    rng = np.random.default_rng(seed)
+    for k in range(4):
+        H, W = int(rng.integers(70, 130)), int(rng.integers(70, 130))
+        y, x = np.mgrid[0:H, 0:W].astype(np.float64)
+        img = np.zeros((H, W, 3))
+        for c in range(3):
+            a = rng.uniform(0, np.pi)
+            img[..., c] = np.where(np.cos(a) * (x - W / 2) + np.sin(a) * (y - H / 2) > rng.uniform(-5, 5),
+                                   rng.uniform(0.6, 1.0), rng.uniform(0.0, 0.4))
+        img += rng.uniform(0, 0.02, size=img.shape)
+        lab = np.zeros((H, W), dtype=np.uint8)
+        j0, i0 = int(H * 0.4), int(W * 0.4)
+        lab[j0:j0 + int(rng.integers(8, 16)), i0:i0 + int(rng.integers(8, 16))] = INPAINT
+        if k % 2:
+            lab[j0 + 2:j0 + 4, i0 + 2:i0 + 4] = BYSTANDER
+        img[lab == INPAINT] = 0.0
+        out.append((f"random_edges_{k}", img, lab))
+    return out

@@ -110,3 +110,39 @@ def test_cli_coherence_preset_matches_oracle(tmp_path):
     assert rep["iterations"] == ref["iterations"]
     assert rep["frontier_sizes"] == [x[1] for x in ref["rows"]]
     assert rep["filled_per_iteration"] == [x[4] for x in ref["rows"]]
+
+
+@pytest.mark.gpu
+def test_cli_inpaint_autodetects_splines(tmp_path):
+    """Without --splines the default guidefill preset detects splines
+    (cli.py:104-105, guide.detect_splines on the device): the fill equals the
+    oracle's with the oracle's detected splines; `splines detect` writes the
+    canonical JSON (test_cli.py:136-148)."""
+    from oracle import detect_oracle as det
+    from oracle import guidefill_oracle as orc
+    from paper_1611_05319_b200 import loads, scenes
+
+    sc = scenes.small_scene(120, 160, band=6, gx=3, gy=2, n_spl=2, seed=9)
+    img = fileio.to_uint8(sc.image).astype(np.float64) / 255.0
+    fileio.save_image(tmp_path / "in.png", img)
+    fileio.save_labels(tmp_path / "m.pgm", sc.labels)
+    r = CliRunner().invoke(main, ["inpaint", "--image", str(tmp_path / "in.png"),
+                                  "--mask", str(tmp_path / "m.pgm"),
+                                  "--out", str(tmp_path / "out.png"),
+                                  "--report", str(tmp_path / "rep.json")])
+    assert r.exit_code == 0, r.output
+    want = det.detect_splines(img, sc.labels)
+    field = orc.guide_field([np.stack([s, e]) for s, e, _ in want], [d for _, _, d in want],
+                            sc.labels)
+    ref = orc.fill(img, sc.labels, field, orc.Params.of(FillParams.guidefill()), tracked=True)
+    rep = json.loads((tmp_path / "rep.json").read_text())
+    assert rep["filled_per_iteration"] == [x[4] for x in ref["rows"]]
+    out = fileio.load_image(tmp_path / "out.png")
+    assert np.abs(out - fileio.to_uint8(ref["u"]) / 255.0).max() <= 1.0 / 255 + 1e-12
+    r = CliRunner().invoke(main, ["splines", "detect", "--image", str(tmp_path / "in.png"),
+                                  "--mask", str(tmp_path / "m.pgm"),
+                                  "--out", str(tmp_path / "det.json")])
+    assert r.exit_code == 0, r.output
+    text = (tmp_path / "det.json").read_text()
+    assert dumps(loads(text)) == text
+    assert len(loads(text)) == len(want)
