@@ -354,6 +354,78 @@ def _run_coherence(image, labels, params, tracked, order_log, dev):
     return out, rep, dict(enter=en, fillshell=fs)
 
 
+class FrontierRuleError(NotImplementedError):
+    """A frontier_update hook returned a frontier other than the tracker's."""
+
+
+def _shell_sets(enter, fillshell, iterations):
+    """Per-shell sorted frontiers and fill masks from the engine's order log
+    (frontier(k) = {p : enter[p] <= k <= fillshell[p]}, never-filled pixels
+    stay until the end): yields (k, frontier, fill)."""
+    enter = np.asarray(enter).reshape(-1)
+    fs = np.asarray(fillshell).reshape(-1)
+    members = np.flatnonzero(enter >= 0)
+    start = enter[members]
+    stop = np.where(fs[members] >= 0, fs[members], iterations)
+    order_in = np.argsort(start, kind="stable")
+    order_out = np.argsort(stop, kind="stable")
+    cur = np.empty(0, dtype=np.int64)
+    a = b = 0
+    for k in range(iterations):
+        lo = a
+        while a < members.size and start[order_in[a]] <= k:
+            a += 1
+        if a > lo:
+            cur = np.union1d(cur, members[order_in[lo:a]])
+        lo = b
+        while b < members.size and stop[order_out[b]] < k:
+            b += 1
+        if b > lo:
+            cur = np.setdiff1d(cur, members[order_out[lo:b]], assume_unique=True)
+        yield k, cur, fs[cur] == k
+
+
+def _fill_loop(image, labels, guide_vecs, params: FillParams, frontier_update=None):
+    """The reference's fill seam (engine.py:286-376): (u, lab, report).
+
+    This is the one function every reference caller goes through (inpaint,
+    run_tracked and their callers), so routing ``guidefill.engine._fill_loop``
+    here reroutes them to the device.  The shell loop itself
+    runs in the persistent kernel; a ``frontier_update`` hook is replayed
+    afterwards from the kernel's order log, one call per shell with exactly
+    the arguments the reference passes (sorted frontier, fill mask, filled
+    indices, labels relabelled so far).  The hook's candidate counts go into
+    the report rows as in the reference; a hook that returns a frontier other
+    than the tracker's (a custom rule the device loop cannot follow) raises
+    FrontierRuleError.
+    """
+    tracked = frontier_update is not None
+    u, report, maps = _run_fill(image, labels, guide_vecs, params, tracked=tracked,
+                                order_log=tracked, validate=True)
+    lab = np.array(labels, dtype=np.uint8, copy=True)
+    if not tracked:
+        lab[lab == INPAINT] = READABLE
+        return u, lab, report
+    flat = lab.reshape(-1)
+    nxt = None
+    rows = []
+    for k, frontier, fill in _shell_sets(maps["enter"], maps["fillshell"], report.iterations):
+        if nxt is not None and not np.array_equal(nxt, frontier):
+            raise FrontierRuleError("the frontier_update hook returned a frontier other than the "
+                                    "tracked update's; custom frontier rules are not supported")
+        filled_idx = frontier[fill]
+        flat[filled_idx] = READABLE
+        candidates, new_frontier = frontier_update(frontier, fill, filled_idx, lab)
+        nxt = np.asarray(new_frontier, dtype=np.int64)
+        rows.append((k, int(frontier.size), int(candidates), int(frontier.size),
+                     int(filled_idx.size)))
+    if report.iterations and nxt.size and not report.unfillable:
+        raise FrontierRuleError("the frontier_update hook kept pixels after the last shell")
+    report.rows = rows
+    lab[lab == INPAINT] = READABLE  # painted (unfillable fallback) pixels too
+    return u, lab, report
+
+
 def inpaint(image, labels, guide=None, params: FillParams | None = None):
     """Fill all Inpaint pixels of ``labels`` in ``image`` (engine.py:379-408).
 

@@ -186,6 +186,22 @@ def _eigen_device(image, readable, points, sigma, rho, lam):
     return eig[:n].cpu().numpy()
 
 
+def _tensor_field(image, indicator, sigma: float, rho: float):
+    """Indicator-weighted structure tensor field (guide.py:91-120) on the
+    device: (J11, J12, J22, rho mass) planes, every pixel queried.  The
+    indicator must be 0 / 1 (all ones: the plain tensor; the Readable mask:
+    the masked one)."""
+    ind = np.asarray(indicator, dtype=np.float64)
+    if not np.all((ind == 0.0) | (ind == 1.0)):
+        raise NotImplementedError("the device tensor takes a 0 / 1 indicator")
+    img = _image3(image)
+    H, W = ind.shape
+    jj, ii = np.mgrid[0:H, 0:W]
+    e = _eigen_device(img, ind == 1.0, np.stack([ii.ravel(), jj.ravel()], axis=1), sigma, rho,
+                      DEFAULT_LAMBDA)
+    return tuple(e[:, c].reshape(H, W).copy() for c in (3, 4, 5, 6))
+
+
 def structure_tensor(image, point, sigma: float = DEFAULT_SIGMA, rho: float = DEFAULT_RHO,
                      labels=None):
     """Smoothed gradient outer-product tensor at one pixel (guide.py:139-156)."""

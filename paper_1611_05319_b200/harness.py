@@ -25,6 +25,7 @@ from dataclasses import dataclass, replace
 
 import numpy as np
 
+from . import engine
 from .grid import INPAINT, READABLE
 
 
@@ -276,3 +277,117 @@ def fit_power_law(points) -> PowerLawFit:
     miss = lv - (alpha * ln + intercept)
     return PowerLawFit(amplitude=float(math.exp(intercept)), alpha=float(alpha),
                        residual=float(np.sqrt(np.mean(miss * miss))))
+
+
+def plot_script(csv_name: str, x: str = "N", y: str = "threads_max") -> str:
+    """A gnuplot script plotting one study CSV on log-log axes (harness.py:346-352)."""
+    return ("set datafile separator ','\n"
+            "set logscale xy\n"
+            f"plot '{csv_name}' using '{x}':'{y}' with linespoints title '{y}'\n")
+
+
+# ---------------------------------------------------------------- analysis
+# Measurements on filled renderings (harness.py:140-258): host arithmetic on
+# the engine's output, the fills themselves run on the device.
+
+def row_profile(u, spec: SyntheticProblem, y_value: float):
+    """Channel 0 along the pixel row whose centre is nearest to continuum y
+    (harness.py:140-144): (x, profile)."""
+    x, y = pixel_centers(spec)
+    row = int(np.argmin(np.abs(y - y_value)))
+    return x, np.asarray(u[row, :, 0], dtype=np.float64)
+
+
+def _crossing(x, p, level, start, step):
+    """Walk from ``start`` in ``step`` while p < level; interpolate the
+    crossing between the last sample below and the first at/above it."""
+    k = start
+    while p[k] < level:
+        k += step
+        if k < 0 or k >= p.size:
+            return None, None
+    a = k - step
+    frac = (level - p[a]) / (p[k] - p[a])
+    return x[a] + frac * (x[k] - x[a]), k
+
+
+def rise_width(x, profile, ink: float, bg: float, lo_frac: float = 0.1,
+               hi_frac: float = 0.9) -> float:
+    """Mean 10-90 transition width of a dark band's two edges, in continuum
+    units (harness.py:147-181); inf once the band no longer reaches the low
+    level or a crossing runs off the row."""
+    p = np.asarray(profile, dtype=np.float64)
+    lo, hi = ink + lo_frac * (bg - ink), ink + hi_frac * (bg - ink)
+    bottom = int(np.argmin(p))
+    if p[bottom] >= lo:
+        return math.inf
+    widths = []
+    for step in (-1, +1):
+        x_lo, k_lo = _crossing(x, p, lo, bottom, step)
+        if x_lo is None:
+            return math.inf
+        x_hi, _ = _crossing(x, p, hi, k_lo, step)
+        if x_hi is None:
+            return math.inf
+        widths.append(abs(x_hi - x_lo))
+    return 0.5 * (widths[0] + widths[1])
+
+
+def measure_line_angle(u, labels, spec: SyntheticProblem, margin_rows: int = 2,
+                       depth_frac: float = 0.4) -> float:
+    """Angle (degrees mod 180) of the dark band the fill extended into the
+    unknown rows: per-row darkness centroids over the first depth_frac of
+    them (after margin_rows), a least-squares slope dx/dy, converted to a
+    continuum angle (harness.py:184-213)."""
+    x, y = pixel_centers(spec)
+    background = float(np.max(_tones(spec.colors)))
+    rows = np.flatnonzero((np.asarray(labels) == INPAINT).any(axis=1))
+    last = max(margin_rows + 2, int(math.ceil(depth_frac * rows.size)))
+    cx, cy = [], []
+    for j in rows[margin_rows:last]:
+        dark = np.clip(background - np.asarray(u[j, :, 0], dtype=np.float64), 0.0, None)
+        mass = float(dark.sum())
+        if mass > 1e-12:
+            cx.append(float((dark * x).sum()) / mass)
+            cy.append(float(y[j]))
+    if len(cx) < 2:
+        raise ValueError("no dark band found in the unknown rows")
+    slope = float(np.polyfit(cy, cx, 1)[0])
+    return math.degrees(math.atan2(1.0, slope)) % 180.0
+
+
+def _line_guide(spec: SyntheticProblem):
+    """Unit guide along the scene's line, image coordinates (rows grow
+    downwards): (cos theta, -sin theta) (harness.py:216-219)."""
+    th = math.radians(spec.theta_deg)
+    return (math.cos(th), -math.sin(th))
+
+
+def degradation_study(spec: SyntheticProblem, resolutions, cross_sections=(0.3, 0.25, 0.0),
+                      params=None) -> list:
+    """Band transition widths across depths and scales (harness.py:222-250):
+    every rendering is filled on the GPU with a fixed guide along the true
+    line and each cross-section's 10-90 width measured."""
+    out = []
+    for res in resolutions:
+        scene = spec.with_resolution(res)
+        image, labels, _ = render_problem(scene)
+        p = params or engine.FillParams(r=3, mu=50.0, order="smart",
+                                        neighborhood="rotated_ball", g_source="fixed",
+                                        g_fixed=_line_guide(scene))
+        filled, report = engine.inpaint(image, labels, None, p)
+        tones = _tones(scene.colors)
+        ink, bg = float(np.min(tones)), float(np.max(tones))
+        for yv in cross_sections:
+            xs, prof = row_profile(filled, scene, float(yv))
+            out.append({"resolution": tuple(scene.resolution), "y": float(yv),
+                        "width": rise_width(xs, prof, ink, bg),
+                        "iterations": report.iterations})
+    return out
+
+
+def degradation_csv(rows) -> str:
+    """W,H,y,width rows of a degradation study (harness.py:253-258)."""
+    body = "".join(f"{r['resolution'][0]},{r['resolution'][1]},{r['y']:.10g},{r['width']:.10g}\n"
+                   for r in rows)
+    return "W,H,y,width\n" + body

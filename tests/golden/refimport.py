@@ -17,6 +17,12 @@ def available() -> bool:
 def load():
     if not available():
         raise ImportError("reference package not present")
+    # tests/ref_suite binds the name guidefill to paper_1611_05319_b200: drop
+    # that alias before importing the real reference
+    mod = sys.modules.get("guidefill")
+    if mod is not None and not str(getattr(mod, "__file__", "")).startswith(REF_SRC):
+        for name in [k for k in sys.modules if k == "guidefill" or k.startswith("guidefill.")]:
+            del sys.modules[name]
     for p in (_STUB, REF_SRC):
         if p not in sys.path:
             sys.path.insert(0, p)

@@ -206,3 +206,62 @@ def test_frame_without_inpaint_pixels():
     ref = orc.fill(case["image"], lab, case["guide"], orc.Params.of(p), tracked=True)
     assert rep.iterations == ref["iterations"] == 0
     assert np.array_equal(u, ref["u"])
+
+
+def test_fill_loop_seam_replays_recording_hooks():
+    """engine._fill_loop (the reference's seam, engine.py:286) with a
+    frontier_update hook: one call per shell with the reference's arguments;
+    the tracker's own update as the hook reproduces run_tracked; a custom
+    rule is refused (INTEGRATION.md)."""
+    case = ALL_CASES[16]  # trk_tracked test_tracker.py:81
+    p = FillParams(**case["params"])
+    calls = []
+
+    def hook(frontier, fill, filled_idx, lab):
+        calls.append((frontier.copy(), fill.copy(), filled_idx.copy()))
+        return orc._tracked_update(frontier, fill, filled_idx, lab, p.periodic_x)
+
+    u, lab, rep = engine._fill_loop(case["image"], case["labels"], case["guide"], p, hook)
+    u_t, wm = tracker.run_tracked(case["image"], case["labels"], case["guide"], p)
+    assert np.array_equal(u, u_t)
+    assert rep.rows == wm.rows
+    assert len(calls) == rep.iterations
+    ref = orc.fill(case["image"], case["labels"], case["guide"], orc.Params.of(p), tracked=True)
+    for k, (fr, fm, fi) in enumerate(calls):
+        want = np.flatnonzero((ref["enter"].reshape(-1) >= 0) & (ref["enter"].reshape(-1) <= k) &
+                              ((ref["fillshell"].reshape(-1) >= k)))
+        assert np.array_equal(fr, want) and np.array_equal(fi, fr[fm])
+    assert not (lab == 255).any()
+    u2, lab2, rep2 = engine._fill_loop(case["image"], case["labels"], case["guide"], p)
+    assert np.array_equal(u2, u_t) and all(r[3] == lab2.size for r in rep2.rows)
+
+    def bad_hook(frontier, fill, filled_idx, lab):
+        cand, nxt = orc._tracked_update(frontier, fill, filled_idx, lab, p.periodic_x)
+        return cand, nxt[1:]
+
+    with pytest.raises(engine.FrontierRuleError):
+        engine._fill_loop(case["image"], case["labels"], case["guide"], p, bad_hook)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_update_frontier_incremental_equals_rescan(seed):
+    """tracker.update_frontier (tracker.py:82-101) on the device: survivors +
+    neighbours of the filled pixels, filtered -- equal to a full rescan, for
+    index and coordinate-set inputs, fills inside and outside the frontier,
+    periodic x (test_tracker.py:23-42)."""
+    from paper_1611_05319_b200 import grid as g
+
+    rng = np.random.default_rng(seed)
+    lab = cases.islands_labels(rng, 20, 60)
+    periodic = bool(seed % 2)
+    fr = tracker.FrontierList.from_labels(lab, periodic)
+    inp = np.flatnonzero(lab.reshape(-1) == 255)
+    pick = rng.choice(inp, size=min(inp.size, int(rng.integers(1, 20))), replace=False)
+    lab2 = lab.copy()
+    lab2.reshape(-1)[pick] = 0
+    want = np.flatnonzero(g.active_boundary_mask(lab2, periodic))
+    got = tracker.update_frontier(fr, pick, lab2, periodic)
+    assert np.array_equal(got.indices, want) and got.generation == 1
+    W = lab.shape[1]
+    got2 = tracker.update_frontier(fr, {(int(q % W), int(q // W)) for q in pick}, lab2, periodic)
+    assert np.array_equal(got2.indices, want)
