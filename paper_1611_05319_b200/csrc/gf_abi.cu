@@ -53,6 +53,7 @@ static int build_ball(const gf_fill_params* p, BallParams& P, BallTables& T) {
       T.n[K] = (double)n;
       T.m[K] = (double)m;
       T.w0[K] = 1.0 / hypot_np((double)n, (double)m);
+      T.w0f[K] = (float)T.w0[K];
       T.ni[K] = n;
       T.mi[K] = m;
       T.kn[K] = -1;

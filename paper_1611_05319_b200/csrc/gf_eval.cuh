@@ -129,7 +129,7 @@ __device__ __forceinline__ void eval_lattice(const BallParams& P, const BallTabl
 #pragma unroll
   for (int t = 0; t < KPL; ++t)
     if ((okm >> t) & 1u) {
-      const float w = (float)T.w0[glane + LG * t];
+      const float w = T.w0f[glane + LG * t];
       num[0] = __fmaf_rn(w, v[t].x, num[0]);
       num[1] = __fmaf_rn(w, v[t].y, num[1]);
       num[2] = __fmaf_rn(w, v[t].z, num[2]);
@@ -137,7 +137,7 @@ __device__ __forceinline__ void eval_lattice(const BallParams& P, const BallTabl
   if (src.c3) {
 #pragma unroll
     for (int t = 0; t < KPL; ++t)
-      if ((okm >> t) & 1u) num[3] = __fmaf_rn((float)T.w0[glane + LG * t], src.c3[q[t]], num[3]);
+      if ((okm >> t) & 1u) num[3] = __fmaf_rn(T.w0f[glane + LG * t], src.c3[q[t]], num[3]);
   }
   const double inv = (acc != 0.0) ? 1.0 / acc : 0.0;
 #pragma unroll

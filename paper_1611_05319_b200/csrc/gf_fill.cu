@@ -85,6 +85,16 @@ __device__ __forceinline__ unsigned int hdilate(unsigned long long m, int R) {
 // 4 byte-wise test results (0xff / 0x00 per byte) -> 4 bits, byte i -> bit i
 __device__ __forceinline__ unsigned nib4(unsigned m) { return ((m & 0x01010101u) * 0x01020408u) >> 24; }
 
+// pixel index -> (column, row) without an integer division: the launch's
+// round-up multiplier for W (host: div_magic)
+__device__ __forceinline__ int row_of(const FillArgs& A, int p) {
+  return A.W == 1 ? p : (int)(__umulhi((unsigned)p, A.w_mul) >> A.w_shr);
+}
+__device__ __forceinline__ void col_row(const FillArgs& A, int p, int& i, int& j) {
+  j = row_of(A, p);
+  i = p - j * A.W;
+}
+
 __device__ __forceinline__ int stamp_of(const float4* work, int q) {
   return __float_as_int(work[q].w);
 }
@@ -1428,7 +1438,9 @@ __device__ __forceinline__ int neighbor_at(const FillArgs& A, int pi, int pj, in
 }
 
 __device__ __forceinline__ int neighbor_of(const FillArgs& A, uint32_t p, int o, bool& in) {
-  return neighbor_at(A, (int)p % A.W, (int)p / A.W, o, in);
+  int i, j;
+  col_row(A, (int)p, i, j);
+  return neighbor_at(A, i, j, o, in);
 }
 
 // Claim Inpaint neighbour q for the next frontier: INACTIVE -> ACTIVE (the
@@ -1798,6 +1810,7 @@ __global__ void __launch_bounds__(kShellThreads, GF_SHELL_MIN_BLOCKS)
     S.tab.n[i] = tables.n[i];
     S.tab.m[i] = tables.m[i];
     S.tab.w0[i] = tables.w0[i];
+    S.tab.w0f[i] = tables.w0f[i];
     S.tab.ni[i] = tables.ni[i];
     S.tab.mi[i] = tables.mi[i];
     S.tab.kn[i] = tables.kn[i];
@@ -1879,6 +1892,8 @@ __global__ void __launch_bounds__(kShellThreads, GF_SHELL_MIN_BLOCKS)
           GF_FINE(const unsigned long long fr0 = fine_after(0u);)
           const uint32_t e = cur_list[(size_t)f * A.cap + A.cap - 1 - rr];
           const uint32_t p = e & kEntryPix;
+          int pi_r, pj_r;
+          col_row(A, (int)p, pi_r, pj_r);
           GF_FINE(const unsigned long long fr1 = fine_after(e);)
           if (f != wf) {
             if (kTracked && wf >= 0) warp_flush(A, reg, wn, wf, nxt_list, nxt);
@@ -1895,8 +1910,8 @@ __global__ void __launch_bounds__(kShellThreads, GF_SHELL_MIN_BLOCKS)
           SampleResult res;
           GF_FINE(const unsigned long long tw0 = A.trace ? gtimer() : 0ULL;)
           if constexpr (R > 0)
-            eval_rot_warp<R>(P, S.tab, src, lane, (double)((int)p % A.W), (double)((int)p / A.W),
-                             gx, gy, g4.z, g4.w, res);
+            eval_rot_warp<R>(P, S.tab, src, lane, (double)pi_r, (double)pj_r, gx, gy, g4.z, g4.w,
+                             res);
           GF_FINE(if (A.trace && lane == 0) trace_max_val(A, k, 7, gtimer() - tw0);)
           GF_FINE(const unsigned long long fr2 = fine_after((unsigned)(__double_as_longlong(res.rw) >> 32));)
           bool filled = false;
@@ -1906,7 +1921,7 @@ __global__ void __launch_bounds__(kShellThreads, GF_SHELL_MIN_BLOCKS)
           if (lane == 0 && filled) ++wfills;
           if (kTracked)
             activate<8>(A, reg, wn, true, nxt_list, nxt, fw, f, k, lane < 8 ? lane : -1, filled, e,
-                        0xffu, (int)p % A.W, (int)p / A.W);
+                        0xffu, pi_r, pj_r);
           GF_FINE(if (lane == 0) fine_put(A, k, 7, fr2 - fr1); (void)fr0; (void)fr3;)
         } else {
           // ---- lattice round: items IPU q .. IPU q + IPU-1 of the concatenated
@@ -1931,7 +1946,8 @@ __global__ void __launch_bounds__(kShellThreads, GF_SHELL_MIN_BLOCKS)
           const int j = valid ? t - pf[fs] : 0;
           const uint32_t e = valid ? cur_list[(size_t)fs * A.cap + j] : 0u;
           const uint32_t p = e & kEntryPix;
-          const int pi = (int)p % A.W, pj = (int)p / A.W;
+          int pi, pj;
+          col_row(A, (int)p, pi, pj);
           GF_FINE(const unsigned long long fl1 = fine_after(e);)
           float4* fw = A.work + (size_t)fs * A.HW;
           WorkSource src{fw, A.c3 ? A.c3 + (size_t)fs * A.HW : nullptr, A.H, A.W, A.C, k};
@@ -1944,8 +1960,8 @@ __global__ void __launch_bounds__(kShellThreads, GF_SHELL_MIN_BLOCKS)
             eval_lattice<R, LG>(P, S.tab, src, lglane, lsub, valid, pi, pj, res);
           } else {
             if (valid && (e & kEntryRot)) frame_guide(A, fs, (int)p, gx, gy);
-            eval_item<NL, 0>(P, S.tab, src, glane, valid, (double)((int)p % A.W),
-                             (double)((int)p / A.W), true, gx, gy, res);
+            eval_item<NL, 0>(P, S.tab, src, glane, valid, (double)pi, (double)pj, true, gx, gy,
+                             res);
           }
           GF_FINE(if (A.trace && valid && lglane == 0) trace_max_val(A, k, 6, gtimer() - te0);)
           GF_FINE(const unsigned long long fl2 = fine_after((unsigned)(__double_as_longlong(res.rw) >> 32));)
@@ -2235,6 +2251,21 @@ static bool launch_prep_tma(bool f64, int C, dim3 grid, cudaStream_t stream, con
 
 static size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
+// round-up multiplier for division by d of dividends below 2^31 (q =
+// umulhi(n, mul) >> shr), the scheme of CUTLASS's FastDivmod
+static void div_magic(int d, unsigned& mul, int& shr) {
+  if (d <= 1) {
+    mul = 0;
+    shr = 0;
+    return;
+  }
+  int l = 0;
+  while ((1LL << l) < d) ++l;
+  const int p = 31 + l;
+  mul = (unsigned)(((1ULL << p) + (unsigned long long)d - 1) / (unsigned long long)d);
+  shr = p - 32;
+}
+
 struct Layout {
   size_t work, c3, list0, list1, conf, gbuf, bys, ints, u64, total;
 };
@@ -2335,6 +2366,7 @@ int fill_launch(const gf_frames* fr, const gf_fill_params* prm, const gf_fill_ou
   FillArgs A;
   memset(&A, 0, sizeof(A));
   A.nF = nF; A.H = H; A.W = W; A.HW = HW; A.C = C; A.cap = HW;
+  div_magic(W, A.w_mul, A.w_shr);
   A.image = fr->image;
   A.labels = fr->labels;
   A.gsrc = fr->guide;

@@ -17,6 +17,8 @@ constexpr int kIntsPerFrame = 28;  // cnt[4] cntR[4] fills[4] anyg[4] + 11 scala
 // Everything the fill kernels need, passed by value (__grid_constant__).
 struct FillArgs {
   int nF, H, W, HW, C, cap;
+  unsigned w_mul;  // fast division by W (round-up multiplier, valid below 2^31)
+  int w_shr;
   int dtype;
   const void* image;
   const uint8_t* labels;

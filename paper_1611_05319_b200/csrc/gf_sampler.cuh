@@ -55,6 +55,7 @@ struct BallTables {
   double n[kMaxK];
   double m[kMaxK];
   double w0[kMaxK];
+  float w0f[kMaxK];  // (float)w0: the fp32 colour numerators' weights
   int ni[kMaxK];  // the same offsets as integers (lattice path)
   int mi[kMaxK];
   signed char kn[kMaxK];  // sample k is 8-neighbour kn[k] of the centre, or -1
