@@ -479,6 +479,65 @@ def e2e_c5(c5, ring=16):
             "d2h_bytes_per_step": int(n * fb)}
 
 
+def bench_deadlock(dev):
+    """SURVEY.md section 7 hard part 2: the 256x256 half-plane at 25 degrees,
+    smart order, mu 50 -- 22,058 shells, 16,636 of them deadlock-guarded
+    (tests/cases.deadlock_scenes, parity in tests/test_gpu_deadlock.py)."""
+    import numpy as np
+    import torch
+
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import cases
+
+    from paper_1611_05319_b200 import FillParams
+    from paper_1611_05319_b200 import _native as N
+    from paper_1611_05319_b200._device import fill_device
+
+    out = {}
+    for th in (25.0, 10.0):
+        case = cases.deadlock_scenes(thetas=(th,), mus=(50.0,))[0]
+        img = torch.from_numpy(case["image"][None].astype(np.float32)).to(dev)
+        lab = torch.from_numpy(case["labels"][None]).to(dev)
+        g = torch.from_numpy(case["guide"][None]).to(dev)
+        p = FillParams(**case["params"])
+        res = fill_device(img, lab, g, p, rows_cap=1 << 16)
+        ws = res["workspace"]
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record()
+        res = fill_device(img, lab, g, p, rows_cap=1 << 16, workspace=ws)
+        e1.record()
+        torch.cuda.synchronize()
+        st = res["stats"][0].cpu().numpy()
+        ms = e0.elapsed_time(e1)
+        out[case["name"]] = {"ms": ms, "shells": int(st[N.STAT_ITERATIONS]),
+                             "guarded_shells": int(st[N.STAT_DEADLOCK]),
+                             "us_per_shell": ms * 1e3 / int(st[N.STAT_ITERATIONS])}
+    a, b = out["halfplane_25deg_mu50"], out["halfplane_10deg_mu50"]
+    # per guarded shell: the 10 degree chain is 97% unguarded shells of the
+    # same kind, so its us/shell prices the unguarded part of the 25 degree one
+    a["us_per_guarded_shell_est"] = ((a["ms"] * 1e3 - (a["shells"] - a["guarded_shells"])
+                                      * b["us_per_shell"]) / a["guarded_shells"])
+    return out
+
+
+def bench_detect():
+    """Automatic spline detection (guide.detect_splines) on the C2 and C4
+    frames through the public API (host f64 image in, Spline list out)."""
+    from paper_1611_05319_b200 import guide, scenes
+
+    out = {}
+    for name in ("C2", "C4"):
+        sc = scenes.config(name)
+        guide.detect_splines(sc.image, sc.labels)  # warm-up
+        t0 = time.perf_counter()
+        spl = guide.detect_splines(sc.image, sc.labels)
+        out[name] = {"ms": (time.perf_counter() - t0) * 1e3, "splines": len(spl),
+                     "path": "guide.detect_splines: gf_detect_edges (ring, Canny, seed strengths), "
+                             "host clustering, gf_structure_eigen, gf_trace_rays"}
+    return out
+
+
 def rank_main(args):
     import torch
     import torch.distributed as dist
@@ -560,6 +619,8 @@ def rank_main(args):
             e2e["video_pipelined_mpx_s"] = c5_line["e2e"]["value"]
             e2e["video_pipelined_ms_per_frame"] = c5_line["e2e"]["ms_per_frame_per_gpu"]
         cpu = None if args.no_cpu else pool_baseline("C2")
+        deadlock = None if args.no_extras else bench_deadlock(dev)
+        detect = None if args.no_extras else bench_detect()
         line = {
             "metric": METRIC, "value": D / (c2["t_ms"] * 1e-3) / 1e6, "unit": "Mpx/s",
             "n_gpus": 1, "steps": args.steps, "warmup": max(3, args.warmup),
@@ -583,6 +644,8 @@ def rank_main(args):
                          "algorithmic_bytes": bf},
             "e2e": e2e,
             "c5": c5_line,
+            "deadlock_regime": deadlock,
+            "spline_detection": detect,
             "gpu_launches": c2["launches"],
             "gpu_launches_note": "library kernels (gf_launch_count) in the C2 timed replays; "
                                  "the whole run launched "
@@ -640,6 +703,8 @@ def parse(argv=None):
     ap.add_argument("--no-c5", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="skip the deadlock-regime and spline-detection timings")
     return ap.parse_args(argv)
 
 

@@ -20,9 +20,9 @@ for r in rows:
         recs.append(dict(zip(hdr, r)))
 agg = collections.defaultdict(lambda: collections.defaultdict(list))
 for d in recs:
-    if "gf::" not in d["Kernel Name"]:
+    if not any(k in d["Kernel Name"] for k in ("k_prep", "k_shells")):
         continue
-    name = d["Kernel Name"].split("(")[0].replace("void ", "")
+    name = d["Kernel Name"].split("(")[0].replace("void ", "").replace("gf::", "")
     agg[name][d["Metric Name"]].append(float(d["Metric Value"].replace(",", "")))
 launch = {k: {m: sum(v) / len(v) for m, v in ms.items()} | {"launches": len(ms["gpu__time_duration.sum"])}
           for k, ms in agg.items()}
@@ -45,10 +45,12 @@ want = ["Duration", "Registers Per Thread", "Achieved Occupancy", "Theoretical O
 full = collections.defaultdict(dict)
 for r in det[1:]:
     if r[mi] in want:
-        name = r[ki].split("(")[0].replace("void ", "")
+        name = r[ki].split("(")[0].replace("void ", "").replace("gf::", "")
         full[name][r[mi]] = f"{r[vi]} {r[ui]}".strip()
 traffic = sum(v["dram__bytes_read.sum"] + v["dram__bytes_write.sum"] for v in launch.values())
-summary = {"tag": tag, "launch_list": launch, "full_capture": full,
+head = subprocess.run(["git", "rev-parse", "--short=12", "HEAD"], capture_output=True,
+                      text=True).stdout.strip()
+summary = {"tag": tag, "head": head, "launch_list": launch, "full_capture": full,
            "fill_dram_bytes_per_launch": traffic, "algorithmic_bytes_per_frame": 53079040}
 json.dump(summary, open(f"profiles/{tag}_ncu_summary.json", "w"), indent=1)
 print(json.dumps(summary, indent=1))
