@@ -358,7 +358,7 @@ def bench_c5(args, dev, ws, rank, local):
     D = int((labels == 255).sum().item())
     splines = [_spl_objs(s) for s in spl_raw]
     graph = BatchGraph(images, labels, splines, params, chunk=args.chunk,
-                       tracked=not args.untracked)
+                       tracked=not args.untracked, streams=args.streams)
     for _ in range(max(3, args.warmup)):
         graph.replay()
     torch.cuda.synchronize()
@@ -545,10 +545,19 @@ def rank_main(args):
     from paper_1611_05319_b200 import _native as N
 
     ws, rank, local = dist_env()
+    # GF_BENCH_ONE_DEVICE=1: every rank on device 0 with gloo -- a functional
+    # check of the multi-rank path on a one-GPU box (times are not measurements:
+    # the ranks share the GPU)
+    one_dev = os.environ.get("GF_BENCH_ONE_DEVICE") == "1"
+    if one_dev:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if ws > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if one_dev:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     launches0 = N.launch_count()
 
     from paper_1611_05319_b200.video import reduce_over_ranks
@@ -700,6 +709,8 @@ def parse(argv=None):
     ap.add_argument("--untracked", action="store_true")
     ap.add_argument("--c5-frames", type=int, default=C5_FRAMES)
     ap.add_argument("--chunk", type=int, default=64, help="frames per batched launch (C5)")
+    ap.add_argument("--streams", type=int, default=1,
+                    help="streams the C5 chunks alternate over (overlap of prep and shells)")
     ap.add_argument("--no-c5", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")

@@ -173,19 +173,19 @@ class BatchGraph:
     """
 
     def __init__(self, images, labels, splines, params, chunk=64, tracked=True, rows_cap=4096,
-                 eta=3.0):
+                 eta=3.0, streams=1):
         import torch
 
         n = images.shape[0]
         self.parts = []
         calls = []
-        ws = None
-        for c0 in range(0, n, chunk):
+        wss = [None] * streams
+        for k, c0 in enumerate(range(0, n, chunk)):
             c1 = min(n, c0 + chunk)
             segs = SegmentSet(list(splines[c0:c1]), images.device, per_frame=True)
             res, call = _fill_setup(images[c0:c1], labels[c0:c1], None, params, tracked, False,
-                                    rows_cap, ws, segs, eta, 0, False)
-            ws = res["workspace"]  # the first (largest) chunk sizes it
+                                    rows_cap, wss[k % streams], segs, eta, 0, False)
+            wss[k % streams] = res["workspace"]  # one workspace per stream
             res["frames"] = (c0, c1)
             self.parts.append(res)
             calls.append(call)
@@ -196,8 +196,21 @@ class BatchGraph:
         self.graph = torch.cuda.CUDAGraph()
         n0 = N.launch_count()
         with torch.cuda.graph(self.graph):
-            for res, call in zip(self.parts, calls):
-                _fill_launch(res, call)
+            if streams == 1:
+                for res, call in zip(self.parts, calls):
+                    _fill_launch(res, call)
+            else:
+                # chunks alternate over forked streams: chunk k+1's prep can run
+                # beside chunk k's shell loop (each stream reuses its workspace)
+                main = torch.cuda.current_stream()
+                side = [torch.cuda.Stream() for _ in range(streams)]
+                for st in side:
+                    st.wait_stream(main)
+                for k, (res, call) in enumerate(zip(self.parts, calls)):
+                    with torch.cuda.stream(side[k % streams]):
+                        _fill_launch(res, call)
+                for st in side:
+                    main.wait_stream(st)
         self.launches_per_replay = N.launch_count() - n0
         torch.cuda.synchronize()
 

@@ -2346,6 +2346,8 @@ static int coop_grid(const void* fn, size_t smem, int* out_grid) {
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kShellThreads, smem) != cudaSuccess ||
       per_sm <= 0)
     return set_error(GF_E_CUDA, "occupancy query failed");
+  // GF_SHELL_BPS caps the blocks per SM (experiments: room for a concurrent prep)
+  if (const char* e = getenv("GF_SHELL_BPS")) per_sm = std::max(1, std::min(per_sm, atoi(e)));
   *out_grid = sms * per_sm;
   std::lock_guard<std::mutex> lock(mu);
   cache.push_back(Entry{dev, fn, smem, *out_grid});

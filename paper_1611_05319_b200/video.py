@@ -39,7 +39,9 @@ def reduce_over_ranks(sums=(), maxes=(), device="cpu"):
         if not vals:
             out.append([])
             continue
-        t = torch.tensor(vals, dtype=torch.float64, device=device)
+        # gloo reduces host tensors; NCCL device ones
+        dev = "cpu" if dist.get_backend() == "gloo" else device
+        t = torch.tensor(vals, dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=op)
         out.append(t.cpu().tolist())
     return out[0], out[1]

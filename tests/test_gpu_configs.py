@@ -610,3 +610,27 @@ def test_bench_line_single_gpu(tmp_path):
     assert line["c5"]["frames_total"] == 6 and line["c5"]["value"] > 0
     assert line["gpu_launches"] == 2 * 3
     assert line["e2e"]["value"] > 0 and line["c5"]["e2e"]["value"] > 0
+
+
+def test_bench_multi_rank_path_on_one_device(tmp_path):
+    """bench.py --gpus 2 spawns its own ranks, splits the C5 batch into frame
+    blocks and reduces over the ranks; on a one-GPU box both ranks share
+    device 0 (gloo bookkeeping): a functional check of the N > 1 line, not a
+    measurement."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, GF_BENCH_ONE_DEVICE="1")
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--steps",
+                          "3", "--warmup", "3", "--c5-frames", "6", "--chunk", "2", "--no-e2e"],
+                         capture_output=True, text=True, timeout=900, cwd=root, env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1  # rank 0 only
+    line = json.loads(lines[0])
+    assert line["n_gpus"] == 2 and line["config"]["global_batch"] == 6
+    assert line["c5"]["frames_per_gpu"] == 3 and line["value"] == line["c5"]["value"]
+    assert line["c5"]["inpaint_px_total"] > 0
