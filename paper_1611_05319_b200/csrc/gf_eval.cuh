@@ -50,13 +50,22 @@ __device__ __forceinline__ void eval_lattice(const BallParams& P, const BallTabl
   // by flat offset; near the border each sample is bounds-checked / wrapped
   const bool inner = pi >= R && pi + R < src.W && pj >= R && pj + R < src.H;
   const int p = pj * src.W + pi;
+  if (__all_sync(0xffffffffu, inner || !valid)) {
+    // the whole warp's items lie inside the lattice (warp-uniform branch)
 #pragma unroll
-  for (int t = 0; t < KPL; ++t) {
-    const int k = glane + LG * t;
-    q[t] = (valid && k < B::K)
-               ? (inner ? p + T.off[k]
-                        : lattice_index(pi + T.ni[k], pj + T.mi[k], src.H, src.W, P.periodic))
-               : -1;
+    for (int t = 0; t < KPL; ++t) {
+      const int k = glane + LG * t;
+      q[t] = (valid && k < B::K) ? p + T.off[k] : -1;
+    }
+  } else {
+#pragma unroll
+    for (int t = 0; t < KPL; ++t) {
+      const int k = glane + LG * t;
+      q[t] = (valid && k < B::K)
+                 ? (inner ? p + T.off[k]
+                          : lattice_index(pi + T.ni[k], pj + T.mi[k], src.H, src.W, P.periodic))
+                 : -1;
+    }
   }
 #ifdef GF_FINE_TRACE
   {

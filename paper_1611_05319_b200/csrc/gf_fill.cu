@@ -1428,8 +1428,9 @@ __device__ __forceinline__ bool decide_and_write(const FillArgs& A, int f, int j
 
 // 8-neighbour o (grid.py:29-33 order) of pixel (pi, pj)
 __device__ __forceinline__ int neighbor_at(const FillArgs& A, int pi, int pj, int o, bool& in) {
-  const int di = (o < 3) ? o - 1 : (o == 3 ? -1 : (o == 4 ? 1 : o - 6));
-  const int dj = (o < 3) ? -1 : (o < 5 ? 0 : 1);
+  // NEIGHBOR_OFFSETS (grid.py:29-33) packed as 2-bit (d + 1) fields: no branches
+  const int di = (int)((0x9224u >> (2 * o)) & 3u) - 1;
+  const int dj = (int)((0xA940u >> (2 * o)) & 3u) - 1;
   int ii = pi + di;
   const int jj = pj + dj;
   if (A.periodic) ii = ii < 0 ? ii + A.W : (ii >= A.W ? ii - A.W : ii);
