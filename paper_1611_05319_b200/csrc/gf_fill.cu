@@ -379,13 +379,10 @@ __global__ void __launch_bounds__(kThreads, GF_PREP_MIN_BLOCKS) k_prep(const __g
         m[2 * b] = __reduce_max_sync(0xffffffffu, any ? ~enc32((float)vlo[b]) : 0u);
         m[2 * b + 1] = __reduce_max_sync(0xffffffffu, any ? enc32((float)vhi[b]) : 0u);
       }
-      if (lane == 0) {  // the fp64 codes, once per warp
+      // the block reduces the 32-bit codes; the fp64 codes are made once
+      // per block below
 #pragma unroll
-        for (int b = 0; b < 2; ++b) {
-          ered[2 * b] = m[2 * b] ? ~enc_ordered((double)dec32(~m[2 * b])) : 0ULL;
-          ered[2 * b + 1] = m[2 * b + 1] ? enc_ordered((double)dec32(m[2 * b + 1])) : 0ULL;
-        }
-      }
+      for (int i = 0; i < 4; ++i) ered[i] = m[i];
     } else {
 #pragma unroll
       for (int b = 0; b < 2; ++b) {
@@ -413,6 +410,12 @@ __global__ void __launch_bounds__(kThreads, GF_PREP_MIN_BLOCKS) k_prep(const __g
       const int i = threadIdx.x;
       unsigned long long e = 0ULL;
       for (int w = 0; w < kThreads / 32; ++w) e = s_red[i][w] > e ? s_red[i][w] : e;
+      if constexpr (sizeof(T) == 4) {
+        // 32-bit order codes of fp32 values -> the fp64 codes of the hull
+        const unsigned m = (unsigned)e;
+        e = (i & 1) ? (m ? enc_ordered((double)dec32(m)) : 0ULL)
+                    : (m ? ~enc_ordered((double)dec32(~m)) : 0ULL);
+      }
       // i < 2: the frame's hull (most tiles cannot move it any more: skip
       // their atomics); i >= 2: the tile's Bystander range, read by the
       // shell loop's clip, and the frame's
@@ -832,13 +835,10 @@ __global__ void __launch_bounds__(kThreads, GF_PREP_MIN_BLOCKS)
         m[2 * b] = __reduce_max_sync(0xffffffffu, any ? ~enc32((float)vlo[b]) : 0u);
         m[2 * b + 1] = __reduce_max_sync(0xffffffffu, any ? enc32((float)vhi[b]) : 0u);
       }
-      if (lane == 0) {  // the fp64 codes, once per warp
+      // the block reduces the 32-bit codes; the fp64 codes are made once
+      // per block below
 #pragma unroll
-        for (int b = 0; b < 2; ++b) {
-          ered[2 * b] = m[2 * b] ? ~enc_ordered((double)dec32(~m[2 * b])) : 0ULL;
-          ered[2 * b + 1] = m[2 * b + 1] ? enc_ordered((double)dec32(m[2 * b + 1])) : 0ULL;
-        }
-      }
+      for (int i = 0; i < 4; ++i) ered[i] = m[i];
     } else {
 #pragma unroll
       for (int b = 0; b < 2; ++b) {
@@ -866,6 +866,12 @@ __global__ void __launch_bounds__(kThreads, GF_PREP_MIN_BLOCKS)
       const int i = threadIdx.x;
       unsigned long long e = 0ULL;
       for (int w = 0; w < kThreads / 32; ++w) e = s_red[i][w] > e ? s_red[i][w] : e;
+      if constexpr (sizeof(T) == 4) {
+        // 32-bit order codes of fp32 values -> the fp64 codes of the hull
+        const unsigned m = (unsigned)e;
+        e = (i & 1) ? (m ? enc_ordered((double)dec32(m)) : 0ULL)
+                    : (m ? ~enc_ordered((double)dec32(~m)) : 0ULL);
+      }
       // i < 2: the frame's hull (most tiles cannot move it any more: skip
       // their atomics); i >= 2: the tile's Bystander range, read by the
       // shell loop's clip, and the frame's
