@@ -316,6 +316,16 @@ int64_t gf_launch_count(void);
 void gf_host_exp(const double* x, double* y, int64_t n);
 void gf_host_hypot(const double* x, const double* y, double* out, int64_t n);
 double gf_host_pairwise_sum(const double* a, int32_t n);
+/* numpy's float64 arctan2 / tanh (SVML __svml_atan28_ha / __svml_tanh8) and
+ * sin / cos (glibc libm, |x| <= 2.426) as the coherence kernels compute them
+ * (gf_npmath.cuh): guide.eigen_2x2, guide.py:123-136. */
+void gf_host_atan2(const double* y, const double* x, double* out, int64_t n);
+void gf_host_tanh(const double* x, double* y, int64_t n);
+void gf_host_sincos(const double* x, double* s, double* c, int64_t n);
+/* The same four on the device, element-wise over n device doubles:
+ * op 0 out = atan2(a, b), 1 tanh(a), 2 sin(a), 3 cos(a). */
+int gf_npmath_eval(int32_t op, int64_t n, const double* a, const double* b, double* out,
+                   void* stream);
 
 /*
  * The plain / masked structure tensor's eigen split at the n queries, as

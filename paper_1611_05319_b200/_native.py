@@ -34,6 +34,7 @@ EXPORTS = (
     "gf_commit_shell", "gf_structure_eigen", "gf_detect_workspace_bytes", "gf_detect_edges",
     "gf_trace_rays", "gf_last_error",
     "gf_abi_version", "gf_launch_count", "gf_host_exp", "gf_host_hypot", "gf_host_pairwise_sum",
+    "gf_host_atan2", "gf_host_tanh", "gf_host_sincos", "gf_npmath_eval",
 )
 
 
@@ -177,6 +178,10 @@ def load(required: bool = True):
     lib.gf_host_exp.argtypes = [P, P, ctypes.c_int64]
     lib.gf_host_hypot.argtypes = [P, P, P, ctypes.c_int64]
     lib.gf_host_pairwise_sum.restype = ctypes.c_double
+    lib.gf_host_atan2.argtypes = [P, P, P, ctypes.c_int64]
+    lib.gf_host_tanh.argtypes = [P, P, ctypes.c_int64]
+    lib.gf_host_sincos.argtypes = [P, P, P, ctypes.c_int64]
+    lib.gf_npmath_eval.argtypes = [ctypes.c_int32, ctypes.c_int64, P, P, P, P]
     lib.gf_host_pairwise_sum.argtypes = [P, ctypes.c_int32]
     _lib = lib
     return lib

@@ -17,6 +17,7 @@
 #include <vector>
 
 #include "gf_internal.cuh"
+#include "gf_npmath.cuh"
 
 namespace gf {
 
@@ -233,6 +234,21 @@ void gf_host_hypot(const double* x, const double* y, double* out, int64_t n) {
 double gf_host_pairwise_sum(const double* a, int32_t n) {
   const PairwisePlan p = make_plan(n);
   return plan_sum(p, a);
+}
+
+void gf_host_atan2(const double* y, const double* x, double* out, int64_t n) {
+  for (int64_t i = 0; i < n; ++i) out[i] = atan2_np(y[i], x[i]);
+}
+
+void gf_host_tanh(const double* x, double* y, int64_t n) {
+  for (int64_t i = 0; i < n; ++i) y[i] = tanh_np(x[i]);
+}
+
+void gf_host_sincos(const double* x, double* s, double* c, int64_t n) {
+  for (int64_t i = 0; i < n; ++i) {
+    s[i] = sin_np(x[i]);
+    c[i] = cos_np(x[i]);
+  }
 }
 
 }  // extern "C"

@@ -22,15 +22,18 @@
 //            g = coh * (-sin phi, cos phi), g = 0 where mass_r <= 0.
 // The weights follow scipy's _gaussian_kernel1d: exp(-0.5 / s^2 * x^2) / sum,
 // with numpy's exp (exp_np) and pairwise sum (plan_sum) restated.
-// arctan2 / sin / cos / tanh are CUDA's (numpy's SVML differs by <= a few
-// ulp): g agrees to ~1e-15, far inside the 1e-4 value tolerance, and the
-// coherence preset fills in onion order, which does not read g.
+// arctan2 / tanh / sin / cos are numpy's own, restated bit for bit
+// (gf_npmath.cuh): the smart-order deadlock argmax can hinge on a 1-ulp
+// difference in g.
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "gf_internal.cuh"
 #include "gf_math.cuh"
+#include "gf_npmath.cuh"
 
 namespace gf {
 
@@ -245,10 +248,10 @@ __global__ void k_ct_query(int H, int W, int n, const int64_t* __restrict__ idx,
   const double mean = (a + c) / 2.0;
   const double h = (a - c) / 2.0;
   const double disc = sqrt(h * h + b * b);
-  const double phi = 0.5 * atan2(2.0 * b, a - c);
+  const double phi = 0.5 * atan2_np(2.0 * b, a - c);
   const double lo = mean - disc, hi = mean + disc;
-  const double coh = tanh((hi - lo) / lam);
-  const double vx = -sin(phi), vy = cos(phi);
+  const double coh = tanh_np((hi - lo) / lam);
+  const double vx = -sin_np(phi), vy = cos_np(phi);
   if (eig) {  // guide.eigen_2x2's minor eigenvector and the coherence (make_spline),
               // the normalised tensor (structure_tensor) and the rho mass
     double* e = eig + 8 * k;
@@ -457,6 +460,32 @@ extern "C" int gf_commit_shell(int32_t channels, int32_t n, const int64_t* front
   k_ct_commit<<<(n + 127) / 128, 128, 0, static_cast<cudaStream_t>(stream)>>>(
       channels, n, frontier, rw, tw, vals, g, ready_mode, c, c2, shell, image, labels, fillshell,
       fill, count);
+  count_launches(1);
+  cudaError_t e = cudaPeekAtLastError();
+  if (e != cudaSuccess) return set_error(GF_E_CUDA, cudaGetErrorString(e));
+  return GF_OK;
+}
+
+namespace gf {
+// The coherence transcendentals on the device, element-wise (test hook for
+// gf_npmath.cuh against numpy; the query kernel inlines the same functions).
+__global__ void k_npmath(int op, int64_t n, const double* __restrict__ a,
+                         const double* __restrict__ b, double* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double x = a[i];
+    out[i] = op == 0 ? atan2_np(x, b[i]) : op == 1 ? tanh_np(x) : op == 2 ? sin_np(x) : cos_np(x);
+  }
+}
+}  // namespace gf
+
+extern "C" int gf_npmath_eval(int32_t op, int64_t n, const double* a, const double* b,
+                              double* out, void* stream) {
+  if (op < 0 || op > 3 || n < 0) return set_error(GF_E_INVALID, "bad op / n");
+  if (n == 0) return GF_OK;
+  if (!a || !out || (op == 0 && !b)) return set_error(GF_E_INVALID, "NULL buffer");
+  const int64_t blocks = std::min<int64_t>((n + 255) / 256, 148 * 16);
+  k_npmath<<<(int)blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(op, n, a, b, out);
   count_launches(1);
   cudaError_t e = cudaPeekAtLastError();
   if (e != cudaSuccess) return set_error(GF_E_CUDA, cudaGetErrorString(e));

@@ -34,7 +34,7 @@ __global__ void __launch_bounds__(kPtThreads)
     const double gx = valid ? g[2 * t] : 0.0, gy = valid ? g[2 * t + 1] : 0.0;
     const bool integral = (x == floor(x)) && (y == floor(y)) && fabs(x) < 1e9 && fabs(y) < 1e9;
     SampleResult r;
-    eval_item<NL, 0>(P, T, src, lane, valid, x, y, integral, gx, gy, r);
+    eval_item<NL, 0, true>(P, T, src, lane, valid, x, y, integral, gx, gy, r);
     if (valid && lane == 0) {
       rw[t] = r.rw;
       tw[t] = r.tw;

@@ -322,8 +322,15 @@ __device__ __forceinline__ double sample_weight(const BallParams& P, const BallT
 // KPL = samples per lane (ceil(K / 8)) as a compile-time bound so every
 //       fetch of a lane is issued before the first one is consumed, or 0
 //       for a runtime loop (large radii).
+// EXACTV: the colour numerator in numpy's einsum("fk,fkc->fc") order
+//       (engine.py:196) instead of per-lane partial sums, so the values are
+//       bit-exact in fp64 (the coherence path feeds them back into the
+//       structure tensor).  For C >= 2 einsum adds the products w_k * v_kc
+//       in k order; for C == 1 both operands are contiguous and its SSE2
+//       loop keeps two lanes (even / odd k), folding each block of 8 from
+//       the top (k+6, k+4, k+2, k) and the tail upwards, then adds the lanes.
 // The result is valid in every lane of the group.
-template <int NL, int KPL, class Src>
+template <int NL, int KPL, bool EXACTV = false, class Src>
 __device__ __forceinline__ void eval_item(const BallParams& P, const BallTables& T,
                                           const Src& src, int lane, bool valid, double fi,
                                           double fj, bool integral, double gx, double gy,
@@ -362,7 +369,81 @@ __device__ __forceinline__ void eval_item(const BallParams& P, const BallTables&
   double num[4] = {0.0, 0.0, 0.0, 0.0};
   const int pi = (int)fi, pj = (int)fj;
 
-  if (gzero && integral) {
+  double ex_s[4] = {0.0, 0.0, 0.0, 0.0};  // EXACTV: C >= 2 sums / C == 1 lanes 0, 1
+  if constexpr (EXACTV) {
+    // one sample per lane per block of kGroup, blocks uniform over the group
+#pragma unroll 1
+    for (int kb = 0; kb < K; kb += kGroup) {
+      const int k = kb + lane;
+      double p[4] = {0.0, 0.0, 0.0, 0.0};
+      if (k < K) {
+        double px = T.n[k], py = T.m[k], w = T.w0[k];
+        if (!gzero) w = sample_weight(P, T, k, gx, gy, ux, uy, safe, thr, px, py);
+        double sv[4] = {0.0, 0.0, 0.0, 0.0};
+        bool ok = false;
+        if (gzero && integral) {
+          const int q = valid ? lattice_index(pi + T.ni[k], pj + T.mi[k], src.H, src.W,
+                                              P.periodic)
+                              : -1;
+          if (q >= 0) {
+            const auto v = src.fetch(q);
+            ok = src.readable(v);
+            if (ok) src.accumulate(v, 1.0, sv);
+          }
+        } else {
+          Corners cn;
+          ghost_corners(fi + px, fj + py, src.H, src.W, P.periodic, cn);
+          ok = valid && !cn.outside;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            if (cn.q[c] >= 0 && valid) {
+              const auto v = src.fetch(cn.q[c]);
+              ok = ok && src.readable(v);
+              src.accumulate(v, cn.w[c], sv);
+            }
+          }
+        }
+        const double wr = ok ? w : 0.0;
+        if (ok) {
+#pragma unroll
+          for (int c = 0; c < 4; ++c) p[c] = wr * sv[c];
+        }
+        acc_sample<NL>(P, k, w, wr, acc_rw, acc_tw, tl_rw, tl_tw);
+      }
+      const int rem = K - kb;  // samples in this block (all lanes agree)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        double q[kGroup];
+#pragma unroll
+        for (int l = 0; l < kGroup; ++l) q[l] = __shfl_sync(0xffffffffu, p[c], l, kGroup);
+        if (c >= src.C) continue;
+        if (src.C == 1) {
+          if (rem >= 8) {
+            ex_s[0] = q[6] + ex_s[0];
+            ex_s[0] = q[4] + ex_s[0];
+            ex_s[0] = q[2] + ex_s[0];
+            ex_s[0] = q[0] + ex_s[0];
+            ex_s[1] = q[7] + ex_s[1];
+            ex_s[1] = q[5] + ex_s[1];
+            ex_s[1] = q[3] + ex_s[1];
+            ex_s[1] = q[1] + ex_s[1];
+          } else {
+#pragma unroll
+            for (int l = 0; l < 8; l += 2) {
+              if (l < rem) {
+                ex_s[0] = q[l] + ex_s[0];
+                ex_s[1] = (l + 1 < rem ? q[l + 1] : 0.0) + ex_s[1];
+              }
+            }
+          }
+        } else {
+#pragma unroll
+          for (int l = 0; l < kGroup; ++l)
+            if (l < rem) ex_s[c] = ex_s[c] + q[l];
+        }
+      }
+    }
+  } else if (gzero && integral) {
     // lattice path (most Inpaint pixels): weights are the host's
     // 1/hypot(n, m); one fetch per sample, all issued up front
     if constexpr (KPL > 0) {
@@ -511,13 +592,19 @@ __device__ __forceinline__ void eval_item(const BallParams& P, const BallTables&
   }
   rw = __shfl_sync(0xffffffffu, rw, 0, kGroup);
   tw = __shfl_sync(0xffffffffu, tw, 0, kGroup);
+  if constexpr (EXACTV) {
+    if (src.C == 1) ex_s[0] = 0.0 + (ex_s[0] + ex_s[1]);
 #pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    double s = num[c];
-    s += __shfl_xor_sync(0xffffffffu, s, 1, kGroup);
-    s += __shfl_xor_sync(0xffffffffu, s, 2, kGroup);
-    s += __shfl_xor_sync(0xffffffffu, s, 4, kGroup);
-    out.v[c] = (rw != 0.0) ? s / rw : 0.0;
+    for (int c = 0; c < 4; ++c) out.v[c] = (c < src.C && rw != 0.0) ? ex_s[c] / rw : 0.0;
+  } else {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      double s = num[c];
+      s += __shfl_xor_sync(0xffffffffu, s, 1, kGroup);
+      s += __shfl_xor_sync(0xffffffffu, s, 2, kGroup);
+      s += __shfl_xor_sync(0xffffffffu, s, 4, kGroup);
+      out.v[c] = (rw != 0.0) ? s / rw : 0.0;
+    }
   }
   out.rw = rw;
   out.tw = tw;

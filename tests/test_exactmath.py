@@ -89,3 +89,88 @@ def test_pairwise_plan_matches_numpy_row_sum(n):
     got = np.array([lib.gf_host_pairwise_sum(np.ascontiguousarray(row).ctypes.data_as(P), n)
                     for row in a])
     assert np.array_equal(got.view(np.int64), ref.view(np.int64))
+
+
+# ---- coherence directions: numpy arctan2 / tanh (SVML) and sin / cos (libm) ----
+# guide.eigen_2x2 (guide.py:123-136): phi = 0.5 * arctan2(2b, a - c),
+# v = (-sin phi, cos phi), coherence tanh((hi - lo) / lam).  gf_npmath.cuh.
+
+def _bits_equal(got, ref):
+    same = got.view(np.int64) == ref.view(np.int64)
+    return bool(np.all(same | (np.isnan(got) & np.isnan(ref))))
+
+
+def host_atan2(y, x):
+    o = np.empty_like(x)
+    lib.gf_host_atan2(y.ctypes.data_as(P), x.ctypes.data_as(P), o.ctypes.data_as(P), x.size)
+    return o
+
+
+def host_tanh(x):
+    o = np.empty_like(x)
+    lib.gf_host_tanh(x.ctypes.data_as(P), o.ctypes.data_as(P), x.size)
+    return o
+
+
+def host_sincos(x):
+    s, c = np.empty_like(x), np.empty_like(x)
+    lib.gf_host_sincos(x.ctypes.data_as(P), s.ctypes.data_as(P), c.ctypes.data_as(P), x.size)
+    return s, c
+
+
+N_EXACT = 10_000_000
+
+
+@pytest.mark.skipif(orc.numpy_exp_flavour() != "svml", reason="numpy has no SVML on this host")
+@pytest.mark.parametrize("span", [(0, 0), (-12, 8)])
+def test_atan2_matches_numpy(span):
+    # 10 M pairs: unit normals, then magnitudes spread over 1e-12 .. 1e8
+    rng = np.random.default_rng(101 + span[0])
+    y = rng.standard_normal(N_EXACT)
+    x = rng.standard_normal(N_EXACT)
+    if span != (0, 0):
+        y *= 10.0 ** rng.uniform(*span, N_EXACT)
+        x *= 10.0 ** rng.uniform(*span, N_EXACT)
+    assert _bits_equal(host_atan2(y, x), np.arctan2(y, x))
+
+
+@pytest.mark.skipif(orc.numpy_exp_flavour() != "svml", reason="numpy has no SVML on this host")
+def test_atan2_structure_tensor_arguments_and_specials():
+    # the coherence arguments (2 J12, J11 - J22) of smoothed squared gradients,
+    # exact ties and near-axis directions included
+    rng = np.random.default_rng(7)
+    a = rng.uniform(0, 1, 2_000_000) ** 2
+    c = rng.uniform(0, 1, 2_000_000) ** 2
+    b = rng.uniform(-1, 1, 2_000_000) * np.sqrt(a * c)
+    b[::7] = 0.0
+    c[::11] = a[::11]
+    y, x = 2.0 * b, a - c
+    assert _bits_equal(host_atan2(y, x), np.arctan2(y, x))
+    sp = np.array([0.0, -0.0, 1.0, -1.0, np.inf, -np.inf, np.nan, 1e-310, -1e-310, 1e300,
+                   -1e300, 5e-324, 1.7e308, -1.7e308, 2.0 ** -1021, 2.0 ** 993, 3e-308])
+    Y, X = (v.ravel().copy() for v in np.meshgrid(sp, sp))
+    assert _bits_equal(host_atan2(Y, X), np.arctan2(Y, X))
+
+
+@pytest.mark.skipif(orc.numpy_exp_flavour() != "svml", reason="numpy has no SVML on this host")
+def test_tanh_matches_numpy():
+    rng = np.random.default_rng(13)
+    z = rng.standard_normal(N_EXACT) * 10.0 ** rng.uniform(-8, 2.5, N_EXACT)
+    assert _bits_equal(host_tanh(z), np.tanh(z))
+    sp = np.array([0.0, -0.0, np.inf, -np.inf, np.nan, 1e-310, 5e-324, 1e308, -1e308, 19.0,
+                   19.1, 20.0, 0.125, 0.140625, 0.1249999, 1.7e308])
+    assert _bits_equal(host_tanh(sp), np.tanh(sp))
+
+
+@pytest.mark.parametrize("lo,hi,logspan", [(-np.pi / 2, np.pi / 2, 0), (-2.4262, 2.4262, 0),
+                                           (-1.0, 1.0, 12)])
+def test_sincos_match_numpy(lo, hi, logspan):
+    # phi = 0.5 * arctan2(...) lies in [-pi/2, pi/2]; small angles exercise the
+    # 2^-26 / 2^-27 shortcuts and the Taylor branch
+    rng = np.random.default_rng(17 + logspan)
+    p = rng.uniform(lo, hi, N_EXACT)
+    if logspan:
+        p *= 10.0 ** rng.uniform(-logspan, 0, N_EXACT)
+    s, c = host_sincos(p)
+    assert _bits_equal(s, np.sin(p))
+    assert _bits_equal(c, np.cos(p))

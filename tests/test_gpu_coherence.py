@@ -3,9 +3,10 @@ engine.py:243-249 -> guide.coherence_directions, guide.py:330-355).
 
 Checked against the reference's own outputs (tests/golden/coherence_golden.npz,
 made by tests/golden/make_coherence_golden.py) and the oracle run live:
-fill order / frontier sets bit-exact, report rows identical, values within
-1e-4; directions within 1e-12 (the reference's own cropping test tolerance,
-test_guide.py:286-300 -- CUDA's atan2/sin/cos/tanh vs numpy's SVML).
+fill order / frontier sets bit-exact on every case (smart-order deadlock
+near-ties included), report rows identical, values within 1e-4; directions
+bit-exact (numpy's arctan2 / tanh / sin / cos restated in gf_npmath.cuh; the
+reference's own cropping test allows 1e-12, test_guide.py:286-300).
 """
 
 import os
@@ -21,7 +22,6 @@ pytestmark = pytest.mark.gpu
 
 GOLD = os.path.join(os.path.dirname(__file__), "golden", "coherence_golden.npz")
 CT_CASES = cases.coherence_scenes()
-TOL = 1e-4
 
 
 @pytest.fixture(scope="module")
@@ -42,7 +42,7 @@ def test_directions_match_reference(gold):
     for s, r in ((2.0, 4.0), (1.0, 2.0)):
         g = coherence_directions_device(u, d_lab, idx, sigma=s, rho=r).cpu().numpy()
         ref = gold[f"dirs_s{s:g}_r{r:g}"]
-        assert np.allclose(g, ref, rtol=0, atol=1e-12), float(np.abs(g - ref).max())
+        assert np.array_equal(g.view(np.int64), ref.view(np.int64)), float(np.abs(g - ref).max())
     # a query with no readable mass in its rho window gets g = 0 (test_guide.py:303-310)
     lab2 = np.zeros((64, 64), dtype=np.uint8)
     lab2[10:54, 10:54] = 255
@@ -52,11 +52,12 @@ def test_directions_match_reference(gold):
     assert g.cpu().numpy().tolist() == [[0.0, 0.0]]
 
 
-# Measured (tools/diag_coherence.py, profiles/round1_coherence.md): these three
-# smart-order noise scenes reach deadlock shells whose two largest confidences
-# (~1e-61) differ by 1-2 ulp; g differs from numpy's by <= 3.3e-16 (CUDA
-# atan2/sin/cos/tanh vs numpy's SVML), which flips the argmax there.
-NEAR_TIE = {"ct_rand8", "ct_rand9", "ct_data_term"}
+# Round 1 xfailed ct_rand8, ct_rand9 and ct_data_term: their smart-order
+# deadlock shells have top-two confidences (~1e-61) 1-2 ulp apart, and CUDA's
+# atan2/sin/cos/tanh moved g by <= 3.3e-16, flipping the argmax
+# (profiles/round1_coherence.md).  With numpy's own transcendentals restated
+# (gf_npmath.cuh) they are expected bit-exact like the rest.
+NEAR_TIE = set()
 
 
 def _run_case(idx):
@@ -90,11 +91,7 @@ def test_coherence_order_prefix(gold, idx):
         f"divergence at shell {k0} is not a one-pixel (argmax) shell"
 
 
-@pytest.mark.parametrize("idx", [
-    pytest.param(i, marks=pytest.mark.xfail(
-        c["name"] in NEAR_TIE, strict=True,
-        reason="deadlock argmax near-tie flipped by ulp-level g (transcendentals not SVML-exact)"))
-    for i, c in enumerate(CT_CASES)])
+@pytest.mark.parametrize("idx", range(len(CT_CASES)))
 def test_coherence_fill(gold, idx):
     key = f"c{idx:03d}"
     case, p, (u, rep, maps) = _run_case(idx)
@@ -105,10 +102,12 @@ def test_coherence_fill(gold, idx):
     stats = [rep.iterations, rep.filled, rep.deadlock_fills, int(rep.unfillable),
              rep.unfillable_count]
     assert stats == gold[f"{key}_stats"].tolist()
+    # the coherence path samples the f64 image with numpy's einsum order
+    # (eval_item EXACTV): the filled values are the reference's bits
     err = float(np.abs(u - gold[f"{key}_u"]).max())
-    assert err <= TOL, err
+    assert np.array_equal(u.view(np.int64), gold[f"{key}_u"].view(np.int64)), err
     ref = orc.fill(case["image"], case["labels"], None, orc.Params.of(p), tracked=case["tracked"])
-    assert float(np.abs(u - ref["u"]).max()) <= TOL
+    assert np.array_equal(u.view(np.int64), ref["u"].view(np.int64))
 
 
 def test_public_entry_points():
@@ -137,3 +136,46 @@ def test_tensor_inputs_and_no_mutation():
         assert [r[4] for r in rep_t.rows] == [r[4] for r in rep.rows]
         tol = 0.0 if t.dtype == torch.float64 else 1e-6
         assert float(np.abs(u_t.numpy() - u_np).max()) <= tol
+
+
+def _device_npmath(op, a, b=None):
+    import ctypes
+
+    import torch
+
+    from paper_1611_05319_b200 import _native
+
+    lib = _native.load()
+    da = torch.from_numpy(a).cuda()
+    db = torch.from_numpy(b).cuda() if b is not None else None
+    out = torch.empty_like(da)
+    P = ctypes.c_void_p
+    stream = torch.cuda.current_stream().cuda_stream
+    _native.check(lib.gf_npmath_eval(op, a.size, P(da.data_ptr()),
+                                     P(db.data_ptr()) if db is not None else None,
+                                     P(out.data_ptr()), P(stream)))
+    return out.cpu().numpy()
+
+
+def _same_bits(got, ref):
+    return bool(np.all((got.view(np.int64) == ref.view(np.int64)) |
+                       (np.isnan(got) & np.isnan(ref))))
+
+
+@pytest.mark.skipif(orc.numpy_exp_flavour() != "svml", reason="numpy has no SVML on this host")
+def test_device_transcendentals_match_numpy():
+    """gf_npmath.cuh as compiled for sm_100a: numpy's arctan2 / tanh / sin /
+    cos bit for bit on 10 M inputs each (the host build is pinned the same way
+    in tests/test_exactmath.py)."""
+    n = 10_000_000
+    rng = np.random.default_rng(23)
+    y = rng.standard_normal(n) * 10.0 ** rng.uniform(-10, 6, n)
+    x = rng.standard_normal(n) * 10.0 ** rng.uniform(-10, 6, n)
+    x[::13] = 0.0
+    y[::17] = 0.0
+    assert _same_bits(_device_npmath(0, y, x), np.arctan2(y, x))
+    z = rng.standard_normal(n) * 10.0 ** rng.uniform(-8, 2.5, n)
+    assert _same_bits(_device_npmath(1, z), np.tanh(z))
+    p = rng.uniform(-np.pi / 2, np.pi / 2, n) * 10.0 ** rng.uniform(-9, 0, n)
+    assert _same_bits(_device_npmath(2, p), np.sin(p))
+    assert _same_bits(_device_npmath(3, p), np.cos(p))
