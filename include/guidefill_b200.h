@@ -303,6 +303,27 @@ int gf_commit_shell(int32_t channels, int32_t n, const int64_t* frontier, const 
                     double c, double c2, int32_t shell, double* image, uint8_t* labels,
                     int32_t* fillshell, uint8_t* fill, int32_t* count, void* stream);
 
+/*
+ * The whole coherence-transport fill (engine._fill_loop, engine.py:286-376,
+ * with g_source = "modified_structure_tensor": guide.coherence_directions,
+ * guide.py:330-355) in one persistent kernel launch: image / labels (device,
+ * f64 [H][W][C] / uint8 [H][W]) are filled and relabelled in place;
+ * fillshell (preset -1) receives each pixel's shell, enter (optional, preset
+ * -1) the shell it joined the frontier, rows[rows_cap][5] the report rows
+ * (iteration, frontier size, candidates, threads, filled) and report[4] =
+ * (done: 0 finished / 2 unfillable / 3 rows_cap exceeded, iterations,
+ * deadlock fills, filled).  Unfillable painting and the hull clip are the
+ * caller's (as engine.py:370-376 after the loop).  params->tracked picks the
+ * frontier tracker; params->r / mu / neighborhood / periodic_x the ball.
+ */
+size_t gf_coherence_fill_workspace_bytes(int32_t height, int32_t width, int32_t channels,
+                                         int64_t n_inpaint);
+int gf_coherence_fill(int32_t height, int32_t width, int32_t channels, double* image,
+                      uint8_t* labels, const gf_fill_params* params, double sigma, double rho,
+                      double lam, int64_t n_inpaint, int32_t* fillshell, int32_t* enter,
+                      int64_t* rows, int32_t rows_cap, int32_t* report, void* workspace,
+                      size_t workspace_bytes, void* stream);
+
 /* Thread-local message for the last failing call on this thread. */
 const char* gf_last_error(void);
 int gf_abi_version(void);

@@ -35,6 +35,7 @@ EXPORTS = (
     "gf_trace_rays", "gf_last_error",
     "gf_abi_version", "gf_launch_count", "gf_host_exp", "gf_host_hypot", "gf_host_pairwise_sum",
     "gf_host_atan2", "gf_host_tanh", "gf_host_sincos", "gf_npmath_eval",
+    "gf_coherence_fill_workspace_bytes", "gf_coherence_fill",
 )
 
 
@@ -182,6 +183,13 @@ def load(required: bool = True):
     lib.gf_host_tanh.argtypes = [P, P, ctypes.c_int64]
     lib.gf_host_sincos.argtypes = [P, P, P, ctypes.c_int64]
     lib.gf_npmath_eval.argtypes = [ctypes.c_int32, ctypes.c_int64, P, P, P, P]
+    lib.gf_coherence_fill_workspace_bytes.restype = ctypes.c_size_t
+    lib.gf_coherence_fill_workspace_bytes.argtypes = [ctypes.c_int32, ctypes.c_int32,
+                                                      ctypes.c_int32, ctypes.c_int64]
+    lib.gf_coherence_fill.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, P, P, P,
+                                      ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                      ctypes.c_int64, P, P, P, ctypes.c_int32, P, P,
+                                      ctypes.c_size_t, P]
     lib.gf_host_pairwise_sum.argtypes = [P, ctypes.c_int32]
     _lib = lib
     return lib

@@ -23,6 +23,7 @@ engine._fill_loop (engine.py:286-376) step for step.
 
 from __future__ import annotations
 
+import ctypes
 import time
 
 import numpy as np
@@ -80,7 +81,66 @@ def _neighbor_mean(u, lab, p, H, W, periodic_x):
 
 
 def run_coherence_fill(u, lab0, params, tracked=True, order_log=False):
-    """engine._fill_loop (engine.py:286-376) with g from the masked structure tensor.
+    """engine._fill_loop (engine.py:286-376) with g from the masked structure tensor:
+    the whole loop in one persistent kernel (gf_coherence_fill).
+
+    ``u``: (H, W, C) float64 CUDA tensor (consumed: filled in place); ``lab0``:
+    (H, W) uint8 CUDA tensor (not modified).  Returns (u, report fields dict,
+    enter, fillshell) with the order maps as int32 CUDA tensors (enter None
+    unless order_log).  A sigma window wider than the fused tile supports
+    (sigma > 3.25) runs the shell-by-shell loop (``run_coherence_fill_shells``).
+    """
+    import torch
+
+    from ._device import params_to_c
+
+    H, W, C = u.shape
+    dev = u.device
+    lab = lab0.clone()
+    readable = lab == READABLE
+    hull = None
+    if bool(readable.any()):
+        seed = u[readable]
+        hull = (seed.min(), seed.max())
+    n_inp = int((lab == INPAINT).sum())
+    lib = N.load()
+    fillshell = torch.full((H * W,), -1, dtype=torch.int32, device=dev)
+    enter = torch.full((H * W,), -1, dtype=torch.int32, device=dev) if order_log else None
+    rows_cap = n_inp + 1
+    rows = torch.zeros((rows_cap, 5), dtype=torch.int64, device=dev)
+    report = torch.zeros(4, dtype=torch.int32, device=dev)
+    ws_bytes = lib.gf_coherence_fill_workspace_bytes(H, W, C, n_inp)
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+    pc = params_to_c(params, tracked, N.GF_G_FIELD)
+    t0 = time.perf_counter()
+    rc = lib.gf_coherence_fill(H, W, C, N.ptr(u), N.ptr(lab), ctypes.byref(pc),
+                               float(params.sigma), float(params.rho),
+                               float(params.coherence_lambda), n_inp, N.ptr(fillshell),
+                               N.ptr(enter), N.ptr(rows), rows_cap, N.ptr(report), N.ptr(ws),
+                               ws_bytes, N.stream_ptr())
+    if rc == N.GF_E_UNSUPPORTED:
+        return run_coherence_fill_shells(u, lab0, params, tracked, order_log)
+    N.check(rc)
+    done, iters, deadlocks, filled = (int(v) for v in report.cpu())
+    if done == 3:
+        raise N.NativeError("coherence fill: report rows capacity exceeded")
+    rep = dict(rows=[tuple(int(x) for x in r) for r in rows[:iters].cpu().tolist()],
+               iterations=iters, filled=filled, deadlock_fills=deadlocks,
+               unfillable=done == 2, unfillable_count=0)
+    if rep["unfillable"]:
+        from .engine import _paint_unfillable_device
+
+        rep["unfillable_count"] = _paint_unfillable_device(u, lab0, fillshell.reshape(H, W))
+    if hull is not None:
+        u.clamp_(hull[0], hull[1])
+    rep["wall_time_s"] = time.perf_counter() - t0
+    return u, rep, enter, fillshell
+
+
+def run_coherence_fill_shells(u, lab0, params, tracked=True, order_log=False):
+    """engine._fill_loop (engine.py:286-376) with g from the masked structure tensor,
+    one host-driven iteration per shell (the kernels of gf_coherence_directions,
+    gf_sample_points, gf_commit_shell and gf_frontier_candidates).
 
     ``u``: (H, W, C) float64 CUDA tensor (consumed: filled in place); ``lab0``:
     (H, W) uint8 CUDA tensor (not modified).  Returns (u, report fields dict,

@@ -223,6 +223,52 @@ int gf_boundary_masks(int32_t height, int32_t width, const uint8_t* labels, int3
                          static_cast<cudaStream_t>(stream));
 }
 
+size_t gf_coherence_fill_workspace_bytes(int32_t height, int32_t width, int32_t channels,
+                                         int64_t n_inpaint) {
+  if (height <= 0 || width <= 0 || channels < 1 || channels > 4 || n_inpaint < 0) return 0;
+  return coherence_fill_workspace(height, width, channels, n_inpaint);
+}
+
+int gf_coherence_fill(int32_t height, int32_t width, int32_t channels, double* image,
+                      uint8_t* labels, const gf_fill_params* params, double sigma, double rho,
+                      double lam, int64_t n_inpaint, int32_t* fillshell, int32_t* enter,
+                      int64_t* rows, int32_t rows_cap, int32_t* report, void* workspace,
+                      size_t workspace_bytes, void* stream) {
+  if (!params || !image || !labels || !fillshell || !rows || !report || !workspace)
+    return set_error(GF_E_INVALID, "NULL argument");
+  if (rows_cap < 1 || n_inpaint < 0) return set_error(GF_E_INVALID, "bad rows_cap / n_inpaint");
+  if (params->order < 0 || params->order > 2) return set_error(GF_E_INVALID, "bad order");
+  BallParams P;
+  BallTables* T = new BallTables;
+  int rc = build_ball(params, P, *T);
+  if (rc == GF_OK) {
+    CoherenceFillArgs a{};
+    a.height = height;
+    a.width = width;
+    a.channels = channels;
+    a.image = image;
+    a.labels = labels;
+    a.sigma = sigma;
+    a.rho = rho;
+    a.lam = lam;
+    a.order = params->order;
+    a.c = params->c;
+    a.c2 = params->c2;
+    a.tracked = params->tracked ? 1 : 0;
+    a.n_inpaint = n_inpaint;
+    a.fillshell = fillshell;
+    a.enter = enter;
+    a.rows = reinterpret_cast<long long*>(rows);
+    a.rows_cap = rows_cap;
+    a.report = report;
+    a.workspace = workspace;
+    a.workspace_bytes = workspace_bytes;
+    rc = coherence_fill_launch(a, P, *T, static_cast<cudaStream_t>(stream));
+  }
+  delete T;
+  return rc;
+}
+
 void gf_host_exp(const double* x, double* y, int64_t n) {
   for (int64_t i = 0; i < n; ++i) y[i] = exp_np(x[i]);
 }

@@ -31,9 +31,13 @@
 
 #include <algorithm>
 
+#include <cooperative_groups.h>
+
 #include "gf_internal.cuh"
 #include "gf_math.cuh"
 #include "gf_npmath.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace gf {
 
@@ -491,3 +495,637 @@ extern "C" int gf_npmath_eval(int32_t op, int64_t n, const double* a, const doub
   if (e != cudaSuccess) return set_error(GF_E_CUDA, cudaGetErrorString(e));
   return GF_OK;
 }
+
+// ---------------------------------------------------------------------------
+// The whole coherence-transport fill as ONE persistent cooperative kernel
+// (engine._fill_loop, engine.py:286-376, with g from guide.coherence_directions,
+// guide.py:330-355).  Per shell s, separated by grid-wide barriers:
+//   B  one warp per query: the rho stage at the query (scipy order) -> g,
+//      then 4 queries per warp through the ball sampler (eval_item, exact
+//      einsum-order values) -> rw, tw, vals of the frontier entry
+//   C  ready predicate (onion / conf > c / |g| > c2 & conf > c) -> fill flags
+//   D  (only when nothing is ready) the deadlock pick: first maximal
+//      confidence (NaN first, ties to the lowest pixel index = numpy's
+//      argmax over the sorted frontier), its average or the 8-neighbour mean
+//   E  commit: scatter the values, relabel, fillshell; every 32 x 8 tile
+//      within sigma_R + 1 of a filled pixel is queued as dirty
+//   A+F  the dirty tiles' tensor field is recomputed from u / labels (seed,
+//      both sigma passes and the gradient tensor fused in shared memory: the
+//      field elsewhere is unchanged, so the planes stay exact), and the
+//      frontier is updated (tracker._update_arrays: survivors and Inpaint
+//      8-neighbours of filled pixels, deduplicated by a per-pixel shell stamp,
+//      active filter; or the full active rescan when untracked)
+// The frontier is kept unsorted: only the deadlock argmax depends on its
+// order, and that is resolved by pixel index.  Per-shell counters live in
+// two parity banks so one bank can be reset while the other is in use.
+// ---------------------------------------------------------------------------
+namespace gf {
+namespace {
+
+constexpr int kLoopThreads = 256;
+constexpr int kLTW = 32, kLTH = 8;  // tensor tile: 32 columns x 8 rows
+constexpr int kLoopRsMax = 6;       // sigma window radius the fused tile supports
+
+enum CtCounter {
+  kCtNF = 0,      // [2] next-frontier appends
+  kCtFill = 2,    // [2] fills
+  kCtCand = 4,    // [2] tracker candidates
+  kCtAnyG = 6,    // [2] any |g| > 0 (data term)
+  kCtTiles = 8,   // [2] dirty tiles queued
+  kCtDone = 10,   // 2: unfillable, 3: rows capacity exceeded
+  kCtIters = 11,
+  kCtDeadlocks = 12,
+  kCtFilled = 13,
+  kCtCount = 16
+};
+
+struct CtLoopArgs {
+  int H, W, C, periodic, tracked, order;
+  double c, c2;
+  double lam;
+  int tiles_x, tiles_y;
+  int rows_cap;
+  long long remaining0;
+  double* u;
+  uint8_t* lab;
+  double* Q;              // [J11, J12, J22] * ind, ind
+  int* fr[2];             // frontier lists (pixel indices), shell s in fr[s & 1]
+  double* eg;             // per frontier entry: g (2), rw, tw, vals (C), fill flag
+  double* erw;
+  double* etw;
+  double* evals;
+  uint8_t* efill;
+  int* stamp;             // tracker dedup: last shell + 1 that claimed the pixel
+  unsigned* tflag;        // tile queued
+  int* tlist[2];          // dirty tile lists (parity banks)
+  int* fillshell;
+  int* enter;             // or nullptr
+  long long* rows;        // [rows_cap][5]
+  int* ctr;
+  double* slot_c;         // deadlock argmax partials, one per block
+  int* slot_k;
+  Taps ts, tr;
+};
+
+__device__ __forceinline__ int ld_cg(const int* p) { return *(const volatile int*)p; }
+
+// NEIGHBOR_OFFSETS (grid.py:29-33) as (di, dj) packed in 2-bit fields
+__device__ __forceinline__ int ct_nb_di(int o) { return (int)((0x9224u >> (2 * o)) & 3u) - 1; }
+__device__ __forceinline__ int ct_nb_dj(int o) { return (int)((0xA940u >> (2 * o)) & 3u) - 1; }
+
+// numpy argmax order on (conf, pixel): NaN first, then larger, ties to the
+// lower pixel index (the reference's frontier is sorted)
+__device__ __forceinline__ bool ct_better(double a, int pa, double b, int pb) {
+  const bool na = a != a, nb = b != b;
+  if (na != nb) return na;
+  if (!na && a != b) return a > b;
+  return pa < pb;
+}
+
+template <int C>
+__device__ void ct_loop_tile(const CtLoopArgs& A, int t, double* sm) {
+  const int R = A.ts.R;
+  const int H = A.H, W = A.W;
+  const int tx = t % A.tiles_x, ty = t / A.tiles_x;
+  const int i0 = tx * kLTW, j0 = ty * kLTH;
+  const int SR = kLTH + 2 + 2 * R, SC = kLTW + 2 + 2 * R, BR = kLTH + 2, VC = kLTW + 2;
+  double* seed = sm;                       // [C + 1][SR][SC]: ind, ind * u_c (0 outside)
+  double* Bv = seed + (C + 1) * SR * SC;   // [C + 1][BR][SC]: sigma axis-0 pass
+  double* V = Bv + (C + 1) * BR * SC;      // [C][BR][VC]: S_c / safe(S_ind)
+  for (int e = threadIdx.x; e < SR * SC; e += blockDim.x) {
+    const int r = e / SC, cc = e - r * SC;
+    const int j = j0 - 1 - R + r, i = i0 - 1 - R + cc;
+    double ind = 0.0, uc[C];
+#pragma unroll
+    for (int f = 0; f < C; ++f) uc[f] = 0.0;
+    if (j >= 0 && j < H && i >= 0 && i < W) {
+      const int64_t p = (int64_t)j * W + i;
+      ind = A.lab[p] == 0 ? 1.0 : 0.0;
+#pragma unroll
+      for (int f = 0; f < C; ++f) uc[f] = ind * A.u[p * C + f];
+    }
+    seed[e] = ind;
+#pragma unroll
+    for (int f = 0; f < C; ++f) seed[(f + 1) * SR * SC + e] = uc[f];
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < BR * SC; e += blockDim.x) {
+    const int r = e / SC, cc = e - r * SC;
+#pragma unroll
+    for (int f = 0; f <= C; ++f) {
+      const double* s = seed + f * SR * SC + (r + R) * SC + cc;
+      double acc = s[0] * A.ts.w[0];
+      for (int k = R; k >= 1; --k) acc += (s[-k * SC] + s[k * SC]) * A.ts.w[k];
+      Bv[f * BR * SC + e] = acc;
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < BR * VC; e += blockDim.x) {
+    const int r = e / VC, cc = e - r * VC;
+    const int i = i0 - 1 + cc;
+    double S[C + 1];
+#pragma unroll
+    for (int f = 0; f <= C; ++f) {
+      const double* b = Bv + f * BR * SC + r * SC + cc + R;
+      double acc = b[0] * A.ts.w[0];
+      for (int k = R; k >= 1; --k) {
+        const double a = i - k >= 0 ? b[-k] : 0.0;
+        const double bb = i + k < W ? b[k] : 0.0;
+        acc += (a + bb) * A.ts.w[k];
+      }
+      S[f] = acc;
+    }
+    const double safe = S[0] > 0.0 ? S[0] : 1.0;
+#pragma unroll
+    for (int f = 0; f < C; ++f) V[f * BR * VC + e] = S[f + 1] / safe;
+  }
+  __syncthreads();
+  const int64_t HW = (int64_t)H * W;
+  for (int e = threadIdx.x; e < kLTH * kLTW; e += blockDim.x) {
+    const int r = e / kLTW, cc = e - r * kLTW;
+    const int j = j0 + r, i = i0 + cc;
+    if (j >= H || i >= W) continue;
+    const int vr = r + 1, vc = cc + 1;
+    double J11 = 0.0, J12 = 0.0, J22 = 0.0;
+#pragma unroll
+    for (int f = 0; f < C; ++f) {
+      const double* v = V + f * BR * VC;
+      double gy, gx;
+      if (j == 0) gy = (v[(vr + 1) * VC + vc] - v[vr * VC + vc]) / 1.0;
+      else if (j == H - 1) gy = (v[vr * VC + vc] - v[(vr - 1) * VC + vc]) / 1.0;
+      else gy = (v[(vr + 1) * VC + vc] - v[(vr - 1) * VC + vc]) / 2.0;
+      if (i == 0) gx = (v[vr * VC + vc + 1] - v[vr * VC + vc]) / 1.0;
+      else if (i == W - 1) gx = (v[vr * VC + vc] - v[vr * VC + vc - 1]) / 1.0;
+      else gx = (v[vr * VC + vc + 1] - v[vr * VC + vc - 1]) / 2.0;
+      J11 += gx * gx;
+      J12 += gx * gy;
+      J22 += gy * gy;
+    }
+    const int64_t p = (int64_t)j * W + i;
+    const double ind = A.lab[p] == 0 ? 1.0 : 0.0;
+    A.Q[3 * HW + p] = ind;
+    A.Q[p] = J11 * ind;
+    A.Q[HW + p] = J12 * ind;
+    A.Q[2 * HW + p] = J22 * ind;
+  }
+  __syncthreads();
+}
+
+// queue every tile within d of pixel (j, i) (parity bank b)
+__device__ __forceinline__ void ct_queue_tiles(const CtLoopArgs& A, int b, int j, int i, int d) {
+  const int ty0 = max(0, j - d) / kLTH, ty1 = min(A.H - 1, j + d) / kLTH;
+  const int tx0 = max(0, i - d) / kLTW, tx1 = min(A.W - 1, i + d) / kLTW;
+  for (int ty = ty0; ty <= ty1; ++ty)
+    for (int tx = tx0; tx <= tx1; ++tx) {
+      const int t = ty * A.tiles_x + tx;
+      if (ld_cg(reinterpret_cast<const int*>(&A.tflag[t])) == 0 && atomicExch(&A.tflag[t], 1u) == 0u)
+        A.tlist[b][atomicAdd(&A.ctr[kCtTiles + b], 1)] = t;
+    }
+}
+
+template <int C>
+__device__ __forceinline__ void ct_run_tiles(const CtLoopArgs& A, int b, double* sm) {
+  const int n = ld_cg(&A.ctr[kCtTiles + b]);
+  for (int q = blockIdx.x; q < n; q += gridDim.x) {
+    const int t = A.tlist[b][q];
+    if (threadIdx.x == 0) A.tflag[t] = 0u;
+    ct_loop_tile<C>(A, t, sm);
+  }
+}
+
+// g at pixel p (guide.coherence_directions for one query), in every lane
+__device__ __forceinline__ void ct_loop_g(const CtLoopArgs& A, int p, double* cols, double& gx,
+                                          double& gy) {
+  const int lane = threadIdx.x & 31;
+  const int H = A.H, W = A.W;
+  const int64_t HW = (int64_t)H * W;
+  const int j = p / W, i = p - j * W;
+  const int R = A.tr.R, ncol = 2 * R + 1;
+  for (int e = lane; e < 4 * ncol; e += 32) {
+    const int plane = e / ncol, c = e - plane * ncol;
+    cols[plane * ncol + c] = ct_col(A.Q + plane * HW, H, W, j, i + c - R, A.tr);
+  }
+  __syncwarp();
+  double red = 0.0;
+  if (lane < 4) {
+    const double* T = cols + lane * ncol + R;
+    double acc = T[0] * A.tr.w[0];
+    for (int d = R; d >= 1; --d) acc += (T[-d] + T[d]) * A.tr.w[d];
+    red = acc;
+  }
+  const double J11 = __shfl_sync(0xffffffffu, red, 0), J12 = __shfl_sync(0xffffffffu, red, 1);
+  const double J22 = __shfl_sync(0xffffffffu, red, 2), mass = __shfl_sync(0xffffffffu, red, 3);
+  __syncwarp();
+  const double safe = mass > 0.0 ? mass : 1.0;
+  const double a = J11 / safe, b = J12 / safe, c = J22 / safe;
+  const double mean = (a + c) / 2.0;
+  const double h = (a - c) / 2.0;
+  const double disc = sqrt(h * h + b * b);
+  const double phi = 0.5 * atan2_np(2.0 * b, a - c);
+  const double lo = mean - disc, hi = mean + disc;
+  const double coh = tanh_np((hi - lo) / A.lam);
+  const double vx = -sin_np(phi), vy = cos_np(phi);
+  gx = coh * vx;
+  gy = coh * vy;
+  if (mass <= 0.0) gx = gy = 0.0;
+}
+
+__device__ __forceinline__ bool ct_loop_active(const CtLoopArgs& A, int p) {
+  const int j = p / A.W, i = p - j * A.W;
+  return ct_active(A.lab, A.H, A.W, A.periodic, j, i);
+}
+
+template <int C, int NL>
+__global__ void __launch_bounds__(kLoopThreads, 2)
+    k_ct_loop(const __grid_constant__ CtLoopArgs A, const __grid_constant__ BallParams P,
+              const __grid_constant__ BallTables tab) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  BallTables& T = *reinterpret_cast<BallTables*>(smraw);
+  double* sm = reinterpret_cast<double*>(smraw + ((sizeof(BallTables) + 15) & ~size_t(15)));
+  for (int k = threadIdx.x; k < P.K; k += blockDim.x) {
+    T.n[k] = tab.n[k];
+    T.m[k] = tab.m[k];
+    T.w0[k] = tab.w0[k];
+    T.ni[k] = tab.ni[k];
+    T.mi[k] = tab.mi[k];
+  }
+  __syncthreads();
+  cg::grid_group grid = cg::this_grid();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int wpb = blockDim.x >> 5;
+  const int gwarp = blockIdx.x * wpb + warp, nwarps = gridDim.x * wpb;
+  const int gtid = blockIdx.x * blockDim.x + threadIdx.x, nthreads = gridDim.x * blockDim.x;
+  const int H = A.H, W = A.W;
+  const int HW = H * W;
+  int* ctr = A.ctr;
+  const RawSource src{A.u, A.lab, H, W, C};
+  const int dq = A.tr.R;          // a query reads the field within rho_R
+  const int dd = A.ts.R + 1;      // a filled pixel changes the field within sigma_R + 1
+
+  // initial frontier (engine.py:298: active boundary, fr[0], counted in bank 1)
+  // and the field around every Inpaint pixel (all a query can ever read)
+  for (int p = gtid; p < HW; p += nthreads) {
+    if (A.lab[p] != 255) continue;
+    const int j = p / W, i = p - j * W;
+    ct_queue_tiles(A, 1, j, i, dq);
+    if (ct_active(A.lab, H, W, A.periodic, j, i)) {
+      A.fr[0][atomicAdd(&ctr[kCtNF + 1], 1)] = p;
+      if (A.enter) A.enter[p] = 0;
+    }
+  }
+  grid.sync();
+  ct_run_tiles<C>(A, 1, sm);
+  grid.sync();
+
+  long long rem = A.remaining0;
+  bool data_live = A.order == 2;
+  int s = 0;
+  for (;; ++s) {
+    const int F = ld_cg(&ctr[kCtNF + ((s + 1) & 1)]);
+    if (s > 0 && gtid == 0)  // candidates of shell s - 1 (complete after its last barrier)
+      A.rows[5 * (int64_t)(s - 1) + 2] =
+          A.tracked ? (long long)ld_cg(&ctr[kCtCand + ((s - 1) & 1)]) : (long long)HW;
+    if (rem <= 0) break;
+    if (F == 0) {
+      if (gtid == 0) ctr[kCtDone] = 2;
+      break;
+    }
+    if (s >= A.rows_cap) {
+      if (gtid == 0) ctr[kCtDone] = 3;
+      break;
+    }
+    const int* fr = A.fr[s & 1];
+    int* frn = A.fr[(s + 1) & 1];
+    const int b = s & 1;
+
+    // ---- B: g and the ball sample at every frontier pixel
+    {
+      double* cols = sm + warp * 4 * (2 * A.tr.R + 1);
+      for (int base = gwarp * 4; base < F; base += nwarps * 4) {
+        double mgx = 0.0, mgy = 0.0;
+        for (int q = 0; q < 4 && base + q < F; ++q) {
+          double gx, gy;
+          ct_loop_g(A, fr[base + q], cols, gx, gy);
+          if ((lane >> 3) == q) {
+            mgx = gx;
+            mgy = gy;
+          }
+        }
+        const int k = base + (lane >> 3);
+        const bool valid = k < F;
+        const int p = valid ? fr[k] : 0;
+        const int pj = p / W, pi = p - pj * W;
+        SampleResult r;
+        eval_item<NL, 0, true>(P, T, src, lane & 7, valid, (double)pi, (double)pj, true, mgx, mgy,
+                               r);
+        if (valid && (lane & 7) == 0) {
+          A.eg[2 * k] = mgx;
+          A.eg[2 * k + 1] = mgy;
+          A.erw[k] = r.rw;
+          A.etw[k] = r.tw;
+#pragma unroll
+          for (int c = 0; c < C; ++c) A.evals[(int64_t)k * C + c] = r.v[c];
+          if (mgx != 0.0 || mgy != 0.0) atomicOr(&ctr[kCtAnyG + b], 1);
+        }
+      }
+    }
+    grid.sync();
+    if (gtid == 0) {  // the other bank: every block has read F and the last row
+      const int o = (s + 1) & 1;
+      ctr[kCtNF + o] = 0;
+      ctr[kCtFill + o] = 0;
+      ctr[kCtCand + o] = 0;
+      ctr[kCtAnyG + o] = 0;
+      ctr[kCtTiles + o] = 0;
+    }
+
+    // ---- C: ready predicate (engine.py:317-330) and fill = ready & rw > 0
+    if (data_live && ld_cg(&ctr[kCtAnyG + b]) == 0) data_live = false;
+    {
+      const int mode = A.order == 0 ? 0 : (data_live ? 2 : 1);
+      for (int k0 = blockIdx.x * blockDim.x; k0 < F; k0 += nthreads) {
+        const int k = k0 + threadIdx.x;
+        bool f = false;
+        if (k < F) {
+          const double rw = A.erw[k];
+          const double conf = rw / A.etw[k];
+          bool ready = true;
+          if (mode == 1) ready = conf > A.c;
+          else if (mode == 2) ready = hypot_np(A.eg[2 * k], A.eg[2 * k + 1]) > A.c2 && conf > A.c;
+          f = ready && rw > 0.0;
+          A.efill[k] = f ? 1 : 0;
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, f);
+        if (lane == 0 && bal) atomicAdd(&ctr[kCtFill + b], __popc(bal));
+      }
+    }
+    grid.sync();
+    int n = ld_cg(&ctr[kCtFill + b]);
+
+    // ---- D: deadlock guard (engine.py:334-348)
+    if (n == 0) {
+      double bc = 0.0;
+      int bk = -1, bp = 0x7fffffff;
+      for (int k = gtid; k < F; k += nthreads) {
+        const double cf = A.erw[k] / A.etw[k];
+        const int p = fr[k];
+        if (bk < 0 || ct_better(cf, p, bc, bp)) {
+          bc = cf;
+          bk = k;
+          bp = p;
+        }
+      }
+      double* rc = sm;
+      int* rk = reinterpret_cast<int*>(sm + blockDim.x);
+      rc[threadIdx.x] = bc;
+      rk[threadIdx.x] = bk;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        double c0 = 0.0;
+        int k0 = -1;
+        for (int t = 0; t < (int)blockDim.x; ++t) {
+          const int kk = rk[t];
+          if (kk < 0) continue;
+          if (k0 < 0 || ct_better(rc[t], fr[kk], c0, fr[k0])) {
+            c0 = rc[t];
+            k0 = kk;
+          }
+        }
+        A.slot_c[blockIdx.x] = c0;
+        A.slot_k[blockIdx.x] = k0;
+      }
+      __syncthreads();
+      grid.sync();
+      if (gtid == 0) {
+        double c0 = 0.0;
+        int k0 = -1;
+        for (int t = 0; t < (int)gridDim.x; ++t) {
+          const int kk = A.slot_k[t];
+          if (kk < 0) continue;
+          if (k0 < 0 || ct_better(A.slot_c[t], fr[kk], c0, fr[k0])) {
+            c0 = A.slot_c[t];
+            k0 = kk;
+          }
+        }
+        bool ok = true;
+        if (!(A.erw[k0] > 0.0)) {
+          // engine._neighbor_mean (engine.py:252-267): readable 8-neighbours
+          const int p = fr[k0];
+          const int j = p / W, i = p - j * W;
+          double acc[C];
+#pragma unroll
+          for (int c = 0; c < C; ++c) acc[c] = 0.0;
+          int cnt = 0;
+          for (int o = 0; o < 8; ++o) {
+            int ii = i + ct_nb_di(o);
+            const int jj = j + ct_nb_dj(o);
+            if (A.periodic) ii = (ii % W + W) % W;
+            if (ii < 0 || ii >= W || jj < 0 || jj >= H) continue;
+            const int64_t q = (int64_t)jj * W + ii;
+            if (A.lab[q] != 0) continue;
+#pragma unroll
+            for (int c = 0; c < C; ++c) acc[c] += A.u[q * C + c];
+            ++cnt;
+          }
+          if (cnt == 0) {
+            ok = false;
+            ctr[kCtDone] = 2;
+          } else {
+#pragma unroll
+            for (int c = 0; c < C; ++c) A.evals[(int64_t)k0 * C + c] = acc[c] / cnt;
+          }
+        }
+        if (ok) {
+          A.efill[k0] = 1;
+          ctr[kCtDeadlocks] += 1;
+        }
+      }
+      grid.sync();
+      if (ld_cg(&ctr[kCtDone]) == 2) break;
+      n = 1;
+    }
+
+    // ---- E: commit (engine.py:350-356) and queue the dirty tiles
+    for (int k = gtid; k < F; k += nthreads) {
+      if (!A.efill[k]) continue;
+      const int p = fr[k];
+#pragma unroll
+      for (int c = 0; c < C; ++c) A.u[(int64_t)p * C + c] = A.evals[(int64_t)k * C + c];
+      A.lab[p] = 0;
+      A.fillshell[p] = s;
+      const int j = p / W, i = p - j * W;
+      ct_queue_tiles(A, b, j, i, dd);
+    }
+    grid.sync();
+    rem -= n;
+
+    // ---- A + F: the field on the dirty tiles; the next frontier
+    ct_run_tiles<C>(A, b, sm);
+    if (A.tracked) {
+      // tracker._update_arrays (tracker.py:59-79)
+      for (int k = gtid; k < F; k += nthreads) {
+        const int p = fr[k];
+        const int j = p / W, i = p - j * W;
+        if (!A.efill[k]) {
+          if (atomicMax(&A.stamp[p], s + 1) < s + 1) {
+            atomicAdd(&ctr[kCtCand + b], 1);
+            if (ct_active(A.lab, H, W, A.periodic, j, i)) frn[atomicAdd(&ctr[kCtNF + b], 1)] = p;
+          }
+          continue;
+        }
+        for (int o = 0; o < 8; ++o) {
+          int ii = i + ct_nb_di(o);
+          const int jj = j + ct_nb_dj(o);
+          if (A.periodic) ii = (ii % W + W) % W;
+          if (ii < 0 || ii >= W || jj < 0 || jj >= H) continue;
+          const int q = jj * W + ii;
+          if (A.lab[q] != 255) continue;
+          if (atomicMax(&A.stamp[q], s + 1) >= s + 1) continue;
+          atomicAdd(&ctr[kCtCand + b], 1);
+          if (ct_active(A.lab, H, W, A.periodic, jj, ii)) {
+            frn[atomicAdd(&ctr[kCtNF + b], 1)] = q;
+            if (A.enter && A.enter[q] < 0) A.enter[q] = s + 1;
+          }
+        }
+      }
+    } else {
+      for (int p = gtid; p < HW; p += nthreads) {
+        if (A.lab[p] != 255) continue;
+        const int j = p / W, i = p - j * W;
+        if (ct_active(A.lab, H, W, A.periodic, j, i)) {
+          frn[atomicAdd(&ctr[kCtNF + b], 1)] = p;
+          if (A.enter && A.enter[p] < 0) A.enter[p] = s + 1;
+        }
+      }
+    }
+    if (gtid == 0) {
+      long long* row = A.rows + 5 * (int64_t)s;
+      row[0] = s;
+      row[1] = F;
+      row[3] = A.tracked ? (long long)F : (long long)HW;
+      row[4] = n;
+    }
+    grid.sync();
+  }
+  if (gtid == 0) {
+    ctr[kCtIters] = s;
+    ctr[kCtFilled] = (int)(A.remaining0 - rem);
+  }
+}
+
+}  // namespace
+
+int coherence_fill_launch(const CoherenceFillArgs& a, const BallParams& P, const BallTables& tab,
+                          cudaStream_t stream) {
+  if (a.height < 2 || a.width < 2 || a.channels < 1 || a.channels > 4)
+    return set_error(GF_E_INVALID, "bad geometry");
+  if ((long long)a.height * a.width >= (1LL << 31)) return set_error(GF_E_UNSUPPORTED, "frame too large");
+  Taps ts, tr;
+  if (make_taps(a.sigma, ts) != GF_OK || make_taps(a.rho, tr) != GF_OK)
+    return set_error(GF_E_UNSUPPORTED, "sigma / rho window outside 1..64 taps");
+  if (ts.R > kLoopRsMax) return set_error(GF_E_UNSUPPORTED, "sigma window too wide for the fused tile");
+  const int H = a.height, W = a.width, C = a.channels;
+  const size_t HW = (size_t)H * W;
+  const int tiles_x = (W + kLTW - 1) / kLTW, tiles_y = (H + kLTH - 1) / kLTH;
+  const size_t ntiles = (size_t)tiles_x * tiles_y;
+  const size_t cap = a.n_inpaint > 0 ? (size_t)a.n_inpaint : 1;
+  if (a.workspace_bytes < coherence_fill_workspace(H, W, C, a.n_inpaint))
+    return set_error(GF_E_WORKSPACE, "workspace too small");
+  // carve the workspace (8-byte aligned pieces first)
+  char* w = static_cast<char*>(a.workspace);
+  auto take = [&](size_t bytes) {
+    char* p = w;
+    w += (bytes + 255) & ~size_t(255);
+    return p;
+  };
+  CtLoopArgs A{};
+  A.H = H;
+  A.W = W;
+  A.C = C;
+  A.periodic = P.periodic;
+  A.tracked = a.tracked;
+  A.order = a.order;
+  A.c = a.c;
+  A.c2 = a.c2;
+  A.lam = a.lam;
+  A.tiles_x = tiles_x;
+  A.tiles_y = tiles_y;
+  A.rows_cap = a.rows_cap;
+  A.remaining0 = a.n_inpaint;
+  A.u = a.image;
+  A.lab = a.labels;
+  A.Q = reinterpret_cast<double*>(take(4 * HW * sizeof(double)));
+  A.eg = reinterpret_cast<double*>(take(2 * cap * sizeof(double)));
+  A.erw = reinterpret_cast<double*>(take(cap * sizeof(double)));
+  A.etw = reinterpret_cast<double*>(take(cap * sizeof(double)));
+  A.evals = reinterpret_cast<double*>(take(cap * C * sizeof(double)));
+  A.slot_c = reinterpret_cast<double*>(take(4096 * sizeof(double)));
+  A.fr[0] = reinterpret_cast<int*>(take(cap * sizeof(int)));
+  A.fr[1] = reinterpret_cast<int*>(take(cap * sizeof(int)));
+  A.stamp = reinterpret_cast<int*>(take(HW * sizeof(int)));
+  A.tflag = reinterpret_cast<unsigned*>(take(ntiles * sizeof(unsigned)));
+  A.tlist[0] = reinterpret_cast<int*>(take(ntiles * sizeof(int)));
+  A.tlist[1] = reinterpret_cast<int*>(take(ntiles * sizeof(int)));
+  A.slot_k = reinterpret_cast<int*>(take(4096 * sizeof(int)));
+  A.ctr = reinterpret_cast<int*>(take(kCtCount * sizeof(int)));
+  A.efill = reinterpret_cast<uint8_t*>(take(cap));
+  A.fillshell = a.fillshell;
+  A.enter = a.enter;
+  A.rows = a.rows;
+  A.ts = ts;
+  A.tr = tr;
+  cudaStream_t s = stream;
+  // stamps / tile flags / counters start at zero; the field needs no init
+  cudaMemsetAsync(A.stamp, 0, HW * sizeof(int), s);
+  cudaMemsetAsync(A.tflag, 0, ntiles * sizeof(unsigned), s);
+  cudaMemsetAsync(A.ctr, 0, kCtCount * sizeof(int), s);
+  const void* fn = nullptr;
+  const bool wide = P.plan.n_leaves > 1;
+  switch (C) {
+    case 1: fn = wide ? (const void*)k_ct_loop<1, kMaxLeaves> : (const void*)k_ct_loop<1, 1>; break;
+    case 2: fn = wide ? (const void*)k_ct_loop<2, kMaxLeaves> : (const void*)k_ct_loop<2, 1>; break;
+    case 3: fn = wide ? (const void*)k_ct_loop<3, kMaxLeaves> : (const void*)k_ct_loop<3, 1>; break;
+    default: fn = wide ? (const void*)k_ct_loop<4, kMaxLeaves> : (const void*)k_ct_loop<4, 1>; break;
+  }
+  const int R = ts.R;
+  const size_t tile_dbl = (size_t)(C + 1) * (kLTH + 2 + 2 * R) * (kLTW + 2 + 2 * R) +
+                          (size_t)(C + 1) * (kLTH + 2) * (kLTW + 2 + 2 * R) +
+                          (size_t)C * (kLTH + 2) * (kLTW + 2);
+  const size_t query_dbl = (size_t)(kLoopThreads / 32) * 4 * (2 * tr.R + 1);
+  const size_t red_dbl = 2 * kLoopThreads;
+  const size_t smem = ((sizeof(BallTables) + 15) & ~size_t(15)) +
+                      std::max(tile_dbl, std::max(query_dbl, red_dbl)) * sizeof(double);
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return set_error(GF_E_CUDA, cudaGetErrorString(cudaGetLastError()));
+  int dev = 0, sms = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kLoopThreads, smem) != cudaSuccess ||
+      per_sm < 1)
+    return set_error(GF_E_CUDA, "coherence loop does not fit on an SM");
+  const int grid = std::min(sms * per_sm, 4096);
+  void* args[] = {(void*)&A, (void*)&P, (void*)&tab};
+  cudaError_t e = cudaLaunchCooperativeKernel(fn, grid, kLoopThreads, args, smem, s);
+  if (e != cudaSuccess) return set_error(GF_E_CUDA, cudaGetErrorString(e));
+  count_launches(1);
+  // report: [iterations, filled, deadlock_fills, done]
+  if (a.report) {
+    e = cudaMemcpyAsync(a.report, A.ctr + kCtDone, 4 * sizeof(int), cudaMemcpyDeviceToDevice, s);
+    if (e != cudaSuccess) return set_error(GF_E_CUDA, cudaGetErrorString(e));
+  }
+  e = cudaPeekAtLastError();
+  if (e != cudaSuccess) return set_error(GF_E_CUDA, cudaGetErrorString(e));
+  return GF_OK;
+}
+
+size_t coherence_fill_workspace(int H, int W, int C, long long n_inpaint) {
+  const size_t HW = (size_t)H * W;
+  const size_t ntiles = (size_t)((W + kLTW - 1) / kLTW) * ((H + kLTH - 1) / kLTH);
+  const size_t cap = n_inpaint > 0 ? (size_t)n_inpaint : 1;
+  auto r = [](size_t b) { return (b + 255) & ~size_t(255); };
+  return r(4 * HW * 8) + r(2 * cap * 8) + 2 * r(cap * 8) + r(cap * C * 8) + r(4096 * 8) +
+         2 * r(cap * 4) + r(HW * 4) + r(ntiles * 4) + 2 * r(ntiles * 4) + r(4096 * 4) +
+         r(kCtCount * 4) + r(cap);
+}
+
+}  // namespace gf

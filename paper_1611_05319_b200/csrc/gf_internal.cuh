@@ -99,6 +99,28 @@ int bilinear_launch(int H, int W, int C, const double* image, const uint8_t* lab
 int boundary_launch(int H, int W, const uint8_t* labels, int periodic, uint8_t* active,
                     uint8_t* inner, uint8_t* outer, cudaStream_t stream);
 
+// gf_coherence.cu: the whole coherence-transport fill in one persistent kernel
+struct CoherenceFillArgs {
+  int height, width, channels;
+  double* image;        // [H][W][C] f64, filled in place
+  uint8_t* labels;      // [H][W], relabelled in place
+  double sigma, rho, lam;
+  int order;            // GF_ORDER_*
+  double c, c2;
+  int tracked;
+  long long n_inpaint;  // Inpaint pixels at the start
+  int32_t* fillshell;   // [H][W], preset to -1
+  int32_t* enter;       // [H][W] preset to -1, or nullptr
+  long long* rows;      // [rows_cap][5]
+  int rows_cap;
+  int32_t* report;      // [4]: done (2 unfillable, 3 rows overflow), iterations, deadlocks, filled
+  void* workspace;
+  size_t workspace_bytes;
+};
+size_t coherence_fill_workspace(int H, int W, int C, long long n_inpaint);
+int coherence_fill_launch(const CoherenceFillArgs& a, const BallParams& P, const BallTables& tab,
+                          cudaStream_t stream);
+
 // gf_guide.cu
 int guide_launch(int H, int W, const uint8_t* labels, int n_seg, const double* seg,
                  const int32_t* seg_spline, int n_splines, const double* dirs, double eta,
