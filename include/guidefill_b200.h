@@ -311,16 +311,19 @@ int gf_commit_shell(int32_t channels, int32_t n, const int64_t* frontier, const 
  * fillshell (preset -1) receives each pixel's shell, enter (optional, preset
  * -1) the shell it joined the frontier, rows[rows_cap][5] the report rows
  * (iteration, frontier size, candidates, threads, filled) and report[4] =
- * (done: 0 finished / 2 unfillable / 3 rows_cap exceeded, iterations,
- * deadlock fills, filled).  Unfillable painting and the hull clip are the
- * caller's (as engine.py:370-376 after the loop).  params->tracked picks the
- * frontier tracker; params->r / mu / neighborhood / periodic_x the ball.
+ * (done: 0 finished / 2 unfillable / 3 capacity exceeded, iterations,
+ * deadlock fills, filled).  The image is clipped to the readable hull
+ * (engine.py:375-376) unless the fill ended unfillable: then the caller paints
+ * the stranded pixels and clips (engine.py:370-376).  capacity bounds the
+ * frontier (>= the Inpaint pixel count; H * W always works).
+ * params->tracked picks the frontier tracker; params->r / mu / neighborhood /
+ * periodic_x the ball.
  */
 size_t gf_coherence_fill_workspace_bytes(int32_t height, int32_t width, int32_t channels,
-                                         int64_t n_inpaint);
+                                         int64_t capacity);
 int gf_coherence_fill(int32_t height, int32_t width, int32_t channels, double* image,
                       uint8_t* labels, const gf_fill_params* params, double sigma, double rho,
-                      double lam, int64_t n_inpaint, int32_t* fillshell, int32_t* enter,
+                      double lam, int64_t capacity, int32_t* fillshell, int32_t* enter,
                       int64_t* rows, int32_t rows_cap, int32_t* report, void* workspace,
                       size_t workspace_bytes, void* stream);
 

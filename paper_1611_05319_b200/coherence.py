@@ -97,42 +97,48 @@ def run_coherence_fill(u, lab0, params, tracked=True, order_log=False):
     H, W, C = u.shape
     dev = u.device
     lab = lab0.clone()
-    readable = lab == READABLE
-    hull = None
-    if bool(readable.any()):
-        seed = u[readable]
-        hull = (seed.min(), seed.max())
-    n_inp = int((lab == INPAINT).sum())
     lib = N.load()
+    cap = H * W  # frontier capacity: >= the Inpaint count, no host count needed
     fillshell = torch.full((H * W,), -1, dtype=torch.int32, device=dev)
     enter = torch.full((H * W,), -1, dtype=torch.int32, device=dev) if order_log else None
-    rows_cap = n_inp + 1
-    rows = torch.zeros((rows_cap, 5), dtype=torch.int64, device=dev)
-    report = torch.zeros(4, dtype=torch.int32, device=dev)
-    ws_bytes = lib.gf_coherence_fill_workspace_bytes(H, W, C, n_inp)
+    rows = torch.empty((cap + 1, 5), dtype=torch.int64, device=dev)
+    report = torch.empty(4, dtype=torch.int32, device=dev)
+    ws_bytes = lib.gf_coherence_fill_workspace_bytes(H, W, C, cap)
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
     pc = params_to_c(params, tracked, N.GF_G_FIELD)
     t0 = time.perf_counter()
     rc = lib.gf_coherence_fill(H, W, C, N.ptr(u), N.ptr(lab), ctypes.byref(pc),
                                float(params.sigma), float(params.rho),
-                               float(params.coherence_lambda), n_inp, N.ptr(fillshell),
-                               N.ptr(enter), N.ptr(rows), rows_cap, N.ptr(report), N.ptr(ws),
+                               float(params.coherence_lambda), cap, N.ptr(fillshell),
+                               N.ptr(enter), N.ptr(rows), cap + 1, N.ptr(report), N.ptr(ws),
                                ws_bytes, N.stream_ptr())
     if rc == N.GF_E_UNSUPPORTED:
         return run_coherence_fill_shells(u, lab0, params, tracked, order_log)
     N.check(rc)
-    done, iters, deadlocks, filled = (int(v) for v in report.cpu())
+    # one synchronisation: the report and the first rows in a single pinned copy
+    head = min(cap + 1, 64)
+    host = torch.empty(4 + 10 * head, dtype=torch.int32, pin_memory=True)
+    host[:4].copy_(report, non_blocking=True)
+    host[4:].view(torch.int64).view(head, 5).copy_(rows[:head], non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    done, iters, deadlocks, filled = (int(v) for v in host[:4])
     if done == 3:
-        raise N.NativeError("coherence fill: report rows capacity exceeded")
-    rep = dict(rows=[tuple(int(x) for x in r) for r in rows[:iters].cpu().tolist()],
-               iterations=iters, filled=filled, deadlock_fills=deadlocks,
-               unfillable=done == 2, unfillable_count=0)
+        raise N.NativeError("coherence fill: frontier capacity exceeded")
+    r_h = host[4:].view(torch.int64).view(head, 5)[:iters] if iters <= head else rows[:iters].cpu()
+    rep = dict(rows=[tuple(int(x) for x in r) for r in r_h.tolist()], iterations=iters,
+               filled=filled, deadlock_fills=deadlocks, unfillable=done == 2, unfillable_count=0)
     if rep["unfillable"]:
+        # the kernel leaves painting and the hull clip to the caller here
         from .engine import _paint_unfillable_device
 
+        readable = lab0 == READABLE
+        hull = None
+        if bool(readable.any()):
+            seed = u[readable]
+            hull = (seed.min(), seed.max())
         rep["unfillable_count"] = _paint_unfillable_device(u, lab0, fillshell.reshape(H, W))
-    if hull is not None:
-        u.clamp_(hull[0], hull[1])
+        if hull is not None:
+            u.clamp_(hull[0], hull[1])
     rep["wall_time_s"] = time.perf_counter() - t0
     return u, rep, enter, fillshell
 

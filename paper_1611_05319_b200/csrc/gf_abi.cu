@@ -224,19 +224,19 @@ int gf_boundary_masks(int32_t height, int32_t width, const uint8_t* labels, int3
 }
 
 size_t gf_coherence_fill_workspace_bytes(int32_t height, int32_t width, int32_t channels,
-                                         int64_t n_inpaint) {
-  if (height <= 0 || width <= 0 || channels < 1 || channels > 4 || n_inpaint < 0) return 0;
-  return coherence_fill_workspace(height, width, channels, n_inpaint);
+                                         int64_t capacity) {
+  if (height <= 0 || width <= 0 || channels < 1 || channels > 4 || capacity < 0) return 0;
+  return coherence_fill_workspace(height, width, channels, capacity);
 }
 
 int gf_coherence_fill(int32_t height, int32_t width, int32_t channels, double* image,
                       uint8_t* labels, const gf_fill_params* params, double sigma, double rho,
-                      double lam, int64_t n_inpaint, int32_t* fillshell, int32_t* enter,
+                      double lam, int64_t capacity, int32_t* fillshell, int32_t* enter,
                       int64_t* rows, int32_t rows_cap, int32_t* report, void* workspace,
                       size_t workspace_bytes, void* stream) {
   if (!params || !image || !labels || !fillshell || !rows || !report || !workspace)
     return set_error(GF_E_INVALID, "NULL argument");
-  if (rows_cap < 1 || n_inpaint < 0) return set_error(GF_E_INVALID, "bad rows_cap / n_inpaint");
+  if (rows_cap < 1 || capacity < 0) return set_error(GF_E_INVALID, "bad rows_cap / capacity");
   if (params->order < 0 || params->order > 2) return set_error(GF_E_INVALID, "bad order");
   BallParams P;
   BallTables* T = new BallTables;
@@ -255,7 +255,7 @@ int gf_coherence_fill(int32_t height, int32_t width, int32_t channels, double* i
     a.c = params->c;
     a.c2 = params->c2;
     a.tracked = params->tracked ? 1 : 0;
-    a.n_inpaint = n_inpaint;
+    a.capacity = capacity;
     a.fillshell = fillshell;
     a.enter = enter;
     a.rows = reinterpret_cast<long long*>(rows);

@@ -29,7 +29,11 @@
 #include <math.h>
 #include <stdint.h>
 
+#include <stdio.h>
+#include <stdlib.h>
+
 #include <algorithm>
+#include <vector>
 
 #include <cooperative_groups.h>
 
@@ -523,20 +527,25 @@ namespace gf {
 namespace {
 
 constexpr int kLoopThreads = 256;
+#ifndef GF_CT_MIN_BLOCKS
+#define GF_CT_MIN_BLOCKS 2  // 2 x 256 threads per SM (3 spills and runs slower)
+#endif
 constexpr int kLTW = 32, kLTH = 8;  // tensor tile: 32 columns x 8 rows
 constexpr int kLoopRsMax = 6;       // sigma window radius the fused tile supports
+static_assert(kLTW * kLTH == kLoopThreads, "one J output per thread");
 
 enum CtCounter {
   kCtNF = 0,      // [2] next-frontier appends
   kCtFill = 2,    // [2] fills
   kCtCand = 4,    // [2] tracker candidates
   kCtAnyG = 6,    // [2] any |g| > 0 (data term)
-  kCtTiles = 8,   // [2] dirty tiles queued
+  kCtTiles = 8,   // [2] dirty tiles processed (trace only)
   kCtDone = 10,   // 2: unfillable, 3: rows capacity exceeded
   kCtIters = 11,
   kCtDeadlocks = 12,
   kCtFilled = 13,
-  kCtCount = 16
+  kCtInpaint = 14,  // Inpaint pixels at the start
+  kCtCount = 16     // then two u64 hull keys (min, max) at ctr + kCtCount
 };
 
 struct CtLoopArgs {
@@ -545,7 +554,7 @@ struct CtLoopArgs {
   double lam;
   int tiles_x, tiles_y;
   int rows_cap;
-  long long remaining0;
+  long long capacity;      // frontier entry capacity (>= Inpaint pixels)
   double* u;
   uint8_t* lab;
   double* Q;              // [J11, J12, J22] * ind, ind
@@ -556,18 +565,70 @@ struct CtLoopArgs {
   double* evals;
   uint8_t* efill;
   int* stamp;             // tracker dedup: last shell + 1 that claimed the pixel
-  unsigned* tflag;        // tile queued
-  int* tlist[2];          // dirty tile lists (parity banks)
+  uint8_t* tflag;         // tile's field is stale (plain stores, cleared when recomputed)
   int* fillshell;
   int* enter;             // or nullptr
   long long* rows;        // [rows_cap][5]
   int* ctr;
   double* slot_c;         // deadlock argmax partials, one per block
   int* slot_k;
+  unsigned long long* trace;  // GF_CT_TRACE: %globaltimer at the phase barriers, or nullptr
   Taps ts, tr;
 };
 
+__device__ __forceinline__ unsigned long long ct_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// phase stamp (block 0, thread 0): slot 0 = init done, then 12 per shell
+// (0..5 barriers, 6 tiles, 7 F, 8 / 9 block 0's own B / E work done,
+// 10 / 11 the last block's B / E work done)
+__device__ __forceinline__ void ct_trace_work(const CtLoopArgs& A, int s, int own, int last) {
+  if (!A.trace || s >= 4096) return;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned long long t = ct_now();
+    if (blockIdx.x == 0) A.trace[1 + 16 * s + own] = t;
+    atomicMax(&A.trace[1 + 16 * s + last], t);
+  }
+}
+__device__ __forceinline__ void ct_trace(const CtLoopArgs& A, int s, int ph) {
+  if (A.trace && blockIdx.x == 0 && threadIdx.x == 0 && s < 4096) A.trace[1 + 16 * s + ph] = ct_now();
+}
+
 __device__ __forceinline__ int ld_cg(const int* p) { return *(const volatile int*)p; }
+
+// order-preserving u64 key of a double (atomicMin / atomicMax of the hull)
+__device__ __forceinline__ unsigned long long ct_key(double x) {
+  const unsigned long long u = (unsigned long long)__double_as_longlong(x);
+  return (u >> 63) ? ~u : (u | 0x8000000000000000ULL);
+}
+__device__ __forceinline__ double ct_unkey(unsigned long long k) {
+  return __longlong_as_double((long long)((k >> 63) ? (k & 0x7fffffffffffffffULL) : ~k));
+}
+
+// warp-aggregated append: every lane of the warp calls it (full mask); lanes
+// with pred get consecutive slots of list from one atomicAdd on *count
+__device__ __forceinline__ void warp_append(bool pred, int value, int* count, int* list) {
+  const int lane = threadIdx.x & 31;
+  const unsigned m = __ballot_sync(0xffffffffu, pred);
+  int base = 0;
+  if (lane == 0 && m) base = atomicAdd(count, __popc(m));
+  base = __shfl_sync(0xffffffffu, base, 0);
+  if (pred) list[base + __popc(m & ((1u << lane) - 1u))] = value;
+}
+
+// a grid-wide counter read once per block and broadcast through shared
+// memory (75k threads polling one L2 line serialise for microseconds);
+// block-uniform call sites only
+__device__ __forceinline__ int block_ld(const int* p) {
+  __shared__ int v;
+  __syncthreads();
+  if (threadIdx.x == 0) v = ld_cg(p);
+  __syncthreads();
+  return v;
+}
 
 // NEIGHBOR_OFFSETS (grid.py:29-33) as (di, dj) packed in 2-bit fields
 __device__ __forceinline__ int ct_nb_di(int o) { return (int)((0x9224u >> (2 * o)) & 3u) - 1; }
@@ -582,17 +643,28 @@ __device__ __forceinline__ bool ct_better(double a, int pa, double b, int pb) {
   return pa < pb;
 }
 
-template <int C>
-__device__ void ct_loop_tile(const CtLoopArgs& A, int t, double* sm) {
-  const int R = A.ts.R;
+// The tensor field of one 32 x 8 tile from u / labels (the sigma radius R a
+// compile-time constant so every tap is unrolled): seed (ind, ind * u_c, 0
+// outside the frame), scipy's axis-0 then axis-1 pass, v = S_c / safe(S_ind),
+// np.gradient and J * ind -- written as one 32-byte record per pixel
+// Q[p] = (J11 ind, J12 ind, J22 ind, ind).
+template <int C, int R>
+__device__ void ct_loop_tile_r(const CtLoopArgs& A, int t, double* sm) {
   const int H = A.H, W = A.W;
   const int tx = t % A.tiles_x, ty = t / A.tiles_x;
   const int i0 = tx * kLTW, j0 = ty * kLTH;
-  const int SR = kLTH + 2 + 2 * R, SC = kLTW + 2 + 2 * R, BR = kLTH + 2, VC = kLTW + 2;
-  double* seed = sm;                       // [C + 1][SR][SC]: ind, ind * u_c (0 outside)
+  constexpr int SR = kLTH + 2 + 2 * R, SC = kLTW + 2 + 2 * R, BR = kLTH + 2, VC = kLTW + 2;
+  double* seed = sm;                       // [C + 1][SR][SC]
   double* Bv = seed + (C + 1) * SR * SC;   // [C + 1][BR][SC]: sigma axis-0 pass
   double* V = Bv + (C + 1) * BR * SC;      // [C][BR][VC]: S_c / safe(S_ind)
-  for (int e = threadIdx.x; e < SR * SC; e += blockDim.x) {
+  double w[R + 1];
+#pragma unroll
+  for (int k = 0; k <= R; ++k) w[k] = A.ts.w[k];
+  constexpr int kSeedIt = (SR * SC + kLoopThreads - 1) / kLoopThreads;
+#pragma unroll
+  for (int it = 0; it < kSeedIt; ++it) {
+    const int e = threadIdx.x + it * kLoopThreads;
+    if (e >= SR * SC) break;
     const int r = e / SC, cc = e - r * SC;
     const int j = j0 - 1 - R + r, i = i0 - 1 - R + cc;
     double ind = 0.0, uc[C];
@@ -600,9 +672,12 @@ __device__ void ct_loop_tile(const CtLoopArgs& A, int t, double* sm) {
     for (int f = 0; f < C; ++f) uc[f] = 0.0;
     if (j >= 0 && j < H && i >= 0 && i < W) {
       const int64_t p = (int64_t)j * W + i;
+      double uv[C];
+#pragma unroll
+      for (int f = 0; f < C; ++f) uv[f] = A.u[p * C + f];
       ind = A.lab[p] == 0 ? 1.0 : 0.0;
 #pragma unroll
-      for (int f = 0; f < C; ++f) uc[f] = ind * A.u[p * C + f];
+      for (int f = 0; f < C; ++f) uc[f] = ind * uv[f];
     }
     seed[e] = ind;
 #pragma unroll
@@ -613,9 +688,10 @@ __device__ void ct_loop_tile(const CtLoopArgs& A, int t, double* sm) {
     const int r = e / SC, cc = e - r * SC;
 #pragma unroll
     for (int f = 0; f <= C; ++f) {
-      const double* s = seed + f * SR * SC + (r + R) * SC + cc;
-      double acc = s[0] * A.ts.w[0];
-      for (int k = R; k >= 1; --k) acc += (s[-k * SC] + s[k * SC]) * A.ts.w[k];
+      const double* sp = seed + f * SR * SC + (r + R) * SC + cc;
+      double acc = sp[0] * w[0];
+#pragma unroll
+      for (int k = R; k >= 1; --k) acc += (sp[-k * SC] + sp[k * SC]) * w[k];
       Bv[f * BR * SC + e] = acc;
     }
   }
@@ -627,11 +703,12 @@ __device__ void ct_loop_tile(const CtLoopArgs& A, int t, double* sm) {
 #pragma unroll
     for (int f = 0; f <= C; ++f) {
       const double* b = Bv + f * BR * SC + r * SC + cc + R;
-      double acc = b[0] * A.ts.w[0];
+      double acc = b[0] * w[0];
+#pragma unroll
       for (int k = R; k >= 1; --k) {
         const double a = i - k >= 0 ? b[-k] : 0.0;
         const double bb = i + k < W ? b[k] : 0.0;
-        acc += (a + bb) * A.ts.w[k];
+        acc += (a + bb) * w[k];
       }
       S[f] = acc;
     }
@@ -640,81 +717,148 @@ __device__ void ct_loop_tile(const CtLoopArgs& A, int t, double* sm) {
     for (int f = 0; f < C; ++f) V[f * BR * VC + e] = S[f + 1] / safe;
   }
   __syncthreads();
-  const int64_t HW = (int64_t)H * W;
-  for (int e = threadIdx.x; e < kLTH * kLTW; e += blockDim.x) {
+  {
+    const int e = threadIdx.x;  // kLTH * kLTW == kLoopThreads
     const int r = e / kLTW, cc = e - r * kLTW;
     const int j = j0 + r, i = i0 + cc;
-    if (j >= H || i >= W) continue;
-    const int vr = r + 1, vc = cc + 1;
-    double J11 = 0.0, J12 = 0.0, J22 = 0.0;
+    if (j < H && i < W) {
+      const int vr = r + 1, vc = cc + 1;
+      double J11 = 0.0, J12 = 0.0, J22 = 0.0;
 #pragma unroll
-    for (int f = 0; f < C; ++f) {
-      const double* v = V + f * BR * VC;
-      double gy, gx;
-      if (j == 0) gy = (v[(vr + 1) * VC + vc] - v[vr * VC + vc]) / 1.0;
-      else if (j == H - 1) gy = (v[vr * VC + vc] - v[(vr - 1) * VC + vc]) / 1.0;
-      else gy = (v[(vr + 1) * VC + vc] - v[(vr - 1) * VC + vc]) / 2.0;
-      if (i == 0) gx = (v[vr * VC + vc + 1] - v[vr * VC + vc]) / 1.0;
-      else if (i == W - 1) gx = (v[vr * VC + vc] - v[vr * VC + vc - 1]) / 1.0;
-      else gx = (v[vr * VC + vc + 1] - v[vr * VC + vc - 1]) / 2.0;
-      J11 += gx * gx;
-      J12 += gx * gy;
-      J22 += gy * gy;
+      for (int f = 0; f < C; ++f) {
+        const double* v = V + f * BR * VC;
+        double gy, gx;
+        if (j == 0) gy = (v[(vr + 1) * VC + vc] - v[vr * VC + vc]) / 1.0;
+        else if (j == H - 1) gy = (v[vr * VC + vc] - v[(vr - 1) * VC + vc]) / 1.0;
+        else gy = (v[(vr + 1) * VC + vc] - v[(vr - 1) * VC + vc]) / 2.0;
+        if (i == 0) gx = (v[vr * VC + vc + 1] - v[vr * VC + vc]) / 1.0;
+        else if (i == W - 1) gx = (v[vr * VC + vc] - v[vr * VC + vc - 1]) / 1.0;
+        else gx = (v[vr * VC + vc + 1] - v[vr * VC + vc - 1]) / 2.0;
+        J11 += gx * gx;
+        J12 += gx * gy;
+        J22 += gy * gy;
+      }
+      const int64_t p = (int64_t)j * W + i;
+      const double ind = A.lab[p] == 0 ? 1.0 : 0.0;
+      double2* q = reinterpret_cast<double2*>(A.Q + 4 * p);
+      q[0] = make_double2(J11 * ind, J12 * ind);
+      q[1] = make_double2(J22 * ind, ind);
     }
-    const int64_t p = (int64_t)j * W + i;
-    const double ind = A.lab[p] == 0 ? 1.0 : 0.0;
-    A.Q[3 * HW + p] = ind;
-    A.Q[p] = J11 * ind;
-    A.Q[HW + p] = J12 * ind;
-    A.Q[2 * HW + p] = J22 * ind;
   }
   __syncthreads();
 }
 
-// queue every tile within d of pixel (j, i) (parity bank b)
-__device__ __forceinline__ void ct_queue_tiles(const CtLoopArgs& A, int b, int j, int i, int d) {
+template <int C>
+__device__ __forceinline__ void ct_loop_tile(const CtLoopArgs& A, int t, double* sm) {
+  switch (A.ts.R) {
+    case 1: ct_loop_tile_r<C, 1>(A, t, sm); break;
+    case 2: ct_loop_tile_r<C, 2>(A, t, sm); break;
+    case 3: ct_loop_tile_r<C, 3>(A, t, sm); break;
+    case 4: ct_loop_tile_r<C, 4>(A, t, sm); break;
+    case 5: ct_loop_tile_r<C, 5>(A, t, sm); break;
+    default: ct_loop_tile_r<C, kLoopRsMax>(A, t, sm); break;
+  }
+}
+
+// flag every tile within d of pixel (j, i) as stale (idempotent plain stores)
+__device__ __forceinline__ void ct_mark_tiles(const CtLoopArgs& A, int j, int i, int d) {
   const int ty0 = max(0, j - d) / kLTH, ty1 = min(A.H - 1, j + d) / kLTH;
   const int tx0 = max(0, i - d) / kLTW, tx1 = min(A.W - 1, i + d) / kLTW;
   for (int ty = ty0; ty <= ty1; ++ty)
-    for (int tx = tx0; tx <= tx1; ++tx) {
-      const int t = ty * A.tiles_x + tx;
-      if (ld_cg(reinterpret_cast<const int*>(&A.tflag[t])) == 0 && atomicExch(&A.tflag[t], 1u) == 0u)
-        A.tlist[b][atomicAdd(&A.ctr[kCtTiles + b], 1)] = t;
-    }
+    for (int tx = tx0; tx <= tx1; ++tx) A.tflag[ty * A.tiles_x + tx] = 1;
 }
 
+// recompute the stale tiles: block b owns tiles b, b + grid, b + 2 grid, ...;
+// it gathers its stale ones into a shared list, then runs them one by one
 template <int C>
-__device__ __forceinline__ void ct_run_tiles(const CtLoopArgs& A, int b, double* sm) {
-  const int n = ld_cg(&A.ctr[kCtTiles + b]);
-  for (int q = blockIdx.x; q < n; q += gridDim.x) {
-    const int t = A.tlist[b][q];
-    if (threadIdx.x == 0) A.tflag[t] = 0u;
-    ct_loop_tile<C>(A, t, sm);
+__device__ __forceinline__ void ct_run_tiles(const CtLoopArgs& A, int bank, double* sm) {
+  __shared__ int list[kLoopThreads];
+  __shared__ int nlist;
+  const int ntiles = A.tiles_x * A.tiles_y;
+  for (int t0 = blockIdx.x; t0 < ntiles; t0 += gridDim.x * (int)blockDim.x) {
+    __syncthreads();
+    if (threadIdx.x == 0) nlist = 0;
+    __syncthreads();
+    const int t = t0 + threadIdx.x * gridDim.x;
+    if (t < ntiles && A.tflag[t]) {
+      A.tflag[t] = 0;
+      list[atomicAdd(&nlist, 1)] = t;
+    }
+    __syncthreads();
+    const int n = nlist;
+    if (threadIdx.x == 0 && n && A.trace) atomicAdd(&A.ctr[kCtTiles + bank], n);
+    for (int q = 0; q < n; ++q) ct_loop_tile<C>(A, list[q], sm);
   }
 }
 
-// g at pixel p (guide.coherence_directions for one query), in every lane
-__device__ __forceinline__ void ct_loop_g(const CtLoopArgs& A, int p, double* cols, double& gx,
-                                          double& gy) {
+// rho stage axis-0 sums at column i, row j, for two planes of the AoS field
+// (pl = 0: J11, J12; pl = 1: J22, ind), every tap load issued up front
+constexpr int kColUnroll = 8;
+__device__ __forceinline__ double2 ct_col2(const double* Q, int H, int W, int j, int i, int pl,
+                                           const Taps& t) {
+  if (i < 0 || i >= W) return make_double2(0.0, 0.0);
+  const int R = t.R;
+  const double2* x = reinterpret_cast<const double2*>(Q + 4 * ((int64_t)j * W + i)) + pl;
+  const int64_t st = 2 * (int64_t)W;  // one row in double2
+  if (R > kColUnroll) {
+    double2 acc = x[0];
+    acc.x *= t.w[0];
+    acc.y *= t.w[0];
+    for (int k = R; k >= 1; --k) {
+      const double2 a = j - k >= 0 ? x[-k * st] : make_double2(0.0, 0.0);
+      const double2 b = j + k < H ? x[k * st] : make_double2(0.0, 0.0);
+      acc.x += (a.x + b.x) * t.w[k];
+      acc.y += (a.y + b.y) * t.w[k];
+    }
+    return acc;
+  }
+  double2 a[kColUnroll + 1], b[kColUnroll + 1];
+#pragma unroll
+  for (int k = 1; k <= kColUnroll; ++k) {
+    a[k] = (k <= R && j - k >= 0) ? x[-k * st] : make_double2(0.0, 0.0);
+    b[k] = (k <= R && j + k < H) ? x[k * st] : make_double2(0.0, 0.0);
+  }
+  const double2 c0 = x[0];
+  double2 acc = make_double2(c0.x * t.w[0], c0.y * t.w[0]);
+#pragma unroll
+  for (int k = kColUnroll; k >= 1; --k)
+    if (k <= R) {
+      acc.x += (a[k].x + b[k].x) * t.w[k];
+      acc.y += (a[k].y + b[k].y) * t.w[k];
+    }
+  return acc;
+}
+
+// g for up to 4 queries at once (guide.coherence_directions): the 4 x 4
+// planes x (2R+1) column sums are spread over the warp, 16 lanes run the
+// ordered row sums, and lane group q (lanes 8q .. 8q+7) gets query q's g
+__device__ __forceinline__ void ct_loop_g4(const CtLoopArgs& A, const int* pix, int nq,
+                                           double* cols, double& gx, double& gy) {
   const int lane = threadIdx.x & 31;
   const int H = A.H, W = A.W;
-  const int64_t HW = (int64_t)H * W;
-  const int j = p / W, i = p - j * W;
   const int R = A.tr.R, ncol = 2 * R + 1;
-  for (int e = lane; e < 4 * ncol; e += 32) {
-    const int plane = e / ncol, c = e - plane * ncol;
-    cols[plane * ncol + c] = ct_col(A.Q + plane * HW, H, W, j, i + c - R, A.tr);
+  const int total = nq * 2 * ncol;  // (query, plane pair, column)
+  for (int e = lane; e < total; e += 32) {
+    const int q = e / (2 * ncol), rem = e - q * 2 * ncol;
+    const int pl = rem / ncol, c = rem - pl * ncol;
+    const int p = pix[q];
+    const int j = p / W, i = p - j * W;
+    const double2 v = ct_col2(A.Q, H, W, j, i + c - R, pl, A.tr);
+    cols[(q * 4 + 2 * pl) * ncol + c] = v.x;
+    cols[(q * 4 + 2 * pl + 1) * ncol + c] = v.y;
   }
   __syncwarp();
   double red = 0.0;
-  if (lane < 4) {
+  if (lane < 4 * nq) {
     const double* T = cols + lane * ncol + R;
     double acc = T[0] * A.tr.w[0];
     for (int d = R; d >= 1; --d) acc += (T[-d] + T[d]) * A.tr.w[d];
     red = acc;
   }
-  const double J11 = __shfl_sync(0xffffffffu, red, 0), J12 = __shfl_sync(0xffffffffu, red, 1);
-  const double J22 = __shfl_sync(0xffffffffu, red, 2), mass = __shfl_sync(0xffffffffu, red, 3);
+  const int g0 = (lane >> 3) * 4;
+  const double J11 = __shfl_sync(0xffffffffu, red, g0), J12 = __shfl_sync(0xffffffffu, red, g0 + 1);
+  const double J22 = __shfl_sync(0xffffffffu, red, g0 + 2);
+  const double mass = __shfl_sync(0xffffffffu, red, g0 + 3);
   __syncwarp();
   const double safe = mass > 0.0 ? mass : 1.0;
   const double a = J11 / safe, b = J12 / safe, c = J22 / safe;
@@ -736,7 +880,7 @@ __device__ __forceinline__ bool ct_loop_active(const CtLoopArgs& A, int p) {
 }
 
 template <int C, int NL>
-__global__ void __launch_bounds__(kLoopThreads, 2)
+__global__ void __launch_bounds__(kLoopThreads, GF_CT_MIN_BLOCKS)
     k_ct_loop(const __grid_constant__ CtLoopArgs A, const __grid_constant__ BallParams P,
               const __grid_constant__ BallTables tab) {
   extern __shared__ __align__(16) unsigned char smraw[];
@@ -750,6 +894,7 @@ __global__ void __launch_bounds__(kLoopThreads, 2)
     T.mi[k] = tab.mi[k];
   }
   __syncthreads();
+  if (A.trace && blockIdx.x == 0 && threadIdx.x == 0) A.trace[4095 * 16 + 2] = ct_now();
   cg::grid_group grid = cg::this_grid();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int wpb = blockDim.x >> 5;
@@ -764,24 +909,71 @@ __global__ void __launch_bounds__(kLoopThreads, 2)
 
   // initial frontier (engine.py:298: active boundary, fr[0], counted in bank 1)
   // and the field around every Inpaint pixel (all a query can ever read)
-  for (int p = gtid; p < HW; p += nthreads) {
-    if (A.lab[p] != 255) continue;
-    const int j = p / W, i = p - j * W;
-    ct_queue_tiles(A, 1, j, i, dq);
-    if (ct_active(A.lab, H, W, A.periodic, j, i)) {
-      A.fr[0][atomicAdd(&ctr[kCtNF + 1], 1)] = p;
-      if (A.enter) A.enter[p] = 0;
+  // and the Inpaint count and the readable hull (engine.py:289-296)
+  unsigned long long* hull = reinterpret_cast<unsigned long long*>(ctr + kCtCount);
+  {
+    int n_inp = 0;
+    double lo = INFINITY, hi = -INFINITY;
+    for (int p0 = gwarp * 32; p0 < HW; p0 += nwarps * 32) {
+      const int p = p0 + lane;
+      bool act = false;
+      if (p < HW) {
+        const uint8_t l = A.lab[p];
+        if (l == 255) {
+          ++n_inp;
+          const int j = p / W, i = p - j * W;
+          ct_mark_tiles(A, j, i, dq);
+          act = ct_active(A.lab, H, W, A.periodic, j, i);
+          if (act && A.enter) A.enter[p] = 0;
+        } else if (l == 0) {
+#pragma unroll
+          for (int c = 0; c < C; ++c) {
+            const double v = A.u[(int64_t)p * C + c];
+            lo = fmin(lo, v);
+            hi = fmax(hi, v);
+          }
+        }
+      }
+      warp_append(act, p, &ctr[kCtNF + 1], A.fr[0]);
+    }
+    __shared__ int s_n;
+    __shared__ unsigned long long s_lo, s_hi;
+    if (threadIdx.x == 0) {
+      s_n = 0;
+      s_lo = ~0ULL;
+      s_hi = 0ULL;
+    }
+    __syncthreads();
+    atomicAdd(&s_n, n_inp);
+    if (lo <= hi) {
+      atomicMin(&s_lo, ct_key(lo));
+      atomicMax(&s_hi, ct_key(hi));
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      if (s_n) atomicAdd(&ctr[kCtInpaint], s_n);
+      if (s_lo <= s_hi) {
+        atomicMin(&hull[0], s_lo);
+        atomicMax(&hull[1], s_hi);
+      }
     }
   }
   grid.sync();
+  if (block_ld(&ctr[kCtInpaint]) > A.capacity) {  // cannot happen with capacity = H * W
+    if (gtid == 0) ctr[kCtDone] = 3;
+    return;
+  }
+  if (A.trace && gtid == 0) A.trace[4095 * 16 + 1] = ct_now();
   ct_run_tiles<C>(A, 1, sm);
   grid.sync();
+  if (A.trace && gtid == 0) A.trace[0] = ct_now();
 
-  long long rem = A.remaining0;
+  const long long remaining0 = block_ld(&ctr[kCtInpaint]);
+  long long rem = remaining0;
   bool data_live = A.order == 2;
   int s = 0;
   for (;; ++s) {
-    const int F = ld_cg(&ctr[kCtNF + ((s + 1) & 1)]);
+    const int F = block_ld(&ctr[kCtNF + ((s + 1) & 1)]);
     if (s > 0 && gtid == 0)  // candidates of shell s - 1 (complete after its last barrier)
       A.rows[5 * (int64_t)(s - 1) + 2] =
           A.tracked ? (long long)ld_cg(&ctr[kCtCand + ((s - 1) & 1)]) : (long long)HW;
@@ -800,17 +992,12 @@ __global__ void __launch_bounds__(kLoopThreads, 2)
 
     // ---- B: g and the ball sample at every frontier pixel
     {
-      double* cols = sm + warp * 4 * (2 * A.tr.R + 1);
+      double* cols = sm + warp * 16 * (2 * A.tr.R + 1);
       for (int base = gwarp * 4; base < F; base += nwarps * 4) {
-        double mgx = 0.0, mgy = 0.0;
-        for (int q = 0; q < 4 && base + q < F; ++q) {
-          double gx, gy;
-          ct_loop_g(A, fr[base + q], cols, gx, gy);
-          if ((lane >> 3) == q) {
-            mgx = gx;
-            mgy = gy;
-          }
-        }
+        const int nq = min(4, F - base);
+        double mgx, mgy;
+        ct_loop_g4(A, fr + base, nq, cols, mgx, mgy);
+        if (A.trace && gtid == 0 && base == 0 && s < 4096) A.trace[1 + 16 * s + 12] = ct_now();
         const int k = base + (lane >> 3);
         const bool valid = k < F;
         const int p = valid ? fr[k] : 0;
@@ -818,6 +1005,7 @@ __global__ void __launch_bounds__(kLoopThreads, 2)
         SampleResult r;
         eval_item<NL, 0, true>(P, T, src, lane & 7, valid, (double)pi, (double)pj, true, mgx, mgy,
                                r);
+        if (A.trace && gtid == 0 && base == 0 && s < 4096) A.trace[1 + 16 * s + 13] = ct_now();
         if (valid && (lane & 7) == 0) {
           A.eg[2 * k] = mgx;
           A.eg[2 * k + 1] = mgy;
@@ -825,11 +1013,14 @@ __global__ void __launch_bounds__(kLoopThreads, 2)
           A.etw[k] = r.tw;
 #pragma unroll
           for (int c = 0; c < C; ++c) A.evals[(int64_t)k * C + c] = r.v[c];
-          if (mgx != 0.0 || mgy != 0.0) atomicOr(&ctr[kCtAnyG + b], 1);
         }
+        const unsigned nz = __ballot_sync(0xffffffffu, valid && (mgx != 0.0 || mgy != 0.0));
+        if (lane == 0 && nz) atomicOr(&ctr[kCtAnyG + b], 1);
       }
     }
+    ct_trace_work(A, s, 8, 10);
     grid.sync();
+    ct_trace(A, s, 0);
     if (gtid == 0) {  // the other bank: every block has read F and the last row
       const int o = (s + 1) & 1;
       ctr[kCtNF + o] = 0;
@@ -840,7 +1031,7 @@ __global__ void __launch_bounds__(kLoopThreads, 2)
     }
 
     // ---- C: ready predicate (engine.py:317-330) and fill = ready & rw > 0
-    if (data_live && ld_cg(&ctr[kCtAnyG + b]) == 0) data_live = false;
+    if (data_live && block_ld(&ctr[kCtAnyG + b]) == 0) data_live = false;
     {
       const int mode = A.order == 0 ? 0 : (data_live ? 2 : 1);
       for (int k0 = blockIdx.x * blockDim.x; k0 < F; k0 += nthreads) {
@@ -860,7 +1051,8 @@ __global__ void __launch_bounds__(kLoopThreads, 2)
       }
     }
     grid.sync();
-    int n = ld_cg(&ctr[kCtFill + b]);
+    ct_trace(A, s, 1);
+    int n = block_ld(&ctr[kCtFill + b]);
 
     // ---- D: deadlock guard (engine.py:334-348)
     if (n == 0) {
@@ -941,7 +1133,8 @@ __global__ void __launch_bounds__(kLoopThreads, 2)
         }
       }
       grid.sync();
-      if (ld_cg(&ctr[kCtDone]) == 2) break;
+      ct_trace(A, s, 2);
+      if (block_ld(&ctr[kCtDone]) == 2) break;
       n = 1;
     }
 
@@ -954,48 +1147,63 @@ __global__ void __launch_bounds__(kLoopThreads, 2)
       A.lab[p] = 0;
       A.fillshell[p] = s;
       const int j = p / W, i = p - j * W;
-      ct_queue_tiles(A, b, j, i, dd);
+      ct_mark_tiles(A, j, i, dd);
     }
+    ct_trace_work(A, s, 9, 11);
     grid.sync();
+    ct_trace(A, s, 3);
     rem -= n;
 
     // ---- A + F: the field on the dirty tiles; the next frontier
+    if (A.trace && gtid == 0 && s < 4096) {
+      A.trace[1 + 16 * s + 7] = (unsigned long long)F;
+    }
     ct_run_tiles<C>(A, b, sm);
+    ct_trace(A, s, 4);  // this block's tiles (block 0's view)
     if (A.tracked) {
-      // tracker._update_arrays (tracker.py:59-79)
-      for (int k = gtid; k < F; k += nthreads) {
-        const int p = fr[k];
+      // tracker._update_arrays (tracker.py:59-79): o < 8 the Inpaint
+      // 8-neighbours of a filled entry, o == 8 the entry itself as survivor
+      for (int k0 = gwarp * 32; k0 < F; k0 += nwarps * 32) {
+        const int k = k0 + lane;
+        const bool valid = k < F;
+        const int p = valid ? fr[k] : 0;
+        const bool filled = valid && A.efill[k];
         const int j = p / W, i = p - j * W;
-        if (!A.efill[k]) {
-          if (atomicMax(&A.stamp[p], s + 1) < s + 1) {
-            atomicAdd(&ctr[kCtCand + b], 1);
-            if (ct_active(A.lab, H, W, A.periodic, j, i)) frn[atomicAdd(&ctr[kCtNF + b], 1)] = p;
+        for (int o = 0; o < 9; ++o) {
+          int q = -1, qj = 0, qi = 0;
+          if (valid) {
+            if (o == 8) {
+              if (!filled) {
+                q = p;
+                qj = j;
+                qi = i;
+              }
+            } else if (filled) {
+              qi = i + ct_nb_di(o);
+              qj = j + ct_nb_dj(o);
+              if (A.periodic) qi = (qi % W + W) % W;
+              if (qi >= 0 && qi < W && qj >= 0 && qj < H && A.lab[qj * W + qi] == 255)
+                q = qj * W + qi;
+            }
           }
-          continue;
-        }
-        for (int o = 0; o < 8; ++o) {
-          int ii = i + ct_nb_di(o);
-          const int jj = j + ct_nb_dj(o);
-          if (A.periodic) ii = (ii % W + W) % W;
-          if (ii < 0 || ii >= W || jj < 0 || jj >= H) continue;
-          const int q = jj * W + ii;
-          if (A.lab[q] != 255) continue;
-          if (atomicMax(&A.stamp[q], s + 1) >= s + 1) continue;
-          atomicAdd(&ctr[kCtCand + b], 1);
-          if (ct_active(A.lab, H, W, A.periodic, jj, ii)) {
-            frn[atomicAdd(&ctr[kCtNF + b], 1)] = q;
-            if (A.enter && A.enter[q] < 0) A.enter[q] = s + 1;
-          }
+          const bool claimed = q >= 0 && atomicMax(&A.stamp[q], s + 1) < s + 1;
+          const bool act = claimed && ct_active(A.lab, H, W, A.periodic, qj, qi);
+          const unsigned mc = __ballot_sync(0xffffffffu, claimed);
+          if (lane == 0 && mc) atomicAdd(&ctr[kCtCand + b], __popc(mc));
+          if (act && A.enter && A.enter[q] < 0) A.enter[q] = s + 1;
+          warp_append(act, q, &ctr[kCtNF + b], frn);
         }
       }
     } else {
-      for (int p = gtid; p < HW; p += nthreads) {
-        if (A.lab[p] != 255) continue;
-        const int j = p / W, i = p - j * W;
-        if (ct_active(A.lab, H, W, A.periodic, j, i)) {
-          frn[atomicAdd(&ctr[kCtNF + b], 1)] = p;
-          if (A.enter && A.enter[p] < 0) A.enter[p] = s + 1;
+      for (int p0 = gwarp * 32; p0 < HW; p0 += nwarps * 32) {
+        const int p = p0 + lane;
+        bool act = false;
+        if (p < HW && A.lab[p] == 255) {
+          const int j = p / W, i = p - j * W;
+          act = ct_active(A.lab, H, W, A.periodic, j, i);
+          if (act && A.enter && A.enter[p] < 0) A.enter[p] = s + 1;
         }
+        warp_append(act, p, &ctr[kCtNF + b], frn);
       }
     }
     if (gtid == 0) {
@@ -1006,10 +1214,27 @@ __global__ void __launch_bounds__(kLoopThreads, 2)
       row[4] = n;
     }
     grid.sync();
+    ct_trace(A, s, 5);
+    if (A.trace && gtid == 0 && s < 4096)
+      A.trace[1 + 16 * s + 6] = (unsigned long long)ld_cg(&ctr[kCtTiles + b]);
   }
   if (gtid == 0) {
     ctr[kCtIters] = s;
-    ctr[kCtFilled] = (int)(A.remaining0 - rem);
+    ctr[kCtFilled] = (int)(remaining0 - rem);
+  }
+  // hull clip of the whole image (engine.py:375-376); the caller clips after
+  // painting when the fill ended unfillable
+  grid.sync();
+  if (block_ld(&ctr[kCtDone]) == 0) {
+    const unsigned long long klo = hull[0], khi = hull[1];
+    if (klo <= khi) {
+      const double lo = ct_unkey(klo), hi = ct_unkey(khi);
+      const int64_t n = (int64_t)HW * C;
+      for (int64_t e = gtid; e < n; e += nthreads) {
+        const double v = A.u[e];
+        A.u[e] = v < lo ? lo : (v > hi ? hi : v);
+      }
+    }
   }
 }
 
@@ -1028,8 +1253,8 @@ int coherence_fill_launch(const CoherenceFillArgs& a, const BallParams& P, const
   const size_t HW = (size_t)H * W;
   const int tiles_x = (W + kLTW - 1) / kLTW, tiles_y = (H + kLTH - 1) / kLTH;
   const size_t ntiles = (size_t)tiles_x * tiles_y;
-  const size_t cap = a.n_inpaint > 0 ? (size_t)a.n_inpaint : 1;
-  if (a.workspace_bytes < coherence_fill_workspace(H, W, C, a.n_inpaint))
+  const size_t cap = a.capacity > 0 ? (size_t)a.capacity : 1;
+  if (a.workspace_bytes < coherence_fill_workspace(H, W, C, a.capacity))
     return set_error(GF_E_WORKSPACE, "workspace too small");
   // carve the workspace (8-byte aligned pieces first)
   char* w = static_cast<char*>(a.workspace);
@@ -1051,7 +1276,7 @@ int coherence_fill_launch(const CoherenceFillArgs& a, const BallParams& P, const
   A.tiles_x = tiles_x;
   A.tiles_y = tiles_y;
   A.rows_cap = a.rows_cap;
-  A.remaining0 = a.n_inpaint;
+  A.capacity = a.capacity;
   A.u = a.image;
   A.lab = a.labels;
   A.Q = reinterpret_cast<double*>(take(4 * HW * sizeof(double)));
@@ -1063,11 +1288,9 @@ int coherence_fill_launch(const CoherenceFillArgs& a, const BallParams& P, const
   A.fr[0] = reinterpret_cast<int*>(take(cap * sizeof(int)));
   A.fr[1] = reinterpret_cast<int*>(take(cap * sizeof(int)));
   A.stamp = reinterpret_cast<int*>(take(HW * sizeof(int)));
-  A.tflag = reinterpret_cast<unsigned*>(take(ntiles * sizeof(unsigned)));
-  A.tlist[0] = reinterpret_cast<int*>(take(ntiles * sizeof(int)));
-  A.tlist[1] = reinterpret_cast<int*>(take(ntiles * sizeof(int)));
+  A.tflag = reinterpret_cast<uint8_t*>(take(ntiles));
   A.slot_k = reinterpret_cast<int*>(take(4096 * sizeof(int)));
-  A.ctr = reinterpret_cast<int*>(take(kCtCount * sizeof(int)));
+  A.ctr = reinterpret_cast<int*>(take(kCtCount * sizeof(int) + 2 * sizeof(unsigned long long)));
   A.efill = reinterpret_cast<uint8_t*>(take(cap));
   A.fillshell = a.fillshell;
   A.enter = a.enter;
@@ -1077,8 +1300,9 @@ int coherence_fill_launch(const CoherenceFillArgs& a, const BallParams& P, const
   cudaStream_t s = stream;
   // stamps / tile flags / counters start at zero; the field needs no init
   cudaMemsetAsync(A.stamp, 0, HW * sizeof(int), s);
-  cudaMemsetAsync(A.tflag, 0, ntiles * sizeof(unsigned), s);
-  cudaMemsetAsync(A.ctr, 0, kCtCount * sizeof(int), s);
+  cudaMemsetAsync(A.tflag, 0, ntiles, s);
+  cudaMemsetAsync(A.ctr, 0, kCtCount * sizeof(int) + 2 * sizeof(unsigned long long), s);
+  cudaMemsetAsync(A.ctr + kCtCount, 0xff, sizeof(unsigned long long), s);  // hull min key
   const void* fn = nullptr;
   const bool wide = P.plan.n_leaves > 1;
   switch (C) {
@@ -1091,10 +1315,11 @@ int coherence_fill_launch(const CoherenceFillArgs& a, const BallParams& P, const
   const size_t tile_dbl = (size_t)(C + 1) * (kLTH + 2 + 2 * R) * (kLTW + 2 + 2 * R) +
                           (size_t)(C + 1) * (kLTH + 2) * (kLTW + 2 + 2 * R) +
                           (size_t)C * (kLTH + 2) * (kLTW + 2);
-  const size_t query_dbl = (size_t)(kLoopThreads / 32) * 4 * (2 * tr.R + 1);
+  const size_t query_dbl = (size_t)(kLoopThreads / 32) * 16 * (2 * tr.R + 1);
   const size_t red_dbl = 2 * kLoopThreads;
   const size_t smem = ((sizeof(BallTables) + 15) & ~size_t(15)) +
                       std::max(tile_dbl, std::max(query_dbl, red_dbl)) * sizeof(double);
+  if (smem > 200 * 1024) return set_error(GF_E_UNSUPPORTED, "rho window too wide for the fused loop");
   if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return set_error(GF_E_CUDA, cudaGetErrorString(cudaGetLastError()));
   int dev = 0, sms = 0, per_sm = 0;
@@ -1104,10 +1329,37 @@ int coherence_fill_launch(const CoherenceFillArgs& a, const BallParams& P, const
       per_sm < 1)
     return set_error(GF_E_CUDA, "coherence loop does not fit on an SM");
   const int grid = std::min(sms * per_sm, 4096);
+  const bool trace = getenv("GF_CT_TRACE") != nullptr;
+  if (trace) {
+    cudaMalloc(&A.trace, 4097 * 16 * sizeof(unsigned long long));
+    cudaMemsetAsync(A.trace, 0, 4097 * 16 * sizeof(unsigned long long), s);
+  }
   void* args[] = {(void*)&A, (void*)&P, (void*)&tab};
   cudaError_t e = cudaLaunchCooperativeKernel(fn, grid, kLoopThreads, args, smem, s);
   if (e != cudaSuccess) return set_error(GF_E_CUDA, cudaGetErrorString(e));
   count_launches(1);
+  if (trace) {  // diagnostics: per-shell phase times (us) on stderr
+    std::vector<unsigned long long> h(4097 * 16);
+    cudaMemcpyAsync(h.data(), A.trace, h.size() * 8, cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    cudaFree(A.trace);
+    fprintf(stderr, "GF_CT_TRACE grid=%d frontier_scan_us=%.1f init_fields_us=%.1f\n", grid,
+            (h[4095 * 16 + 1] - h[4095 * 16 + 2]) * 1e-3, (h[0] - h[4095 * 16 + 1]) * 1e-3);
+    unsigned long long prev = h[0];
+    for (int sh = 0; sh < 4095 && h[1 + 16 * sh + 5]; ++sh) {
+      const unsigned long long* t = &h[1 + 16 * sh];
+      const unsigned long long c_end = t[2] ? t[2] : t[1];
+      fprintf(stderr,
+              "shell %d (F %llu, tiles %llu): B %.1f (blk0 %.1f last %.1f) C %.1f D %.1f E %.1f "
+              "(blk0 %.1f last %.1f) A(blk0) %.1f AF %.1f total %.1f | chunk0 g %.1f eval %.1f\n",
+              sh, t[7], t[6], (t[0] - prev) * 1e-3, (t[8] - prev) * 1e-3, (t[10] - prev) * 1e-3,
+              (t[1] - t[0]) * 1e-3, t[2] ? (t[2] - t[1]) * 1e-3 : 0.0, (t[3] - c_end) * 1e-3,
+              (t[9] - c_end) * 1e-3, (t[11] - c_end) * 1e-3, (t[4] - t[3]) * 1e-3,
+              (t[5] - t[3]) * 1e-3, (t[5] - prev) * 1e-3, (t[12] - prev) * 1e-3,
+              (t[13] - t[12]) * 1e-3);
+      prev = t[5];
+    }
+  }
   // report: [iterations, filled, deadlock_fills, done]
   if (a.report) {
     e = cudaMemcpyAsync(a.report, A.ctr + kCtDone, 4 * sizeof(int), cudaMemcpyDeviceToDevice, s);
@@ -1118,14 +1370,14 @@ int coherence_fill_launch(const CoherenceFillArgs& a, const BallParams& P, const
   return GF_OK;
 }
 
-size_t coherence_fill_workspace(int H, int W, int C, long long n_inpaint) {
+size_t coherence_fill_workspace(int H, int W, int C, long long capacity) {
   const size_t HW = (size_t)H * W;
   const size_t ntiles = (size_t)((W + kLTW - 1) / kLTW) * ((H + kLTH - 1) / kLTH);
-  const size_t cap = n_inpaint > 0 ? (size_t)n_inpaint : 1;
+  const size_t cap = capacity > 0 ? (size_t)capacity : 1;
   auto r = [](size_t b) { return (b + 255) & ~size_t(255); };
   return r(4 * HW * 8) + r(2 * cap * 8) + 2 * r(cap * 8) + r(cap * C * 8) + r(4096 * 8) +
-         2 * r(cap * 4) + r(HW * 4) + r(ntiles * 4) + 2 * r(ntiles * 4) + r(4096 * 4) +
-         r(kCtCount * 4) + r(cap);
+         2 * r(cap * 4) + r(HW * 4) + r(ntiles) + r(4096 * 4) +
+         r(kCtCount * 4 + 16) + r(cap);
 }
 
 }  // namespace gf

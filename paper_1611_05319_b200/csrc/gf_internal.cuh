@@ -108,7 +108,7 @@ struct CoherenceFillArgs {
   int order;            // GF_ORDER_*
   double c, c2;
   int tracked;
-  long long n_inpaint;  // Inpaint pixels at the start
+  long long capacity;   // frontier entries (>= Inpaint pixels)
   int32_t* fillshell;   // [H][W], preset to -1
   int32_t* enter;       // [H][W] preset to -1, or nullptr
   long long* rows;      // [rows_cap][5]
@@ -117,7 +117,7 @@ struct CoherenceFillArgs {
   void* workspace;
   size_t workspace_bytes;
 };
-size_t coherence_fill_workspace(int H, int W, int C, long long n_inpaint);
+size_t coherence_fill_workspace(int H, int W, int C, long long capacity);
 int coherence_fill_launch(const CoherenceFillArgs& a, const BallParams& P, const BallTables& tab,
                           cudaStream_t stream);
 

@@ -377,30 +377,49 @@ __device__ __forceinline__ void eval_item(const BallParams& P, const BallTables&
       const int k = kb + lane;
       double p[4] = {0.0, 0.0, 0.0, 0.0};
       if (k < K) {
-        double px = T.n[k], py = T.m[k], w = T.w0[k];
-        if (!gzero) w = sample_weight(P, T, k, gx, gy, ux, uy, safe, thr, px, py);
+        // sample position, then every pixel fetch, then the weight (which
+        // does not depend on the fetches): the loads overlap the exp / hypot
+        double px = T.n[k], py = T.m[k];
+        if (!gzero && P.rotated) {
+          px = T.n[k] * uy + T.m[k] * ux;
+          py = (-T.n[k]) * ux + T.m[k] * uy;
+        }
         double sv[4] = {0.0, 0.0, 0.0, 0.0};
         bool ok = false;
         if (gzero && integral) {
           const int q = valid ? lattice_index(pi + T.ni[k], pj + T.mi[k], src.H, src.W,
                                               P.periodic)
                               : -1;
+          const auto v = src.fetch(q >= 0 ? q : 0);
           if (q >= 0) {
-            const auto v = src.fetch(q);
             ok = src.readable(v);
             if (ok) src.accumulate(v, 1.0, sv);
           }
         } else {
           Corners cn;
           ghost_corners(fi + px, fj + py, src.H, src.W, P.periodic, cn);
+          decltype(src.fetch(0)) v[4];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) v[c] = src.fetch(cn.q[c] >= 0 ? cn.q[c] : 0);
           ok = valid && !cn.outside;
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
             if (cn.q[c] >= 0 && valid) {
-              const auto v = src.fetch(cn.q[c]);
-              ok = ok && src.readable(v);
-              src.accumulate(v, cn.w[c], sv);
+              ok = ok && src.readable(v[c]);
+              src.accumulate(v[c], cn.w[c], sv);
             }
+          }
+        }
+        double w = T.w0[k];
+        if (!gzero) {
+          // sample_weight (engine.py:131-147) at the offset above
+          const double dist = hypot_np(px, py);
+          if (P.mu_inf) {
+            const double d = ((-gy) * px + gx * py) / safe;
+            w = (d * d <= thr) ? 1.0 / dist : 0.0;
+          } else {
+            const double d = (-gy) * px + gx * py;
+            w = exp_np((P.coef * d) * d) / dist;
           }
         }
         const double wr = ok ? w : 0.0;
