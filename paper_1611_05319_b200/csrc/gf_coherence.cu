@@ -539,13 +539,14 @@ enum CtCounter {
   kCtFill = 2,    // [2] fills
   kCtCand = 4,    // [2] tracker candidates
   kCtAnyG = 6,    // [2] any |g| > 0 (data term)
-  kCtTiles = 8,   // [2] dirty tiles processed (trace only)
+  kCtTiles = 8,   // [2] dirty tiles queued (tile list length)
   kCtDone = 10,   // 2: unfillable, 3: rows capacity exceeded
   kCtIters = 11,
   kCtDeadlocks = 12,
   kCtFilled = 13,
   kCtInpaint = 14,  // Inpaint pixels at the start
-  kCtCount = 16     // then two u64 hull keys (min, max) at ctr + kCtCount
+  kCtGrab = 16,     // [2] next tile-list entry to take
+  kCtCount = 20     // then two u64 hull keys (min, max) at ctr + kCtCount
 };
 
 struct CtLoopArgs {
@@ -565,7 +566,8 @@ struct CtLoopArgs {
   double* evals;
   uint8_t* efill;
   int* stamp;             // tracker dedup: last shell + 1 that claimed the pixel
-  uint8_t* tflag;         // tile's field is stale (plain stores, cleared when recomputed)
+  unsigned* tflag;        // tile queued for recomputation (cleared when recomputed)
+  int* tlist;             // queued tiles, taken in order by whichever block is free
   int* fillshell;
   int* enter;             // or nullptr
   long long* rows;        // [rows_cap][5]
@@ -760,34 +762,79 @@ __device__ __forceinline__ void ct_loop_tile(const CtLoopArgs& A, int t, double*
   }
 }
 
-// flag every tile within d of pixel (j, i) as stale (idempotent plain stores)
+// flag every tile within d of pixel (j, i) (idempotent plain stores; the
+// initial scan only -- compacted into the list by ct_list_flags)
 __device__ __forceinline__ void ct_mark_tiles(const CtLoopArgs& A, int j, int i, int d) {
   const int ty0 = max(0, j - d) / kLTH, ty1 = min(A.H - 1, j + d) / kLTH;
   const int tx0 = max(0, i - d) / kLTW, tx1 = min(A.W - 1, i + d) / kLTW;
   for (int ty = ty0; ty <= ty1; ++ty)
-    for (int tx = tx0; tx <= tx1; ++tx) A.tflag[ty * A.tiles_x + tx] = 1;
+    for (int tx = tx0; tx <= tx1; ++tx) A.tflag[ty * A.tiles_x + tx] = 1u;
 }
 
-// recompute the stale tiles: block b owns tiles b, b + grid, b + 2 grid, ...;
-// it gathers its stale ones into a shared list, then runs them one by one
+// every flagged tile into the list (block b scans tiles b, b + grid, ...)
+__device__ __forceinline__ void ct_list_flags(const CtLoopArgs& A, int bank) {
+  const int ntiles = A.tiles_x * A.tiles_y;
+  const int per = (ntiles + gridDim.x - 1) / gridDim.x;
+  for (int m0 = 0; m0 < per; m0 += blockDim.x) {
+    const int t = blockIdx.x + (m0 + threadIdx.x) * gridDim.x;
+    const bool q = m0 + (int)threadIdx.x < per && t < ntiles && A.tflag[t] != 0u;
+    warp_append(q, t, &A.ctr[kCtTiles + bank], A.tlist);
+  }
+}
+
+// queue the tiles within d of a filled pixel (warp-uniform: every lane calls,
+// f = this lane filled a pixel at (j, i)); a tile is listed once
+constexpr int kQueueRows = (2 * (kLoopRsMax + 1)) / kLTH + 2;
+constexpr int kQueueCols = (2 * (kLoopRsMax + 1)) / kLTW + 2;
+__device__ __forceinline__ void ct_queue_tiles(const CtLoopArgs& A, int bank, bool f, int j, int i,
+                                               int d) {
+  const int ty0 = max(0, j - d) / kLTH, ty1 = min(A.H - 1, j + d) / kLTH;
+  const int tx0 = max(0, i - d) / kLTW, tx1 = min(A.W - 1, i + d) / kLTW;
+  bool fresh[kQueueRows * kQueueCols];
+  int tt[kQueueRows * kQueueCols];
+#pragma unroll
+  for (int a = 0; a < kQueueRows; ++a)
+#pragma unroll
+    for (int c = 0; c < kQueueCols; ++c) {
+      const int ty = ty0 + a, tx = tx0 + c;
+      const int t = ty * A.tiles_x + tx;
+      tt[a * kQueueCols + c] = t;
+      fresh[a * kQueueCols + c] = f && ty <= ty1 && tx <= tx1 && atomicExch(&A.tflag[t], 1u) == 0u;
+    }
+  // one atomicAdd per warp for all of its lanes' fresh tiles
+  const int lane = threadIdx.x & 31;
+  int mine = 0;
+#pragma unroll
+  for (int e = 0; e < kQueueRows * kQueueCols; ++e) mine += fresh[e] ? 1 : 0;
+  int incl = mine;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  const int total = __shfl_sync(0xffffffffu, incl, 31);
+  int base = 0;
+  if (lane == 0 && total) base = atomicAdd(&A.ctr[kCtTiles + bank], total);
+  base = __shfl_sync(0xffffffffu, base, 0) + incl - mine;
+#pragma unroll
+  for (int e = 0; e < kQueueRows * kQueueCols; ++e)
+    if (fresh[e]) A.tlist[base++] = tt[e];
+}
+
+// recompute the listed tiles; blocks take the next entry as they free up
 template <int C>
 __device__ __forceinline__ void ct_run_tiles(const CtLoopArgs& A, int bank, double* sm) {
-  __shared__ int list[kLoopThreads];
-  __shared__ int nlist;
-  const int ntiles = A.tiles_x * A.tiles_y;
-  for (int t0 = blockIdx.x; t0 < ntiles; t0 += gridDim.x * (int)blockDim.x) {
+  __shared__ int s_idx;
+  const int n = block_ld(&A.ctr[kCtTiles + bank]);
+  for (;;) {
     __syncthreads();
-    if (threadIdx.x == 0) nlist = 0;
+    if (threadIdx.x == 0) s_idx = atomicAdd(&A.ctr[kCtGrab + bank], 1);
     __syncthreads();
-    const int t = t0 + threadIdx.x * gridDim.x;
-    if (t < ntiles && A.tflag[t]) {
-      A.tflag[t] = 0;
-      list[atomicAdd(&nlist, 1)] = t;
-    }
-    __syncthreads();
-    const int n = nlist;
-    if (threadIdx.x == 0 && n && A.trace) atomicAdd(&A.ctr[kCtTiles + bank], n);
-    for (int q = 0; q < n; ++q) ct_loop_tile<C>(A, list[q], sm);
+    const int idx = s_idx;
+    if (idx >= n) break;
+    const int t = A.tlist[idx];
+    if (threadIdx.x == 0) A.tflag[t] = 0u;
+    ct_loop_tile<C>(A, t, sm);
   }
 }
 
@@ -885,13 +932,15 @@ __global__ void __launch_bounds__(kLoopThreads, GF_CT_MIN_BLOCKS)
               const __grid_constant__ BallTables tab) {
   extern __shared__ __align__(16) unsigned char smraw[];
   BallTables& T = *reinterpret_cast<BallTables*>(smraw);
-  double* sm = reinterpret_cast<double*>(smraw + ((sizeof(BallTables) + 15) & ~size_t(15)));
+  double* tdist = reinterpret_cast<double*>(smraw + ((sizeof(BallTables) + 15) & ~size_t(15)));
+  double* sm = tdist + kMaxK;
   for (int k = threadIdx.x; k < P.K; k += blockDim.x) {
     T.n[k] = tab.n[k];
     T.m[k] = tab.m[k];
     T.w0[k] = tab.w0[k];
     T.ni[k] = tab.ni[k];
     T.mi[k] = tab.mi[k];
+    tdist[k] = hypot_np(tab.n[k], tab.m[k]);  // the axis ball's sample distances
   }
   __syncthreads();
   if (A.trace && blockIdx.x == 0 && threadIdx.x == 0) A.trace[4095 * 16 + 2] = ct_now();
@@ -963,6 +1012,8 @@ __global__ void __launch_bounds__(kLoopThreads, GF_CT_MIN_BLOCKS)
     if (gtid == 0) ctr[kCtDone] = 3;
     return;
   }
+  ct_list_flags(A, 1);
+  grid.sync();
   if (A.trace && gtid == 0) A.trace[4095 * 16 + 1] = ct_now();
   ct_run_tiles<C>(A, 1, sm);
   grid.sync();
@@ -1004,7 +1055,7 @@ __global__ void __launch_bounds__(kLoopThreads, GF_CT_MIN_BLOCKS)
         const int pj = p / W, pi = p - pj * W;
         SampleResult r;
         eval_item<NL, 0, true>(P, T, src, lane & 7, valid, (double)pi, (double)pj, true, mgx, mgy,
-                               r);
+                               r, tdist);
         if (A.trace && gtid == 0 && base == 0 && s < 4096) A.trace[1 + 16 * s + 13] = ct_now();
         if (valid && (lane & 7) == 0) {
           A.eg[2 * k] = mgx;
@@ -1028,6 +1079,7 @@ __global__ void __launch_bounds__(kLoopThreads, GF_CT_MIN_BLOCKS)
       ctr[kCtCand + o] = 0;
       ctr[kCtAnyG + o] = 0;
       ctr[kCtTiles + o] = 0;
+      ctr[kCtGrab + o] = 0;
     }
 
     // ---- C: ready predicate (engine.py:317-330) and fill = ready & rw > 0
@@ -1139,15 +1191,20 @@ __global__ void __launch_bounds__(kLoopThreads, GF_CT_MIN_BLOCKS)
     }
 
     // ---- E: commit (engine.py:350-356) and queue the dirty tiles
-    for (int k = gtid; k < F; k += nthreads) {
-      if (!A.efill[k]) continue;
-      const int p = fr[k];
+    for (int k0 = gwarp * 32; k0 < F; k0 += nwarps * 32) {
+      const int k = k0 + lane;
+      const bool f = k < F && A.efill[k];
+      int j = 0, i = 0;
+      if (f) {
+        const int p = fr[k];
 #pragma unroll
-      for (int c = 0; c < C; ++c) A.u[(int64_t)p * C + c] = A.evals[(int64_t)k * C + c];
-      A.lab[p] = 0;
-      A.fillshell[p] = s;
-      const int j = p / W, i = p - j * W;
-      ct_mark_tiles(A, j, i, dd);
+        for (int c = 0; c < C; ++c) A.u[(int64_t)p * C + c] = A.evals[(int64_t)k * C + c];
+        A.lab[p] = 0;
+        A.fillshell[p] = s;
+        j = p / W;
+        i = p - j * W;
+      }
+      ct_queue_tiles(A, b, f, j, i, dd);
     }
     ct_trace_work(A, s, 9, 11);
     grid.sync();
@@ -1158,8 +1215,6 @@ __global__ void __launch_bounds__(kLoopThreads, GF_CT_MIN_BLOCKS)
     if (A.trace && gtid == 0 && s < 4096) {
       A.trace[1 + 16 * s + 7] = (unsigned long long)F;
     }
-    ct_run_tiles<C>(A, b, sm);
-    ct_trace(A, s, 4);  // this block's tiles (block 0's view)
     if (A.tracked) {
       // tracker._update_arrays (tracker.py:59-79): o < 8 the Inpaint
       // 8-neighbours of a filled entry, o == 8 the entry itself as survivor
@@ -1206,6 +1261,8 @@ __global__ void __launch_bounds__(kLoopThreads, GF_CT_MIN_BLOCKS)
         warp_append(act, p, &ctr[kCtNF + b], frn);
       }
     }
+    ct_run_tiles<C>(A, b, sm);
+    ct_trace(A, s, 4);  // block 0 out of tiles
     if (gtid == 0) {
       long long* row = A.rows + 5 * (int64_t)s;
       row[0] = s;
@@ -1288,7 +1345,8 @@ int coherence_fill_launch(const CoherenceFillArgs& a, const BallParams& P, const
   A.fr[0] = reinterpret_cast<int*>(take(cap * sizeof(int)));
   A.fr[1] = reinterpret_cast<int*>(take(cap * sizeof(int)));
   A.stamp = reinterpret_cast<int*>(take(HW * sizeof(int)));
-  A.tflag = reinterpret_cast<uint8_t*>(take(ntiles));
+  A.tflag = reinterpret_cast<unsigned*>(take(ntiles * sizeof(unsigned)));
+  A.tlist = reinterpret_cast<int*>(take(ntiles * sizeof(int)));
   A.slot_k = reinterpret_cast<int*>(take(4096 * sizeof(int)));
   A.ctr = reinterpret_cast<int*>(take(kCtCount * sizeof(int) + 2 * sizeof(unsigned long long)));
   A.efill = reinterpret_cast<uint8_t*>(take(cap));
@@ -1300,7 +1358,7 @@ int coherence_fill_launch(const CoherenceFillArgs& a, const BallParams& P, const
   cudaStream_t s = stream;
   // stamps / tile flags / counters start at zero; the field needs no init
   cudaMemsetAsync(A.stamp, 0, HW * sizeof(int), s);
-  cudaMemsetAsync(A.tflag, 0, ntiles, s);
+  cudaMemsetAsync(A.tflag, 0, ntiles * sizeof(unsigned), s);
   cudaMemsetAsync(A.ctr, 0, kCtCount * sizeof(int) + 2 * sizeof(unsigned long long), s);
   cudaMemsetAsync(A.ctr + kCtCount, 0xff, sizeof(unsigned long long), s);  // hull min key
   const void* fn = nullptr;
@@ -1317,7 +1375,7 @@ int coherence_fill_launch(const CoherenceFillArgs& a, const BallParams& P, const
                           (size_t)C * (kLTH + 2) * (kLTW + 2);
   const size_t query_dbl = (size_t)(kLoopThreads / 32) * 16 * (2 * tr.R + 1);
   const size_t red_dbl = 2 * kLoopThreads;
-  const size_t smem = ((sizeof(BallTables) + 15) & ~size_t(15)) +
+  const size_t smem = ((sizeof(BallTables) + 15) & ~size_t(15)) + kMaxK * sizeof(double) +
                       std::max(tile_dbl, std::max(query_dbl, red_dbl)) * sizeof(double);
   if (smem > 200 * 1024) return set_error(GF_E_UNSUPPORTED, "rho window too wide for the fused loop");
   if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
@@ -1376,7 +1434,7 @@ size_t coherence_fill_workspace(int H, int W, int C, long long capacity) {
   const size_t cap = capacity > 0 ? (size_t)capacity : 1;
   auto r = [](size_t b) { return (b + 255) & ~size_t(255); };
   return r(4 * HW * 8) + r(2 * cap * 8) + 2 * r(cap * 8) + r(cap * C * 8) + r(4096 * 8) +
-         2 * r(cap * 4) + r(HW * 4) + r(ntiles) + r(4096 * 4) +
+         2 * r(cap * 4) + r(HW * 4) + 2 * r(ntiles * 4) + r(4096 * 4) +
          r(kCtCount * 4 + 16) + r(cap);
 }
 

@@ -322,6 +322,7 @@ __device__ __forceinline__ double sample_weight(const BallParams& P, const BallT
 // KPL = samples per lane (ceil(K / 8)) as a compile-time bound so every
 //       fetch of a lane is issued before the first one is consumed, or 0
 //       for a runtime loop (large radii).
+// axis_dist: optional hypot(n_k, m_k) table (EXACTV path, axis ball).
 // EXACTV: the colour numerator in numpy's einsum("fk,fkc->fc") order
 //       (engine.py:196) instead of per-lane partial sums, so the values are
 //       bit-exact in fp64 (the coherence path feeds them back into the
@@ -334,7 +335,7 @@ template <int NL, int KPL, bool EXACTV = false, class Src>
 __device__ __forceinline__ void eval_item(const BallParams& P, const BallTables& T,
                                           const Src& src, int lane, bool valid, double fi,
                                           double fj, bool integral, double gx, double gy,
-                                          SampleResult& out) {
+                                          SampleResult& out, const double* axis_dist = nullptr) {
   const int K = P.K;
   const bool gzero = (gx == 0.0) && (gy == 0.0);
   double ux = 0.0, uy = 1.0;
@@ -412,8 +413,9 @@ __device__ __forceinline__ void eval_item(const BallParams& P, const BallTables&
         }
         double w = T.w0[k];
         if (!gzero) {
-          // sample_weight (engine.py:131-147) at the offset above
-          const double dist = hypot_np(px, py);
+          // sample_weight (engine.py:131-147) at the offset above; an axis
+          // ball's distances hypot(n, m) may come from a table (axis_dist)
+          const double dist = (axis_dist && !P.rotated) ? axis_dist[k] : hypot_np(px, py);
           if (P.mu_inf) {
             const double d = ((-gy) * px + gx * py) / safe;
             w = (d * d <= thr) ? 1.0 / dist : 0.0;
