@@ -530,7 +530,7 @@ constexpr int kLoopThreads = 256;
 #ifndef GF_CT_MIN_BLOCKS
 #define GF_CT_MIN_BLOCKS 2  // 2 x 256 threads per SM (3 spills and runs slower)
 #endif
-constexpr int kLTW = 32, kLTH = 8;  // tensor tile: 32 columns x 8 rows
+constexpr int kLTW = 16, kLTH = 16;  // tensor tile: 16 x 16 pixels
 constexpr int kLoopRsMax = 6;       // sigma window radius the fused tile supports
 static_assert(kLTW * kLTH == kLoopThreads, "one J output per thread");
 

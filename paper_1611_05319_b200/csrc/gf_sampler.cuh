@@ -372,66 +372,9 @@ __device__ __forceinline__ void eval_item(const BallParams& P, const BallTables&
 
   double ex_s[4] = {0.0, 0.0, 0.0, 0.0};  // EXACTV: C >= 2 sums / C == 1 lanes 0, 1
   if constexpr (EXACTV) {
-    // one sample per lane per block of kGroup, blocks uniform over the group
-#pragma unroll 1
-    for (int kb = 0; kb < K; kb += kGroup) {
-      const int k = kb + lane;
-      double p[4] = {0.0, 0.0, 0.0, 0.0};
-      if (k < K) {
-        // sample position, then every pixel fetch, then the weight (which
-        // does not depend on the fetches): the loads overlap the exp / hypot
-        double px = T.n[k], py = T.m[k];
-        if (!gzero && P.rotated) {
-          px = T.n[k] * uy + T.m[k] * ux;
-          py = (-T.n[k]) * ux + T.m[k] * uy;
-        }
-        double sv[4] = {0.0, 0.0, 0.0, 0.0};
-        bool ok = false;
-        if (gzero && integral) {
-          const int q = valid ? lattice_index(pi + T.ni[k], pj + T.mi[k], src.H, src.W,
-                                              P.periodic)
-                              : -1;
-          const auto v = src.fetch(q >= 0 ? q : 0);
-          if (q >= 0) {
-            ok = src.readable(v);
-            if (ok) src.accumulate(v, 1.0, sv);
-          }
-        } else {
-          Corners cn;
-          ghost_corners(fi + px, fj + py, src.H, src.W, P.periodic, cn);
-          decltype(src.fetch(0)) v[4];
-#pragma unroll
-          for (int c = 0; c < 4; ++c) v[c] = src.fetch(cn.q[c] >= 0 ? cn.q[c] : 0);
-          ok = valid && !cn.outside;
-#pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            if (cn.q[c] >= 0 && valid) {
-              ok = ok && src.readable(v[c]);
-              src.accumulate(v[c], cn.w[c], sv);
-            }
-          }
-        }
-        double w = T.w0[k];
-        if (!gzero) {
-          // sample_weight (engine.py:131-147) at the offset above; an axis
-          // ball's distances hypot(n, m) may come from a table (axis_dist)
-          const double dist = (axis_dist && !P.rotated) ? axis_dist[k] : hypot_np(px, py);
-          if (P.mu_inf) {
-            const double d = ((-gy) * px + gx * py) / safe;
-            w = (d * d <= thr) ? 1.0 / dist : 0.0;
-          } else {
-            const double d = (-gy) * px + gx * py;
-            w = exp_np((P.coef * d) * d) / dist;
-          }
-        }
-        const double wr = ok ? w : 0.0;
-        if (ok) {
-#pragma unroll
-          for (int c = 0; c < 4; ++c) p[c] = wr * sv[c];
-        }
-        acc_sample<NL>(P, k, w, wr, acc_rw, acc_tw, tl_rw, tl_tw);
-      }
-      const int rem = K - kb;  // samples in this block (all lanes agree)
+    // numpy einsum order for the numerator: block of kGroup samples folded
+    // in k order (lanes hold consecutive k; the fold is warp-uniform)
+    auto fold = [&](const double (&p)[4], int rem) {
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         double q[kGroup];
@@ -462,6 +405,99 @@ __device__ __forceinline__ void eval_item(const BallParams& P, const BallTables&
           for (int l = 0; l < kGroup; ++l)
             if (l < rem) ex_s[c] = ex_s[c] + q[l];
         }
+      }
+    };
+    // weight of sample k at offset (px, py) (engine.py:131-147); an axis
+    // ball's distances hypot(n, m) may come from the axis_dist table
+    auto weight = [&](int k, double px, double py) {
+      if (gzero) return T.w0[k];
+      const double dist = (axis_dist && !P.rotated) ? axis_dist[k] : hypot_np(px, py);
+      if (P.mu_inf) {
+        const double d = ((-gy) * px + gx * py) / safe;
+        return (d * d <= thr) ? 1.0 / dist : 0.0;
+      }
+      const double d = (-gy) * px + gx * py;
+      return exp_np((P.coef * d) * d) / dist;
+    };
+    if (integral && (gzero || !P.rotated)) {
+      // an integral centre with lattice offsets (g = 0, or the axis ball at
+      // any g) samples one pixel with bilinear weight 1: grid.py's ghost
+      // gather reduces to the lattice value (the other corners are not
+      // live).  Two blocks per iteration: both fetches and both weight
+      // chains in flight together.
+#pragma unroll 1
+      for (int kb = 0; kb < K; kb += 2 * kGroup) {
+        int kk[2], q[2];
+        decltype(src.fetch(0)) v[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          kk[h] = kb + h * kGroup + lane;
+          const int kc = kk[h] < K ? kk[h] : 0;
+          q[h] = (valid && kk[h] < K)
+                     ? lattice_index(pi + T.ni[kc], pj + T.mi[kc], src.H, src.W, P.periodic)
+                     : -1;
+          v[h] = src.fetch(q[h] >= 0 ? q[h] : 0);
+        }
+        double w[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int kc = kk[h] < K ? kk[h] : 0;
+          w[h] = weight(kc, T.n[kc], T.m[kc]);
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int b0 = kb + h * kGroup;
+          if (b0 >= K) break;  // uniform
+          double p[4] = {0.0, 0.0, 0.0, 0.0};
+          if (kk[h] < K) {
+            double sv[4] = {0.0, 0.0, 0.0, 0.0};
+            const bool ok = q[h] >= 0 && src.readable(v[h]);
+            if (ok) src.accumulate(v[h], 1.0, sv);
+            const double wr = ok ? w[h] : 0.0;
+            if (ok) {
+#pragma unroll
+              for (int c = 0; c < 4; ++c) p[c] = wr * sv[c];
+            }
+            acc_sample<NL>(P, kk[h], w[h], wr, acc_rw, acc_tw, tl_rw, tl_tw);
+          }
+          fold(p, K - b0);
+        }
+      }
+    } else {
+      // ghost samples: one per lane per block of kGroup
+#pragma unroll 1
+      for (int kb = 0; kb < K; kb += kGroup) {
+        const int k = kb + lane;
+        double p[4] = {0.0, 0.0, 0.0, 0.0};
+        if (k < K) {
+          double px = T.n[k], py = T.m[k];
+          if (!gzero && P.rotated) {
+            px = T.n[k] * uy + T.m[k] * ux;
+            py = (-T.n[k]) * ux + T.m[k] * uy;
+          }
+          Corners cn;
+          ghost_corners(fi + px, fj + py, src.H, src.W, P.periodic, cn);
+          decltype(src.fetch(0)) v[4];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) v[c] = src.fetch(cn.q[c] >= 0 ? cn.q[c] : 0);
+          const double w = weight(k, px, py);
+          double sv[4] = {0.0, 0.0, 0.0, 0.0};
+          bool ok = valid && !cn.outside;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            if (cn.q[c] >= 0 && valid) {
+              ok = ok && src.readable(v[c]);
+              src.accumulate(v[c], cn.w[c], sv);
+            }
+          }
+          const double wr = ok ? w : 0.0;
+          if (ok) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) p[c] = wr * sv[c];
+          }
+          acc_sample<NL>(P, k, w, wr, acc_rw, acc_tw, tl_rw, tl_tw);
+        }
+        fold(p, K - kb);
       }
     }
   } else if (gzero && integral) {
