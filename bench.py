@@ -521,6 +521,49 @@ def bench_deadlock(dev):
     return out
 
 
+def bench_coherence(dev, reps=7):
+    """the coherence-transport preset (FillParams.coherence_transport:
+    g from the masked structure tensor every shell) on the C2 frame -- the whole
+    fill in one persistent kernel (coherence.run_coherence_fill); device-resident
+    f64 frame, and through the public API from host numpy arrays."""
+    import numpy as np
+    import torch
+
+    from paper_1611_05319_b200 import FillParams, engine, scenes
+    from paper_1611_05319_b200.coherence import run_coherence_fill
+
+    sc = scenes.config("C2")
+    p = FillParams.coherence_transport()
+    img = torch.from_numpy(np.ascontiguousarray(sc.image, dtype=np.float64)).to(dev)
+    lab = torch.from_numpy(sc.labels).to(dev)
+    for _ in range(2):
+        run_coherence_fill(img.clone(), lab, p, tracked=True)
+    ts = []
+    rep = None
+    for _ in range(reps):
+        u = img.clone()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        _, rep, _, _ = run_coherence_fill(u, lab, p, tracked=True)
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    engine.coherence_transport_mode(sc.image, sc.labels)  # warm-up
+    t0 = time.perf_counter()
+    engine.coherence_transport_mode(sc.image, sc.labels)
+    api_ms = (time.perf_counter() - t0) * 1e3
+    return {"ms_per_frame": min(ts), "ms_median": sorted(ts)[len(ts) // 2], "ms_all": ts,
+            "shells": rep["iterations"], "filled": rep["filled"],
+            "mpx_s": rep["filled"] / (min(ts) * 1e3),
+            "host_api_ms": api_ms,
+            "host_api_path": "engine.coherence_transport_mode(numpy f64 image, labels)",
+            "path": "coherence.run_coherence_fill: one cooperative launch of k_ct_loop "
+                    "(gf_coherence_fill) for all shells, f64 frame resident, one host sync",
+            "workload": "C2 1920x1080, 77,440 Inpaint px, r=5 axis ball, onion, "
+                        "sigma 2, rho 4, lambda 1e-5"}
+
+
 def bench_detect():
     """Automatic spline detection (guide.detect_splines) on the C2 and C4
     frames through the public API (host f64 image in, Spline list out)."""
@@ -630,6 +673,7 @@ def rank_main(args):
         cpu = None if args.no_cpu else pool_baseline("C2")
         deadlock = None if args.no_extras else bench_deadlock(dev)
         detect = None if args.no_extras else bench_detect()
+        coherence = None if args.no_extras else bench_coherence(dev)
         line = {
             "metric": METRIC, "value": D / (c2["t_ms"] * 1e-3) / 1e6, "unit": "Mpx/s",
             "n_gpus": 1, "steps": args.steps, "warmup": max(3, args.warmup),
@@ -655,6 +699,7 @@ def rank_main(args):
             "c5": c5_line,
             "deadlock_regime": deadlock,
             "spline_detection": detect,
+            "coherence_transport": coherence,
             "gpu_launches": c2["launches"],
             "gpu_launches_note": "library kernels (gf_launch_count) in the C2 timed replays; "
                                  "the whole run launched "

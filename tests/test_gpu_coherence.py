@@ -179,3 +179,38 @@ def test_device_transcendentals_match_numpy():
     p = rng.uniform(-np.pi / 2, np.pi / 2, n) * 10.0 ** rng.uniform(-9, 0, n)
     assert _same_bits(_device_npmath(2, p), np.sin(p))
     assert _same_bits(_device_npmath(3, p), np.cos(p))
+
+
+@pytest.mark.parametrize("idx", range(len(CT_CASES)))
+def test_persistent_loop_equals_shell_loop(idx):
+    """The one-launch loop (gf_coherence_fill) and the shell-by-shell loop
+    (run_coherence_fill_shells, the fallback for wide sigma windows) agree bit
+    for bit: order maps, report rows and values."""
+    import torch
+
+    from paper_1611_05319_b200.coherence import run_coherence_fill, run_coherence_fill_shells
+
+    case = CT_CASES[idx]
+    p = FillParams(**case["params"])
+    img = torch.from_numpy(np.ascontiguousarray(case["image"], dtype=np.float64)).cuda()
+    lab = torch.from_numpy(case["labels"]).cuda()
+    u1, r1, e1, f1 = run_coherence_fill(img.clone(), lab, p, case["tracked"], True)
+    u2, r2, e2, f2 = run_coherence_fill_shells(img.clone(), lab, p, case["tracked"], True)
+    assert torch.equal(f1, f2) and torch.equal(e1, e2)
+    assert r1["rows"] == [tuple(int(x) for x in r) for r in r2["rows"]]
+    for k in ("iterations", "filled", "deadlock_fills", "unfillable", "unfillable_count"):
+        assert r1[k] == r2[k], k
+    assert torch.equal(u1.view(torch.int64), u2.view(torch.int64))
+
+
+def test_wide_sigma_window_runs_the_shell_loop():
+    """sigma = 3.5 (a 15-tap window) is past the fused tile's reach: the fill
+    takes the shell-by-shell path and still matches the oracle bit for bit."""
+    img, lab = cases.edge_block()
+    p = FillParams(r=5, neighborhood="axis_ball", order="onion",
+                   g_source="modified_structure_tensor", sigma=3.5, rho=4.0)
+    u, rep, maps = engine._run_fill(img, lab, None, p, tracked=True, order_log=True)
+    ref = orc.fill(img, lab, None, orc.Params.of(p), tracked=True)
+    assert np.array_equal(maps["fillshell"], ref["fillshell"])
+    assert [tuple(r) for r in rep.rows] == [tuple(r) for r in ref["rows"]]
+    assert np.array_equal(u.view(np.int64), ref["u"].view(np.int64))
