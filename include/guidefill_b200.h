@@ -308,8 +308,8 @@ int gf_commit_shell(int32_t channels, int32_t n, const int64_t* frontier, const 
  * with g_source = "modified_structure_tensor": guide.coherence_directions,
  * guide.py:330-355) in one persistent kernel launch: image / labels (device,
  * f64 [H][W][C] / uint8 [H][W]) are filled and relabelled in place;
- * fillshell (preset -1) receives each pixel's shell, enter (optional, preset
- * -1) the shell it joined the frontier, rows[rows_cap][5] the report rows
+ * fillshell receives each pixel's shell (-1 if never filled), enter (optional)
+ * the shell it joined the frontier (-1 never), rows[rows_cap][5] the report rows
  * (iteration, frontier size, candidates, threads, filled) and report[4] =
  * (done: 0 finished / 2 unfillable / 3 capacity exceeded, iterations,
  * deadlock fills, filled).  The image is clipped to the readable hull

@@ -80,6 +80,41 @@ def _neighbor_mean(u, lab, p, H, W, periodic_x):
     return acc / n
 
 
+_PINNED = {}
+
+
+def _pinned_report(n):
+    """A reusable pinned int32 host buffer per stream (page-locking per call
+    costs more than the fill's last shells)."""
+    import torch
+
+    key = (torch.cuda.current_stream().cuda_stream, n)
+    buf = _PINNED.get(key)
+    if buf is None:
+        buf = _PINNED[key] = torch.empty(n, dtype=torch.int32, pin_memory=True)
+    return buf
+
+
+_SCRATCH = {}
+
+
+def _scratch(dev, H, W, C, cap):
+    """Report rows, report and workspace of gf_coherence_fill, kept per (device,
+    stream, geometry): the kernel initialises what it reads, and calls on one
+    stream run in order, so they are reused as is."""
+    import torch
+
+    key = (str(dev), torch.cuda.current_stream(dev).cuda_stream, H, W, C)
+    hit = _SCRATCH.get(key)
+    if hit is None:
+        lib = N.load()
+        ws_bytes = lib.gf_coherence_fill_workspace_bytes(H, W, C, cap)
+        hit = _SCRATCH[key] = (torch.empty((cap + 1, 5), dtype=torch.int64, device=dev),
+                               torch.empty(4, dtype=torch.int32, device=dev),
+                               torch.empty(ws_bytes, dtype=torch.uint8, device=dev), ws_bytes)
+    return hit
+
+
 def run_coherence_fill(u, lab0, params, tracked=True, order_log=False):
     """engine._fill_loop (engine.py:286-376) with g from the masked structure tensor:
     the whole loop in one persistent kernel (gf_coherence_fill).
@@ -99,12 +134,9 @@ def run_coherence_fill(u, lab0, params, tracked=True, order_log=False):
     lab = lab0.clone()
     lib = N.load()
     cap = H * W  # frontier capacity: >= the Inpaint count, no host count needed
-    fillshell = torch.full((H * W,), -1, dtype=torch.int32, device=dev)
-    enter = torch.full((H * W,), -1, dtype=torch.int32, device=dev) if order_log else None
-    rows = torch.empty((cap + 1, 5), dtype=torch.int64, device=dev)
-    report = torch.empty(4, dtype=torch.int32, device=dev)
-    ws_bytes = lib.gf_coherence_fill_workspace_bytes(H, W, C, cap)
-    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+    fillshell = torch.empty(H * W, dtype=torch.int32, device=dev)  # the kernel presets -1
+    enter = torch.empty(H * W, dtype=torch.int32, device=dev) if order_log else None
+    rows, report, ws, ws_bytes = _scratch(dev, H, W, C, cap)
     pc = params_to_c(params, tracked, N.GF_G_FIELD)
     t0 = time.perf_counter()
     rc = lib.gf_coherence_fill(H, W, C, N.ptr(u), N.ptr(lab), ctypes.byref(pc),
@@ -117,7 +149,7 @@ def run_coherence_fill(u, lab0, params, tracked=True, order_log=False):
     N.check(rc)
     # one synchronisation: the report and the first rows in a single pinned copy
     head = min(cap + 1, 64)
-    host = torch.empty(4 + 10 * head, dtype=torch.int32, pin_memory=True)
+    host = _pinned_report(4 + 10 * head)
     host[:4].copy_(report, non_blocking=True)
     host[4:].view(torch.int64).view(head, 5).copy_(rows[:head], non_blocking=True)
     torch.cuda.current_stream().synchronize()

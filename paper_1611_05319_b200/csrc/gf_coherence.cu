@@ -33,6 +33,7 @@
 #include <stdlib.h>
 
 #include <algorithm>
+#include <mutex>
 #include <vector>
 
 #include <cooperative_groups.h>
@@ -968,12 +969,12 @@ __global__ void __launch_bounds__(kLoopThreads, GF_CT_MIN_BLOCKS)
       bool act = false;
       if (p < HW) {
         const uint8_t l = A.lab[p];
+        A.fillshell[p] = -1;
         if (l == 255) {
           ++n_inp;
           const int j = p / W, i = p - j * W;
           ct_mark_tiles(A, j, i, dq);
           act = ct_active(A.lab, H, W, A.periodic, j, i);
-          if (act && A.enter) A.enter[p] = 0;
         } else if (l == 0) {
 #pragma unroll
           for (int c = 0; c < C; ++c) {
@@ -983,6 +984,7 @@ __global__ void __launch_bounds__(kLoopThreads, GF_CT_MIN_BLOCKS)
           }
         }
       }
+      if (A.enter && p < HW) A.enter[p] = act ? 0 : -1;
       warp_append(act, p, &ctr[kCtNF + 1], A.fr[0]);
     }
     __shared__ int s_n;
@@ -1378,15 +1380,36 @@ int coherence_fill_launch(const CoherenceFillArgs& a, const BallParams& P, const
   const size_t smem = ((sizeof(BallTables) + 15) & ~size_t(15)) + kMaxK * sizeof(double) +
                       std::max(tile_dbl, std::max(query_dbl, red_dbl)) * sizeof(double);
   if (smem > 200 * 1024) return set_error(GF_E_UNSUPPORTED, "rho window too wide for the fused loop");
-  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-    return set_error(GF_E_CUDA, cudaGetErrorString(cudaGetLastError()));
-  int dev = 0, sms = 0, per_sm = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kLoopThreads, smem) != cudaSuccess ||
-      per_sm < 1)
-    return set_error(GF_E_CUDA, "coherence loop does not fit on an SM");
-  const int grid = std::min(sms * per_sm, 4096);
+  // grid size per (device, kernel, smem), cached: the attribute and occupancy
+  // queries cost host microseconds per call otherwise
+  struct GridEntry {
+    int dev;
+    const void* fn;
+    size_t smem;
+    int grid;
+  };
+  static std::mutex mu;
+  static std::vector<GridEntry> cache;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return set_error(GF_E_CUDA, "no device");
+  int grid = 0;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    for (const GridEntry& g : cache)
+      if (g.dev == dev && g.fn == fn && g.smem == smem) grid = g.grid;
+  }
+  if (!grid) {
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+      return set_error(GF_E_CUDA, cudaGetErrorString(cudaGetLastError()));
+    int sms = 0, per_sm = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kLoopThreads, smem) != cudaSuccess ||
+        per_sm < 1)
+      return set_error(GF_E_CUDA, "coherence loop does not fit on an SM");
+    grid = std::min(sms * per_sm, 4096);
+    std::lock_guard<std::mutex> lock(mu);
+    cache.push_back({dev, fn, smem, grid});
+  }
   const bool trace = getenv("GF_CT_TRACE") != nullptr;
   if (trace) {
     cudaMalloc(&A.trace, 4097 * 16 * sizeof(unsigned long long));
