@@ -1380,8 +1380,8 @@ int coherence_fill_launch(const CoherenceFillArgs& a, const BallParams& P, const
   const size_t smem = ((sizeof(BallTables) + 15) & ~size_t(15)) + kMaxK * sizeof(double) +
                       std::max(tile_dbl, std::max(query_dbl, red_dbl)) * sizeof(double);
   if (smem > 200 * 1024) return set_error(GF_E_UNSUPPORTED, "rho window too wide for the fused loop");
-  // grid size per (device, kernel, smem), cached: the attribute and occupancy
-  // queries cost host microseconds per call otherwise
+  // grid size per (device, kernel, smem), cached: the occupancy query costs
+  // host microseconds per call otherwise
   struct GridEntry {
     int dev;
     const void* fn;
@@ -1398,9 +1398,10 @@ int coherence_fill_launch(const CoherenceFillArgs& a, const BallParams& P, const
     for (const GridEntry& g : cache)
       if (g.dev == dev && g.fn == fn && g.smem == smem) grid = g.grid;
   }
+  // the attribute is per function: set it for this launch's size every time
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return set_error(GF_E_CUDA, cudaGetErrorString(cudaGetLastError()));
   if (!grid) {
-    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-      return set_error(GF_E_CUDA, cudaGetErrorString(cudaGetLastError()));
     int sms = 0, per_sm = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kLoopThreads, smem) != cudaSuccess ||
