@@ -314,10 +314,13 @@ def _run_fill(image, labels, guide_vecs, params: FillParams, tracked: bool, orde
 
 
 def _run_coherence(image, labels, params, tracked, order_log, dev):
-    """Coherence-transport g source (engine.py:243-249): the shell-by-shell device
-    loop of coherence.run_coherence_fill.  Same return layout as _run_fill."""
+    """Coherence-transport g source (engine.py:243-249): the one-launch device loop
+    of coherence.run_coherence_fill.  Same return layout as _run_fill; host frames
+    travel like _run_fill's (chunked pinned upload mirrored back into the result
+    buffer, then only the changed pixels come down)."""
     import torch
 
+    from . import _staging
     from .coherence import run_coherence_fill
 
     t0 = time.perf_counter()
@@ -331,11 +334,33 @@ def _run_coherence(image, labels, params, tracked, order_log, dev):
     if bool(bad.any()):
         grid.validate_labels(labels)
         raise ValueError("label mask holds values outside {0, 128, 255}")
+    mirror = None
     if as_tensor:
-        d_img = image.to(dev, torch.float64).contiguous().clone()
+        timg = image.to(torch.float64).contiguous()
+        if (not timg.is_cuda and timg.is_pinned() and timg.numel() * 8 >= (1 << 20)
+                and _staging.mirror_supported(dev)):
+            d_img, mirror = _staging.upload_mirrored(timg, dev, True)
+        else:
+            d_img = timg.to(dev, non_blocking=timg.is_pinned())
     else:
-        d_img = torch.from_numpy(np.ascontiguousarray(image, dtype=np.float64)).to(dev)
-    u, r, enter, fillshell = run_coherence_fill(d_img, d_lab, params, tracked, order_log)
+        img = np.ascontiguousarray(image, dtype=np.float64)
+        if img.nbytes >= (1 << 20) and _staging.mirror_supported(dev):
+            d_img, mirror = _staging.upload_mirrored(img, dev, False)
+        else:
+            d_img = _staging.upload(img, dev, "img")
+    # the fill works in place: keep the input (the caller's tensor, or the
+    # delta's reference) intact
+    aliased = as_tensor and image.is_cuda and d_img.data_ptr() == image.data_ptr()
+    work = d_img.clone() if (mirror is not None or aliased) else d_img
+    try:
+        u, r, enter, fillshell = run_coherence_fill(work, d_lab, params, tracked, order_log)
+        if mirror is not None:
+            mirror.finish(d_img, u)
+            torch.cuda.current_stream().synchronize()
+    except BaseException:
+        if mirror is not None:
+            mirror.side.synchronize()
+        raise
     rep = FillReport()
     rep.iterations = r["iterations"]
     rep.filled = r["filled"]
@@ -343,7 +368,10 @@ def _run_coherence(image, labels, params, tracked, order_log, dev):
     rep.unfillable = r["unfillable"]
     rep.unfillable_count = r["unfillable_count"]
     rep.rows = r["rows"]
-    out = u.cpu() if as_tensor else u.cpu().numpy()
+    if mirror is not None:
+        out = mirror.result
+    else:
+        out = u.cpu() if as_tensor else u.cpu().numpy()
     fs = None
     if order_log or rep.unfillable:
         fs = fillshell.reshape(H, W).cpu().numpy()

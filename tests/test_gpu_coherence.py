@@ -214,3 +214,29 @@ def test_wide_sigma_window_runs_the_shell_loop():
     assert np.array_equal(maps["fillshell"], ref["fillshell"])
     assert [tuple(r) for r in rep.rows] == [tuple(r) for r in ref["rows"]]
     assert np.array_equal(u.view(np.int64), ref["u"].view(np.int64))
+
+
+def test_host_frames_take_the_mirrored_upload():
+    """A host frame above 1 MB goes up through the pinned stager mirrored into
+    the result buffer, and only the changed pixels come back: the result equals
+    the device-resident fill bit for bit, and the caller's array is untouched."""
+    import torch
+
+    from paper_1611_05319_b200.coherence import run_coherence_fill
+
+    rng = np.random.default_rng(77)
+    lab = cases.islands_labels(rng, 256, 320)
+    img = rng.uniform(size=lab.shape + (3,))
+    img0 = img.copy()
+    p = FillParams.coherence_transport()
+    u_host, rep = engine.coherence_transport_mode(img, lab)
+    assert np.array_equal(img, img0)
+    # engine.inpaint's frontier is the untracked rescan (engine.py:357-360)
+    u_dev, r, _, _ = run_coherence_fill(torch.from_numpy(img).cuda(), torch.from_numpy(lab).cuda(),
+                                        p, tracked=False)
+    assert np.array_equal(u_host.view(np.int64), u_dev.cpu().numpy().view(np.int64))
+    assert [tuple(x) for x in rep.rows] == r["rows"]
+    pinned = torch.from_numpy(img).pin_memory()
+    u_t, _ = engine.coherence_transport_mode(pinned, torch.from_numpy(lab))
+    assert torch.equal(u_t.view(torch.int64), u_dev.cpu().view(torch.int64))
+    assert torch.equal(pinned, torch.from_numpy(img0))
