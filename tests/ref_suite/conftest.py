@@ -5,9 +5,10 @@ unchanged apart from a header.  They import ``guidefill``; here that name is
 bound to ``paper_1611_05319_b200`` (package and submodules), so every test
 exercises the B200 engine through exactly the API a reference user calls --
 the drop-in claim of INTEGRATION.md, checked by the reference's own asserts.
-The CLI suite runs too (the reference's commands minus ``serve``); the project
-store and service suites are out of scope.
-All of them need the GPU (marked ``gpu``).
+The CLI suite runs too (the reference's commands minus ``serve``), and so do
+the project store and HTTP service suites (the callers of
+the fill path, ``project.py`` / ``service.py`` of this package routing to the
+GPU engine).  All of them need the GPU (marked ``gpu``).
 """
 
 import importlib
@@ -18,7 +19,7 @@ import pytest
 import paper_1611_05319_b200 as _pkg
 
 for _name in ("engine", "grid", "guide", "splines", "tracker", "harness", "limits", "fileio",
-              "cli"):
+              "cli", "project", "service"):
     sys.modules[f"guidefill.{_name}"] = importlib.import_module(f"paper_1611_05319_b200.{_name}")
 sys.modules["guidefill"] = _pkg
 
