@@ -71,7 +71,9 @@ extern "C" {
 
 /* FillParams (engine.py:33-60), minus the coherence-transport knobs */
 typedef struct gf_fill_params {
-  int32_t r;            /* ball radius epsilon in pixels, 1..GF_MAX_RADIUS */
+  int32_t r;            /* ball radius epsilon in pixels: 1..GF_MAX_RADIUS for
+                           gf_fill* / gf_coherence_fill, any r >= 1 for
+                           gf_sample_points (tables in device memory)      */
   double mu;            /* guidance strength, >= 0, +inf allowed           */
   double c;             /* smart-order confidence threshold                */
   double c2;            /* data-term threshold                             */

@@ -175,10 +175,15 @@ def run_coherence_fill(u, lab0, params, tracked=True, order_log=False):
     return u, rep, enter, fillshell
 
 
-def run_coherence_fill_shells(u, lab0, params, tracked=True, order_log=False):
-    """engine._fill_loop (engine.py:286-376) with g from the masked structure tensor,
-    one host-driven iteration per shell (the kernels of gf_coherence_directions,
-    gf_sample_points, gf_commit_shell and gf_frontier_candidates).
+def run_coherence_fill_shells(u, lab0, params, tracked=True, order_log=False, g_at=None):
+    """engine._fill_loop (engine.py:286-376) with one host-driven iteration per
+    shell (the kernels of gf_coherence_directions, gf_sample_points,
+    gf_commit_shell and gf_frontier_candidates).
+
+    g comes from the masked structure tensor unless ``g_at(u, lab, frontier,
+    pts)`` is given: it returns the frontier's (F, 2) float64 g and writes
+    the pixels' (x, y) into ``pts`` (run_field_fill_shells: a guide field or a
+    fixed g, for balls beyond the persistent kernels' tables).
 
     ``u``: (H, W, C) float64 CUDA tensor (consumed: filled in place); ``lab0``:
     (H, W) uint8 CUDA tensor (not modified).  Returns (u, report fields dict,
@@ -204,7 +209,12 @@ def run_coherence_fill_shells(u, lab0, params, tracked=True, order_log=False):
     fillshell = torch.full((H * W,), -1, dtype=torch.int32, device=dev)
     enter = torch.full((H * W,), -1, dtype=torch.int32, device=dev) if order_log else None
     lib = N.load()
-    ws = torch.empty(lib.gf_coherence_workspace_bytes(H, W, C), dtype=torch.uint8, device=dev)
+    if g_at is None:
+        ws = torch.empty(lib.gf_coherence_workspace_bytes(H, W, C), dtype=torch.uint8, device=dev)
+
+        def g_at(u_, lab_, fr, pts):
+            return coherence_directions_device(u_, lab_, fr, params.sigma, params.rho,
+                                               params.coherence_lambda, ws, pts)
     mark = torch.zeros(H * W, dtype=torch.uint8, device=dev)
     count = torch.zeros(1, dtype=torch.int32, device=dev)
     rep = dict(rows=[], iterations=0, filled=0, deadlock_fills=0, unfillable=False,
@@ -220,8 +230,7 @@ def run_coherence_fill_shells(u, lab0, params, tracked=True, order_log=False):
             cur = enter[frontier]
             enter[frontier] = torch.where(cur < 0, torch.full_like(cur, it), cur)
         pts = torch.empty((F, 2), dtype=torch.float64, device=dev)
-        g = coherence_directions_device(u, lab, frontier, params.sigma, params.rho,
-                                        params.coherence_lambda, ws, pts)
+        g = g_at(u, lab, frontier, pts)
         rw, tw, vals = sample_points_device(u, lab, pts, g, params)
         if params.order == "onion":
             mode = 0
@@ -285,3 +294,28 @@ def run_coherence_fill_shells(u, lab0, params, tracked=True, order_log=False):
         u.clamp_(hull[0], hull[1])
     rep["wall_time_s"] = time.perf_counter() - t0
     return u, rep, enter, fillshell
+
+
+def run_field_fill_shells(u, lab0, params, field=None, tracked=True, order_log=False):
+    """engine._fill_loop for a fixed or guide-field g (engine.py:234-242) through
+    the shell-by-shell loop -- the path of balls with r > GF_MAX_RADIUS, whose
+    sampler (gf_sample_points' large-ball kernel) keeps its tables in HBM.
+    ``field``: (H, W, 2) float64 CUDA guide field, or None."""
+    import torch
+
+    H, W, _ = u.shape
+    if params.g_source == "fixed":
+        gf = params.g_fixed or (0.0, 0.0)
+        const = torch.tensor([float(gf[0]), float(gf[1])], dtype=torch.float64, device=u.device)
+    flat = field.reshape(-1, 2) if field is not None else None
+
+    def g_at(u_, lab_, fr, pts):
+        pts[:, 0] = (fr % W).to(torch.float64)
+        pts[:, 1] = torch.div(fr, W, rounding_mode="floor").to(torch.float64)
+        if params.g_source == "fixed":
+            return const.expand(fr.numel(), 2).contiguous()
+        if flat is None:
+            return torch.zeros((fr.numel(), 2), dtype=torch.float64, device=u.device)
+        return flat[fr].contiguous()
+
+    return run_coherence_fill_shells(u, lab0, params, tracked, order_log, g_at=g_at)

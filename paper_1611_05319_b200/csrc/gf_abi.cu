@@ -89,6 +89,94 @@ static int check_frames(const gf_frames* f) {
   return GF_OK;
 }
 
+// numpy's pairwise summation tree for any K (gf_math.cuh's make_plan without
+// the leaf cap): leaves of <= 128 elements, split at n/2 rounded down to a
+// multiple of 8, as a postfix program
+static void plan_dyn(int lo, int n, std::vector<int>& leaf_lo, std::vector<int>& leaf_n,
+                     std::vector<int>& prog) {
+  if (n <= 128) {
+    prog.push_back((int)leaf_lo.size());
+    leaf_lo.push_back(lo);
+    leaf_n.push_back(n);
+    return;
+  }
+  int n2 = n / 2;
+  n2 -= n2 % 8;
+  plan_dyn(lo, n2, leaf_lo, leaf_n, prog);
+  plan_dyn(lo + n2, n - n2, leaf_lo, leaf_n, prog);
+  prog.push_back(-1);
+}
+
+// gf_sample_points for r > GF_MAX_RADIUS: the ball (grid.py:109-124 order,
+// engine.py:131-147 constants) in a temporary device buffer
+static int sample_points_big(int H, int W, int C, const double* image, const uint8_t* labels,
+                             int n, const double* points, const double* g,
+                             const gf_fill_params* p, double* rw, double* tw, double* vals,
+                             cudaStream_t s) {
+  if (!(p->mu >= 0.0)) return set_error(GF_E_INVALID, "mu must be >= 0 (inf allowed)");
+  if (p->neighborhood < 0 || p->neighborhood > 1) return set_error(GF_E_INVALID, "bad neighborhood");
+  if (n <= 0) return GF_OK;
+  const int r = p->r;
+  std::vector<double> dn, dm, w0;
+  std::vector<int> ni, mi;
+  for (int m = -r; m <= r; ++m)
+    for (int q = -r; q <= r; ++q) {
+      if (q * q + m * m > r * r || (q == 0 && m == 0)) continue;
+      dn.push_back((double)q);
+      dm.push_back((double)m);
+      w0.push_back(1.0 / hypot_np((double)q, (double)m));
+      ni.push_back(q);
+      mi.push_back(m);
+    }
+  const int K = (int)dn.size();
+  std::vector<int> leaf_lo, leaf_n, prog;
+  plan_dyn(0, K, leaf_lo, leaf_n, prog);
+  const size_t nd = 3 * (size_t)K, nint = 2 * (size_t)K + 2 * leaf_lo.size() + prog.size();
+  std::vector<unsigned char> host(nd * 8 + nint * 4);
+  double* hd = reinterpret_cast<double*>(host.data());
+  int* hi = reinterpret_cast<int*>(host.data() + nd * 8);
+  std::copy(dn.begin(), dn.end(), hd);
+  std::copy(dm.begin(), dm.end(), hd + K);
+  std::copy(w0.begin(), w0.end(), hd + 2 * K);
+  int* o = hi;
+  o = std::copy(ni.begin(), ni.end(), o);
+  o = std::copy(mi.begin(), mi.end(), o);
+  o = std::copy(leaf_lo.begin(), leaf_lo.end(), o);
+  o = std::copy(leaf_n.begin(), leaf_n.end(), o);
+  std::copy(prog.begin(), prog.end(), o);
+  void* dev = nullptr;
+  cudaError_t e = cudaMallocAsync(&dev, host.size(), s);
+  if (e != cudaSuccess) return set_error(GF_E_CUDA, cudaGetErrorString(e));
+  e = cudaMemcpyAsync(dev, host.data(), host.size(), cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);  // the host vector is freed on return
+  if (e != cudaSuccess) {
+    cudaFreeAsync(dev, s);
+    return set_error(GF_E_CUDA, cudaGetErrorString(e));
+  }
+  const double* dd = static_cast<const double*>(dev);
+  const int* di = reinterpret_cast<const int*>(static_cast<unsigned char*>(dev) + nd * 8);
+  BigBall B{};
+  B.K = K;
+  B.n = dd;
+  B.m = dd + K;
+  B.w0 = dd + 2 * K;
+  B.ni = di;
+  B.mi = di + K;
+  B.n_leaves = (int)leaf_lo.size();
+  B.leaf_lo = di + 2 * K;
+  B.leaf_n = B.leaf_lo + leaf_lo.size();
+  B.n_prog = (int)prog.size();
+  B.prog = B.leaf_n + leaf_n.size();
+  B.rotated = p->neighborhood == GF_BALL_ROTATED;
+  B.periodic = p->periodic_x != 0;
+  B.mu_inf = isinf(p->mu) ? 1 : 0;
+  B.coef = (-(p->mu * p->mu)) / (2.0 * (double)(r * r));
+  B.tol_inf = 1e-12 * std::max(1.0, (double)(r * r));
+  const int rc = sample_points_big_launch(H, W, C, image, labels, n, points, g, B, rw, tw, vals, s);
+  cudaFreeAsync(dev, s);
+  return rc;
+}
+
 }  // namespace gf
 
 using namespace gf;
@@ -197,6 +285,9 @@ int gf_sample_points(int32_t height, int32_t width, int32_t channels, const doub
                      void* stream) {
   if (height <= 0 || width <= 0 || channels < 1 || channels > 4)
     return set_error(GF_E_INVALID, "bad geometry");
+  if (params && params->r > GF_MAX_RADIUS)
+    return sample_points_big(height, width, channels, image, labels, n, points, g, params, rw, tw,
+                             vals, static_cast<cudaStream_t>(stream));
   BallParams P;
   BallTables* T = new BallTables;
   int rc = build_ball(params, P, *T);

@@ -89,6 +89,25 @@ int fill_launch(const gf_frames* fr, const gf_fill_params* prm, const gf_fill_ou
                 const BallParams& P, const BallTables& host_tab);
 
 // gf_points.cu
+// a ball beyond the kernels' fixed tables (r > GF_MAX_RADIUS): device arrays
+struct BigBall {
+  int K;
+  const double* n;
+  const double* m;
+  const double* w0;
+  const int* ni;
+  const int* mi;
+  int n_leaves;
+  const int* leaf_lo;  // numpy pairwise plan: leaves (start, length) and the
+  const int* leaf_n;   // postfix program (>= 0 push leaf, -1 add the top two)
+  int n_prog;
+  const int* prog;
+  int rotated, periodic, mu_inf;
+  double coef, tol_inf;
+};
+int sample_points_big_launch(int H, int W, int C, const double* image, const uint8_t* labels,
+                             int n, const double* points, const double* g, const BigBall& B,
+                             double* rw, double* tw, double* vals, cudaStream_t stream);
 int sample_points_launch(int H, int W, int C, const double* image, const uint8_t* labels, int n,
                          const double* points, const double* g, const BallParams& P,
                          const BallTables& tab, double* rw, double* tw, double* vals,

@@ -223,6 +223,9 @@ def _run_fill(image, labels, guide_vecs, params: FillParams, tracked: bool, orde
     dev = N.require_cuda()
     if params.g_source == "modified_structure_tensor":
         return _run_coherence(image, labels, params, tracked, order_log, dev)
+    if params.r > N.GF_MAX_RADIUS:
+        return _run_large_ball(image, labels, guide_vecs, params, tracked, order_log, dev,
+                               splines, eta)
     from . import _staging
     from ._device import SegmentSet, fill_device
 
@@ -313,16 +316,43 @@ def _run_fill(image, labels, guide_vecs, params: FillParams, tracked: bool, orde
     return (u_t if as_tensor else u), rep, dict(enter=enter, fillshell=fillshell)
 
 
-def _run_coherence(image, labels, params, tracked, order_log, dev):
+def _run_large_ball(image, labels, guide_vecs, params, tracked, order_log, dev, splines, eta):
+    """Balls with r > GF_MAX_RADIUS (the reference takes any r >= 1,
+    engine.py:51-52): the shell-by-shell device loop with the large-ball
+    sampler (coherence.run_field_fill_shells).  Same return layout as _run_fill."""
+    import torch
+
+    from ._device import SegmentSet, guide_field_device
+    from .coherence import run_field_fill_shells
+
+    def runner(work, d_lab):
+        field = None
+        if params.g_source == "guide_field":
+            if splines is not None:
+                segs = SegmentSet.cached(list(splines), dev) if len(splines) else None
+                if segs is not None:
+                    field = guide_field_device(d_lab, segs, eta)
+            elif guide_vecs is not None:
+                field = torch.from_numpy(np.ascontiguousarray(guide_vecs, dtype=np.float64)).to(dev)
+        return run_field_fill_shells(work, d_lab, params, field, tracked, order_log)
+
+    return _run_coherence(image, labels, params, tracked, order_log, dev, runner)
+
+
+def _run_coherence(image, labels, params, tracked, order_log, dev, runner=None):
     """Coherence-transport g source (engine.py:243-249): the one-launch device loop
-    of coherence.run_coherence_fill.  Same return layout as _run_fill; host frames
-    travel like _run_fill's (chunked pinned upload mirrored back into the result
-    buffer, then only the changed pixels come down)."""
+    of coherence.run_coherence_fill (or ``runner(work, d_lab)``, the large-ball
+    loop).  Same return layout as _run_fill; host frames travel like _run_fill's
+    (chunked pinned upload mirrored back into the result buffer, then only the
+    changed pixels come down)."""
     import torch
 
     from . import _staging
     from .coherence import run_coherence_fill
 
+    if runner is None:
+        def runner(work, d_lab):
+            return run_coherence_fill(work, d_lab, params, tracked, order_log)
     t0 = time.perf_counter()
     as_tensor = isinstance(image, torch.Tensor)
     if isinstance(labels, torch.Tensor):
@@ -353,7 +383,7 @@ def _run_coherence(image, labels, params, tracked, order_log, dev):
     aliased = as_tensor and image.is_cuda and d_img.data_ptr() == image.data_ptr()
     work = d_img.clone() if (mirror is not None or aliased) else d_img
     try:
-        u, r, enter, fillshell = run_coherence_fill(work, d_lab, params, tracked, order_log)
+        u, r, enter, fillshell = runner(work, d_lab)
         if mirror is not None:
             mirror.finish(d_img, u)
             torch.cuda.current_stream().synchronize()
