@@ -9,6 +9,7 @@ bit-exact (numpy's arctan2 / tanh / sin / cos restated in gf_npmath.cuh; the
 reference's own cropping test allows 1e-12, test_guide.py:286-300).
 """
 
+import math
 import os
 
 import numpy as np
@@ -240,3 +241,38 @@ def test_host_frames_take_the_mirrored_upload():
     u_t, _ = engine.coherence_transport_mode(pinned, torch.from_numpy(lab))
     assert torch.equal(u_t.view(torch.int64), u_dev.cpu().view(torch.int64))
     assert torch.equal(pinned, torch.from_numpy(img0))
+
+
+@pytest.mark.parametrize("order,tracked", [("smart", True), ("smart_with_data_term", False)])
+def test_persistent_loop_long_smart_fill(order, tracked):
+    """Smart order on a noise scene (tens of shells) and on a half-plane under
+    25-degree stripes, where g follows the stripes and the fill runs as a
+    deadlock chain (one guarded pixel per shell, the persistent loop's D
+    phase): order, rows and values identical to the oracle."""
+    rng = np.random.default_rng(2024 if tracked else 2025)
+    lab = np.zeros((128, 128), dtype=np.uint8)
+    lab[30:100, 20:110] = 255
+    lab[60:66, 50:56] = 128
+    img = rng.uniform(size=(128, 128, 2))
+    img[lab == 255] = 0.0
+    H = W = 64
+    jj, ii = np.mgrid[0:H, 0:W]
+    th = math.radians(25.0)
+    stripes = 0.5 + 0.4 * np.sin(2 * math.pi * (-ii * math.sin(th) + jj * math.cos(th)) / 9.0)
+    lab2 = np.zeros((H, W), dtype=np.uint8)
+    lab2[H // 2:, :] = 255
+    img2 = np.repeat(stripes[..., None], 3, axis=2)
+    img2[lab2 == 255] = 0.0
+    p = FillParams(r=3, mu=50.0, order=order, c2=0.4, neighborhood="rotated_ball",
+                   g_source="modified_structure_tensor")
+    chains = 0
+    for im, lb in ((img, lab), (img2, lab2)):
+        u, rep, maps = engine._run_fill(im, lb, None, p, tracked=tracked, order_log=True)
+        ref = orc.fill(im, lb, None, orc.Params.of(p), tracked=tracked)
+        assert rep.deadlock_fills == ref["deadlock_fills"]
+        chains += rep.deadlock_fills
+        assert np.array_equal(maps["fillshell"], ref["fillshell"])
+        assert np.array_equal(maps["enter"], ref["enter"])
+        assert [tuple(r) for r in rep.rows] == [tuple(r) for r in ref["rows"]]
+        assert np.array_equal(u.view(np.int64), ref["u"].view(np.int64))
+    assert chains > 0
