@@ -822,6 +822,18 @@ __device__ __forceinline__ void ct_queue_tiles(const CtLoopArgs& A, int bank, bo
     if (fresh[e]) A.tlist[base++] = tt[e];
 }
 
+// ct_queue_tiles for one thread (the guarded pixel)
+__device__ __forceinline__ void ct_queue_tiles_one(const CtLoopArgs& A, int bank, int j, int i,
+                                                   int d) {
+  const int ty0 = max(0, j - d) / kLTH, ty1 = min(A.H - 1, j + d) / kLTH;
+  const int tx0 = max(0, i - d) / kLTW, tx1 = min(A.W - 1, i + d) / kLTW;
+  for (int ty = ty0; ty <= ty1; ++ty)
+    for (int tx = tx0; tx <= tx1; ++tx) {
+      const int t = ty * A.tiles_x + tx;
+      if (atomicExch(&A.tflag[t], 1u) == 0u) A.tlist[atomicAdd(&A.ctr[kCtTiles + bank], 1)] = t;
+    }
+}
+
 // recompute the listed tiles; blocks take the next entry as they free up
 template <int C>
 __device__ __forceinline__ void ct_run_tiles(const CtLoopArgs& A, int bank, double* sm) {
@@ -1084,13 +1096,17 @@ __global__ void __launch_bounds__(kLoopThreads, GF_CT_MIN_BLOCKS)
       ctr[kCtGrab + o] = 0;
     }
 
-    // ---- C: ready predicate (engine.py:317-330) and fill = ready & rw > 0
+    // ---- C: ready predicate (engine.py:317-330), fill = ready & rw > 0, and
+    // the commit of the filled pixels (engine.py:350-356) with their dirty
+    // tiles queued: no phase of this shell reads u or labels any more, and a
+    // shell with nothing ready has written nothing (the guard below commits)
     if (data_live && block_ld(&ctr[kCtAnyG + b]) == 0) data_live = false;
     {
       const int mode = A.order == 0 ? 0 : (data_live ? 2 : 1);
-      for (int k0 = blockIdx.x * blockDim.x; k0 < F; k0 += nthreads) {
-        const int k = k0 + threadIdx.x;
+      for (int k0 = gwarp * 32; k0 < F; k0 += nwarps * 32) {
+        const int k = k0 + lane;
         bool f = false;
+        int j = 0, i = 0;
         if (k < F) {
           const double rw = A.erw[k];
           const double conf = rw / A.etw[k];
@@ -1099,11 +1115,22 @@ __global__ void __launch_bounds__(kLoopThreads, GF_CT_MIN_BLOCKS)
           else if (mode == 2) ready = hypot_np(A.eg[2 * k], A.eg[2 * k + 1]) > A.c2 && conf > A.c;
           f = ready && rw > 0.0;
           A.efill[k] = f ? 1 : 0;
+          if (f) {
+            const int p = fr[k];
+#pragma unroll
+            for (int c = 0; c < C; ++c) A.u[(int64_t)p * C + c] = A.evals[(int64_t)k * C + c];
+            A.lab[p] = 0;
+            A.fillshell[p] = s;
+            j = p / W;
+            i = p - j * W;
+          }
         }
+        ct_queue_tiles(A, b, f, j, i, dd);
         const unsigned bal = __ballot_sync(0xffffffffu, f);
         if (lane == 0 && bal) atomicAdd(&ctr[kCtFill + b], __popc(bal));
       }
     }
+    ct_trace_work(A, s, 9, 11);
     grid.sync();
     ct_trace(A, s, 1);
     int n = block_ld(&ctr[kCtFill + b]);
@@ -1182,8 +1209,15 @@ __global__ void __launch_bounds__(kLoopThreads, GF_CT_MIN_BLOCKS)
           }
         }
         if (ok) {
+          // the guarded pixel's commit
+          const int p = fr[k0];
+#pragma unroll
+          for (int c = 0; c < C; ++c) A.u[(int64_t)p * C + c] = A.evals[(int64_t)k0 * C + c];
+          A.lab[p] = 0;
+          A.fillshell[p] = s;
           A.efill[k0] = 1;
           ctr[kCtDeadlocks] += 1;
+          ct_queue_tiles_one(A, b, p / W, p % W, dd);
         }
       }
       grid.sync();
@@ -1191,25 +1225,6 @@ __global__ void __launch_bounds__(kLoopThreads, GF_CT_MIN_BLOCKS)
       if (block_ld(&ctr[kCtDone]) == 2) break;
       n = 1;
     }
-
-    // ---- E: commit (engine.py:350-356) and queue the dirty tiles
-    for (int k0 = gwarp * 32; k0 < F; k0 += nwarps * 32) {
-      const int k = k0 + lane;
-      const bool f = k < F && A.efill[k];
-      int j = 0, i = 0;
-      if (f) {
-        const int p = fr[k];
-#pragma unroll
-        for (int c = 0; c < C; ++c) A.u[(int64_t)p * C + c] = A.evals[(int64_t)k * C + c];
-        A.lab[p] = 0;
-        A.fillshell[p] = s;
-        j = p / W;
-        i = p - j * W;
-      }
-      ct_queue_tiles(A, b, f, j, i, dd);
-    }
-    ct_trace_work(A, s, 9, 11);
-    grid.sync();
     ct_trace(A, s, 3);
     rem -= n;
 
