@@ -976,28 +976,41 @@ __global__ void __launch_bounds__(kLoopThreads, GF_CT_MIN_BLOCKS)
   {
     int n_inp = 0;
     double lo = INFINITY, hi = -INFINITY;
-    for (int p0 = gwarp * 32; p0 < HW; p0 += nwarps * 32) {
-      const int p = p0 + lane;
-      bool act = false;
-      if (p < HW) {
-        const uint8_t l = A.lab[p];
-        A.fillshell[p] = -1;
-        if (l == 255) {
-          ++n_inp;
-          const int j = p / W, i = p - j * W;
-          ct_mark_tiles(A, j, i, dq);
-          act = ct_active(A.lab, H, W, A.periodic, j, i);
-        } else if (l == 0) {
+    // 4 x 32 consecutive pixels per warp step: the labels and the colours of
+    // all four rounds are loaded before any is used
+    constexpr int kScan = 4;
+    for (int p0 = gwarp * 32 * kScan; p0 < HW; p0 += nwarps * 32 * kScan) {
+      uint8_t l[kScan];
+      double v[kScan][C];
 #pragma unroll
-          for (int c = 0; c < C; ++c) {
-            const double v = A.u[(int64_t)p * C + c];
-            lo = fmin(lo, v);
-            hi = fmax(hi, v);
-          }
-        }
+      for (int q = 0; q < kScan; ++q) {
+        const int p = p0 + 32 * q + lane;
+        l[q] = p < HW ? A.lab[p] : 128;
+#pragma unroll
+        for (int c = 0; c < C; ++c) v[q][c] = p < HW ? A.u[(int64_t)p * C + c] : 0.0;
       }
-      if (A.enter && p < HW) A.enter[p] = act ? 0 : -1;
-      warp_append(act, p, &ctr[kCtNF + 1], A.fr[0]);
+#pragma unroll
+      for (int q = 0; q < kScan; ++q) {
+        const int p = p0 + 32 * q + lane;
+        bool act = false;
+        if (p < HW) {
+          A.fillshell[p] = -1;
+          if (l[q] == 255) {
+            ++n_inp;
+            const int j = p / W, i = p - j * W;
+            ct_mark_tiles(A, j, i, dq);
+            act = ct_active(A.lab, H, W, A.periodic, j, i);
+          } else if (l[q] == 0) {
+#pragma unroll
+            for (int c = 0; c < C; ++c) {
+              lo = fmin(lo, v[q][c]);
+              hi = fmax(hi, v[q][c]);
+            }
+          }
+          if (A.enter) A.enter[p] = act ? 0 : -1;
+        }
+        warp_append(act, p, &ctr[kCtNF + 1], A.fr[0]);
+      }
     }
     __shared__ int s_n;
     __shared__ unsigned long long s_lo, s_hi;
