@@ -59,25 +59,34 @@ def _active(lab, periodic_x):
 
 
 def _neighbor_mean(u, lab, p, H, W, periodic_x):
-    """engine._neighbor_mean (engine.py:252-267): readable 8-neighbours, fixed order."""
+    """engine._neighbor_mean (engine.py:252-267): readable 8-neighbours, fixed order.
+
+    The 3x3 block comes to the host and the mean is numpy's (sequential sum,
+    then a true division: torch divides a CUDA tensor by a Python scalar as a
+    multiplication by its reciprocal, one ulp off)."""
     import torch
 
     C = u.shape[2]
-    flat_u = u.reshape(-1, C)
-    flat_l = lab.reshape(-1)
-    acc = torch.zeros(C, dtype=torch.float64, device=u.device)
-    n = 0
     j, i = divmod(p, W)
+    rows = [jj for jj in (j - 1, j, j + 1) if 0 <= jj < H]
+    cols = [(i + di) % W if periodic_x else i + di for di in (-1, 0, 1)]
+    keep = [c for c in cols if 0 <= c < W]
+    idx = torch.tensor([jj * W + c for jj in rows for c in keep], device=u.device)
+    vals = u.reshape(-1, C)[idx].cpu().numpy()
+    labs = lab.reshape(-1)[idx].cpu().numpy()
+    pos = {int(q): k for k, q in enumerate(idx.tolist())}
+    acc = np.zeros(C)
+    n = 0
     for di, dj in NEIGHBOR_OFFSETS:
         ii, jj = i + di, j + dj
         if periodic_x:
             ii %= W
-        if 0 <= ii < W and 0 <= jj < H and int(flat_l[jj * W + ii]) == READABLE:
-            acc += flat_u[jj * W + ii]
+        if 0 <= ii < W and 0 <= jj < H and labs[pos[jj * W + ii]] == READABLE:
+            acc += vals[pos[jj * W + ii]]
             n += 1
     if n == 0:
         return None
-    return acc / n
+    return torch.from_numpy(acc / n).to(u.device)
 
 
 _PINNED = {}

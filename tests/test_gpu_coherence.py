@@ -276,3 +276,37 @@ def test_persistent_loop_long_smart_fill(order, tracked):
         assert [tuple(r) for r in rep.rows] == [tuple(r) for r in ref["rows"]]
         assert np.array_equal(u.view(np.int64), ref["u"].view(np.int64))
     assert chains > 0
+
+
+def test_persistent_loop_random_sweep():
+    """40 random scenes and parameter sets, each filled twice by the persistent
+    loop and once by the shell loop: all three bitwise identical (a race in the
+    loop's counters, tile queue or frontier appends would break the first or
+    the second equality)."""
+    import torch
+
+    from paper_1611_05319_b200.coherence import run_coherence_fill, run_coherence_fill_shells
+
+    rng = np.random.default_rng(31337)
+    for it in range(40):
+        lab = cases.islands_labels(rng, 24, 90)
+        H, W = lab.shape
+        C = int(rng.integers(1, 5))
+        img = rng.uniform(size=(H, W, C))
+        img[lab == 255] = 0.0
+        order = ["onion", "smart", "smart_with_data_term"][it % 3]
+        p = FillParams(r=int(rng.integers(1, 7)), mu=float(rng.choice([0.0, 10.0, 50.0, math.inf])),
+                       order=order, c2=float(rng.uniform(0.1, 0.8)),
+                       neighborhood=["rotated_ball", "axis_ball"][it % 2],
+                       g_source="modified_structure_tensor", periodic_x=bool(it % 5 == 0),
+                       sigma=float(rng.choice([1.0, 2.0, 2.5])), rho=float(rng.choice([2.0, 4.0])))
+        tracked = bool(it % 4 != 3)
+        d_img = torch.from_numpy(img).cuda()
+        d_lab = torch.from_numpy(lab).cuda()
+        outs = [run_coherence_fill(d_img.clone(), d_lab, p, tracked, True) for _ in range(2)]
+        outs.append(run_coherence_fill_shells(d_img.clone(), d_lab, p, tracked, True))
+        (u0, r0, e0, f0) = outs[0]
+        for u, r, e, f in outs[1:]:
+            assert torch.equal(f, f0) and torch.equal(e, e0), (it, p)
+            assert [tuple(int(x) for x in row) for row in r["rows"]] == r0["rows"], (it, p)
+            assert torch.equal(u.view(torch.int64), u0.view(torch.int64)), (it, p)
