@@ -311,6 +311,26 @@ __device__ __forceinline__ void eval_rot_warp(const BallParams& P, const BallTab
     rw = rw + __shfl_sync(0xffffffffu, wr[i >> 5], i & 31);
     tw = tw + __shfl_sync(0xffffffffu, w[i >> 5], i & 31);
   }
+  if (e_max < -1000 && e_max > -2000) {
+    // every readable weight is near the bottom of the fp64 range (high mu,
+    // tiny r: Eq. 3.2 weights of ~1e-320): the scaling above would leave
+    // the double range, and numpy's own products wr * v round to multiples
+    // of 2^-1074 there.  Form those products in fp64 as numpy does; sums of
+    // such tiny values are exact in any order.
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      double part = 0.0;
+#pragma unroll
+      for (int s = 0; s < KPW; ++s)
+        if (wr[s] != 0.0) part += wr[s] * (double)sv[s][c];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+      out.v[c] = (c < 3 || src.c3) ? part / rw : 0.0;
+    }
+    out.rw = rw;
+    out.tw = tw;
+    return;
+  }
   const double inv = (rw != 0.0) ? 1.0 / rw : 0.0;
   const double up = scalbn(1.0, e_use);
 #pragma unroll
