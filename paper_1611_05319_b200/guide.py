@@ -20,6 +20,8 @@ and the Spline records are host work, as in the reference.
 
 from __future__ import annotations
 
+import math
+
 import numpy as np
 
 from .grid import INPAINT, READABLE
@@ -266,7 +268,12 @@ def _splines_from_seeds(seeds, image, labels, sigma, rho, lam, ids):
         direction = v if sign > 0 else -v
         start = np.array([float(i), float(j)])
         end = start + t_end * direction
-        coherence = float(eig[k, 2])
+        # make_spline's coherence is Python's math.tanh of the eigenvalue gap
+        # (guide.py:224-225), not numpy's: the gap from the device's tensor
+        # (a, b, c) with eigen_2x2's numpy ops, then glibc tanh on the host
+        a, b, c = float(eig[k, 3]), float(eig[k, 4]), float(eig[k, 5])
+        lo, hi = eigen_2x2(a, b, c)[:2]
+        coherence = math.tanh((float(hi) - float(lo)) / lam)
         out.append(Spline(id=ids(k), source="auto",
                           direction=(coherence * direction[0], coherence * direction[1]),
                           points=np.stack([start, end])))
