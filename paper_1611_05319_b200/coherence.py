@@ -114,8 +114,12 @@ def _scratch(dev, H, W, C, cap):
     import torch
 
     key = (str(dev), torch.cuda.current_stream(dev).cuda_stream, H, W, C)
-    hit = _SCRATCH.get(key)
-    if hit is None:
+    hit = _SCRATCH.pop(key, None)
+    if hit is not None:
+        _SCRATCH[key] = hit  # most recent last
+    else:
+        while len(_SCRATCH) >= 4:  # a few hundred MB each at 1080p: keep the last four
+            _SCRATCH.pop(next(iter(_SCRATCH)))
         lib = N.load()
         ws_bytes = lib.gf_coherence_fill_workspace_bytes(H, W, C, cap)
         hit = _SCRATCH[key] = (torch.empty((cap + 1, 5), dtype=torch.int64, device=dev),
