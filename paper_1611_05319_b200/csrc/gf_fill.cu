@@ -1415,8 +1415,14 @@ __device__ __forceinline__ bool decide_and_write(const FillArgs& A, int f, int j
     ready = (hypot_np(gx, gy) > A.c2) && (conf > A.c);
   }
   const bool fill = ready && (r.rw > 0.0);
-  // the guard only reads confidences of frames where no item filled
-  if (!fill) A.conf[(size_t)f * A.cap + j] = conf;
+  // the guard only reads confidences of frames where no item filled, and
+  // fills its pick with the value sampled here (no second evaluation)
+  if (!fill) {
+    A.conf[(size_t)f * A.cap + j] = conf;
+    if (r.rw > 0.0)
+      A.gval[(size_t)f * A.HW + p] =
+          make_float4((float)r.v[0], (float)r.v[1], (float)r.v[2], (float)r.v[3]);
+  }
   if (fill) {
     float4 o;
     o.x = (float)r.v[0];
@@ -1647,24 +1653,24 @@ template <int R, bool kTracked>
 __device__ __forceinline__ void guard_fill_frame(const FillArgs& A, const BallParams& P, Smem& S,
                                                  int f_in, bool fvalid, int k, int cur, int nxt,
                                                  uint32_t* nxt_list) {
-  constexpr int NL = R > 0 ? 1 : kMaxLeaves;
   const int lane = threadIdx.x & 31;
-  const int glane = lane & (kGroup - 1);
         const int f = f_in;
-        const bool valid = fvalid && lane < kGroup;
         const int p = fvalid ? A.best_p[f] : 0;
         const int fs = fvalid ? f : 0;
-        double gx = 0.0, gy = 0.0;
-        if (fvalid) frame_guide(A, f, p, gx, gy);
         float4* fw = A.work + (size_t)fs * A.HW;
         WorkSource src{fw, A.c3 ? A.c3 + (size_t)fs * A.HW : nullptr, A.H, A.W, A.C, k};
-        SampleResult r;
-        // the generic evaluator: compact code on this rarely taken path keeps
-        // the fill phase's register allocation intact
-        eval_item<NL, 0>(P, S.tab, src, glane, valid, (double)(p % A.W), (double)(p / A.W), true,
-                         gx, gy, r);
-        double v[4] = {r.v[0], r.v[1], r.v[2], r.v[3]};
-        bool ok = r.rw > 0.0;
+        // rw > 0 <=> the best confidence rw / tw is > 0 (NaN: tw = rw = 0);
+        // then the value this shell's fill phase sampled for p
+        const unsigned long long bk = fvalid ? A.best_key[f] : 0ULL;
+        bool ok = bk != ~0ULL && bk != 0ULL;
+        double v[4] = {0.0, 0.0, 0.0, 0.0};
+        if (ok) {
+          const float4 gv = A.gval[(size_t)fs * A.HW + p];
+          v[0] = gv.x;
+          v[1] = gv.y;
+          v[2] = gv.z;
+          v[3] = gv.w;
+        }
         if (fvalid && lane == 0 && !ok) {
           // mean of readable 8-neighbours, engine.py:252-267
           double acc[4] = {0.0, 0.0, 0.0, 0.0};
@@ -1799,6 +1805,7 @@ __device__ __forceinline__ void guard_argmax(const FillArgs& A, Smem& S, int f, 
       }
     }
     A.best_p[f] = pix;
+    A.best_key[f] = key;
   }
 }
 
@@ -2274,7 +2281,7 @@ static void div_magic(int d, unsigned& mul, int& shr) {
 }
 
 struct Layout {
-  size_t work, c3, list0, list1, conf, gbuf, bys, ints, u64, total;
+  size_t work, c3, list0, list1, conf, gval, gbuf, bys, ints, u64, total;
 };
 
 static int tiles_of(int H, int W) {
@@ -2292,6 +2299,7 @@ static Layout layout_for(int nF, int H, int W, int C, bool need_g) {
   L.list0 = off; off = align_up(off + n * sizeof(uint32_t));
   L.list1 = off; off = align_up(off + n * sizeof(uint32_t));
   L.conf = off; off = align_up(off + n * sizeof(double));
+  L.gval = off; off = align_up(off + n * sizeof(float4));
   L.bys = off; off = align_up(off + (size_t)nF * tiles_of(H, W) * 2 * sizeof(unsigned long long));
   L.ints = off; off = align_up(off + (size_t)nF * kIntsPerFrame * sizeof(int));
   L.u64 = off; off = align_up(off + (size_t)nF * 6 * sizeof(unsigned long long));
@@ -2397,6 +2405,7 @@ int fill_launch(const gf_frames* fr, const gf_fill_params* prm, const gf_fill_ou
   A.list0 = reinterpret_cast<uint32_t*>(base + L.list0);
   A.list1 = reinterpret_cast<uint32_t*>(base + L.list1);
   A.conf = reinterpret_cast<double*>(base + L.conf);
+  A.gval = reinterpret_cast<float4*>(base + L.gval);
   int* ints = reinterpret_cast<int*>(base + L.ints);
   A.cnt = ints;              ints += 4 * nF;
   A.cntR = ints;             ints += 4 * nF;

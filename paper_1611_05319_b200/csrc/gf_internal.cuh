@@ -30,6 +30,7 @@ struct FillArgs {
   uint32_t* list0;
   uint32_t* list1;
   double* conf;
+  float4* gval;    // [nF][HW] sampled value of an unfilled item with rw > 0 (the guard's fill)
   int* cnt;        // [4][nF] frontier list front part (lattice entries)
   int* cntR;       // [4][nF] frontier list back part (rotated-ball entries)
   int* fills;      // [4][nF] pixels filled in the shell
