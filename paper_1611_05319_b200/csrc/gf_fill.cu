@@ -136,6 +136,34 @@ __device__ __forceinline__ void timeline_mark(const FillArgs& A, int stage, bool
   atomicMax(&row[2 * stage + (start ? 0 : 1)], start ? ~t : t);
 }
 
+#ifdef GF_PREP_PROF
+// experiment builds only: per-block stage stamps of the prep pass
+// [0] start, [1..6] stages, [7] smid | flags << 32
+__device__ unsigned long long g_prep_prof[16384][12];
+// k_shells: first block entry, first / last return from the PDL wait
+__device__ unsigned long long g_shell_prof[3];
+extern "C" int gf_prep_prof_read(void* host, int n) {
+  if (n == -2) return (int)cudaMemcpyToSymbol(g_shell_prof, host, 24);  // reset
+  if (n < 0) return (int)cudaMemcpyFromSymbol(host, g_shell_prof, 24);
+  return (int)cudaMemcpyFromSymbol(host, g_prep_prof, (size_t)n * 96);
+}
+#define PREP_PROF_T0 \
+  if (threadIdx.x == 0 && tile < 16384) g_prep_prof[tile][0] = gtimer0()
+#define PREP_STAGE(k) \
+  if (threadIdx.x == 0 && tile < 16384) g_prep_prof[tile][k] = gtimer0()
+#define PREP_PROF(flags)                                                      \
+  if (threadIdx.x == 0 && tile < 16384) {                                     \
+    unsigned sm_;                                                             \
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm_));                          \
+    g_prep_prof[tile][10] = gtimer0();                                        \
+    g_prep_prof[tile][11] = sm_ | ((unsigned long long)(flags) << 32);         \
+  }
+#else
+#define PREP_PROF_T0
+#define PREP_STAGE(k)
+#define PREP_PROF(flags)
+#endif
+
 // Programmatic dependent launch: each k_prep block signals at its start, so
 // the shell kernel's launch and block set-up overlap the last prep wave; the
 // shell kernel waits for k_prep's completion (and memory) before its first
@@ -199,6 +227,9 @@ __global__ void __launch_bounds__(kThreads, GF_PREP_MIN_BLOCKS) k_prep(const __g
   __shared__ unsigned long long s_rrow64[kTileExt];
   __shared__ int s_cand[kMaxCand];
   __shared__ int s_ncand;
+  __shared__ uint16_t s_inp[kTile * kTile];
+  __shared__ unsigned int s_rotb[kTile];
+  __shared__ int s_ninp, s_anyg;
   __shared__ int s_cnt[kThreads / 32];
   __shared__ int s_wl[kThreads / 32], s_wr[kThreads / 32];
   __shared__ int s_bL, s_bR;
@@ -216,7 +247,12 @@ __global__ void __launch_bounds__(kThreads, GF_PREP_MIN_BLOCKS) k_prep(const __g
   //    tiles read 32-bit words, two rows per warp instruction, and pack each
   //    word's 4 byte tests into a nibble (one multiply); the OR of 16 lanes'
   //    nibbles is one redux.  Edge tiles fall back to byte loads + ballots.
-  if (threadIdx.x == 0) s_ncand = 0;
+  if (threadIdx.x == 0) {
+    s_ncand = 0;
+    s_ninp = 0;
+    s_anyg = 0;
+  }
+  if (threadIdx.x < kTile) s_rotb[threadIdx.x] = 0u;
   bool any_inp = false;
   const int sh = (tx0 - R) & 3;       // ext column 0 within its aligned word
   const int ws = tx0 - R - sh;        // first word's global column
@@ -461,11 +497,14 @@ __global__ void __launch_bounds__(kThreads, GF_PREP_MIN_BLOCKS) k_prep(const __g
   }
   __syncthreads();
 
-  // 3. four consecutive pixels per thread: row ry, columns c0 .. c0+3
+  // 3. four consecutive pixels per thread: row ry, columns c0 .. c0+3.
+  //    The cheap per-pixel work (stamps, enter map, activity) runs here; the
+  //    Inpaint pixels are queued in shared memory for step 4, so the guide
+  //    evaluation (raster, exp, hypot in fp64) runs one pixel per thread over
+  //    a dense list instead of four serial, divergent pixels per thread.
   const unsigned int vmask = s_vrow[ry];
   int n_inp = 0;
-  bool anyg = false;
-  uint32_t ent[4];
+  unsigned act4 = 0;  // bit u: own pixel u is an active Inpaint pixel
 #pragma unroll
   for (int u = 0; u < 4; ++u) {
     const int c = c0 + u;
@@ -474,7 +513,8 @@ __global__ void __launch_bounds__(kThreads, GF_PREP_MIN_BLOCKS) k_prep(const __g
     const int p = gy * A.W + gx;
     const uint8_t l = (uint8_t)(own4 >> (8 * u));
     const bool near = (vmask >> c) & 1u;
-    bool active = false, rot = false;
+    bool active = false;
+    const bool inp = in && l == 255;
     if (in) {
       if (l == 0) {
         if (near) {
@@ -484,73 +524,111 @@ __global__ void __launch_bounds__(kThreads, GF_PREP_MIN_BLOCKS) k_prep(const __g
           work[p] = make_float4(cv[0], cv[1], cv[2], __int_as_float(kStampReadable));
           if (C > 3) A.c3[(size_t)f * A.HW + p] = cv[3];
         }
-      } else if (l == 255) {
+      } else if (inp) {
         ++n_inp;
         // a Readable 8-neighbour (the pixel itself is not Readable): the
         // three ext columns c+R-1 .. c+R+1 of the rows above, at and below
         const unsigned long long nb = s_rrow64[ry + R - 1] | s_rrow64[ry + R] | s_rrow64[ry + R + 1];
         active = ((nb >> (c + R - 1)) & 7ull) != 0;
-        double gxv = 0.0, gyv = 0.0;
-        if (raster) {
-          const bool exhaustive = s_ncand > kMaxCand;
-          const int e0 = (exhaustive && A.frame_seg) ? A.frame_seg[f] : 0;
-          const int n_eval = exhaustive ? (A.frame_seg ? A.frame_seg[f + 1] - e0 : A.n_seg) : s_ncand;
-          double dmin = INFINITY;
-          int nearest = 0x7fffffff;
-          const double fx = (double)gx, fy = (double)gy;
-          // a segment whose bounding box lies farther than 3 eta cannot give
-          // this pixel a non-zero g (d > cut for it), so its exact distance
-          // is skipped; the bound is padded well past rounding, keeping every
-          // segment with d <= cut -- the only ones that decide g
-          const double cut2 = A.cut * A.cut * (1.0 + 1e-9) + 1e-9;
-          for (int cc = 0; cc < n_eval; ++cc) {
-            const int sidx = exhaustive ? e0 + cc : s_cand[cc];
-            const double4 sg = A.seg[sidx];
-            const double bx = fmax(fmax(fmin(sg.x, sg.z) - fx, fx - fmax(sg.x, sg.z)), 0.0);
-            const double by = fmax(fmax(fmin(sg.y, sg.w) - fy, fy - fmax(sg.y, sg.w)), 0.0);
-            if (bx * bx + by * by > cut2) continue;
-            const double d = seg_dist(fx, fy, sg);
-            const int sp = A.seg_spline[sidx];
-            if (d < dmin || (d == dmin && sp < nearest)) {
-              dmin = d;
-              nearest = sp;
-            }
-          }
-          if (dmin <= A.cut) {
-            const double fall = exp_np((-(dmin * dmin)) / A.c2eta);
-            const double2 dir = A.dirs[nearest];
-            gxv = dir.x * fall;
-            gyv = dir.y * fall;
-          }
-        } else if (A.g_mode == 2) {
-          const double2 g = reinterpret_cast<const double2*>(A.gsrc)[(size_t)f * A.HW + p];
-          gxv = g.x;
-          gyv = g.y;
-        } else if (A.g_mode == 1) {
-          gxv = A.gfx;
-          gyv = A.gfy;
-        }
-        rot = (gxv != 0.0 || gyv != 0.0);
-        if (active && rot) anyg = true;
-        if (A.gbuf) {
-          // the unit guide of the rotated ball (engine.py:155-158), once per pixel
-          double ux = 0.0, uy = 1.0;
-          if (rot) {
-            const double nr = hypot_np(gxv, gyv);
-            ux = gxv / nr;
-            uy = gyv / nr;
-          }
-          A.gbuf[(size_t)f * A.HW + p] = make_double4(gxv, gyv, ux, uy);
-        }
-        const int st = (active ? kStampActive : kStampInactive) | (rot ? kRotBit : 0);
-        work[p] = make_float4(0.f, 0.f, 0.f, __int_as_float(st));
       } else if (near) {
         work[p] = make_float4(0.f, 0.f, 0.f, __int_as_float(kStampBystander));
       }
       if (A.enter) A.enter[(size_t)f * A.HW + p] = active ? 0 : -1;
     }
-    // initial frontier entry of this pixel (published per block below)
-    ent[u] = active ? ((uint32_t)p | (rot ? kEntryRot : 0u)) : 0xffffffffu;
+    act4 |= active ? 1u << u : 0u;
+    // queue the Inpaint pixel (warp-aggregated slot)
+    const unsigned m = __ballot_sync(0xffffffffu, inp);
+    if (m) {
+      int base = 0;
+      if (lane == __ffs(m) - 1) base = atomicAdd(&s_ninp, __popc(m));
+      base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
+      if (inp) s_inp[base + __popc(m & ((1u << lane) - 1))] = (uint16_t)((ry << 5) | c | (active ? 0x8000 : 0));
+    }
+  }
+  __syncthreads();
+  // 4. the guide at every Inpaint pixel of the tile (one per thread), its
+  //    unit vector for the rotated ball, the pixel's stamp; the rotated-ball
+  //    bit goes back to the owning thread through s_rotb
+  {
+    const int n_q = s_ninp;
+#pragma unroll 1
+    for (int k = threadIdx.x; k < n_q; k += kThreads) {
+      const unsigned e = s_inp[k];
+      const int lx = e & 31, ly = (e >> 5) & 31;
+      const bool active = (e & 0x8000u) != 0;
+      const int gx = tx0 + lx, gyq = ty0 + ly;
+      const int p = gyq * A.W + gx;
+      double gxv = 0.0, gyv = 0.0;
+      if (raster) {
+        const bool exhaustive = s_ncand > kMaxCand;
+        const int e0 = (exhaustive && A.frame_seg) ? A.frame_seg[f] : 0;
+        const int n_eval = exhaustive ? (A.frame_seg ? A.frame_seg[f + 1] - e0 : A.n_seg) : s_ncand;
+        double dmin = INFINITY;
+        int nearest = 0x7fffffff;
+        const double fx = (double)gx, fy = (double)gyq;
+        // a segment whose bounding box lies farther than 3 eta cannot give
+        // this pixel a non-zero g (d > cut for it), so its exact distance
+        // is skipped; the bound is padded well past rounding, keeping every
+        // segment with d <= cut -- the only ones that decide g
+        const double cut2 = A.cut * A.cut * (1.0 + 1e-9) + 1e-9;
+        for (int cc = 0; cc < n_eval; ++cc) {
+          const int sidx = exhaustive ? e0 + cc : s_cand[cc];
+          const double4 sg = A.seg[sidx];
+          const double bx = fmax(fmax(fmin(sg.x, sg.z) - fx, fx - fmax(sg.x, sg.z)), 0.0);
+          const double by = fmax(fmax(fmin(sg.y, sg.w) - fy, fy - fmax(sg.y, sg.w)), 0.0);
+          if (bx * bx + by * by > cut2) continue;
+          const double d = seg_dist(fx, fy, sg);
+          const int sp = A.seg_spline[sidx];
+          if (d < dmin || (d == dmin && sp < nearest)) {
+            dmin = d;
+            nearest = sp;
+          }
+        }
+        if (dmin <= A.cut) {
+          const double fall = exp_np((-(dmin * dmin)) / A.c2eta);
+          const double2 dir = A.dirs[nearest];
+          gxv = dir.x * fall;
+          gyv = dir.y * fall;
+        }
+      } else if (A.g_mode == 2) {
+        const double2 g = reinterpret_cast<const double2*>(A.gsrc)[(size_t)f * A.HW + p];
+        gxv = g.x;
+        gyv = g.y;
+      } else if (A.g_mode == 1) {
+        gxv = A.gfx;
+        gyv = A.gfy;
+      }
+      const bool rot = (gxv != 0.0 || gyv != 0.0);
+      if (rot) {
+        atomicOr(&s_rotb[ly], 1u << lx);
+        if (active) s_anyg = 1;
+      }
+      if (A.gbuf) {
+        // the unit guide of the rotated ball (engine.py:155-158), once per pixel
+        double ux = 0.0, uy = 1.0;
+        if (rot) {
+          const double nr = hypot_np(gxv, gyv);
+          ux = gxv / nr;
+          uy = gyv / nr;
+        }
+        A.gbuf[(size_t)f * A.HW + p] = make_double4(gxv, gyv, ux, uy);
+      }
+      const int st = (active ? kStampActive : kStampInactive) | (rot ? kRotBit : 0);
+      work[p] = make_float4(0.f, 0.f, 0.f, __int_as_float(st));
+    }
+  }
+  __syncthreads();
+  const bool anyg = s_anyg != 0;
+  uint32_t ent[4];
+  {
+    const unsigned rotb = s_rotb[ry];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int c = c0 + u;
+      const bool rot = (rotb >> c) & 1u;
+      // initial frontier entry of this pixel (published per block below)
+      ent[u] = ((act4 >> u) & 1u) ? ((uint32_t)(gy * A.W + tx0 + c) | (rot ? kEntryRot : 0u)) : 0xffffffffu;
+    }
   }
   // block-aggregated append of the initial frontier (lattice entries to the
   // front of the list, rotated-ball entries to the back when split), |D| and
@@ -676,6 +754,7 @@ __global__ void __launch_bounds__(kThreads, GF_PREP_MIN_BLOCKS)
   const int tx0 = tix * kTile;
   const int ty0 = tiy * kTile;
   timeline_mark(A, 0, true);
+  PREP_PROF_T0;
   // every prep block is resident once all have passed here: the shell
   // kernel may start launching (it waits for this grid's completion)
   pdl_trigger();
@@ -688,30 +767,61 @@ __global__ void __launch_bounds__(kThreads, GF_PREP_MIN_BLOCKS)
   __shared__ __align__(128) T s_img[kTile * kTile * C];
   __shared__ __align__(128) uint8_t s_lab[kTileExt * kLabBoxMax];
   __shared__ __align__(8) unsigned long long s_bar;
-  if (threadIdx.x == 0) {
-    mbar_init(&s_bar, 1);
-    fence_mbar_init();
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    mbar_expect_tx(&s_bar, (unsigned)(sizeof(T) * kTile * kTile * C + M.lab_bw * ext));
-    tma_load_3d(s_img, &M.img, tx0 * C, ty0, f, &s_bar);
-    tma_load_3d(s_lab, &M.lab, tx0 - 16, ty0 - R, f, &s_bar);
-  }
   __shared__ unsigned int s_hrow[kTileExt];
   __shared__ unsigned int s_vrow[kTile];
   __shared__ unsigned long long s_hrow64[kTileExt];
   __shared__ unsigned long long s_rrow64[kTileExt];
   __shared__ int s_cand[kMaxCand];
   __shared__ int s_ncand;
+  __shared__ uint16_t s_inp[kTile * kTile];
+  __shared__ unsigned int s_rotb[kTile];
+  __shared__ int s_ninp, s_anyg;
   __shared__ int s_cnt[kThreads / 32];
   __shared__ int s_wl[kThreads / 32], s_wr[kThreads / 32];
   __shared__ int s_bL, s_bR;
   __shared__ unsigned long long s_red[4][kThreads / 32];
+  if (threadIdx.x == 0) {
+    mbar_init(&s_bar, 1);
+    fence_mbar_init();
+    s_ncand = 0;
+    s_ninp = 0;
+    s_anyg = 0;
+  }
+  if (threadIdx.x < kTile) s_rotb[threadIdx.x] = 0u;
+  // the frame's hull as last seen (a filter for the hull atomics below: the
+  // hull only grows, so a stale value skips no needed update), read while
+  // the tile loads
+  unsigned long long hull_seen = 0ULL;
+  if (threadIdx.x < 4)
+    hull_seen = *(volatile unsigned long long*)(threadIdx.x < 2 ? &A.hull[2 * f + threadIdx.x]
+                                                                 : &A.bys_frame[2 * f + threadIdx.x - 2]);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    mbar_expect_tx(&s_bar, (unsigned)(sizeof(T) * kTile * kTile * C + M.lab_bw * ext));
+    tma_load_3d(s_img, &M.img, tx0 * C, ty0, f, &s_bar);
+    tma_load_3d(s_lab, &M.lab, tx0 - 16, ty0 - R, f, &s_bar);
+  }
+  const bool raster = A.n_seg > 0;
+  const int s0 = A.frame_seg ? A.frame_seg[f] : 0;
+  const int s1 = A.frame_seg ? A.frame_seg[f + 1] : A.n_seg;
+  // the segments whose cut box meets the tile (tiles that need the guide;
+  // culling here, while the tile loads, measured slower)
+  auto cull = [&]() {
+    const double x0 = (double)tx0, x1 = (double)min(A.W - 1, tx0 + kTile - 1);
+    const double y0 = (double)ty0, y1 = (double)min(A.H - 1, ty0 + kTile - 1);
+    for (int i = s0 + threadIdx.x; i < s1; i += kThreads) {
+      const double4 sg = A.seg[i];
+      const double lo_x = fmin(sg.x, sg.z) - A.cut, hi_x = fmax(sg.x, sg.z) + A.cut;
+      const double lo_y = fmin(sg.y, sg.w) - A.cut, hi_y = fmax(sg.y, sg.w) + A.cut;
+      if (hi_x >= x0 && lo_x <= x1 && hi_y >= y0 && lo_y <= y1) {
+        const int slot = atomicAdd(&s_ncand, 1);
+        if (slot < kMaxCand) s_cand[slot] = i;
+      }
+    }
+  };
   const uint8_t* lab = A.labels + (size_t)f * A.HW;
   const T* img = reinterpret_cast<const T*>(A.image) + (size_t)f * A.HW * C;
   float4* work = A.work + (size_t)f * A.HW;
-  const bool raster = A.n_seg > 0;
   const int ry = threadIdx.x >> 3;
   const int c0 = (threadIdx.x & 7) * 4;
   const int gy = ty0 + ry;
@@ -720,7 +830,6 @@ __global__ void __launch_bounds__(kThreads, GF_PREP_MIN_BLOCKS)
   //    column x; out of lattice = neither -- TMA fills those cells with 0,
   //    so the lattice bounds mask them), four threads per ext row, 16 label
   //    bytes each, packed 4 at a time (one multiply per word)
-  if (threadIdx.x == 0) s_ncand = 0;
   bool any_inp = false;
   const unsigned long long ext_mask = ext >= 64 ? ~0ULL : ((1ULL << ext) - 1);
   // ext columns inside the lattice
@@ -728,6 +837,7 @@ __global__ void __launch_bounds__(kThreads, GF_PREP_MIN_BLOCKS)
   if (tx0 - R < 0) col_ok &= ~0ULL << (R - tx0);
   if (tx0 - R + ext > A.W) col_ok &= (A.W - (tx0 - R)) >= 64 ? ~0ULL : ((1ULL << (A.W - (tx0 - R))) - 1);
   mbar_wait(&s_bar, 0);
+  PREP_STAGE(1);
   if (threadIdx.x == 0) {
     fence_proxy_async();
     tma_store_3d(&M.out, tx0 * C, ty0, f, s_img);
@@ -804,6 +914,7 @@ __global__ void __launch_bounds__(kThreads, GF_PREP_MIN_BLOCKS)
     }
   }
   const bool tile_d = __syncthreads_or(any_inp);
+  PREP_STAGE(2);
   // value hull of the Readable pixels (the copy is the TMA store above)
   {
     // [0] value hull of the Readable pixels, [1] range of the Bystanders
@@ -876,10 +987,11 @@ __global__ void __launch_bounds__(kThreads, GF_PREP_MIN_BLOCKS)
       // their atomics); i >= 2: the tile's Bystander range, read by the
       // shell loop's clip, and the frame's
       unsigned long long* fr = i < 2 ? &A.hull[2 * f + i] : &A.bys_frame[2 * f + i - 2];
-      if (e != 0ULL && e > *(volatile unsigned long long*)fr) atomicMax(fr, e);
+      if (e != 0ULL && e > hull_seen) atomicMax(fr, e);
       if (i >= 2) A.bys[((size_t)f * A.ntiles + tile) * 2 + i - 2] = e;
     }
   }
+  PREP_STAGE(3);
   if (!tile_d) {
     // no Inpaint pixel within reach: nothing of this tile is ever sampled
     if (A.enter && row_in) {
@@ -890,23 +1002,10 @@ __global__ void __launch_bounds__(kThreads, GF_PREP_MIN_BLOCKS)
     }
     timeline_mark(A, 0, false);
     if (threadIdx.x == 0) bulk_wait_read0();
+    PREP_PROF(0);
     return;
   }
-  if (raster) {
-    const double x0 = (double)tx0, x1 = (double)min(A.W - 1, tx0 + kTile - 1);
-    const double y0 = (double)ty0, y1 = (double)min(A.H - 1, ty0 + kTile - 1);
-    const int s0 = A.frame_seg ? A.frame_seg[f] : 0;
-    const int s1 = A.frame_seg ? A.frame_seg[f + 1] : A.n_seg;
-    for (int i = s0 + threadIdx.x; i < s1; i += kThreads) {
-      const double4 sg = A.seg[i];
-      const double lo_x = fmin(sg.x, sg.z) - A.cut, hi_x = fmax(sg.x, sg.z) + A.cut;
-      const double lo_y = fmin(sg.y, sg.w) - A.cut, hi_y = fmax(sg.y, sg.w) + A.cut;
-      if (hi_x >= x0 && lo_x <= x1 && hi_y >= y0 && lo_y <= y1) {
-        const int slot = atomicAdd(&s_ncand, 1);
-        if (slot < kMaxCand) s_cand[slot] = i;
-      }
-    }
-  }
+  if (raster) cull();
   // 2. dilation of the Inpaint indicator (the rows were dilated horizontally
   //    when they were built; visible since the label barrier)
   // ... and vertical: bit c of s_vrow[y] <=> an Inpaint pixel within
@@ -918,11 +1017,15 @@ __global__ void __launch_bounds__(kThreads, GF_PREP_MIN_BLOCKS)
   }
   __syncthreads();
 
-  // 3. four consecutive pixels per thread: row ry, columns c0 .. c0+3
+  PREP_STAGE(4);
+  // 3. four consecutive pixels per thread: row ry, columns c0 .. c0+3.
+  //    The cheap per-pixel work (stamps, enter map, activity) runs here; the
+  //    Inpaint pixels are queued in shared memory for step 4, so the guide
+  //    evaluation (raster, exp, hypot in fp64) runs one pixel per thread over
+  //    a dense list instead of four serial, divergent pixels per thread.
   const unsigned int vmask = s_vrow[ry];
   int n_inp = 0;
-  bool anyg = false;
-  uint32_t ent[4];
+  unsigned act4 = 0;  // bit u: own pixel u is an active Inpaint pixel
 #pragma unroll
   for (int u = 0; u < 4; ++u) {
     const int c = c0 + u;
@@ -931,7 +1034,8 @@ __global__ void __launch_bounds__(kThreads, GF_PREP_MIN_BLOCKS)
     const int p = gy * A.W + gx;
     const uint8_t l = (uint8_t)(own4 >> (8 * u));
     const bool near = (vmask >> c) & 1u;
-    bool active = false, rot = false;
+    bool active = false;
+    const bool inp = in && l == 255;
     if (in) {
       if (l == 0) {
         if (near) {
@@ -941,73 +1045,113 @@ __global__ void __launch_bounds__(kThreads, GF_PREP_MIN_BLOCKS)
           work[p] = make_float4(cv[0], cv[1], cv[2], __int_as_float(kStampReadable));
           if (C > 3) A.c3[(size_t)f * A.HW + p] = cv[3];
         }
-      } else if (l == 255) {
+      } else if (inp) {
         ++n_inp;
         // a Readable 8-neighbour (the pixel itself is not Readable): the
         // three ext columns c+R-1 .. c+R+1 of the rows above, at and below
         const unsigned long long nb = s_rrow64[ry + R - 1] | s_rrow64[ry + R] | s_rrow64[ry + R + 1];
         active = ((nb >> (c + R - 1)) & 7ull) != 0;
-        double gxv = 0.0, gyv = 0.0;
-        if (raster) {
-          const bool exhaustive = s_ncand > kMaxCand;
-          const int e0 = (exhaustive && A.frame_seg) ? A.frame_seg[f] : 0;
-          const int n_eval = exhaustive ? (A.frame_seg ? A.frame_seg[f + 1] - e0 : A.n_seg) : s_ncand;
-          double dmin = INFINITY;
-          int nearest = 0x7fffffff;
-          const double fx = (double)gx, fy = (double)gy;
-          // a segment whose bounding box lies farther than 3 eta cannot give
-          // this pixel a non-zero g (d > cut for it), so its exact distance
-          // is skipped; the bound is padded well past rounding, keeping every
-          // segment with d <= cut -- the only ones that decide g
-          const double cut2 = A.cut * A.cut * (1.0 + 1e-9) + 1e-9;
-          for (int cc = 0; cc < n_eval; ++cc) {
-            const int sidx = exhaustive ? e0 + cc : s_cand[cc];
-            const double4 sg = A.seg[sidx];
-            const double bx = fmax(fmax(fmin(sg.x, sg.z) - fx, fx - fmax(sg.x, sg.z)), 0.0);
-            const double by = fmax(fmax(fmin(sg.y, sg.w) - fy, fy - fmax(sg.y, sg.w)), 0.0);
-            if (bx * bx + by * by > cut2) continue;
-            const double d = seg_dist(fx, fy, sg);
-            const int sp = A.seg_spline[sidx];
-            if (d < dmin || (d == dmin && sp < nearest)) {
-              dmin = d;
-              nearest = sp;
-            }
-          }
-          if (dmin <= A.cut) {
-            const double fall = exp_np((-(dmin * dmin)) / A.c2eta);
-            const double2 dir = A.dirs[nearest];
-            gxv = dir.x * fall;
-            gyv = dir.y * fall;
-          }
-        } else if (A.g_mode == 2) {
-          const double2 g = reinterpret_cast<const double2*>(A.gsrc)[(size_t)f * A.HW + p];
-          gxv = g.x;
-          gyv = g.y;
-        } else if (A.g_mode == 1) {
-          gxv = A.gfx;
-          gyv = A.gfy;
-        }
-        rot = (gxv != 0.0 || gyv != 0.0);
-        if (active && rot) anyg = true;
-        if (A.gbuf) {
-          // the unit guide of the rotated ball (engine.py:155-158), once per pixel
-          double ux = 0.0, uy = 1.0;
-          if (rot) {
-            const double nr = hypot_np(gxv, gyv);
-            ux = gxv / nr;
-            uy = gyv / nr;
-          }
-          A.gbuf[(size_t)f * A.HW + p] = make_double4(gxv, gyv, ux, uy);
-        }
-        const int st = (active ? kStampActive : kStampInactive) | (rot ? kRotBit : 0);
-        work[p] = make_float4(0.f, 0.f, 0.f, __int_as_float(st));
       } else if (near) {
         work[p] = make_float4(0.f, 0.f, 0.f, __int_as_float(kStampBystander));
       }
       if (A.enter) A.enter[(size_t)f * A.HW + p] = active ? 0 : -1;
     }
-    // initial frontier entry of this pixel (published per block below)
-    ent[u] = active ? ((uint32_t)p | (rot ? kEntryRot : 0u)) : 0xffffffffu;
+    act4 |= active ? 1u << u : 0u;
+    // queue the Inpaint pixel (warp-aggregated slot)
+    const unsigned m = __ballot_sync(0xffffffffu, inp);
+    if (m) {
+      int base = 0;
+      if (lane == __ffs(m) - 1) base = atomicAdd(&s_ninp, __popc(m));
+      base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
+      if (inp) s_inp[base + __popc(m & ((1u << lane) - 1))] = (uint16_t)((ry << 5) | c | (active ? 0x8000 : 0));
+    }
+  }
+  __syncthreads();
+  PREP_STAGE(5);
+  // 4. the guide at every Inpaint pixel of the tile (one per thread), its
+  //    unit vector for the rotated ball, the pixel's stamp; the rotated-ball
+  //    bit goes back to the owning thread through s_rotb
+  {
+    const int n_q = s_ninp;
+#pragma unroll 1
+    for (int k = threadIdx.x; k < n_q; k += kThreads) {
+      const unsigned e = s_inp[k];
+      const int lx = e & 31, ly = (e >> 5) & 31;
+      const bool active = (e & 0x8000u) != 0;
+      const int gx = tx0 + lx, gyq = ty0 + ly;
+      const int p = gyq * A.W + gx;
+      double gxv = 0.0, gyv = 0.0;
+      if (raster) {
+        const bool exhaustive = s_ncand > kMaxCand;
+        const int e0 = (exhaustive && A.frame_seg) ? A.frame_seg[f] : 0;
+        const int n_eval = exhaustive ? (A.frame_seg ? A.frame_seg[f + 1] - e0 : A.n_seg) : s_ncand;
+        double dmin = INFINITY;
+        int nearest = 0x7fffffff;
+        const double fx = (double)gx, fy = (double)gyq;
+        // a segment whose bounding box lies farther than 3 eta cannot give
+        // this pixel a non-zero g (d > cut for it), so its exact distance
+        // is skipped; the bound is padded well past rounding, keeping every
+        // segment with d <= cut -- the only ones that decide g
+        const double cut2 = A.cut * A.cut * (1.0 + 1e-9) + 1e-9;
+        for (int cc = 0; cc < n_eval; ++cc) {
+          const int sidx = exhaustive ? e0 + cc : s_cand[cc];
+          const double4 sg = A.seg[sidx];
+          const double bx = fmax(fmax(fmin(sg.x, sg.z) - fx, fx - fmax(sg.x, sg.z)), 0.0);
+          const double by = fmax(fmax(fmin(sg.y, sg.w) - fy, fy - fmax(sg.y, sg.w)), 0.0);
+          if (bx * bx + by * by > cut2) continue;
+          const double d = seg_dist(fx, fy, sg);
+          const int sp = A.seg_spline[sidx];
+          if (d < dmin || (d == dmin && sp < nearest)) {
+            dmin = d;
+            nearest = sp;
+          }
+        }
+        if (dmin <= A.cut) {
+          const double fall = exp_np((-(dmin * dmin)) / A.c2eta);
+          const double2 dir = A.dirs[nearest];
+          gxv = dir.x * fall;
+          gyv = dir.y * fall;
+        }
+      } else if (A.g_mode == 2) {
+        const double2 g = reinterpret_cast<const double2*>(A.gsrc)[(size_t)f * A.HW + p];
+        gxv = g.x;
+        gyv = g.y;
+      } else if (A.g_mode == 1) {
+        gxv = A.gfx;
+        gyv = A.gfy;
+      }
+      const bool rot = (gxv != 0.0 || gyv != 0.0);
+      if (rot) {
+        atomicOr(&s_rotb[ly], 1u << lx);
+        if (active) s_anyg = 1;
+      }
+      if (A.gbuf) {
+        // the unit guide of the rotated ball (engine.py:155-158), once per pixel
+        double ux = 0.0, uy = 1.0;
+        if (rot) {
+          const double nr = hypot_np(gxv, gyv);
+          ux = gxv / nr;
+          uy = gyv / nr;
+        }
+        A.gbuf[(size_t)f * A.HW + p] = make_double4(gxv, gyv, ux, uy);
+      }
+      const int st = (active ? kStampActive : kStampInactive) | (rot ? kRotBit : 0);
+      work[p] = make_float4(0.f, 0.f, 0.f, __int_as_float(st));
+    }
+  }
+  __syncthreads();
+  PREP_STAGE(6);
+  const bool anyg = s_anyg != 0;
+  uint32_t ent[4];
+  {
+    const unsigned rotb = s_rotb[ry];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int c = c0 + u;
+      const bool rot = (rotb >> c) & 1u;
+      // initial frontier entry of this pixel (published per block below)
+      ent[u] = ((act4 >> u) & 1u) ? ((uint32_t)(gy * A.W + tx0 + c) | (rot ? kEntryRot : 0u)) : 0xffffffffu;
+    }
   }
   // block-aggregated append of the initial frontier (lattice entries to the
   // front of the list, rotated-ball entries to the back when split), |D| and
@@ -1051,7 +1195,9 @@ __global__ void __launch_bounds__(kThreads, GF_PREP_MIN_BLOCKS)
       }
       if (ag) A.anyg[f] = 1;
     }
+    PREP_STAGE(7);
     __syncthreads();
+    PREP_STAGE(8);
     int bL = s_bL + s_wl[warp], bR = s_bR + s_wr[warp];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
@@ -1067,6 +1213,7 @@ __global__ void __launch_bounds__(kThreads, GF_PREP_MIN_BLOCKS)
   }
   timeline_mark(A, 0, false);
   if (threadIdx.x == 0) bulk_wait_read0();
+  PREP_PROF(1u | ((unsigned)s_ncand << 1));
 }
 
 
@@ -1820,6 +1967,9 @@ __global__ void __launch_bounds__(kShellThreads, GF_SHELL_MIN_BLOCKS)
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Smem& S = *reinterpret_cast<Smem*>(smem_raw);
+#ifdef GF_PREP_PROF
+  if (threadIdx.x == 0) atomicMin(&g_shell_prof[0], gtimer0());
+#endif
   for (int i = threadIdx.x; i < P.K; i += blockDim.x) {
     S.tab.n[i] = tables.n[i];
     S.tab.m[i] = tables.m[i];
@@ -1831,6 +1981,13 @@ __global__ void __launch_bounds__(kShellThreads, GF_SHELL_MIN_BLOCKS)
     S.tab.off[i] = tables.ni[i] + tables.mi[i] * A.W;
   }
   pdl_wait();
+#ifdef GF_PREP_PROF
+  if (threadIdx.x == 0) {
+    const unsigned long long t = gtimer0();
+    atomicMin(&g_shell_prof[1], t);
+    atomicMax(&g_shell_prof[2], t);
+  }
+#endif
   timeline_mark(A, 1, true);
   __syncthreads();
 
