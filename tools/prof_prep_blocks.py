@@ -75,4 +75,8 @@ out["end_hist_2us"] = np.bincount((en // 2).astype(int)).tolist()
 # longest blocks
 idx = np.argsort(-dur)[:8]
 out["longest"] = [[int(i), float(dur[i]), int(fl[i] & 1), int(fl[i] >> 1), float(st[i])] for i in idx]
+def stages(i):
+    ks = [k for k in (0, 1, 2, 3, 4, 5, 6, 7, 8, 10) if B[i, k] != 0]
+    return {f"{a}->{b}": float((B[i, b] - B[i, a]) / 1e3) for a, b in zip(ks, ks[1:])}
+out["longest_stages"] = [stages(int(i)) for i in idx]
 print(json.dumps(out, indent=1))
