@@ -73,7 +73,7 @@ class ClockSampler:
     REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
                "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
 
-    def __init__(self, index=0, period_s=0.002):
+    def __init__(self, index=0, period_s=0.0005):
         self.index = index
         self.period = period_s
         self.samples = []
@@ -101,6 +101,11 @@ class ClockSampler:
 
             self._t = threading.Thread(target=poll, daemon=True)
             self._t.start()
+            # NVML's first query is slow: start timing once the poller runs
+            t_end = time.time() + 1.0
+            while not self.samples and time.time() < t_end:
+                time.sleep(0.0002)
+            self.samples.clear()
         except Exception:
             self._t = None
         return self
