@@ -515,15 +515,21 @@ def bench_deadlock(dev):
         p = FillParams(**case["params"])
         res = fill_device(img, lab, g, p, rows_cap=1 << 16)
         ws = res["workspace"]
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        torch.cuda.synchronize()
-        e0.record()
-        res = fill_device(img, lab, g, p, rows_cap=1 << 16, workspace=ws)
-        e1.record()
-        torch.cuda.synchronize()
+        # median of 3 timed fills: this runs right after the CPU pool
+        # baseline, and the first fill after seconds of GPU idle can run
+        # while the clocks ramp back up (measured 19.6 vs 11.6 us per shell)
+        runs = []
+        for _ in range(3):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record()
+            res = fill_device(img, lab, g, p, rows_cap=1 << 16, workspace=ws)
+            e1.record()
+            torch.cuda.synchronize()
+            runs.append(e0.elapsed_time(e1))
         st = res["stats"][0].cpu().numpy()
-        ms = e0.elapsed_time(e1)
-        out[case["name"]] = {"ms": ms, "shells": int(st[N.STAT_ITERATIONS]),
+        ms = sorted(runs)[1]
+        out[case["name"]] = {"ms": ms, "ms_runs": runs, "shells": int(st[N.STAT_ITERATIONS]),
                              "guarded_shells": int(st[N.STAT_DEADLOCK]),
                              "us_per_shell": ms * 1e3 / int(st[N.STAT_ITERATIONS])}
     a, b = out["halfplane_25deg_mu50"], out["halfplane_10deg_mu50"]
