@@ -282,6 +282,18 @@ class Mirror:
             ctypes.c_void_p(self.buf.data_ptr() + lo), hi - lo, _MIRROR_CHUNK, N.stream_ptr(),
             ctypes.c_void_p(self.side.cuda_stream)))
 
+    def settle(self):
+        """Error path: let every transfer touching the result buffer land
+        (the side stream's mirror, and the current stream's H2D reads and
+        delta writes) before the buffer can go back to the pool."""
+        import torch
+
+        for s in (self.side, torch.cuda.current_stream()):
+            try:
+                s.synchronize()
+            except Exception:
+                pass
+
     def finish(self, d_in, d_out):
         """Enqueue the delta write on the current stream (after the mirror);
         the caller's next synchronisation makes ``result`` final."""
@@ -306,9 +318,10 @@ class Mirror:
 def upload_mirrored(src, device, as_tensor: bool):
     """Host frame (numpy array, or pinned CPU tensor) -> (CUDA tensor, Mirror).
 
-    Pinned tensors are DMA'd straight from the caller's memory; numpy arrays
-    go through the chunked pinned stager.  Either way each landed chunk is
-    mirrored back into the result buffer on the side stream.
+    Pinned sources are DMA'd straight from the caller's memory and each
+    landed chunk is mirrored back into the result buffer on the side stream.
+    Pageable numpy arrays are copied by host threads into the result buffer
+    itself, which then serves as the H2D source (no mirror needed).
     """
     import torch
 
@@ -326,16 +339,22 @@ def upload_mirrored(src, device, as_tensor: bool):
         # page-locked numpy memory (e.g. a result of this package): DMA directly
         mir.upload(a.ctypes.data, dst.data_ptr(), 0, n)
         return dst, mir
-    stage = _staging(n, "img")
+    # pageable memory: the host threads copy the frame straight into the
+    # pinned RESULT buffer, chunk by chunk, and each landed chunk is DMA'd to
+    # the device from there.  The result is then already seeded with the
+    # input (no D2H mirror), and host memory carries 150 MB per 1080p f64
+    # frame instead of 200 (copy into a staging buffer, H2D from it, D2H
+    # into the result) -- the bound of this path on the B200 box.
     srcb = a.reshape(-1).view(np.uint8)
-    host = stage.numpy()
+    host = mir.buf.numpy()
+    dflat = dst.view(-1).view(torch.uint8)
+    # (smaller copy pieces than the DMA chunk measured slower: future and
+    # GIL overhead; tools/exp_numpy_ab.sh)
     parts = _chunks_of(n, _CHUNK)
     futs = [_executor().submit(np.copyto, host[lo:hi], srcb[lo:hi]) for lo, hi in parts]
     for (lo, hi), fut in zip(parts, futs):
         fut.result()
-        mir.upload(stage.data_ptr(), dst.data_ptr(), lo, hi)
-    # the staging buffer is reused by the next call: wait for the H2D
-    torch.cuda.current_stream().synchronize()
+        dflat[lo:hi].copy_(mir.buf[lo:hi], non_blocking=True)
     return dst, mir
 
 

@@ -279,7 +279,7 @@ def _run_fill(image, labels, guide_vecs, params: FillParams, tracked: bool, orde
         if mirror is not None:
             # the mirror DMA still targets the pooled result buffer: let it land
             # before the buffer can be handed to another caller
-            mirror.side.synchronize()
+            mirror.settle()
         raise
     if validate and stats[N.STAT_BAD_LABELS]:
         grid.validate_labels(labels)  # k_prep saw a bad label: the reference's message
@@ -389,7 +389,7 @@ def _run_coherence(image, labels, params, tracked, order_log, dev, runner=None):
             torch.cuda.current_stream().synchronize()
     except BaseException:
         if mirror is not None:
-            mirror.side.synchronize()
+            mirror.settle()
         raise
     rep = FillReport()
     rep.iterations = r["iterations"]
