@@ -392,6 +392,36 @@ def test_mirrored_path_concurrent_threads():
         assert np.array_equal(u, want[i % 3])
 
 
+def test_pageable_staging_never_writes_a_live_result():
+    """Pageable numpy frames are copied by host threads into a pooled pinned
+    result buffer before the DMA: a result (or only a view of it) kept by
+    the caller is never the buffer a later call of the same size stages
+    into, and a released one is recycled without stale pixels."""
+    import gc
+
+    from paper_1611_05319_b200 import tracker
+
+    cases = [scenes.small_scene(270, 480, band=8, gx=5, gy=3, n_spl=4, seed=70 + s)
+             for s in range(3)]
+    assert cases[0].image.nbytes >= (1 << 20)
+    run = [lambda sc=sc: tracker.run_tracked(sc.image, sc.labels, _splines(sc),
+                                             FillParams(**sc.params))[0] for sc in cases]
+    first = run[0]()
+    want0 = first.copy()
+    view = first[..., 1]  # keep only a view of the first result
+    del first
+    gc.collect()
+    second = run[1]()
+    third = run[2]()
+    assert np.array_equal(view, want0[..., 1])
+    want2 = third.copy()
+    del second, third
+    gc.collect()
+    again = run[2]()  # recycled buffer: fully rewritten
+    assert np.array_equal(again, want2)
+    assert np.array_equal(view, want0[..., 1])
+
+
 def test_page_locked_numpy_inputs_take_the_direct_dma():
     """numpy arrays living in page-locked memory (a field returned by
     build_guide_field, a view of a pinned tensor) are DMA'd without the
